@@ -1,0 +1,238 @@
+/*
+ * rcg_b200.h -- C-ABI of the B200-native deflated-ICCG hot path (librcg_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures.  Every vector
+ * argument may be a HOST pointer (pageable or pinned; the call stages it through HBM) or a
+ * DEVICE pointer on the context's GPU (used in place) -- the library inspects the pointer.
+ *
+ * Each entry point names the reference declaration it replaces (paths relative to
+ * /root/reference/proj/include/recycg).  Status codes map 1:1 onto the reference's exception
+ * types so a C++ or ctypes binding can rethrow them:
+ *   RCG_E_INVALID   -> std::invalid_argument   (config / size errors)
+ *   RCG_E_BREAKDOWN -> recycg::BreakdownError  (non-SPD, pivot failure, W^T A W not SPD)
+ *   RCG_E_PARSE     -> recycg::ParseError      (CSR validation failure)
+ *   RCG_E_CUDA      -> runtime error           (no GPU, CUDA fault, out of device memory)
+ * There is no CPU fallback: without a usable sm_100 device every compute call returns RCG_E_CUDA.
+ */
+#ifndef RCG_B200_H
+#define RCG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCG_OK 0
+#define RCG_E_INVALID 1
+#define RCG_E_BREAKDOWN 2
+#define RCG_E_PARSE 3
+#define RCG_E_CUDA 4
+
+typedef struct rcg_ctx rcg_ctx;         /* one GPU, one stream, workspaces */
+typedef struct rcg_matrix rcg_matrix;   /* device CSR (CsrMatrix) */
+typedef struct rcg_ic rcg_ic;           /* device IC(0) factor + sweep schedules (IcFactor) */
+typedef struct rcg_tall rcg_tall;       /* device n x k column block (TallDense) */
+typedef struct rcg_basis rcg_basis;     /* W, AW, chol(W^T A W) (DeflationOperator / SC state) */
+typedef struct rcg_sampler rcg_sampler; /* device snapshot slots (SamplerState) */
+
+/* message of the last failing call on this thread; "" after success */
+const char* rcg_last_error(void);
+const char* rcg_build_info(void);
+
+/* ------------------------------------------------------------------ context */
+int rcg_ctx_create(int device, rcg_ctx** out);
+void rcg_ctx_destroy(rcg_ctx* ctx);
+int rcg_ctx_synchronize(rcg_ctx* ctx);
+/* number of kernels this context has launched (for gpu_launches accounting) */
+int64_t rcg_ctx_launch_count(const rcg_ctx* ctx);
+/* device time (ms) accumulated by the named kernel class since the last reset, measured with
+ * CUDA events on the context stream when profiling is enabled (class: 0 spmv, 1 fwd sweep,
+ * 2 bwd sweep, 3 vector ops, 4 projection).  Used by bench.py for the roofline. */
+int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable);
+int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launches);
+void rcg_ctx_reset_stats(rcg_ctx* ctx);
+
+/* ------------------------------------------------------------------ CSR (csr_matrix.hpp) */
+/* CsrMatrix(n, row_start, col_idx, values) -- csr_matrix.hpp:28-30.  validate != 0 runs the
+ * reference invariants of CsrMatrix::validate (csr_matrix.cpp:36-87) on the host arrays and
+ * returns RCG_E_PARSE with the reference message on failure. */
+int rcg_matrix_create(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const int32_t* col_idx,
+                      const double* values, int validate, rcg_matrix** out);
+void rcg_matrix_destroy(rcg_matrix* a);
+int32_t rcg_matrix_n(const rcg_matrix* a);
+int64_t rcg_matrix_nnz(const rcg_matrix* a);
+int rcg_matrix_values(rcg_ctx* ctx, const rcg_matrix* a, double* values_out);
+/* spmv(a, x, y) -- csr_matrix.hpp:54; bitwise equal to the reference (sequential row sums) */
+int rcg_spmv(rcg_ctx* ctx, const rcg_matrix* a, const double* x, double* y);
+/* spmv_dual(a, x1, x2, y1, y2) -- csr_matrix.hpp:56-59; each output bitwise equal to rcg_spmv */
+int rcg_spmv_dual(rcg_ctx* ctx, const rcg_matrix* a, const double* x1, const double* x2,
+                  double* y1, double* y2);
+/* diagonal_scale(a) -- scaling.hpp:24-26: returns the scaled matrix and d_inv_sqrt (length n) */
+int rcg_diagonal_scale(rcg_ctx* ctx, const rcg_matrix* a, rcg_matrix** scaled, double* d_inv_sqrt);
+
+/* ------------------------------------------------------------------ IC(0) (ic_preconditioner.hpp) */
+/* ic0_factorize(a, shift, num_blocks) -- ic_preconditioner.hpp:44: zero-fill L D L^T with the
+ * reference shift ladder, computed on the host (one-time setup) from host CSR arrays, then
+ * uploaded with its level schedules. */
+int rcg_ic0_factorize(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const int32_t* col_idx,
+                      const double* values, double shift, int num_blocks, rcg_ic** out);
+/* upload an existing IcFactor (ic_preconditioner.hpp:18-37) so the operator is identical */
+int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_bounds,
+                  const int32_t* l_row_start, const int32_t* l_col, const double* l_val,
+                  const double* d, const int32_t* u_row_start, const int32_t* u_col,
+                  const double* u_val, double shift_used, rcg_ic** out);
+void rcg_ic_destroy(rcg_ic* f);
+/* factor metadata: nnz of L, shift used, forward/backward level counts */
+int rcg_ic_info(const rcg_ic* f, int64_t* nnz_l, double* shift_used, int32_t* fwd_levels,
+                int32_t* bwd_levels);
+/* copy the host image of the factor out (arrays sized n+1 / nnz_l / n) */
+int rcg_ic_export(const rcg_ic* f, int32_t* block_bounds, int32_t* l_row_start, int32_t* l_col,
+                  double* l_val, double* d, int32_t* u_row_start, int32_t* u_col, double* u_val);
+/* ic_apply(f, r, z) -- ic_preconditioner.hpp:47; bitwise equal to the reference */
+int rcg_ic_apply(rcg_ctx* ctx, const rcg_ic* f, const double* r, double* z);
+
+/* ------------------------------------------------------------------ TallDense (dense.hpp) */
+int rcg_tall_create(rcg_ctx* ctx, int32_t n, int k, const double* cols, rcg_tall** out);
+void rcg_tall_destroy(rcg_tall* t);
+int rcg_tall_k(const rcg_tall* t);
+int32_t rcg_tall_n(const rcg_tall* t);
+/* column-major n x k, leading dimension n */
+int rcg_tall_download(rcg_ctx* ctx, const rcg_tall* t, double* cols_out);
+/* mgs_orthonormalize(v, drop_tol) -- dense.hpp:50 */
+int rcg_mgs_orthonormalize(rcg_ctx* ctx, const rcg_tall* v, double drop_tol, rcg_tall** out);
+
+/* ------------------------------------------------------------------ samplers (sampling.hpp) */
+#define RCG_SAMPLER_A 0
+#define RCG_SAMPLER_B 1
+/* SamplerState::method_a(m, cap) / method_b(m, eps) -- sampling.hpp:30-34 (slots of length n) */
+int rcg_sampler_create(rcg_ctx* ctx, int method, int m, int iteration_cap, double eps, int32_t n,
+                       rcg_sampler** out);
+void rcg_sampler_destroy(rcg_sampler* s);
+/* SamplerState::offer -- sampling.hpp:37 (host-driven offer of an arbitrary payload) */
+int rcg_sampler_offer(rcg_ctx* ctx, rcg_sampler* s, int iteration, double relres,
+                      const double* payload);
+/* occupied()/stored_iteration() for all m slots; stored_count() returned */
+int rcg_sampler_state(const rcg_sampler* s, int* occupied, int* stored_iter);
+int rcg_sampler_slot(rcg_ctx* ctx, const rcg_sampler* s, int slot, double* out);
+
+/* ------------------------------------------------------------------ recycling (recycling.hpp) */
+/* harvest_errors(x_final, s) -- recycling.hpp:19 */
+int rcg_harvest_errors(rcg_ctx* ctx, const double* x_final, const rcg_sampler* s, rcg_tall** out);
+/* harvest_stored(s) -- recycling.hpp:23 */
+int rcg_harvest_stored(rcg_ctx* ctx, const rcg_sampler* s, rcg_tall** out);
+/* rayleigh_ritz(a, e) -- recycling.hpp:38: values (k, host) and optional Ritz vectors */
+int rcg_rayleigh_ritz(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* e, double* values,
+                      rcg_tall** vectors);
+/* build_aux_matrix(a, errors, theta) -- recycling.hpp:47.  keep_count > 0 replaces theta by the
+ * midpoint between the keep_count-th and (keep_count+1)-th Ritz values (all kept if fewer);
+ * the chosen threshold is written to *theta_used.  values must hold errors->k doubles. */
+int rcg_build_aux_matrix(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* errors, double theta,
+                         int keep_count, int* m_bar, double* values, double* theta_used,
+                         rcg_tall** w);
+
+/* ------------------------------------------------------------------ W basis */
+#define RCG_BASIS_DEFLATION 0 /* build_deflation_operator -- deflation.hpp:37 */
+#define RCG_BASIS_SC 1        /* ScPreconditioner ctor   -- subspace_correction.hpp:24-25 */
+int rcg_basis_create(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* w, int who, rcg_basis** out);
+void rcg_basis_destroy(rcg_basis* b);
+int rcg_basis_k(const rcg_basis* b);
+/* DeflationOperator::project_pt / project_p / direct_component -- deflation.hpp:24-32 */
+int rcg_project_pt(rcg_ctx* ctx, const rcg_basis* b, const double* y, double* out);
+int rcg_project_p(rcg_ctx* ctx, const rcg_basis* b, const double* x, double* out);
+int rcg_direct_component(rcg_ctx* ctx, const rcg_basis* b, const double* rhs, double* out);
+
+/* ------------------------------------------------------------------ Krylov solvers (pcg.hpp) */
+typedef struct {
+    double eps;         /* SolverConfig::eps, in (0,1) */
+    int max_iter;       /* SolverConfig::max_iter, >= 1 */
+    int record_history; /* SolverConfig::record_history */
+} rcg_solver_config;
+
+typedef struct {
+    int iterations;
+    int converged;
+    double wall_time;   /* seconds around the iteration loop (device events) */
+    int cap;            /* capacity of the optional host arrays below */
+    double* history;    /* relres per iteration (SolveReport::history) */
+    double* alphas;     /* CG alpha_i per iteration (Lanczos input), optional */
+    double* betas;      /* CG beta_i per iteration, 0 at i = 1, optional */
+} rcg_solve_report;
+
+#define RCG_PREC_IDENTITY 0 /* IdentityPreconditioner -- preconditioner.hpp:23 */
+#define RCG_PREC_IC 1       /* IcPreconditioner       -- ic_preconditioner.hpp:51 */
+#define RCG_PREC_SC 2       /* ScPreconditioner       -- subspace_correction.hpp:22 (inner = ic or identity) */
+typedef struct {
+    int kind;
+    const rcg_ic* ic;
+    const rcg_basis* sc;
+} rcg_prec;
+
+#define RCG_PAYLOAD_X 0 /* error_sampling_observer    -- sampling.hpp:67 */
+#define RCG_PAYLOAD_R 1 /* residual_sampling_observer -- sampling.hpp:70 */
+
+/* pcg_solve(a, b, m, x, cfg, observer) -- pcg.hpp:39-41.  observer: NULL or a sampler fed the
+ * iterate (payload RCG_PAYLOAD_X) or residual (RCG_PAYLOAD_R) of each continuing iteration. */
+int rcg_pcg_solve(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const rcg_prec* m, double* x,
+                  const rcg_solver_config* cfg, rcg_sampler* observer, int payload,
+                  rcg_solve_report* rep);
+/* deflated_pcg_solve(a, b, m, defl, x, cfg) -- pcg.hpp:50-52; defl NULL = empty W */
+int rcg_deflated_pcg_solve(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const rcg_prec* m,
+                           const rcg_basis* defl, double* x, const rcg_solver_config* cfg,
+                           rcg_solve_report* rep);
+
+/* ------------------------------------------------------------------ condest (condest.hpp) */
+typedef struct {
+    double lambda_max;
+    double lambda_min;
+    double kappa;
+    int power_iterations;
+    int power_unsettled;
+    int lambda_min_available;
+    int nritz;
+    double* ritz_values;   /* caller buffer of >= m_samples doubles, optional */
+    /* Lanczos tridiagonal estimate from the CG alpha/beta (no reference counterpart):
+     * extreme eigenvalues of T estimate the spectrum of M^-1 A */
+    double lanczos_lambda_min;
+    double lanczos_lambda_max;
+    double lanczos_kappa;
+} rcg_cond_estimate;
+/* pcg_with_condest(a, b, m, x, cfg, m_samples, v0_seed) -- condest.hpp:46-48 */
+int rcg_pcg_with_condest(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const rcg_prec* m,
+                         double* x, const rcg_solver_config* cfg, int m_samples, uint64_t v0_seed,
+                         rcg_solve_report* rep, rcg_cond_estimate* est);
+/* Lanczos extremes from k alpha/beta pairs (host arithmetic, shared by every solver) */
+int rcg_lanczos_extremes(int k, const double* alphas, const double* betas, double* lambda_min,
+                         double* lambda_max);
+
+/* ------------------------------------------------------------------ host generators
+ * Seeded synthetic inputs shared by the GPU path, the oracle harness and bench.py (the
+ * reference ships none).  Arrays are malloc'ed by the library; free with rcg_host_free. */
+#define RCG_GEN_POISSON7 0   /* C1: 7-pt, diag 6, off -1, Dirichlet eliminated */
+#define RCG_GEN_FV7_CONTRAST 1 /* C2/C4: 7-pt FV, harmonic faces, cube inclusions */
+#define RCG_GEN_Q1_27PT 2    /* C3: trilinear hex stiffness, log-normal element coefficient */
+#define RCG_GEN_KNN 3        /* C5: symmetric kNN graph Laplacian + shift */
+typedef struct {
+    int kind;
+    int32_t grid;        /* N (stencils) or number of points (kNN) */
+    int inclusions;      /* FV: number of cubes */
+    int inclusion_size;  /* FV: cube edge in cells */
+    double contrast;     /* FV: inclusion coefficient */
+    double sigma;        /* Q1: std-dev of log coefficient */
+    int knn_k;           /* kNN: neighbours per point */
+    uint64_t seed;
+} rcg_gen_params;
+int rcg_generate(const rcg_gen_params* p, int32_t* n, int64_t* nnz, int32_t** row_start,
+                 int32_t** col_idx, double** values);
+/* UniformPm1 stream (rng.hpp:18-41): draws [skip, skip+n) of seed into out */
+void rcg_uniform_pm1(uint64_t seed, uint64_t skip, int64_t n, double* out);
+/* N(0,1) by Box-Muller over the same mt19937_64 stream (2 draws per pair) */
+void rcg_normal(uint64_t seed, uint64_t skip, int64_t n, double* out);
+void rcg_host_free(void* p);
+/* IC(0) level depth of the natural ordering (diagnostics) */
+int rcg_level_depth(int32_t n, const int32_t* row_start, const int32_t* col_idx, int32_t* depth);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,519 @@
+"""Python host mirror of the reference solver API (proj/include/recycg), over the C-ABI.
+
+Names and argument meaning follow the reference declarations (pcg.hpp, deflation.hpp,
+subspace_correction.hpp, sampling.hpp, recycling.hpp, condest.hpp, ic_preconditioner.hpp);
+exceptions follow its types: ``InvalidArgument`` (std::invalid_argument), ``BreakdownError``,
+``ParseError``.  Vectors may be numpy float64 arrays (host; the call stages them through HBM)
+or CUDA torch tensors (used in place).  Every operation runs on the GPU through
+librcg_b200.so; there is no CPU code path for any of them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import BreakdownError, CudaError, InvalidArgument, ParseError, check, lib
+
+__all__ = [
+    "Context", "CsrMatrix", "IcFactor", "TallDense", "SamplerState", "Basis", "Identity", "Ic",
+    "Sc", "SolveReport", "CondEstimate", "pcg_solve", "deflated_pcg_solve", "pcg_with_condest",
+    "harvest_errors", "harvest_stored", "mgs_orthonormalize", "rayleigh_ritz", "build_aux_matrix",
+    "diagonal_scale", "lanczos_extremes", "BreakdownError", "ParseError", "InvalidArgument",
+    "CudaError",
+]
+
+
+def _ptr(a) -> int:
+    """Raw address of a float64/int32 buffer (numpy host array or CUDA torch tensor)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise InvalidArgument("array must be contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise InvalidArgument("tensor must be contiguous")
+        return a.data_ptr()
+    raise InvalidArgument(f"unsupported buffer type {type(a)!r}")
+
+
+def _f64(a, n=None, name="vector"):
+    if isinstance(a, np.ndarray):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+    elif hasattr(a, "data_ptr"):
+        import torch
+
+        if a.dtype != torch.float64:
+            raise InvalidArgument(f"{name} must be float64")
+    else:
+        a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if n is not None and (a.shape[0] if a.ndim else 0) != n:
+        raise InvalidArgument(f"{name}: size does not match matrix")
+    return a
+
+
+class Context:
+    """One GPU and one CUDA stream (rcg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib.rcg_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            lib.rcg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        check(lib.rcg_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(lib.rcg_ctx_launch_count(self.h))
+
+    def set_profiling(self, on: bool):
+        check(lib.rcg_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_stats(self, cls: int):
+        ms = C.c_double()
+        cnt = C.c_int64()
+        check(lib.rcg_ctx_kernel_stats(self.h, cls, C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
+    def reset_stats(self):
+        lib.rcg_ctx_reset_stats(self.h)
+
+
+class CsrMatrix:
+    """Device CSR (CsrMatrix, csr_matrix.hpp:20-51); validated like the reference by default."""
+
+    def __init__(self, ctx: Context, n, row_start, col_idx, values, validate: bool = True, _handle=None):
+        self.ctx = ctx
+        if _handle is not None:
+            self.h = _handle
+        else:
+            rs = np.ascontiguousarray(row_start, dtype=np.int32) if isinstance(row_start, (np.ndarray, list)) else row_start
+            ci = np.ascontiguousarray(col_idx, dtype=np.int32) if isinstance(col_idx, (np.ndarray, list)) else col_idx
+            va = _f64(values, name="values")
+            h = C.c_void_p()
+            check(lib.rcg_matrix_create(ctx.h, int(n), _ptr(rs), _ptr(ci), _ptr(va), 1 if validate else 0, C.byref(h)))
+            self.h = h
+        self.n = int(lib.rcg_matrix_n(self.h))
+        self.nnz = int(lib.rcg_matrix_nnz(self.h))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.rcg_matrix_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def values(self) -> np.ndarray:
+        out = np.empty(self.nnz)
+        check(lib.rcg_matrix_values(self.ctx.h, self.h, _ptr(out)))
+        return out
+
+    def spmv(self, x, y=None):
+        x = _f64(x, self.n, "x")
+        if y is None:
+            y = np.empty(self.n) if isinstance(x, np.ndarray) else x.new_empty(self.n)
+        check(lib.rcg_spmv(self.ctx.h, self.h, _ptr(x), _ptr(y)))
+        return y
+
+    def spmv_dual(self, x1, x2):
+        x1 = _f64(x1, self.n, "x1")
+        x2 = _f64(x2, self.n, "x2")
+        y1, y2 = np.empty(self.n), np.empty(self.n)
+        check(lib.rcg_spmv_dual(self.ctx.h, self.h, _ptr(x1), _ptr(x2), _ptr(y1), _ptr(y2)))
+        return y1, y2
+
+
+def diagonal_scale(ctx: Context, a: CsrMatrix):
+    """diagonal_scale (scaling.hpp:24-26): (A_scaled, d_inv_sqrt)."""
+    h = C.c_void_p()
+    dis = np.empty(a.n)
+    check(lib.rcg_diagonal_scale(ctx.h, a.h, C.byref(h), _ptr(dis)))
+    return CsrMatrix(ctx, 0, None, None, None, _handle=h), dis
+
+
+class IcFactor:
+    """Device IC(0) factor with level schedules (IcFactor, ic_preconditioner.hpp:18-37)."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+        nnz = C.c_int64()
+        sh = C.c_double()
+        fl = C.c_int32()
+        bl = C.c_int32()
+        check(lib.rcg_ic_info(self.h, C.byref(nnz), C.byref(sh), C.byref(fl), C.byref(bl)))
+        self.nnz_l, self.shift_used, self.fwd_levels, self.bwd_levels = nnz.value, sh.value, fl.value, bl.value
+
+    @classmethod
+    def factorize(cls, ctx: Context, n, row_start, col_idx, values, shift: float = 0.0, num_blocks: int = 1):
+        """ic0_factorize (ic_preconditioner.hpp:44) from host CSR arrays."""
+        rs = np.ascontiguousarray(row_start, dtype=np.int32)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        va = np.ascontiguousarray(values, dtype=np.float64)
+        h = C.c_void_p()
+        check(lib.rcg_ic0_factorize(ctx.h, int(n), _ptr(rs), _ptr(ci), _ptr(va), float(shift), int(num_blocks),
+                                    C.byref(h)))
+        f = cls(ctx, h)
+        f.n = int(n)
+        f.num_blocks = int(num_blocks)
+        return f
+
+    @classmethod
+    def from_arrays(cls, ctx: Context, n, block_bounds, l_row_start, l_col, l_val, d, u_row_start, u_col, u_val,
+                    shift_used=0.0):
+        arrs = [np.ascontiguousarray(block_bounds, dtype=np.int32), np.ascontiguousarray(l_row_start, dtype=np.int32),
+                np.ascontiguousarray(l_col, dtype=np.int32), np.ascontiguousarray(l_val, dtype=np.float64),
+                np.ascontiguousarray(d, dtype=np.float64), np.ascontiguousarray(u_row_start, dtype=np.int32),
+                np.ascontiguousarray(u_col, dtype=np.int32), np.ascontiguousarray(u_val, dtype=np.float64)]
+        h = C.c_void_p()
+        check(lib.rcg_ic_create(ctx.h, int(n), len(arrs[0]) - 1, *[_ptr(a) for a in arrs], float(shift_used),
+                                C.byref(h)))
+        f = cls(ctx, h)
+        f.n = int(n)
+        f.num_blocks = len(arrs[0]) - 1
+        return f
+
+    def export(self):
+        n, nnz = self.n, self.nnz_l
+        out = dict(block_bounds=np.empty(self.num_blocks + 1, np.int32), l_row_start=np.empty(n + 1, np.int32),
+                   l_col=np.empty(nnz, np.int32), l_val=np.empty(nnz), d=np.empty(n),
+                   u_row_start=np.empty(n + 1, np.int32), u_col=np.empty(nnz, np.int32), u_val=np.empty(nnz))
+        check(lib.rcg_ic_export(self.h, *[_ptr(v) for v in out.values()]))
+        return out
+
+    def apply(self, r, z=None):
+        """ic_apply (ic_preconditioner.hpp:47)."""
+        r = _f64(r, self.n, "r")
+        if z is None:
+            z = np.empty(self.n) if isinstance(r, np.ndarray) else r.new_empty(self.n)
+        check(lib.rcg_ic_apply(self.ctx.h, self.h, _ptr(r), _ptr(z)))
+        return z
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.rcg_ic_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class TallDense:
+    """Device n x k column block (TallDense, dense.hpp:11-22)."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+
+    @classmethod
+    def from_columns(cls, ctx: Context, n: int, cols):
+        """cols: array of shape (k, n) -- column j is cols[j] (reference TallDense::cols order)."""
+        cols = np.ascontiguousarray(cols, dtype=np.float64).reshape(-1, n) if n > 0 else np.zeros((0, 0))
+        k = cols.shape[0] if n > 0 else 0
+        h = C.c_void_p()
+        check(lib.rcg_tall_create(ctx.h, int(n), int(k), _ptr(cols) if k else None, C.byref(h)))
+        return cls(ctx, h)
+
+    @property
+    def k(self) -> int:
+        return int(lib.rcg_tall_k(self.h))
+
+    @property
+    def n(self) -> int:
+        return int(lib.rcg_tall_n(self.h))
+
+    def columns(self) -> np.ndarray:
+        out = np.empty((self.k, self.n))
+        if self.k:
+            check(lib.rcg_tall_download(self.ctx.h, self.h, _ptr(out)))
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.rcg_tall_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class SamplerState:
+    """Device snapshot store (SamplerState, sampling.hpp:26-64)."""
+
+    def __init__(self, ctx: Context, handle, m: int, n: int):
+        self.ctx, self.h, self.m, self.n = ctx, handle, m, n
+
+    @classmethod
+    def method_a(cls, ctx: Context, m: int, iteration_cap: int, n: int):
+        h = C.c_void_p()
+        check(lib.rcg_sampler_create(ctx.h, L.RCG_SAMPLER_A, int(m), int(iteration_cap), 0.5, int(n), C.byref(h)))
+        return cls(ctx, h, m, n)
+
+    @classmethod
+    def method_b(cls, ctx: Context, m: int, eps: float, n: int):
+        h = C.c_void_p()
+        check(lib.rcg_sampler_create(ctx.h, L.RCG_SAMPLER_B, int(m), 1, float(eps), int(n), C.byref(h)))
+        return cls(ctx, h, m, n)
+
+    def offer(self, iteration: int, relres: float, payload):
+        payload = _f64(payload, self.n, "payload")
+        check(lib.rcg_sampler_offer(self.ctx.h, self.h, int(iteration), float(relres), _ptr(payload)))
+
+    def state(self):
+        occ = np.zeros(self.m, np.int32)
+        it = np.zeros(self.m, np.int32)
+        c = lib.rcg_sampler_state(self.h, _ptr(occ), _ptr(it))
+        if c < 0:
+            check(-c)
+        return occ.astype(bool), it
+
+    def stored_count(self) -> int:
+        return int(self.state()[0].sum())
+
+    def occupied(self, s: int) -> bool:
+        return bool(self.state()[0][s])
+
+    def stored_iteration(self, s: int) -> int:
+        return int(self.state()[1][s])
+
+    def slot(self, s: int) -> np.ndarray:
+        out = np.empty(self.n)
+        check(lib.rcg_sampler_slot(self.ctx.h, self.h, int(s), _ptr(out)))
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.rcg_sampler_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class Basis:
+    """W with AW and chol(W^T A W): DeflationOperator (who='deflation') or the state of
+    ScPreconditioner (who='sc')."""
+
+    def __init__(self, ctx: Context, a: CsrMatrix, w: TallDense, who: str = "deflation"):
+        self.ctx = ctx
+        self.n = a.n
+        h = C.c_void_p()
+        check(lib.rcg_basis_create(ctx.h, a.h, w.h, L.RCG_BASIS_SC if who == "sc" else L.RCG_BASIS_DEFLATION,
+                                   C.byref(h)))
+        self.h = h
+
+    @property
+    def k(self) -> int:
+        return int(lib.rcg_basis_k(self.h))
+
+    def empty(self) -> bool:
+        return self.k == 0
+
+    def _proj(self, fn, v):
+        v = _f64(v, self.n)
+        out = np.empty(self.n)
+        check(fn(self.ctx.h, self.h, _ptr(v), _ptr(out)))
+        return out
+
+    def project_pt(self, y):
+        return self._proj(lib.rcg_project_pt, y)
+
+    def project_p(self, x):
+        return self._proj(lib.rcg_project_p, x)
+
+    def direct_component(self, b):
+        return self._proj(lib.rcg_direct_component, b)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib.rcg_basis_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+# ---- preconditioner descriptors (dispatch by kind, preconditioner.hpp:10-20)
+@dataclass
+class Identity:
+    kind: int = L.RCG_PREC_IDENTITY
+
+
+@dataclass
+class Ic:
+    factor: IcFactor
+    kind: int = L.RCG_PREC_IC
+
+
+@dataclass
+class Sc:
+    basis: Basis
+    inner: Optional[IcFactor] = None
+    kind: int = L.RCG_PREC_SC
+
+
+def _prec(m) -> L.Prec:
+    p = L.Prec()
+    p.kind = m.kind
+    if isinstance(m, Ic):
+        p.ic = m.factor.h
+    elif isinstance(m, Sc):
+        p.ic = m.inner.h if m.inner is not None else None
+        p.sc = m.basis.h
+    elif not isinstance(m, Identity):
+        raise InvalidArgument("unknown preconditioner type (no CPU fallback exists)")
+    return p
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    converged: bool = False
+    wall_time: float = 0.0
+    history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    alphas: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    betas: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+@dataclass
+class CondEstimate:
+    lambda_max: float = 0.0
+    lambda_min: float = float("nan")
+    kappa: float = float("nan")
+    power_iterations: int = 0
+    power_unsettled: bool = True
+    lambda_min_available: bool = False
+    ritz_values: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    lanczos_lambda_min: float = float("nan")
+    lanczos_lambda_max: float = float("nan")
+    lanczos_kappa: float = float("nan")
+
+
+def _report(max_iter):
+    rep = L.SolveReport()
+    bufs = (np.zeros(max_iter), np.zeros(max_iter), np.zeros(max_iter))
+    rep.cap = max_iter
+    rep.history = bufs[0].ctypes.data_as(L.dp)
+    rep.alphas = bufs[1].ctypes.data_as(L.dp)
+    rep.betas = bufs[2].ctypes.data_as(L.dp)
+    return rep, bufs
+
+
+def _finish(rep, bufs) -> SolveReport:
+    k = rep.iterations
+    return SolveReport(k, bool(rep.converged), rep.wall_time, bufs[0][:k].copy(), bufs[1][:k].copy(),
+                       bufs[2][:k].copy())
+
+
+def _cfg(eps, max_iter, record_history=True):
+    c = L.SolverConfig()
+    c.eps, c.max_iter, c.record_history = float(eps), int(max_iter), 1 if record_history else 0
+    return c
+
+
+def pcg_solve(ctx: Context, a: CsrMatrix, b, m, x, eps: float = 1e-8, max_iter: int = 1000,
+              observer: Optional[SamplerState] = None, payload: str = "x") -> SolveReport:
+    """pcg_solve (pcg.hpp:39-41); x is updated in place.  observer: a SamplerState fed the
+    iterate (payload 'x', error_sampling_observer) or the residual ('r')."""
+    b = _f64(b, a.n, "b")
+    cfg = _cfg(eps, max_iter)
+    rep, bufs = _report(max(1, int(max_iter)))
+    p = _prec(m)
+    check(lib.rcg_pcg_solve(ctx.h, a.h, _ptr(b), C.byref(p), _ptr(x), C.byref(cfg),
+                            observer.h if observer is not None else None,
+                            L.RCG_PAYLOAD_R if payload == "r" else L.RCG_PAYLOAD_X, C.byref(rep)))
+    return _finish(rep, bufs)
+
+
+def deflated_pcg_solve(ctx: Context, a: CsrMatrix, b, m, defl: Optional[Basis], x, eps: float = 1e-8,
+                       max_iter: int = 1000) -> SolveReport:
+    """deflated_pcg_solve (pcg.hpp:50-52); defl None is the empty W."""
+    b = _f64(b, a.n, "b")
+    cfg = _cfg(eps, max_iter)
+    rep, bufs = _report(max(1, int(max_iter)))
+    p = _prec(m)
+    check(lib.rcg_deflated_pcg_solve(ctx.h, a.h, _ptr(b), C.byref(p), defl.h if defl is not None else None, _ptr(x),
+                                     C.byref(cfg), C.byref(rep)))
+    return _finish(rep, bufs)
+
+
+def pcg_with_condest(ctx: Context, a: CsrMatrix, b, m, x, eps: float = 1e-8, max_iter: int = 1000,
+                     m_samples: int = 20, v0_seed: int = 42):
+    """pcg_with_condest (condest.hpp:46-48) plus the Lanczos estimate; returns (report, estimate)."""
+    b = _f64(b, a.n, "b")
+    cfg = _cfg(eps, max_iter)
+    rep, bufs = _report(max(1, int(max_iter)))
+    est = L.CondEstimate()
+    ritz = np.zeros(max(1, m_samples))
+    est.ritz_values = ritz.ctypes.data_as(L.dp)
+    p = _prec(m)
+    check(lib.rcg_pcg_with_condest(ctx.h, a.h, _ptr(b), C.byref(p), _ptr(x), C.byref(cfg), int(m_samples),
+                                   C.c_uint64(v0_seed), C.byref(rep), C.byref(est)))
+    e = CondEstimate(est.lambda_max, est.lambda_min, est.kappa, est.power_iterations, bool(est.power_unsettled),
+                     bool(est.lambda_min_available), ritz[: est.nritz].copy(), est.lanczos_lambda_min,
+                     est.lanczos_lambda_max, est.lanczos_kappa)
+    return _finish(rep, bufs), e
+
+
+def harvest_errors(ctx: Context, x_final, s: SamplerState) -> TallDense:
+    x_final = _f64(x_final, s.n, "x_final")
+    h = C.c_void_p()
+    check(lib.rcg_harvest_errors(ctx.h, _ptr(x_final), s.h, C.byref(h)))
+    return TallDense(ctx, h)
+
+
+def harvest_stored(ctx: Context, s: SamplerState) -> TallDense:
+    h = C.c_void_p()
+    check(lib.rcg_harvest_stored(ctx.h, s.h, C.byref(h)))
+    return TallDense(ctx, h)
+
+
+def mgs_orthonormalize(ctx: Context, v: TallDense, drop_tol: float = 1e-12) -> TallDense:
+    h = C.c_void_p()
+    check(lib.rcg_mgs_orthonormalize(ctx.h, v.h, float(drop_tol), C.byref(h)))
+    return TallDense(ctx, h)
+
+
+def rayleigh_ritz(ctx: Context, a: CsrMatrix, e: TallDense, vectors: bool = True):
+    vals = np.zeros(max(1, e.k))
+    h = C.c_void_p()
+    check(lib.rcg_rayleigh_ritz(ctx.h, a.h, e.h, _ptr(vals), C.byref(h) if vectors else None))
+    return vals[: e.k].copy(), (TallDense(ctx, h) if vectors else None)
+
+
+def build_aux_matrix(ctx: Context, a: CsrMatrix, errors: TallDense, theta: float, keep_count: int = 0):
+    """build_aux_matrix (recycling.hpp:47): returns (m_bar, ritz_values, theta_used, W)."""
+    vals = np.zeros(max(1, errors.k))
+    mb = C.c_int()
+    th = C.c_double()
+    h = C.c_void_p()
+    check(lib.rcg_build_aux_matrix(ctx.h, a.h, errors.h, float(theta), int(keep_count), C.byref(mb), _ptr(vals),
+                                   C.byref(th), C.byref(h)))
+    return mb.value, vals[: mb.value].copy(), th.value, TallDense(ctx, h)
+
+
+def lanczos_extremes(alphas, betas):
+    a = np.ascontiguousarray(alphas, dtype=np.float64)
+    b = np.ascontiguousarray(betas, dtype=np.float64)
+    lo, hi = C.c_double(), C.c_double()
+    check(lib.rcg_lanczos_extremes(len(a), _ptr(a), _ptr(b), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value

@@ -1,0 +1,483 @@
+// icsweep.cu -- IC(0) preconditioner on the device (K3-K5): the reference factor is uploaded
+// unchanged and applied by two sync-free, level-ordered triangular sweeps.
+//
+// Operator identity.  Each row i is computed exactly as src/ic_preconditioner.cpp:130-143 does:
+// forward  s = r_i;  s -= l_ik * y_k  (stored entry order);  y_i = s
+// backward s = y_i / d_i;  s -= u_ik * z_k  (stored entry order);  z_i = s
+// with separate multiply/subtract roundings.  Only the ORDER IN WHICH ROWS ARE VISITED changes
+// (topological level order instead of 0..n-1 / n-1..0), and every row still sees final values
+// of its dependencies, so the result is bitwise equal to the reference ic_apply.
+//
+// Schedule.  Host side, rows are sorted by DAG level (level = 1 + max level of the columns the
+// row reads; ties by row index) and the factor rows are copied into that order so a warp's rows
+// are contiguous in HBM.  Device side, a CTA takes the next 128-row tile from an atomic ticket
+// (so every tile it can wait on is already owned by a running CTA -- no deadlock), prefetches
+// its rows' entries, and spins on each dependency with a relaxed gpu-scope load until the value
+// differs from a NaN sentinel; a finished row is published with one relaxed 64-bit store (the
+// value is its own ready flag, no fence needed).  Buffers are refilled with the sentinel at the
+// start of each solve; the consumer of each buffer resets it in passing.
+// Roofline: 12 nnz_L + 28 n bytes per sweep (entries, perm, row starts, in, out); the natural
+// ordering's level count bounds it by dependency latency on C1-C3.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+
+namespace rcg {
+
+constexpr int kDepChunk = 8;
+
+// Sum of one value per thread over the block; then a two-level deterministic grid reduction
+// keyed by tile: tiles -> groups of kGroup -> total.  Returns true in the block that owns the
+// final total (written to *tot).
+__device__ bool tile_reduce(double v, int tile, int ntiles, SweepArgs& a, double* red, double* tot) {
+    __shared__ bool s_last_group, s_last;
+    double acc[1] = {v};
+    block_sum<1>(acc, red);
+    const int g = tile / kGroup;
+    const int ngroups = (ntiles + kGroup - 1) / kGroup;
+    const int gsize = min(kGroup, ntiles - g * kGroup);
+    if (threadIdx.x == 0) {
+        a.partials[tile] = acc[0];
+        __threadfence();
+        s_last_group = atomicAdd(&a.gcount[g], 1u) == static_cast<unsigned>(gsize) - 1u;
+    }
+    __syncthreads();
+    if (!s_last_group) return false;
+    __threadfence();
+    double gs[1] = {threadIdx.x < gsize ? __ldcg(a.partials + g * kGroup + threadIdx.x) : 0.0};
+    block_sum<1>(gs, red);
+    if (threadIdx.x == 0) {
+        a.gpart[g] = gs[0];
+        a.gcount[g] = 0u;
+        __threadfence();
+        s_last = atomicAdd(reinterpret_cast<unsigned int*>(&a.tickets[2]), 1u) ==
+                 static_cast<unsigned>(ngroups) - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    double ts[1] = {0.0};
+    for (int i = threadIdx.x; i < ngroups; i += blockDim.x) ts[0] = __dadd_rn(ts[0], __ldcg(a.gpart + i));
+    block_sum<1>(ts, red);
+    if (threadIdx.x == 0) {
+        *tot = ts[0];
+        a.tickets[2] = 0;
+    }
+    __syncthreads();
+    return true;
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
+    __shared__ int s_tile;
+    __shared__ double red[32];
+    __shared__ double tot;
+    if (a.st->done) return;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int ntiles = (a.n + kSweepThreads - 1) / kSweepThreads;
+    const int pos = tile * kSweepThreads + threadIdx.x;
+    double contrib = 0.0;
+    if (pos < a.n) {
+        const int32_t row = __ldg(a.perm + pos);
+        const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
+        double s;
+        if (BWD) {
+            s = __ddiv_rn(a.in[row], __ldg(a.d + row));
+            if (a.in_reset) a.in_reset[row] = sentinel();
+        } else {
+            s = a.in[row];
+        }
+        for (int32_t e0 = beg; e0 < end; e0 += kDepChunk) {
+            const int cnt = min(kDepChunk, end - e0);
+            int32_t col[kDepChunk];
+            double val[kDepChunk], dep[kDepChunk];
+#pragma unroll
+            for (int j = 0; j < kDepChunk; ++j)
+                if (j < cnt) {
+                    col[j] = __ldcs(a.pcol + e0 + j);
+                    val[j] = __ldcs(a.pval + e0 + j);
+                }
+#pragma unroll
+            for (int j = 0; j < kDepChunk; ++j)
+                if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
+#pragma unroll
+            for (int j = 0; j < kDepChunk; ++j)
+                if (j < cnt) {
+                    // bounded wait: a schedule bug must surface as an error, never hang the GPU
+                    unsigned spins = 0;
+                    while (is_sentinel(dep[j])) {
+                        dep[j] = ld_relaxed(a.out + col[j]);
+                        if (++spins == (1u << 26)) {
+                            atomicExch(&a.tickets[3], 1);
+                            dep[j] = 0.0;
+                        }
+                    }
+                }
+#pragma unroll
+            for (int j = 0; j < kDepChunk; ++j)
+                if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
+        }
+        st_relaxed(a.out + row, publishable(s));
+        if (BWD) {
+            double z = s;
+            if (a.zout) {
+                for (int j = 0; j < a.k; ++j) z = fadd_mul(z, __ldg(a.u + j), __ldg(a.w + j * a.ldw + row));
+                a.zout[row] = z;
+            }
+            if (a.r) contrib = __dmul_rn(a.r[row], z);
+        }
+    }
+    if (BWD && a.r) {
+        if (tile_reduce(contrib, tile, ntiles, a, red, &tot) && threadIdx.x == 0) {
+            // (r, z) complete: breakdown test and beta of src/pcg.cpp:65-71
+            DevState* st = a.st;
+            const double rho = tot;
+            st->rho = rho;
+            if (rho <= 0.0) {
+                st->done = kBroken;
+                st->status = kBrkRz;
+            }
+            st->beta = st->iter > 1 ? rho / st->rho_prev : 0.0;
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x) - 1) {
+            a.tickets[0] = 0;
+            a.tickets[1] = 0;
+        }
+    }
+}
+
+SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
+    SweepArgs a{};
+    a.perm = backward ? f->b_perm : f->f_perm;
+    a.prs = backward ? f->b_prs : f->f_prs;
+    a.pcol = backward ? f->b_col : f->f_col;
+    a.pval = backward ? f->b_val : f->f_val;
+    a.d = f->d;
+    a.n = f->n;
+    a.tickets = ctx->ws.tickets + (backward ? 4 : 0);
+    a.partials = ctx->ws.partials;
+    a.gpart = ctx->ws.gpart;
+    a.gcount = ctx->ws.gcount;
+    a.st = ctx->ws.st;
+    return a;
+}
+
+void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
+    if (f->n == 0) return;
+    const int grid = (f->n + kSweepThreads - 1) / kSweepThreads;
+    KTimer t(ctx, backward ? 2 : 1);
+    if (backward)
+        k_sweep<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
+    else
+        k_sweep<false><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
+    RCG_LAUNCHED(ctx);
+}
+
+// raises if any sweep hit the bounded dependency wait (clears the flags)
+void check_sweep_watchdog(rcg_ctx* ctx) {
+    if (!ctx->ws.tickets) return;
+    int h[8];
+    RCG_CK(cudaMemcpyAsync(h, ctx->ws.tickets, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    RCG_CK(cudaStreamSynchronize(ctx->stream));
+    if (h[3] || h[7]) {
+        RCG_CK(cudaMemsetAsync(ctx->ws.tickets, 0, 16 * sizeof(int), ctx->stream));
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+        throw Error(RCG_E_CUDA, "IC sweep: dependency wait timed out (schedule fault)");
+    }
+}
+
+// workspace needed by the sweeps of an n-row factor
+static void ensure_sweep_ws(rcg_ctx* ctx, int32_t n, int k, int64_t max_iter, int pending) {
+    const int64_t ntiles = (n + kSweepThreads - 1) / kSweepThreads;
+    const int64_t ngroups = (ntiles + kGroup - 1) / kGroup;
+    const int64_t red = std::max<int64_t>(ntiles, static_cast<int64_t>(kMaxRed) * ctx->num_sms * 8);
+    ensure_workspace(ctx, n, k, max_iter, red, ngroups, pending);
+}
+
+void ic_apply_dev(rcg_ctx* ctx, const rcg_ic* f, const double* r, double* z) {
+    ensure_sweep_ws(ctx, f->n, 1, 1, 1);
+    Workspace& w = ctx->ws;
+    RCG_CK(cudaMemsetAsync(w.st, 0, sizeof(DevState), ctx->stream));
+    launch_fill_bits(ctx, w.ybuf, f->n, kSentinelBits);
+    launch_fill_bits(ctx, z, f->n, kSentinelBits);
+    SweepArgs fw = sweep_args(ctx, f, false);
+    fw.in = r;
+    fw.out = w.ybuf;
+    launch_sweep(ctx, f, false, fw);
+    SweepArgs bw = sweep_args(ctx, f, true);
+    bw.in = w.ybuf;
+    bw.out = z;
+    launch_sweep(ctx, f, true, bw);
+}
+
+// ------------------------------------------------------------------ host: schedule + upload
+template <class T>
+static T* upload(rcg_ctx* ctx, const std::vector<T>& h) {
+    void* p = nullptr;
+    RCG_CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(h.size(), 1)));
+    if (!h.empty()) RCG_CK(cudaMemcpyAsync(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+    return static_cast<T*>(p);
+}
+
+// Level-sorted copy of a row-wise triangular factor.  `descending` walks rows n-1..0 (U).
+static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vector<int32_t>& col,
+                              const std::vector<double>& val, bool descending, std::vector<int32_t>& perm,
+                              std::vector<int32_t>& prs, std::vector<int32_t>& pcol, std::vector<double>& pval) {
+    std::vector<int32_t> level(n, 0);
+    int32_t nlev = 0;
+    for (int32_t t = 0; t < n; ++t) {
+        const int32_t i = descending ? n - 1 - t : t;
+        int32_t lv = 0;
+        for (int32_t p = rs[i]; p < rs[i + 1]; ++p) lv = std::max(lv, level[col[p]] + 1);
+        level[i] = lv;
+        nlev = std::max(nlev, lv + 1);
+    }
+    std::vector<int64_t> start(static_cast<size_t>(nlev) + 1, 0);
+    for (int32_t i = 0; i < n; ++i) start[level[i] + 1]++;
+    for (int32_t l = 0; l < nlev; ++l) start[l + 1] += start[l];
+    perm.assign(n, 0);
+    for (int32_t t = 0; t < n; ++t) {
+        const int32_t i = descending ? n - 1 - t : t;
+        perm[start[level[i]]++] = i;
+    }
+    prs.assign(static_cast<size_t>(n) + 1, 0);
+    for (int32_t pos = 0; pos < n; ++pos) prs[pos + 1] = prs[pos] + (rs[perm[pos] + 1] - rs[perm[pos]]);
+    pcol.resize(col.size());
+    pval.resize(val.size());
+    for (int32_t pos = 0; pos < n; ++pos) {
+        const int32_t i = perm[pos];
+        std::copy(col.begin() + rs[i], col.begin() + rs[i + 1], pcol.begin() + prs[pos]);
+        std::copy(val.begin() + rs[i], val.begin() + rs[i + 1], pval.begin() + prs[pos]);
+    }
+    return nlev;
+}
+
+static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
+    std::vector<int32_t> perm, prs, pcol;
+    std::vector<double> pval;
+    f->fwd_levels = build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval);
+    f->f_perm = upload(ctx, perm);
+    f->f_prs = upload(ctx, prs);
+    f->f_col = upload(ctx, pcol);
+    f->f_val = upload(ctx, pval);
+    RCG_CK(cudaStreamSynchronize(ctx->stream));
+    f->bwd_levels = build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval);
+    f->b_perm = upload(ctx, perm);
+    f->b_prs = upload(ctx, prs);
+    f->b_col = upload(ctx, pcol);
+    f->b_val = upload(ctx, pval);
+    f->d = upload(ctx, f->h_d);
+    RCG_CK(cudaStreamSynchronize(ctx->stream));
+}
+
+// ------------------------------------------------------------------ host IC(0) (setup only)
+// Restates src/ic_preconditioner.cpp:12-121: zero-fill L D L^T of A + shift diag(A), sorted
+// row merge for the shared pattern, block-Jacobi drop of columns before the block start, shift
+// ladder 0 -> 0.01 -> x2 (20 retries), then the row-wise transpose for the backward sweep.
+// It runs once per matrix on the host; the per-iteration operator is the device sweep above.
+static bool factor_attempt(int32_t n, const int32_t* rs, const int32_t* ci, const double* va, double shift,
+                           rcg_ic* f) {
+    f->h_lrs.assign(static_cast<size_t>(n) + 1, 0);
+    f->h_lcol.clear();
+    f->h_lval.clear();
+    f->h_d.assign(n, 0.0);
+    f->shift = shift;
+    std::vector<int32_t>& lc = f->h_lcol;
+    std::vector<double>& lv = f->h_lval;
+    std::vector<double>& d = f->h_d;
+    size_t blk = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        while (i >= f->h_bounds[blk + 1]) ++blk;
+        const int32_t lo = f->h_bounds[blk];
+        const int32_t first = static_cast<int32_t>(lc.size());
+        f->h_lrs[i] = first;
+        double diag = 0.0;
+        for (int32_t k = rs[i]; k < rs[i + 1]; ++k) {
+            const int32_t j = ci[k];
+            if (j >= i) {
+                if (j == i) diag = va[k];
+                break;
+            }
+            if (j < lo) continue;
+            double acc = va[k];
+            int32_t pa = first, pb = f->h_lrs[j];
+            const int32_t ea = static_cast<int32_t>(lc.size()), eb = f->h_lrs[j + 1];
+            while (pa < ea && pb < eb) {
+                if (lc[pa] == lc[pb]) {
+                    acc -= lv[pa] * d[lc[pa]] * lv[pb];
+                    ++pa;
+                    ++pb;
+                } else if (lc[pa] < lc[pb]) {
+                    ++pa;
+                } else {
+                    ++pb;
+                }
+            }
+            lc.push_back(j);
+            lv.push_back(acc / d[j]);
+        }
+        double piv = diag * (1.0 + shift);
+        for (size_t p = first; p < lc.size(); ++p) piv -= lv[p] * lv[p] * d[lc[p]];
+        if (piv <= 0.0) return false;
+        d[i] = piv;
+        f->h_lrs[i + 1] = static_cast<int32_t>(lc.size());
+    }
+    return true;
+}
+
+static void transpose_factor(rcg_ic* f) {
+    const int32_t n = f->n;
+    f->h_urs.assign(static_cast<size_t>(n) + 1, 0);
+    f->h_ucol.assign(f->h_lcol.size(), 0);
+    f->h_uval.assign(f->h_lval.size(), 0.0);
+    for (int32_t c : f->h_lcol) f->h_urs[c + 1]++;
+    std::partial_sum(f->h_urs.begin(), f->h_urs.end(), f->h_urs.begin());
+    std::vector<int32_t> fillpos(f->h_urs.begin(), f->h_urs.end() - 1);
+    for (int32_t i = 0; i < n; ++i)
+        for (int32_t k = f->h_lrs[i]; k < f->h_lrs[i + 1]; ++k) {
+            const int32_t dst = fillpos[f->h_lcol[k]]++;
+            f->h_ucol[dst] = i;
+            f->h_uval[dst] = f->h_lval[k];
+        }
+}
+
+}  // namespace rcg
+
+using namespace rcg;
+
+extern "C" {
+
+int rcg_ic0_factorize(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const int32_t* col_idx,
+                      const double* values, double shift, int num_blocks, rcg_ic** out) {
+    return guard([&] {
+        *out = nullptr;
+        if (num_blocks < 1 || num_blocks > std::max<int32_t>(n, 1))
+            throw Error(RCG_E_INVALID, "ic0_factorize: num_blocks must be in [1, n]");
+        if (shift < 0.0) throw Error(RCG_E_INVALID, "ic0_factorize: shift must be >= 0");
+        require(!is_device_ptr(row_start), "rcg_ic0_factorize: CSR arrays must be host memory");
+        auto* f = new rcg_ic();
+        try {
+            f->n = n;
+            f->h_bounds.resize(static_cast<size_t>(num_blocks) + 1);
+            for (int b = 0; b <= num_blocks; ++b)
+                f->h_bounds[b] = static_cast<int32_t>((static_cast<int64_t>(b) * n) / num_blocks);
+            double s = shift;
+            bool ok = false;
+            const int retries = 20;
+            for (int attempt = 0; attempt <= retries && !ok; ++attempt) {
+                ok = factor_attempt(n, row_start, col_idx, values, s, f);
+                if (!ok) s = (s == 0.0) ? 0.01 : 2.0 * s;
+            }
+            if (!ok) {
+                char buf[160];
+                std::snprintf(buf, sizeof buf,
+                              "IC breakdown: no positive-pivot factorization after %d shift retries (last shift %f)",
+                              retries, s);
+                throw Error(RCG_E_BREAKDOWN, buf);
+            }
+            f->nnz_l = static_cast<int64_t>(f->h_lval.size());
+            transpose_factor(f);
+            finish_ic(ctx, f);
+        } catch (...) {
+            rcg_ic_destroy(f);
+            throw;
+        }
+        *out = f;
+    });
+}
+
+int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_bounds,
+                  const int32_t* l_row_start, const int32_t* l_col, const double* l_val,
+                  const double* d, const int32_t* u_row_start, const int32_t* u_col,
+                  const double* u_val, double shift_used, rcg_ic** out) {
+    return guard([&] {
+        *out = nullptr;
+        require(n >= 0 && num_blocks >= 1, "rcg_ic_create: bad dimensions");
+        auto* f = new rcg_ic();
+        try {
+            f->n = n;
+            f->shift = shift_used;
+            f->h_bounds.assign(block_bounds, block_bounds + num_blocks + 1);
+            f->h_lrs.assign(l_row_start, l_row_start + n + 1);
+            f->nnz_l = f->h_lrs[n];
+            f->h_lcol.assign(l_col, l_col + f->nnz_l);
+            f->h_lval.assign(l_val, l_val + f->nnz_l);
+            f->h_d.assign(d, d + n);
+            f->h_urs.assign(u_row_start, u_row_start + n + 1);
+            require(f->h_urs[n] == f->nnz_l, "rcg_ic_create: L and U entry counts differ");
+            f->h_ucol.assign(u_col, u_col + f->nnz_l);
+            f->h_uval.assign(u_val, u_val + f->nnz_l);
+            for (int64_t p = 0; p < f->nnz_l; ++p)
+                require(f->h_lcol[p] >= 0 && f->h_lcol[p] < n && f->h_ucol[p] >= 0 && f->h_ucol[p] < n,
+                        "rcg_ic_create: factor column out of range");
+            for (int32_t i = 0; i < n; ++i) {
+                for (int32_t p = f->h_lrs[i]; p < f->h_lrs[i + 1]; ++p)
+                    require(f->h_lcol[p] < i, "rcg_ic_create: L entry on or above the diagonal");
+                for (int32_t p = f->h_urs[i]; p < f->h_urs[i + 1]; ++p)
+                    require(f->h_ucol[p] > i, "rcg_ic_create: U entry on or below the diagonal");
+            }
+            finish_ic(ctx, f);
+        } catch (...) {
+            rcg_ic_destroy(f);
+            throw;
+        }
+        *out = f;
+    });
+}
+
+void rcg_ic_destroy(rcg_ic* f) {
+    if (!f) return;
+    for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
+                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d})
+        dev_free(p);
+    delete f;
+}
+
+int rcg_ic_info(const rcg_ic* f, int64_t* nnz_l, double* shift_used, int32_t* fwd_levels, int32_t* bwd_levels) {
+    return guard([&] {
+        if (nnz_l) *nnz_l = f->nnz_l;
+        if (shift_used) *shift_used = f->shift;
+        if (fwd_levels) *fwd_levels = f->fwd_levels;
+        if (bwd_levels) *bwd_levels = f->bwd_levels;
+    });
+}
+
+int rcg_ic_export(const rcg_ic* f, int32_t* block_bounds, int32_t* l_row_start, int32_t* l_col,
+                  double* l_val, double* d, int32_t* u_row_start, int32_t* u_col, double* u_val) {
+    return guard([&] {
+        auto cp = [](auto* dst, const auto& v) {
+            if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(v[0]) * v.size());
+        };
+        cp(block_bounds, f->h_bounds);
+        cp(l_row_start, f->h_lrs);
+        cp(l_col, f->h_lcol);
+        cp(l_val, f->h_lval);
+        cp(d, f->h_d);
+        cp(u_row_start, f->h_urs);
+        cp(u_col, f->h_ucol);
+        cp(u_val, f->h_uval);
+    });
+}
+
+int rcg_ic_apply(rcg_ctx* ctx, const rcg_ic* f, const double* r, double* z) {
+    return guard([&] {
+        Staged rs, zs;
+        stage_in(ctx, r, f->n, rs);
+        stage_out_begin(ctx, z, f->n, zs);
+        ic_apply_dev(ctx, f, rs.dev, zs.dev);
+        stage_out_end(ctx, z, f->n, zs);
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+        check_sweep_watchdog(ctx);
+    });
+}
+
+}  // extern "C"

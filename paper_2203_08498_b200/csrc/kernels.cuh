@@ -1,0 +1,50 @@
+// kernels.cuh -- argument blocks and launchers shared between the kernel translation units.
+#pragma once
+
+#include "internal.cuh"
+
+namespace rcg {
+
+struct SpmvArgs {
+    const int32_t* rs;
+    const int32_t* ci;
+    const double* va;
+    int32_t n;
+    const double* x[2];
+    double* y[2];
+    double* partials;
+};
+
+// one IC sweep (forward on L, or backward on U with the 1/d pass folded in)
+struct SweepArgs {
+    const int32_t* perm;   // processing position -> row
+    const int32_t* prs;    // position-indexed row starts
+    const int32_t* pcol;   // original column indices, reference entry order
+    const double* pval;
+    const double* d;       // pivots (backward)
+    int32_t n;
+    const double* in;      // forward: r ; backward: y (undivided forward result)
+    double* out;           // sentinel-initialised result the dependants poll
+    double* in_reset;      // backward: y is reset to the sentinel after use (nullable)
+    // backward epilogue
+    double* zout;          // subspace correction: z = out + W u (nullable)
+    const double* w;
+    int64_t ldw;
+    int k;
+    const double* u;
+    const double* r;       // rho = (r, z) partials when non-null
+    int* tickets;          // [0] tile ticket, [1] exit count, [2] group ticket
+    double* partials;
+    double* gpart;
+    unsigned int* gcount;
+    DevState* st;
+};
+
+int spmv_grid(const rcg_ctx* ctx, int32_t n);
+int stream_grid(const rcg_ctx* ctx, int64_t n);
+void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const double* x, double* r);
+void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
+SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward);
+void check_sweep_watchdog(rcg_ctx* ctx);
+
+}  // namespace rcg

@@ -1,0 +1,137 @@
+"""Seeded synthetic problems for the BASELINE.json configurations (C1-C5) and the right-hand
+side streams of each sequence.  The reference ships no generators; SURVEY.md section 8(d)
+defines them and the C++ implementation lives in csrc/generators.cpp (host code, shared by the
+GPU path, the oracle harness and bench.py).  The paper's SuiteSparse matrices are not in this
+environment: these seeded problems with the configs' shapes and coefficient distributions stand
+in for them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import check, lib
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    kind: int
+    grid: int                 # N per axis, or the number of points (kNN)
+    n_rhs: int
+    rhs: str                  # 'uniform' | 'normal' | 'drift'
+    sampler_m: int
+    keep: int                 # m~ Ritz vectors kept (count-based selection)
+    method: str               # 'deflation' | 'sc'
+    condest: bool = False
+    inclusions: int = 0
+    inclusion_size: int = 0
+    contrast: float = 1.0
+    sigma: float = 0.0
+    knn_k: int = 10
+    seed: int = 20220317
+    rhs_seed: int = 1
+    eps: float = 1e-8
+    max_iter: int = 5000
+    blocks: int = 1
+    note: str = ""
+
+
+CONFIGS = {
+    "c1": Config("c1_poisson7_32", L.RCG_GEN_POISSON7, 32, 4, "uniform", 16, 8, "deflation",
+                 note="32^3 7-pt Poisson, IC(0)-CG, 4 RHS, 16 samples, deflation m=8 (CPU-runnable case)"),
+    "c2": Config("c2_fv7_contrast_128", L.RCG_GEN_FV7_CONTRAST, 128, 10, "normal", 32, 16, "sc",
+                 inclusions=8, inclusion_size=8, contrast=1e6,
+                 note="128^3 high-contrast 7-pt FV, 8 inclusions 8^3 at 1e6, 10 RHS, 32 samples, SC m=16"),
+    "c3": Config("c3_q1_27pt_256", L.RCG_GEN_Q1_27PT, 256, 20, "drift", 64, 32, "deflation", sigma=2.0,
+                 note="256^3 Q1 27-pt, log-normal exp(N(0,4)), 20 RHS drifting, 64 samples, deflation m=32"),
+    "c4": Config("c4_fv7_contrast_512", L.RCG_GEN_FV7_CONTRAST, 512, 8, "normal", 64, 32, "deflation",
+                 inclusions=64, inclusion_size=16, contrast=1e6,
+                 note="512^3 high-contrast 7-pt, 64 inclusions 16^3, 8 RHS, deflation m=32"),
+    "c5": Config("c5_knn_laplacian_4M", L.RCG_GEN_KNN, 4_000_000, 16, "normal", 48, 24, "deflation", condest=True,
+                 knn_k=10, note="4M-point kNN (k=10) graph Laplacian, 16 solves, condest each solve, deflation m=24"),
+}
+
+# scaled-down variants with the same structure, for parity tests the oracle finishes in seconds
+SMALL = {
+    "c1": CONFIGS["c1"],
+    "c2": replace(CONFIGS["c2"], name="c2_small_24", grid=24, n_rhs=4, inclusions=2, inclusion_size=4, sampler_m=16,
+                  keep=6),
+    "c3": replace(CONFIGS["c3"], name="c3_small_12", grid=12, n_rhs=4, sampler_m=16, keep=6),
+    "c4": replace(CONFIGS["c4"], name="c4_small_28", grid=28, n_rhs=3, inclusions=4, inclusion_size=4, sampler_m=16,
+                  keep=6),
+    "c5": replace(CONFIGS["c5"], name="c5_small_8k", grid=8000, n_rhs=3, sampler_m=16, keep=6),
+}
+
+
+@dataclass
+class HostCsr:
+    n: int
+    row_start: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_start[-1])
+
+
+def _adopt(ptr, count, ctype, dtype):
+    """numpy view of a malloc'ed library buffer, freed with rcg_host_free when collected."""
+    if count == 0:
+        lib.rcg_host_free(C.cast(ptr, C.c_void_p))
+        return np.zeros(0, dtype)
+    arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(count,))
+    weakref.finalize(arr, lib.rcg_host_free, C.cast(ptr, C.c_void_p).value)
+    return arr
+
+
+def generate(cfg: Config) -> HostCsr:
+    p = L.GenParams(cfg.kind, cfg.grid, cfg.inclusions, cfg.inclusion_size, cfg.contrast, cfg.sigma, cfg.knn_k,
+                    cfg.seed)
+    n = C.c_int32()
+    nnz = C.c_int64()
+    rs = L.i32p()
+    ci = L.i32p()
+    va = L.dp()
+    check(lib.rcg_generate(C.byref(p), C.byref(n), C.byref(nnz), C.byref(rs), C.byref(ci), C.byref(va)))
+    return HostCsr(n.value, _adopt(rs, n.value + 1, C.c_int32, np.int32), _adopt(ci, nnz.value, C.c_int32, np.int32),
+                   _adopt(va, nnz.value, C.c_double, np.float64))
+
+
+def uniform_pm1(seed: int, skip: int, n: int) -> np.ndarray:
+    out = np.empty(n)
+    lib.rcg_uniform_pm1(C.c_uint64(seed), C.c_uint64(skip), n, out.ctypes.data)
+    return out
+
+
+def normal(seed: int, skip: int, n: int) -> np.ndarray:
+    out = np.empty(n)
+    lib.rcg_normal(C.c_uint64(seed), C.c_uint64(skip), n, out.ctypes.data)
+    return out
+
+
+def solution_stream(cfg: Config, n: int, k: int) -> np.ndarray:
+    """x_k (0-based k) of the sequence: b_k = A x_k.  'uniform' follows make_rhs (driver.cpp:97-106)
+    block k of the UniformPm1 stream; 'normal' is block k of the N(0,1) stream; 'drift' is
+    x_0 ~ N(0,1), x_{k+1} = x_k + 0.1 N(0,1)."""
+    if cfg.rhs == "uniform":
+        return uniform_pm1(cfg.rhs_seed, k * n, n)
+    if cfg.rhs == "normal":
+        return normal(cfg.rhs_seed, k * n, n)
+    if cfg.rhs == "drift":
+        x = normal(cfg.rhs_seed, 0, n)
+        for j in range(1, k + 1):
+            x = x + 0.1 * normal(cfg.rhs_seed, j * n, n)
+        return x
+    raise ValueError(cfg.rhs)
+
+
+def level_depth(a: HostCsr) -> int:
+    d = C.c_int32()
+    check(lib.rcg_level_depth(a.n, a.row_start.ctypes.data, a.col_idx.ctypes.data, C.byref(d)))
+    return d.value

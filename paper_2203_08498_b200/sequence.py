@@ -1,0 +1,101 @@
+"""The sequence protocol on the GPU -- the caller of the hot path, mirroring run_sequence
+(proj/src/driver.cpp:108-222): scale, IC(0), solve 1 with the method-A error sampler,
+Rayleigh-Ritz basis (count-based selection of `keep` vectors), then SC-preconditioned or
+deflated solves 2..k from x0 = 0.  All solver work runs through librcg_b200.so; the host only
+scales right-hand sides / solutions (driver.cpp:147,182,191) and reports.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import api
+from .problems import Config, HostCsr, solution_stream
+
+
+@dataclass
+class Prepared:
+    ctx: api.Context
+    cfg: Config
+    host: HostCsr
+    a_orig: api.CsrMatrix
+    a: api.CsrMatrix
+    dis: np.ndarray
+    ic: api.IcFactor
+    setup_s: float = 0.0
+
+
+def prepare(ctx: api.Context, cfg: Config, host: HostCsr, validate: bool = True, blocks: int | None = None) -> Prepared:
+    t0 = time.perf_counter()
+    a_orig = api.CsrMatrix(ctx, host.n, host.row_start, host.col_idx, host.values, validate=validate)
+    a, dis = api.diagonal_scale(ctx, a_orig)
+    scaled = a.values()
+    ic = api.IcFactor.factorize(ctx, host.n, host.row_start, host.col_idx, scaled, 0.0,
+                                cfg.blocks if blocks is None else blocks)
+    return Prepared(ctx, cfg, host, a_orig, a, dis, ic, time.perf_counter() - t0)
+
+
+def rhs(p: Prepared, k: int) -> tuple[np.ndarray, np.ndarray]:
+    """(b_orig, b_scaled) of solve k (0-based): b = A x_k, scaled by D^-1/2 (scaling.cpp:8-12)."""
+    x = solution_stream(p.cfg, p.host.n, k)
+    b = p.a_orig.spmv(x)
+    return b, p.dis * b
+
+
+@dataclass
+class SequenceResult:
+    iterations: list = field(default_factory=list)
+    converged: list = field(default_factory=list)
+    histories: list = field(default_factory=list)
+    solutions: list = field(default_factory=list)
+    true_relres: list = field(default_factory=list)
+    wall: list = field(default_factory=list)
+    sampled_iterations: list = field(default_factory=list)
+    m_bar: int = 0
+    m_tilde: int = 0
+    ritz_values: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    basis_build_s: float = 0.0
+
+
+def run_sequence(p: Prepared, rhs_scaled: list, rhs_orig: list | None = None, n_solves: int | None = None,
+                 keep_solutions: bool = True) -> SequenceResult:
+    ctx, cfg, n = p.ctx, p.cfg, p.host.n
+    k_t = len(rhs_scaled) if n_solves is None else n_solves
+    res = SequenceResult()
+    sampler = api.SamplerState.method_a(ctx, cfg.sampler_m, cfg.max_iter, n)
+    x1 = np.zeros(n)
+    r1 = api.pcg_solve(ctx, p.a, rhs_scaled[0], api.Ic(p.ic), x1, cfg.eps, cfg.max_iter, observer=sampler)
+    _record(p, res, r1, x1, rhs_orig[0] if rhs_orig else None, keep_solutions)
+    occ, it = sampler.state()
+    res.sampled_iterations = sorted(int(v) for v in it[occ])
+    t0 = time.perf_counter()
+    errors = api.harvest_errors(ctx, x1, sampler)
+    m_bar, vals, _theta, w = api.build_aux_matrix(ctx, p.a, errors, 1e-3, keep_count=cfg.keep)
+    res.m_bar, res.m_tilde, res.ritz_values = m_bar, w.k, vals
+    basis = api.Basis(ctx, p.a, w, "sc" if cfg.method == "sc" else "deflation") if w.k > 0 else None
+    res.basis_build_s = time.perf_counter() - t0
+    for k in range(1, k_t):
+        xk = np.zeros(n)
+        if basis is None:
+            rk = api.pcg_solve(ctx, p.a, rhs_scaled[k], api.Ic(p.ic), xk, cfg.eps, cfg.max_iter)
+        elif cfg.method == "sc":
+            rk = api.pcg_solve(ctx, p.a, rhs_scaled[k], api.Sc(basis, p.ic), xk, cfg.eps, cfg.max_iter)
+        else:
+            rk = api.deflated_pcg_solve(ctx, p.a, rhs_scaled[k], api.Ic(p.ic), basis, xk, cfg.eps, cfg.max_iter)
+        _record(p, res, rk, xk, rhs_orig[k] if rhs_orig else None, keep_solutions)
+    return res
+
+
+def _record(p: Prepared, res: SequenceResult, rep, x, b_orig, keep):
+    res.iterations.append(rep.iterations)
+    res.converged.append(rep.converged)
+    res.histories.append(rep.history)
+    res.wall.append(rep.wall_time)
+    if keep:
+        res.solutions.append(x.copy())
+    if b_orig is not None:
+        x_orig = p.dis * x
+        r = b_orig - p.a_orig.spmv(x_orig)
+        res.true_relres.append(float(np.linalg.norm(r) / np.linalg.norm(b_orig)))

@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the pinned CPU oracle on identical
+seeded inputs.  Bars (BASELINE.json north_star): SpMV / IC sweeps / scaling bitwise; per-RHS
+iteration counts within +-2; solution relative difference <= 1e-8 at equal iteration counts;
+Ritz values relative <= 1e-6; condition estimate within 1%."""
+import numpy as np
+import pytest
+
+from conftest import laplacian_2d, random_sdd_spd, spectral_fixture
+from oracle import Matrix
+
+pytestmark = pytest.mark.gpu
+
+SOL_TOL = 1e-8     # solution relative difference at equal iteration counts
+RITZ_TOL = 1e-6    # Ritz values, relative
+KAPPA_TOL = 0.01   # condition estimate, relative
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def probs(oracle, problems):
+    out = {k: problems.generate(problems.SMALL[k]) for k in ("c1", "c2", "c3", "c4", "c5")}
+    n, rs, ci, va = random_sdd_spd(150, 0.05, 71, oracle)
+    out["sdd"] = problems.HostCsr(n, rs, ci, va)
+    n, rs, ci, va = laplacian_2d(20)
+    out["lap2d"] = problems.HostCsr(n, rs, ci, va)
+    n, rs, ci, va, lam, q = spectral_fixture(300, [1e-4, 3e-4, 1e-3], 12345, oracle)
+    out["dense300"] = problems.HostCsr(n, rs, ci, va)  # rows longer than one staging chunk
+    return out
+
+
+def _dev(ctx, h):
+    from paper_2203_08498_b200 import api
+
+    return api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+
+
+ALL = ["c1", "c2", "c3", "c4", "c5", "sdd", "lap2d", "dense300"]
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_spmv_bitwise(ctx, oracle, probs, name):
+    h = probs[name]
+    a = Matrix.of(h)
+    d = _dev(ctx, h)
+    x1, x2 = oracle.uniform_pm1(3, 0, h.n), oracle.uniform_pm1(4, 0, h.n)
+    assert np.array_equal(d.spmv(x1), oracle.spmv(a, x1))
+    y1, y2 = d.spmv_dual(x1, x2)
+    assert np.array_equal(y1, oracle.spmv(a, x1)) and np.array_equal(y2, oracle.spmv(a, x2))
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_diagonal_scale_bitwise(ctx, oracle, probs, name):
+    from paper_2203_08498_b200 import api
+
+    h = probs[name]
+    sa, dis = oracle.diagonal_scale(Matrix.of(h))
+    ds, ddis = api.diagonal_scale(ctx, _dev(ctx, h))
+    assert np.array_equal(ds.values(), sa.va) and np.array_equal(ddis, dis)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "sdd", "dense300"])
+@pytest.mark.parametrize("nblocks", [1, 3])
+def test_ic_factor_and_apply_bitwise(ctx, oracle, probs, name, nblocks):
+    from paper_2203_08498_b200 import api
+
+    h = probs[name]
+    sa, _ = oracle.diagonal_scale(Matrix.of(h))
+    of = oracle.ic0_factorize(sa, 0.0, nblocks)
+    gf = api.IcFactor.factorize(ctx, h.n, h.row_start, h.col_idx, sa.va, 0.0, nblocks)
+    ga, oa = gf.export(), of.arrays()
+    for k in oa:
+        assert np.array_equal(ga[k], oa[k]), k
+    for seed in (5, 6):
+        r = oracle.uniform_pm1(seed, 0, h.n)
+        assert np.array_equal(gf.apply(r), oracle.ic_apply(of, r))
+    # uploaded reference factor gives the same operator
+    up = api.IcFactor.from_arrays(ctx, h.n, **oa, shift_used=of.shift_used)
+    r = oracle.uniform_pm1(7, 0, h.n)
+    assert np.array_equal(up.apply(r), oracle.ic_apply(of, r))
+
+
+def _setup(ctx, oracle, h):
+    from paper_2203_08498_b200 import api
+
+    sa, dis = oracle.diagonal_scale(Matrix.of(h))
+    of = oracle.ic0_factorize(sa)
+    ga = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, sa.va)
+    gf = api.IcFactor.factorize(ctx, h.n, h.row_start, h.col_idx, sa.va)
+    return sa, of, ga, gf
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "lap2d"])
+@pytest.mark.parametrize("prec", ["identity", "ic"])
+def test_pcg_matches_oracle(ctx, oracle, probs, name, prec):
+    from paper_2203_08498_b200 import api
+
+    h = probs[name]
+    sa, of, ga, gf = _setup(ctx, oracle, h)
+    b = oracle.uniform_pm1(1, 0, h.n)
+    smp_o = oracle.sampler_a(8, 4000, h.n)
+    smp_g = api.SamplerState.method_a(ctx, 8, 4000, h.n)
+    xo, xg = np.zeros(h.n), np.zeros(h.n)
+    kind = 1 if prec == "ic" else 0
+    ro = oracle.pcg_solve(sa, b, xo, kind=kind, ic=of if kind else None, max_iter=4000, sampler=smp_o)
+    m = api.Ic(gf) if kind else api.Identity()
+    rg = api.pcg_solve(ctx, ga, b, m, xg, 1e-8, 4000, observer=smp_g)
+    assert rg.converged and ro.converged
+    assert abs(rg.iterations - ro.iterations) <= 2
+    if rg.iterations == ro.iterations:
+        assert _rel(xg, xo) <= SOL_TOL
+        assert np.allclose(rg.history, ro.history, rtol=1e-6, atol=0)
+        occ_g, it_g = smp_g.state()
+        occ_o, it_o = smp_o.state()
+        assert np.array_equal(occ_g, occ_o) and np.array_equal(it_g, it_o)
+        for s in np.nonzero(occ_o)[0]:
+            assert _rel(smp_g.slot(s), smp_o.slot(s)) <= SOL_TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_rr_on_oracle_errors(ctx, oracle, probs, name):
+    from paper_2203_08498_b200 import api
+
+    h = probs[name]
+    sa, of, ga, gf = _setup(ctx, oracle, h)
+    b = oracle.uniform_pm1(1, 0, h.n)
+    s = oracle.sampler_a(16, 4000, h.n)
+    x = np.zeros(h.n)
+    oracle.pcg_solve(sa, b, x, kind=1, ic=of, max_iter=4000, sampler=s)
+    errors = oracle.harvest_errors(x, s)
+    mb, vals, w = oracle.build_aux(sa, errors, float("inf"))
+    e_dev = api.TallDense.from_columns(ctx, h.n, errors)
+    gmb, gvals, _, gw = api.build_aux_matrix(ctx, ga, e_dev, 1e-3, keep_count=6)
+    assert gmb == mb
+    assert np.max(np.abs(gvals - vals) / np.abs(vals)) <= RITZ_TOL
+    cols = gw.columns()
+    assert cols.shape[0] == min(6, mb)
+    for j in range(cols.shape[0]):  # Ritz vectors up to sign/rotation inside clusters
+        assert abs(abs(np.dot(cols[j], w[j])) - 1.0) <= 1e-4
+
+
+def test_empty_deflation_is_pcg_bitwise(ctx, oracle, probs):
+    from paper_2203_08498_b200 import api
+
+    h = probs["c2"]
+    sa, of, ga, gf = _setup(ctx, oracle, h)
+    b = oracle.uniform_pm1(2, 0, h.n)
+    x1, x2 = np.zeros(h.n), np.zeros(h.n)
+    r1 = api.pcg_solve(ctx, ga, b, api.Ic(gf), x1)
+    r2 = api.deflated_pcg_solve(ctx, ga, b, api.Ic(gf), None, x2)
+    assert r1.iterations == r2.iterations and np.array_equal(r1.history, r2.history) and np.array_equal(x1, x2)
+
+
+def test_condest_rides_along_bitwise_and_matches_oracle(ctx, oracle, probs):
+    from paper_2203_08498_b200 import api
+
+    n, rs, ci, va = laplacian_2d(20)
+    h = probs["lap2d"]
+    sa, of, ga, gf = _setup(ctx, oracle, h)
+    b = oracle.uniform_pm1(1, 0, h.n)
+    xg, xp, xo = np.zeros(h.n), np.zeros(h.n), np.zeros(h.n)
+    rg, eg = api.pcg_with_condest(ctx, ga, b, api.Identity(), xg, 1e-8, 3000, m_samples=20)
+    rp = api.pcg_solve(ctx, ga, b, api.Identity(), xp, 1e-8, 3000)
+    assert rg.iterations == rp.iterations and np.array_equal(rg.history, rp.history) and np.array_equal(xg, xp)
+    ro, eo = oracle.pcg_with_condest(sa, b, xo, max_iter=3000, m_samples=20)
+    assert abs(rg.iterations - ro.iterations) <= 2
+    assert abs(eg.kappa - eo.kappa) / eo.kappa <= KAPPA_TOL
+    assert abs(eg.lambda_max - eo.lambda_max) / eo.lambda_max <= 1e-6
+    c = np.cos(np.pi / 21)
+    assert eg.lanczos_lambda_min == pytest.approx(1 - c, rel=1e-6)
+    assert eg.lanczos_lambda_max == pytest.approx(1 + c, rel=1e-6)
+
+
+def test_condest_known_answers(ctx):
+    from paper_2203_08498_b200 import api
+
+    a = api.CsrMatrix(ctx, 2, [0, 1, 2], [0, 1], [0.1, 1.0])
+    x = np.zeros(2)
+    rep, est = api.pcg_with_condest(ctx, a, np.array([0.0, 1.0]), api.Identity(), x, m_samples=20)
+    assert rep.converged and rep.iterations == 1 and not est.lambda_min_available and np.isnan(est.kappa)
+    x = np.zeros(2)
+    rep, est = api.pcg_with_condest(ctx, a, np.array([1e-3, 1.0]), api.Identity(), x, m_samples=20)
+    assert rep.iterations == 2 and est.lambda_min == pytest.approx(0.1, rel=1e-6)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("method", ["deflation", "sc"])
+def test_sequence_matches_oracle(ctx, oracle, problems, probs, name, method):
+    from dataclasses import replace
+
+    from oracle.sequence import run_sequence as oracle_sequence
+    from paper_2203_08498_b200 import sequence
+
+    cfg = replace(problems.SMALL[name], method=method)
+    h = probs[name]
+    ores = oracle_sequence(oracle, cfg, h)
+    p = sequence.prepare(ctx, cfg, h)
+    gres = sequence.run_sequence(p, ores["scaled_rhs"])
+    assert gres.m_bar == ores["m_bar"] and gres.m_tilde == ores["m_tilde"]
+    assert gres.sampled_iterations == ores["sampled_iterations"]
+    assert np.max(np.abs(gres.ritz_values - ores["ritz_values"]) / np.abs(ores["ritz_values"])) <= RITZ_TOL
+    for k, (gi, oi) in enumerate(zip(gres.iterations, ores["iterations"])):
+        assert abs(gi - oi) <= 2, (k, gres.iterations, ores["iterations"])
+        if gi == oi:
+            assert _rel(gres.solutions[k], ores["solutions"][k]) <= SOL_TOL
+
+
+def test_c1_full_sequence_golden(ctx, problems):
+    from paper_2203_08498_b200 import sequence
+
+    cfg = problems.CONFIGS["c1"]
+    h = problems.generate(cfg)
+    p = sequence.prepare(ctx, cfg, h)
+    pairs = [sequence.rhs(p, k) for k in range(cfg.n_rhs)]
+    res = sequence.run_sequence(p, [s for _, s in pairs], [b for b, _ in pairs])
+    assert all(abs(g - o) <= 2 for g, o in zip(res.iterations, [34, 29, 29, 30]))
+    assert all(r <= 1e-7 for r in res.true_relres)
+
+
+def test_projections_match_oracle(ctx, oracle, probs):
+    from paper_2203_08498_b200 import api
+
+    h = probs["c1"]
+    sa, of, ga, gf = _setup(ctx, oracle, h)
+    w = np.stack([oracle.uniform_pm1(20 + j, 0, h.n) for j in range(4)])
+    ob = oracle.basis(sa, w, 0)
+    gb = api.Basis(ctx, ga, api.TallDense.from_columns(ctx, h.n, w))
+    y = oracle.uniform_pm1(9, 0, h.n)
+    assert _rel(gb.project_pt(y), ob.project_pt(y)) <= 1e-10
+    assert _rel(gb.project_p(y), ob.project_p(y)) <= 1e-10
+    assert _rel(gb.direct_component(y), ob.direct_component(y)) <= 1e-10
+    # P^T (A W u) = 0 (test_recycling.cpp:130-145)
+    u = np.array([0.3, -1.2, 0.5, 2.0])
+    awu = sum(u[j] * oracle.spmv(sa, w[j]) for j in range(4))
+    assert np.max(np.abs(gb.project_pt(awu))) <= 1e-10 * np.max(np.abs(sa.va))
+
+
+def test_errors_map_to_reference_exceptions(ctx, oracle):
+    from paper_2203_08498_b200 import api
+
+    a = api.CsrMatrix(ctx, 2, [0, 2, 4], [0, 1, 0, 1], [1.0, 2.0, 2.0, 1.0])
+    with pytest.raises(api.BreakdownError):
+        api.pcg_solve(ctx, a, np.array([1.0, 0.0]), api.Identity(), np.zeros(2))
+    with pytest.raises(api.InvalidArgument):
+        api.pcg_solve(ctx, a, np.array([1.0, 0.0]), api.Identity(), np.zeros(2), eps=1.0)
+    with pytest.raises(api.InvalidArgument):
+        api.pcg_solve(ctx, a, np.array([1.0, 0.0]), api.Identity(), np.zeros(2), max_iter=0)
+    with pytest.raises(api.ParseError):
+        api.CsrMatrix(ctx, 2, [0, 1, 2], [1, 0], [1.0, 1.0])  # missing diagonal
+    n, rs, ci, va = random_sdd_spd(20, 0.2, 149, oracle)
+    d = api.CsrMatrix(ctx, n, rs, ci, va)
+    c = oracle.uniform_pm1(14, 0, n)
+    with pytest.raises(api.BreakdownError):
+        api.Basis(ctx, d, api.TallDense.from_columns(ctx, n, np.stack([c, c])))
+
+
+def test_zero_rhs_and_start_at_solution(ctx, oracle):
+    from paper_2203_08498_b200 import api
+
+    n, rs, ci, va = laplacian_2d(4)
+    a = api.CsrMatrix(ctx, n, rs, ci, va)
+    x = np.ones(n)
+    rep = api.pcg_solve(ctx, a, np.zeros(n), api.Identity(), x)
+    assert rep.converged and rep.iterations == 0 and (x == 0).all()
+    xt = oracle.uniform_pm1(3, 0, n)
+    b = oracle.spmv(Matrix(n, rs, ci, va), xt)
+    x = xt.copy()
+    rep = api.pcg_solve(ctx, a, b, api.Identity(), x)
+    assert rep.converged and rep.iterations == 0
+
+
+def test_iteration_cap_and_observer_count(ctx, oracle):
+    from paper_2203_08498_b200 import api
+
+    n, rs, ci, va = laplacian_2d(16)
+    a = api.CsrMatrix(ctx, n, rs, ci, va)
+    b = oracle.uniform_pm1(5, 0, n)
+    rep = api.pcg_solve(ctx, a, b, api.Identity(), np.zeros(n), max_iter=5)
+    assert not rep.converged and rep.iterations == 5
+    # method-A observer sees T-1 iterations: slots hold iterations < T
+    s = api.SamplerState.method_a(ctx, 4, 1000, n)
+    rep = api.pcg_solve(ctx, a, b, api.Identity(), np.zeros(n), observer=s)
+    occ, it = s.state()
+    assert rep.converged and it[occ].max() <= rep.iterations - 1
+
+
+def test_residual_sampling_and_method_b(ctx, oracle, probs):
+    from paper_2203_08498_b200 import api
+
+    h = probs["c1"]
+    sa, of, ga, gf = _setup(ctx, oracle, h)
+    b = oracle.uniform_pm1(1, 0, h.n)
+    so = oracle.sampler_b(6, 1e-8, h.n)
+    sg = api.SamplerState.method_b(ctx, 6, 1e-8, h.n)
+    xo, xg = np.zeros(h.n), np.zeros(h.n)
+    ro = oracle.pcg_solve(sa, b, xo, kind=1, ic=of, sampler=so, payload=1)
+    rg = api.pcg_solve(ctx, ga, b, api.Ic(gf), xg, observer=sg, payload="r")
+    assert ro.iterations == rg.iterations
+    oo, io = so.state()
+    og, ig = sg.state()
+    assert np.array_equal(oo, og) and np.array_equal(io, ig)
+    for s in np.nonzero(oo)[0]:
+        assert _rel(sg.slot(s), so.slot(s)) <= SOL_TOL
