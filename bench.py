@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark: the paper's sequence protocol on BASELINE.json configs[1] (C2: 128^3 high-contrast
+7-point FV, 10 right-hand sides, 32 error samples in solve 1, subspace-corrected ICCG with m=16)
+on B200, fp64.
+
+One step = the whole sequence on device-resident inputs: ICCG solve 1 with the method-A error
+sampler, the Rayleigh-Ritz basis (MGS, A E, E^T A E, eig, Ritz vectors), the SC operator build
+(A W, W^T A W, Cholesky), then 9 SC-ICCG solves from x0 = 0.  value = PCG iterations of the step
+/ device time of the step (CUDA events on the library stream).  e2e = the same step through the
+public API with pinned HOST right-hand sides and solutions (H2D/D2H inside the timed region).
+
+--impl reference runs the reference library itself (oracle/_ref, compiled from the reference
+sources) on the host cores: fixed iteration windows of ICCG and SC-ICCG on the same matrix, one
+independent sample per host thread (the reference is serial; samples are independent solves).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+For N > 1 launch with torch.distributed.run; ranks run independent replicas of the workload
+(scaling "weak"; the row-slab partition is not in this build -- see DESIGN.md).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG iters/s (fp64 sequence: ICCG solve 1 + RR + SC-ICCG solves)"
+UNIT = "iters/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2203_08498_b200 import api, problems, sequence
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = api.Context(local_rank)
+    cfg = problems.CONFIGS[args.config]
+    host = problems.generate(cfg)
+    prep = sequence.prepare(ctx, cfg, host, validate=True)
+    n = host.n
+    pairs = [sequence.rhs(prep, k) for k in range(cfg.n_rhs)]
+    b_dev = [torch.from_numpy(s).to(dev) for _, s in pairs]
+    b_pin = [torch.from_numpy(s).pin_memory() for _, s in pairs]
+    x_pin = [torch.zeros(n, dtype=torch.float64).pin_memory() for _ in pairs]
+    n_nnz = host.nnz
+    nnz_l = prep.ic.nnz_l
+
+    def step_device():
+        xs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(cfg.n_rhs)]
+        return _sequence(api, ctx, prep, cfg, b_dev, xs)
+
+    def step_e2e():
+        # host inputs in pinned memory; each solve stages b in and x out through the C-ABI
+        for x in x_pin:
+            x.zero_()
+        return _sequence(api, ctx, prep, cfg, [b.numpy() for b in b_pin], [x.numpy() for x in x_pin])
+
+    for _ in range(args.warmup):
+        step_device()
+    if world > 1:
+        torch.distributed.barrier()
+    ctx.synchronize()
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    launches0 = ctx.launches
+    iters = 0
+    with Clocks(local_rank) as clk:
+        ctx.record(0)
+        for _ in range(args.steps):
+            iters += step_device()
+        ctx.record(1)
+        ms = ctx.elapsed_ms(0, 1)
+    launches = ctx.launches - launches0
+    stats = {c: ctx.kernel_stats(c) for c in range(5)}
+    ctx.set_profiling(False)
+    # e2e through the public API with host buffers
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    ctx.synchronize()
+    ctx.record(2)
+    e2e_iters = 0
+    for _ in range(args.steps):
+        e2e_iters += step_e2e()
+    ctx.record(3)
+    e2e_ms = ctx.elapsed_ms(2, 3)
+    # max over ranks
+    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    it = torch.tensor([float(iters), float(e2e_iters)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(it, op=torch.distributed.ReduceOp.SUM)
+    ms, e2e_ms = t.tolist()
+    iters, e2e_iters = it.tolist()
+    if rank != 0:
+        return
+    peak, peak_src = peaks()
+    m_t = cfg.keep
+    # algorithmic bytes per launch
+    per_launch = {
+        0: 12 * n_nnz + 20 * n,                       # SpMV q = A p (+ (p,q))
+        1: 12 * nnz_l + 32 * n,                       # forward sweep: L entries, perm+prs, r in, y out
+        2: 12 * nnz_l + 48 * n + 8 * m_t * n,         # backward sweep: U, perm+prs, y, d, z out, W u, r
+        4: 8 * m_t * n + 8 * n,                       # W^T r projection
+    }
+    names = {0: "spmv (k_spmv_pq)", 1: "ic fwd sweep (k_sweep<false>)", 2: "ic bwd sweep + SC (k_sweep<true>)",
+             3: "vector ops", 4: "W^T r (k_tallt)"}
+    dom = max((c for c in stats if stats[c][1] > 0), key=lambda c: stats[c][0])
+    kernels = {}
+    for c, (tot_ms, cnt) in stats.items():
+        if cnt == 0:
+            continue
+        avg = tot_ms / cnt
+        entry = {"launches": cnt, "avg_us": round(avg * 1e3, 3), "share": round(tot_ms / ms, 4)}
+        if c in per_launch:
+            entry["algorithmic_bytes"] = per_launch[c]
+            entry["achieved_gbs"] = round(per_launch[c] / (avg * 1e-3) / 1e9, 1)
+        kernels[names[c]] = entry
+    roof_c = dom if dom in per_launch else 0
+    avg_roof = stats[roof_c][0] / stats[roof_c][1]
+    achieved = per_launch[roof_c] / (avg_roof * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(names[roof_c])
+    line = {
+        "metric": METRIC,
+        "value": round(iters / (ms / 1e3), 2),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md 8(d); no network for SuiteSparse)",
+        "config": {"workload": cfg.name, "n": n, "nnz": n_nnz, "n_rhs": cfg.n_rhs, "samples": cfg.sampler_m,
+                   "m_tilde": cfg.keep, "method": cfg.method, "eps": cfg.eps,
+                   "iterations_per_step": iters / args.steps / world,
+                   "time_to_solution_ms_per_rhs": round(ms / args.steps / cfg.n_rhs, 3),
+                   "l2": "inputs larger than L2 (A 183 MB + IC factor + W/AW 536 MB)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+        "e2e": {"value": round(e2e_iters / (e2e_ms / 1e3), 2), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * n * cfg.n_rhs, "d2h_bytes_per_step": 8 * n * cfg.n_rhs,
+                "time_to_solution_ms_per_rhs": round(e2e_ms / args.steps / cfg.n_rhs, 3)},
+        "roofline": {"bound": "hbm", "kernel": names[roof_c], "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src},
+        "kernels": kernels,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, host, threads=1, reps=1)
+    print(json.dumps(line), flush=True)
+
+
+def _sequence(api, ctx, prep, cfg, bs, xs):
+    """One full sequence; returns its PCG iteration count."""
+    n = prep.host.n
+    sampler = api.SamplerState.method_a(ctx, cfg.sampler_m, cfg.max_iter, n)
+    r = api.pcg_solve(ctx, prep.a, bs[0], api.Ic(prep.ic), xs[0], cfg.eps, cfg.max_iter, observer=sampler)
+    total = r.iterations
+    errors = api.harvest_errors(ctx, xs[0], sampler)
+    _, _, _, w = api.build_aux_matrix(ctx, prep.a, errors, 1e-3, keep_count=cfg.keep)
+    basis = api.Basis(ctx, prep.a, w, "sc" if cfg.method == "sc" else "deflation")
+    for k in range(1, len(bs)):
+        if cfg.method == "sc":
+            r = api.pcg_solve(ctx, prep.a, bs[k], api.Sc(basis, prep.ic), xs[k], cfg.eps, cfg.max_iter)
+        else:
+            r = api.deflated_pcg_solve(ctx, prep.a, bs[k], api.Ic(prep.ic), basis, xs[k], cfg.eps, cfg.max_iter)
+        total += r.iterations
+    return total
+
+
+# --------------------------------------------------------------------------- reference arm
+WINDOW = 8  # iterations per timed window of the bounded CPU sample
+
+
+def _ref_setup(cfg, host):
+    from oracle import Matrix, RefLib
+    from paper_2203_08498_b200 import problems
+
+    ref = RefLib()
+    a_orig = Matrix.of(host)
+    m0 = ref.matrix(a_orig)
+    va, dis = ref.diagonal_scale(m0, host.nnz)
+    a = Matrix(host.n, host.row_start, host.col_idx, va)
+    m = ref.matrix(a)
+    f = ref.ic0(m)
+    ic = ref.prec_ic(f)
+    # a cost-equivalent basis of m~ orthonormal columns (per-iteration work depends on m~ only)
+    w = ref.mgs(np.stack([problems.normal(99 + j, 0, host.n) for j in range(cfg.keep)]))
+    sc = ref.prec_sc(ic, m, w) if cfg.method == "sc" else None
+    defl = ref.deflation(m, w) if cfg.method != "sc" else None
+    return dict(ref=ref, m=m, ic=ic, sc=sc, defl=defl, dis=dis, a_orig=a_orig)
+
+
+def _ref_sample(st, cfg, host, k):
+    """ICCG window + accelerated window on right-hand side k; returns (iterations, seconds)."""
+    from paper_2203_08498_b200 import problems
+
+    ref, m = st["ref"], st["m"]
+    b = st["dis"] * host_spmv(host, problems.solution_stream(cfg, host.n, k))
+    t0 = time.perf_counter()
+    x = np.zeros(host.n)
+    r1 = ref.pcg_solve(m, b, st["ic"], x, cfg.eps, WINDOW)
+    x = np.zeros(host.n)
+    if st["sc"] is not None:
+        r2 = ref.pcg_solve(m, b, st["sc"], x, cfg.eps, WINDOW)
+    else:
+        r2 = ref.deflated_pcg_solve(m, b, st["ic"], st["defl"], x, cfg.eps, WINDOW)
+    return r1.iterations + r2.iterations, time.perf_counter() - t0
+
+
+def host_spmv(host, x):
+    from oracle import Matrix, Oracle
+
+    return Oracle().spmv(Matrix.of(host), x)
+
+
+def cpu_baseline(cfg, host, threads=1, reps=1):
+    st = _ref_setup(cfg, host)
+    iters, secs = 0, 0.0
+    for r in range(reps):
+        i, s = _ref_sample(st, cfg, host, 1 + r)
+        iters += i
+        secs += s
+    return {"value": round(iters / secs, 3), "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{cfg.name}: {WINDOW}-iteration ICCG window + {WINDOW}-iteration "
+                      f"{'SC' if cfg.method == 'sc' else 'deflated'}-ICCG window (m~={cfg.keep}), "
+                      f"oracle/_ref (reference sources, -O3 -ffp-contract=off), 1 thread"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2203_08498_b200 import problems
+
+    cfg = problems.CONFIGS[args.config]
+    host = problems.generate(cfg)
+    st = _ref_setup(cfg, host)
+    threads = max(1, min(os.cpu_count() or 1, args.ref_threads or (os.cpu_count() or 1)))
+    rhs = {}
+    for k in range(threads):
+        x = problems.solution_stream(cfg, host.n, 1 + k % (cfg.n_rhs - 1))
+        rhs[k] = st["dis"] * host_spmv(host, x)
+
+    def sample(k, out):
+        ref, m = st["ref"], st["m"]
+        x = np.zeros(host.n)
+        r1 = ref.pcg_solve(m, rhs[k], st["ic"], x, cfg.eps, WINDOW)
+        x = np.zeros(host.n)
+        if st["sc"] is not None:
+            r2 = ref.pcg_solve(m, rhs[k], st["sc"], x, cfg.eps, WINDOW)
+        else:
+            r2 = ref.deflated_pcg_solve(m, rhs[k], st["ic"], st["defl"], x, cfg.eps, WINDOW)
+        out[k] = r1.iterations + r2.iterations
+
+    def step():
+        out = {}
+        ths = [threading.Thread(target=sample, args=(k, out)) for k in range(threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return sum(out.values())
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    iters = 0
+    for _ in range(args.steps):
+        iters += step()
+    secs = time.perf_counter() - t0
+    value = round(iters / secs, 3)
+    sample_desc = (f"{cfg.name}: per step {threads} independent samples (one per host thread), each a "
+                   f"{WINDOW}-iteration ICCG window + {WINDOW}-iteration "
+                   f"{'SC' if cfg.method == 'sc' else 'deflated'}-ICCG window (m~={cfg.keep})")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": host.n, "nnz": host.nnz, "method": cfg.method, "m_tilde": cfg.keep},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample_desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-threads", type=int, default=0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

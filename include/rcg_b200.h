@@ -50,6 +50,9 @@ int64_t rcg_ctx_launch_count(const rcg_ctx* ctx);
  * CUDA events on the context stream when profiling is enabled (class: 0 spmv, 1 fwd sweep,
  * 2 bwd sweep, 3 vector ops, 4 projection).  Used by bench.py for the roofline. */
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable);
+/* CUDA events on the context stream (slots 0..15) for device-side timing by callers */
+int rcg_ctx_event_record(rcg_ctx* ctx, int slot);
+int rcg_ctx_event_elapsed(rcg_ctx* ctx, int slot_a, int slot_b, double* ms);
 int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launches);
 void rcg_ctx_reset_stats(rcg_ctx* ctx);
 

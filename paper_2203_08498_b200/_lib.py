@@ -99,6 +99,8 @@ SIGNATURES = {
     "rcg_ctx_synchronize": (C.c_int, vp),
     "rcg_ctx_launch_count": (C.c_int64, vp),
     "rcg_ctx_set_profiling": (C.c_int, vp, C.c_int),
+    "rcg_ctx_event_record": (C.c_int, vp, C.c_int),
+    "rcg_ctx_event_elapsed": (C.c_int, vp, C.c_int, C.c_int, dp),
     "rcg_ctx_kernel_stats": (C.c_int, vp, C.c_int, dp, i64p),
     "rcg_ctx_reset_stats": (None, vp),
     "rcg_matrix_create": (C.c_int, vp, C.c_int32, vp, vp, vp, C.c_int, C.POINTER(vp)),

@@ -87,6 +87,15 @@ class Context:
     def set_profiling(self, on: bool):
         check(lib.rcg_ctx_set_profiling(self.h, 1 if on else 0))
 
+    def record(self, slot: int):
+        """CUDA event on the library stream (device-side timing)."""
+        check(lib.rcg_ctx_event_record(self.h, slot))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        check(lib.rcg_ctx_event_elapsed(self.h, a, b, C.byref(ms)))
+        return ms.value
+
     def kernel_stats(self, cls: int):
         ms = C.c_double()
         cnt = C.c_int64()

@@ -243,6 +243,8 @@ void rcg_ctx_destroy(rcg_ctx* ctx) {
         cudaEventDestroy(t.stop);
     }
     for (auto e : ctx->ev_free) cudaEventDestroy(e);
+    for (auto e : ctx->user_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -257,6 +259,26 @@ int64_t rcg_ctx_launch_count(const rcg_ctx* ctx) { return ctx ? ctx->launches : 
 
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable) {
     return guard([&] { ctx->profiling = enable != 0; });
+}
+
+int rcg_ctx_event_record(rcg_ctx* ctx, int slot) {
+    return guard([&] {
+        require(slot >= 0 && slot < 16, "rcg_ctx_event_record: slot out of range");
+        if (!ctx->user_ev[slot]) RCG_CK(cudaEventCreate(&ctx->user_ev[slot]));
+        RCG_CK(cudaEventRecord(ctx->user_ev[slot], ctx->stream));
+    });
+}
+
+int rcg_ctx_event_elapsed(rcg_ctx* ctx, int slot_a, int slot_b, double* ms) {
+    return guard([&] {
+        require(slot_a >= 0 && slot_a < 16 && slot_b >= 0 && slot_b < 16 && ctx->user_ev[slot_a] &&
+                    ctx->user_ev[slot_b],
+                "rcg_ctx_event_elapsed: slot not recorded");
+        RCG_CK(cudaEventSynchronize(ctx->user_ev[slot_b]));
+        float f = 0.f;
+        RCG_CK(cudaEventElapsedTime(&f, ctx->user_ev[slot_a], ctx->user_ev[slot_b]));
+        *ms = f;
+    });
 }
 
 int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launches) {

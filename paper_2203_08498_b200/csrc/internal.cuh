@@ -157,6 +157,7 @@ struct rcg_ctx {
     };
     std::vector<TimedLaunch> ev_pending;
     std::vector<cudaEvent_t> ev_free;
+    cudaEvent_t user_ev[16] = {};
 };
 
 struct rcg_matrix {
