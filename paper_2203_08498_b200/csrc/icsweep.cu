@@ -28,7 +28,7 @@
 
 namespace rcg {
 
-constexpr int kDepChunk = 8;
+constexpr int kDepChunk = 16;
 
 // Sum of one value per thread over the block; then a two-level deterministic grid reduction
 // keyed by tile: tiles -> groups of kGroup -> total.  Returns true in the block that owns the
@@ -71,79 +71,87 @@ __device__ bool tile_reduce(double v, int tile, int ntiles, SweepArgs& a, double
     return true;
 }
 
+// Persistent sweep: a grid of at most (SMs x blocks_per_sm) CTAs pulls 128-row tiles of the
+// level-sorted order from an atomic ticket until none is left.  Bounding the resident CTAs
+// bounds how many future-level rows spin at once.
 template <bool BWD>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
     __shared__ int s_tile;
     __shared__ double red[32];
     __shared__ double tot;
     if (a.st->done) return;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
-    __syncthreads();
-    const int tile = s_tile;
     const int ntiles = (a.n + kSweepThreads - 1) / kSweepThreads;
-    const int pos = tile * kSweepThreads + threadIdx.x;
-    double contrib = 0.0;
-    if (pos < a.n) {
-        const int32_t row = __ldg(a.perm + pos);
-        const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
-        double s;
-        if (BWD) {
-            s = __ddiv_rn(a.in[row], __ldg(a.d + row));
-            if (a.in_reset) a.in_reset[row] = sentinel();
-        } else {
-            s = a.in[row];
-        }
-        for (int32_t e0 = beg; e0 < end; e0 += kDepChunk) {
-            const int cnt = min(kDepChunk, end - e0);
-            int32_t col[kDepChunk];
-            double val[kDepChunk], dep[kDepChunk];
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
+        __syncthreads();
+        const int tile = s_tile;
+        __syncthreads();
+        if (tile >= ntiles) break;
+        const int pos = tile * kSweepThreads + threadIdx.x;
+        double contrib = 0.0;
+        if (pos < a.n) {
+            const int32_t row = __ldg(a.perm + pos);
+            const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
+            double s;
+            if (BWD) {
+                s = __ddiv_rn(a.in[row], __ldg(a.d + row));
+                if (a.in_reset) a.in_reset[row] = sentinel();
+            } else {
+                s = a.in[row];
+            }
+            for (int32_t e0 = beg; e0 < end; e0 += kDepChunk) {
+                const int cnt = min(kDepChunk, end - e0);
+                int32_t col[kDepChunk];
+                double val[kDepChunk], dep[kDepChunk];
 #pragma unroll
-            for (int j = 0; j < kDepChunk; ++j)
-                if (j < cnt) {
-                    col[j] = __ldcs(a.pcol + e0 + j);
-                    val[j] = __ldcs(a.pval + e0 + j);
-                }
+                for (int j = 0; j < kDepChunk; ++j)
+                    if (j < cnt) {
+                        col[j] = __ldcs(a.pcol + e0 + j);
+                        val[j] = __ldcs(a.pval + e0 + j);
+                    }
 #pragma unroll
-            for (int j = 0; j < kDepChunk; ++j)
-                if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
+                for (int j = 0; j < kDepChunk; ++j)
+                    if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
+                // re-poll every still-missing dependency of the row together, so the row pays
+                // one L2 round trip after its last parent is published (not one per parent)
+                unsigned spins = 0;
+                while (true) {
+                    bool missing = false;
 #pragma unroll
-            for (int j = 0; j < kDepChunk; ++j)
-                if (j < cnt) {
-                    // bounded wait: a schedule bug must surface as an error, never hang the GPU
-                    unsigned spins = 0;
-                    while (is_sentinel(dep[j])) {
-                        dep[j] = ld_relaxed(a.out + col[j]);
-                        if (++spins == (1u << 26)) {
-                            atomicExch(&a.tickets[3], 1);
-                            dep[j] = 0.0;
-                        }
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j < cnt && is_sentinel(dep[j])) missing = true;
+                    if (!missing) break;
+                    if (a.backoff_ns) __nanosleep(a.backoff_ns);
+#pragma unroll
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j < cnt && is_sentinel(dep[j])) dep[j] = ld_relaxed(a.out + col[j]);
+                    if (++spins == (1u << 24)) {  // bounded: a schedule fault is an error, never a hang
+                        atomicExch(&a.tickets[3], 1);
+#pragma unroll
+                        for (int j = 0; j < kDepChunk; ++j)
+                            if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
                     }
                 }
 #pragma unroll
-            for (int j = 0; j < kDepChunk; ++j)
-                if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
-        }
-        st_relaxed(a.out + row, publishable(s));
-        if (BWD) {
-            double z = s;
-            if (a.zout) {
-                for (int j = 0; j < a.k; ++j) z = fadd_mul(z, __ldg(a.u + j), __ldg(a.w + j * a.ldw + row));
-                a.zout[row] = z;
+                for (int j = 0; j < kDepChunk; ++j)
+                    if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
             }
-            if (a.r) contrib = __dmul_rn(a.r[row], z);
+            st_relaxed(a.out + row, publishable(s));
+            if (BWD && a.r) contrib = __dmul_rn(a.r[row], s);
         }
-    }
-    if (BWD && a.r) {
-        if (tile_reduce(contrib, tile, ntiles, a, red, &tot) && threadIdx.x == 0) {
-            // (r, z) complete: breakdown test and beta of src/pcg.cpp:65-71
-            DevState* st = a.st;
-            const double rho = tot;
-            st->rho = rho;
-            if (rho <= 0.0) {
-                st->done = kBroken;
-                st->status = kBrkRz;
+        if (BWD && a.r) {
+            if (tile_reduce(contrib, tile, ntiles, a, red, &tot) && threadIdx.x == 0) {
+                // (r, z) complete: breakdown test and beta of src/pcg.cpp:65-71.  With subspace
+                // correction z = z_ic + W u, so (r, z) = (r, z_ic) + (W^T r) . u (st->scal[2])
+                DevState* st = a.st;
+                const double rho = a.add_sc ? tot + st->scal[2] : tot;
+                st->rho = rho;
+                if (rho <= 0.0) {
+                    st->done = kBroken;
+                    st->status = kBrkRz;
+                }
+                st->beta = st->iter > 1 ? rho / st->rho_prev : 0.0;
             }
-            st->beta = st->iter > 1 ? rho / st->rho_prev : 0.0;
         }
     }
     if (threadIdx.x == 0) {
@@ -173,7 +181,9 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
 
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
-    const int grid = (f->n + kSweepThreads - 1) / kSweepThreads;
+    const int ntiles = (f->n + kSweepThreads - 1) / kSweepThreads;
+    const int grid = std::max(1, std::min(ntiles, ctx->num_sms * ctx->sweep_bps));
+    a.backoff_ns = ctx->sweep_backoff_ns;
     KTimer t(ctx, backward ? 2 : 1);
     if (backward)
         k_sweep<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);

@@ -158,6 +158,8 @@ struct rcg_ctx {
     std::vector<TimedLaunch> ev_pending;
     std::vector<cudaEvent_t> ev_free;
     cudaEvent_t user_ev[16] = {};
+    int sweep_bps = 4;          // resident sweep CTAs per SM (RCG_SWEEP_BPS)
+    int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
 };
 
 struct rcg_matrix {

@@ -26,13 +26,9 @@ struct SweepArgs {
     const double* in;      // forward: r ; backward: y (undivided forward result)
     double* out;           // sentinel-initialised result the dependants poll
     double* in_reset;      // backward: y is reset to the sentinel after use (nullable)
-    // backward epilogue
-    double* zout;          // subspace correction: z = out + W u (nullable)
-    const double* w;
-    int64_t ldw;
-    int k;
-    const double* u;
-    const double* r;       // rho = (r, z) partials when non-null
+    const double* r;       // backward: rho = (r, z) partials when non-null
+    int add_sc;            // backward: rho += (W^T r) . u (subspace correction)
+    int backoff_ns;        // first __nanosleep of a dependency wait
     int* tickets;          // [0] tile ticket, [1] exit count, [2] group ticket
     double* partials;
     double* gpart;

@@ -27,13 +27,19 @@ constexpr int kTallKC = 32;   // W^T y columns accumulated per pass in registers
 
 // ------------------------------------------------------------------ kernels
 // p = z (first iteration) or z + beta p  (src/pcg.cpp:67-71); optionally resets the sweep buffer
+// With W != null (IC inner + subspace correction) z_i = z_ic,i + sum_j u_j W_ij first, in the
+// reference's accumulation order (src/subspace_correction.cpp:53-56).
 __global__ void __launch_bounds__(kStreamThreads) k_pupdate(const double* __restrict__ z, double* __restrict__ p,
-                                                            double* __restrict__ zs_reset, int32_t n, DevState* st) {
+                                                            double* __restrict__ zs_reset, int32_t n, DevState* st,
+                                                            const double* __restrict__ W, int64_t ldw, int k,
+                                                            const double* __restrict__ u) {
     if (st->done) return;
     const bool first = st->iter == 1;
     const double beta = st->beta;
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const double zi = z[i];
+        double zi = z[i];
+        if (W)
+            for (int j = 0; j < k; ++j) zi = fadd_mul(zi, __ldg(u + j), __ldg(W + j * ldw + i));
         p[i] = first ? zi : fadd_mul(zi, beta, p[i]);
         if (zs_reset) zs_reset[i] = sentinel();
     }
@@ -139,10 +145,16 @@ __global__ void __launch_bounds__(kStreamThreads) k_tallt(const double* __restri
     }
     if (grid_reduce_dyn(bvals, k, partials, &st->tick[2], tot)) {
         if (threadIdx.x < 32) {
-            if (mode == 1)
+            if (mode >= 1) {
                 warp_chol_solve(L, k, tot, out, sol);
-            else
+                if (mode == 2 && threadIdx.x == 0) {  // f . u = (W^T r) . (W^T A W)^-1 W^T r
+                    double fu = 0.0;
+                    for (int j = 0; j < k; ++j) fu = fadd_mul(fu, tot[j], sol[j]);
+                    st->scal[2] = fu;
+                }
+            } else {
                 for (int j = threadIdx.x; j < k; j += 32) out[j] = tot[j];
+            }
         }
     }
 }
@@ -486,7 +498,7 @@ struct Solve {
         }
         if (sc) {
             k_tallt<<<sg, kStreamThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w.r, n, w.partials, scb->l, w.u2,
-                                                             1, w.st, 1);
+                                                             2, w.st, 1);
             RCG_LAUNCHED(ctx);
         }
         if (condest) {  // v0 already uploaded into w.v; normalise (src/condest.cpp:47-52)
@@ -509,16 +521,8 @@ struct Solve {
             ba.in_reset = w.ybuf;
             ba.out = w.zs;
             ba.r = w.r;
-            if (sc) {
-                ba.zout = w.z;
-                ba.w = scb->w;
-                ba.ldw = scb->ld;
-                ba.k = scb->k;
-                ba.u = w.u2;
-                z = w.z;
-            } else {
-                z = w.zs;
-            }
+            ba.add_sc = sc ? 1 : 0;
+            z = w.zs;
             launch_sweep(ctx, m->ic, true, ba);
         } else if (sc) {
             k_sc_identity<<<sg, kStreamThreads, 0, ctx->stream>>>(w.r, w.z, scb->w, scb->ld, scb->k, w.u2, n,
@@ -527,8 +531,12 @@ struct Solve {
             z = w.z;
         }
         {
+            // IC + SC: z = z_ic + W u is formed here, coalesced, instead of inside the sweep
             KTimer t(ctx, 3);
-            k_pupdate<<<sg, kStreamThreads, 0, ctx->stream>>>(z, w.p, ic ? w.zs : nullptr, n, st);
+            const bool fold = ic && sc;
+            k_pupdate<<<sg, kStreamThreads, 0, ctx->stream>>>(z, w.p, ic ? w.zs : nullptr, n, st,
+                                                               fold ? scb->w : nullptr, fold ? scb->ld : 0,
+                                                               fold ? scb->k : 0, w.u2);
             RCG_LAUNCHED(ctx);
         }
         const bool dfl = defl && defl->k > 0;
@@ -569,7 +577,7 @@ struct Solve {
         if (sc) {  // W^T r for the next apply (src/subspace_correction.cpp:50-51)
             KTimer t(ctx, 4);
             k_tallt<<<sg, kStreamThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w.r, n, w.partials, scb->l,
-                                                             w.u2, 1, st, 1);
+                                                             w.u2, 2, st, 1);
             RCG_LAUNCHED(ctx);
         }
     }

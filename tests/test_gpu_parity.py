@@ -127,7 +127,11 @@ def test_pcg_matches_oracle(ctx, oracle, probs, name, prec):
                           sampler=smp_p)
     # +-2 iterations; unpreconditioned CG on the 1e6-contrast problem is rounding-chaotic (the
     # oracle itself moves when b moves by one ulp), so the window widens to twice that response
-    assert abs(rg.iterations - ro.iterations) <= max(2, 2 * abs(rp.iterations - ro.iterations))
+    spread = abs(rp.iterations - ro.iterations)
+    for seed in (12, 13):
+        spread = max(spread, abs(oracle.pcg_solve(sa, _ulp_perturb(b, seed), np.zeros(h.n), kind=kind,
+                                                  ic=of if kind else None, max_iter=4000).iterations - ro.iterations))
+    assert abs(rg.iterations - ro.iterations) <= max(2, 2 * spread)
     if rg.iterations == ro.iterations:
         tol = _sol_tol(_rel(xp, xo)) if rp.iterations == ro.iterations else 1e-6
         assert _rel(xg, xo) <= tol, (_rel(xg, xo), tol)
