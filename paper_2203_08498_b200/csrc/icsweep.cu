@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
     __shared__ double red[32];
     __shared__ double tot;
     if (a.st->done) return;
-    const int ntiles = (a.n + kSweepThreads - 1) / kSweepThreads;
+    const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
         __syncthreads();
@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
         if (tile >= ntiles) break;
         const int pos = tile * kSweepThreads + threadIdx.x;
         double contrib = 0.0;
-        if (pos < a.n) {
-            const int32_t row = __ldg(a.perm + pos);
+        const int32_t row = pos < a.npos ? __ldg(a.perm + pos) : -1;  // -1: level padding
+        if (row >= 0) {
             const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
             double s;
             if (BWD) {
@@ -99,6 +99,71 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
             } else {
                 s = a.in[row];
             }
+            if (end - beg <= kDepChunk) {
+                // common case: one chunk; the row is published from inside the wait loop, so a
+                // lane never waits for slower lanes of its warp before releasing its dependants
+                const int cnt = end - beg;
+                int32_t col[kDepChunk];
+                double val[kDepChunk], dep[kDepChunk];
+#pragma unroll
+                for (int j = 0; j < kDepChunk; ++j)
+                    if (j < cnt) {
+                        col[j] = __ldcs(a.pcol + beg + j);
+                        val[j] = __ldcs(a.pval + beg + j);
+                    }
+#pragma unroll
+                for (int j = 0; j < kDepChunk; ++j)
+                    if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
+                unsigned spins = 0;
+                if (cnt > 0) {
+                    // spin on the critical parent only (the one of highest level, chosen on the
+                    // host); the others are almost always ready by then.  Polling one address per
+                    // row instead of all parents keeps L2 free for the rows being computed.
+                    const int c = a.pcrit ? __ldg(a.pcrit + pos) : 0;
+                    double cv = 0.0;
+                    int32_t cc = 0;
+#pragma unroll
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j == c) {
+                            cv = dep[j];
+                            cc = col[j];
+                        }
+                    while (is_sentinel(cv)) {
+                        cv = ld_relaxed(a.out + cc);
+                        if (++spins == (1u << 24)) {
+                            atomicExch(&a.tickets[3], 1);
+                            cv = 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j == c) dep[j] = cv;
+                }
+                while (true) {
+                    bool missing = false;
+#pragma unroll
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j < cnt && is_sentinel(dep[j])) missing = true;
+                    if (!missing) {
+#pragma unroll
+                        for (int j = 0; j < kDepChunk; ++j)
+                            if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
+                        st_relaxed(a.out + row, publishable(s));
+                        break;
+                    }
+                    if (a.backoff_ns) __nanosleep(a.backoff_ns);
+#pragma unroll
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j < cnt && is_sentinel(dep[j])) dep[j] = ld_relaxed(a.out + col[j]);
+                    if (++spins == (1u << 24)) {  // bounded: a schedule fault is an error, never a hang
+                        atomicExch(&a.tickets[3], 1);
+#pragma unroll
+                        for (int j = 0; j < kDepChunk; ++j)
+                            if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
+                    }
+                }
+                if (BWD && a.r) contrib = __dmul_rn(a.r[row], s);
+            } else {
             for (int32_t e0 = beg; e0 < end; e0 += kDepChunk) {
                 const int cnt = min(kDepChunk, end - e0);
                 int32_t col[kDepChunk];
@@ -138,6 +203,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
             }
             st_relaxed(a.out + row, publishable(s));
             if (BWD && a.r) contrib = __dmul_rn(a.r[row], s);
+            }
         }
         if (BWD && a.r) {
             if (tile_reduce(contrib, tile, ntiles, a, red, &tot) && threadIdx.x == 0) {
@@ -169,8 +235,10 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
     a.prs = backward ? f->b_prs : f->f_prs;
     a.pcol = backward ? f->b_col : f->f_col;
     a.pval = backward ? f->b_val : f->f_val;
+    a.pcrit = backward ? f->b_crit : f->f_crit;
     a.d = f->d;
     a.n = f->n;
+    a.npos = backward ? f->b_npos : f->f_npos;
     a.tickets = ctx->ws.tickets + (backward ? 4 : 0);
     a.partials = ctx->ws.partials;
     a.gpart = ctx->ws.gpart;
@@ -181,7 +249,7 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
 
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
-    const int ntiles = (f->n + kSweepThreads - 1) / kSweepThreads;
+    const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * ctx->sweep_bps));
     a.backoff_ns = ctx->sweep_backoff_ns;
     KTimer t(ctx, backward ? 2 : 1);
@@ -206,15 +274,21 @@ void check_sweep_watchdog(rcg_ctx* ctx) {
 }
 
 // workspace needed by the sweeps of an n-row factor
-static void ensure_sweep_ws(rcg_ctx* ctx, int32_t n, int k, int64_t max_iter, int pending) {
-    const int64_t ntiles = (n + kSweepThreads - 1) / kSweepThreads;
+int64_t sweep_tiles(const rcg_ic* f) {
+    const int64_t npos = std::max<int64_t>(std::max(f->f_npos, f->b_npos), f->n);
+    return (npos + kSweepThreads - 1) / kSweepThreads;
+}
+
+static void ensure_sweep_ws(rcg_ctx* ctx, const rcg_ic* f, int k, int64_t max_iter, int pending) {
+    const int32_t n = f->n;
+    const int64_t ntiles = sweep_tiles(f);
     const int64_t ngroups = (ntiles + kGroup - 1) / kGroup;
     const int64_t red = std::max<int64_t>(ntiles, static_cast<int64_t>(kMaxRed) * ctx->num_sms * 8);
     ensure_workspace(ctx, n, k, max_iter, red, ngroups, pending);
 }
 
 void ic_apply_dev(rcg_ctx* ctx, const rcg_ic* f, const double* r, double* z) {
-    ensure_sweep_ws(ctx, f->n, 1, 1, 1);
+    ensure_sweep_ws(ctx, f, 1, 1, 1);
     Workspace& w = ctx->ws;
     RCG_CK(cudaMemsetAsync(w.st, 0, sizeof(DevState), ctx->stream));
     launch_fill_bits(ctx, w.ybuf, f->n, kSentinelBits);
@@ -241,7 +315,8 @@ static T* upload(rcg_ctx* ctx, const std::vector<T>& h) {
 // Level-sorted copy of a row-wise triangular factor.  `descending` walks rows n-1..0 (U).
 static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vector<int32_t>& col,
                               const std::vector<double>& val, bool descending, std::vector<int32_t>& perm,
-                              std::vector<int32_t>& prs, std::vector<int32_t>& pcol, std::vector<double>& pval) {
+                              std::vector<int32_t>& prs, std::vector<int32_t>& pcol, std::vector<double>& pval,
+                              std::vector<uint8_t>& crit, int32_t& npos) {
     std::vector<int32_t> level(n, 0);
     int32_t nlev = 0;
     for (int32_t t = 0; t < n; ++t) {
@@ -251,22 +326,38 @@ static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const s
         level[i] = lv;
         nlev = std::max(nlev, lv + 1);
     }
+    // each level starts on a warp boundary (padding positions hold perm = -1), so no warp mixes
+    // rows of two levels and a level's rows never wait on lanes of the next one
     std::vector<int64_t> start(static_cast<size_t>(nlev) + 1, 0);
     for (int32_t i = 0; i < n; ++i) start[level[i] + 1]++;
-    for (int32_t l = 0; l < nlev; ++l) start[l + 1] += start[l];
-    perm.assign(n, 0);
+    for (int32_t l = 0; l < nlev; ++l) start[l + 1] = start[l] + round_up(start[l + 1], 32);
+    const int64_t total = start[nlev];
+    require(total < (1LL << 31), "IC schedule: padded length exceeds int32");
+    npos = static_cast<int32_t>(total);
+    perm.assign(total, -1);
     for (int32_t t = 0; t < n; ++t) {
         const int32_t i = descending ? n - 1 - t : t;
         perm[start[level[i]]++] = i;
     }
-    prs.assign(static_cast<size_t>(n) + 1, 0);
-    for (int32_t pos = 0; pos < n; ++pos) prs[pos + 1] = prs[pos] + (rs[perm[pos] + 1] - rs[perm[pos]]);
+    prs.assign(static_cast<size_t>(total) + 1, 0);
+    for (int64_t pos = 0; pos < total; ++pos) {
+        const int32_t i = perm[pos];
+        prs[pos + 1] = prs[pos] + (i >= 0 ? rs[i + 1] - rs[i] : 0);
+    }
     pcol.resize(col.size());
     pval.resize(val.size());
-    for (int32_t pos = 0; pos < n; ++pos) {
+    crit.assign(total, 0);
+    for (int64_t pos = 0; pos < total; ++pos) {
         const int32_t i = perm[pos];
+        if (i < 0) continue;
         std::copy(col.begin() + rs[i], col.begin() + rs[i + 1], pcol.begin() + prs[pos]);
         std::copy(val.begin() + rs[i], val.begin() + rs[i + 1], pval.begin() + prs[pos]);
+        int32_t best = -1;
+        for (int32_t p = rs[i]; p < rs[i + 1]; ++p)
+            if (p - rs[i] < 255 && level[col[p]] >= best) {
+                best = level[col[p]];
+                crit[pos] = static_cast<uint8_t>(p - rs[i]);
+            }
     }
     return nlev;
 }
@@ -274,17 +365,22 @@ static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const s
 static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
     std::vector<int32_t> perm, prs, pcol;
     std::vector<double> pval;
-    f->fwd_levels = build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval);
+    std::vector<uint8_t> crit;
+    f->fwd_levels =
+        build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval, crit, f->f_npos);
     f->f_perm = upload(ctx, perm);
     f->f_prs = upload(ctx, prs);
     f->f_col = upload(ctx, pcol);
     f->f_val = upload(ctx, pval);
+    f->f_crit = upload(ctx, crit);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    f->bwd_levels = build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval);
+    f->bwd_levels =
+        build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval, crit, f->b_npos);
     f->b_perm = upload(ctx, perm);
     f->b_prs = upload(ctx, prs);
     f->b_col = upload(ctx, pcol);
     f->b_val = upload(ctx, pval);
+    f->b_crit = upload(ctx, crit);
     f->d = upload(ctx, f->h_d);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
 }
@@ -447,7 +543,8 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
-                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d})
+                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->f_crit,
+                    (void*)f->b_crit})
         dev_free(p);
     delete f;
 }

@@ -180,6 +180,8 @@ struct rcg_ic {
     std::vector<double> h_lval, h_d, h_uval;
     // device schedules
     int32_t fwd_levels = 0, bwd_levels = 0;
+    int32_t f_npos = 0, b_npos = 0;   // schedule lengths with each level padded to a warp multiple
+    uint8_t *f_crit = nullptr, *b_crit = nullptr;
     int32_t *f_perm = nullptr, *f_prs = nullptr, *f_col = nullptr;
     double* f_val = nullptr;
     int32_t *b_perm = nullptr, *b_prs = nullptr, *b_col = nullptr;

@@ -21,8 +21,10 @@ struct SweepArgs {
     const int32_t* prs;    // position-indexed row starts
     const int32_t* pcol;   // original column indices, reference entry order
     const double* pval;
+    const uint8_t* pcrit;  // per position: entry index of the highest-level parent (spin target)
     const double* d;       // pivots (backward)
     int32_t n;
+    int32_t npos;          // level-padded length of the schedule (multiple of 32 per level)
     const double* in;      // forward: r ; backward: y (undivided forward result)
     double* out;           // sentinel-initialised result the dependants poll
     double* in_reset;      // backward: y is reset to the sentinel after use (nullable)
@@ -42,5 +44,6 @@ void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const d
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
 SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward);
 void check_sweep_watchdog(rcg_ctx* ctx);
+int64_t sweep_tiles(const rcg_ic* f);
 
 }  // namespace rcg

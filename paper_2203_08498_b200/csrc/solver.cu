@@ -420,7 +420,7 @@ struct Solve {
         int k = 1;
         if (sc) k = std::max(k, scb->k);
         if (defl) k = std::max(k, defl->k);
-        const int64_t ntiles = (n + kSweepThreads - 1) / kSweepThreads;
+        const int64_t ntiles = ic ? sweep_tiles(m->ic) : (n + kSweepThreads - 1) / kSweepThreads;
         const int64_t ngroups = (ntiles + kGroup - 1) / kGroup;
         const int64_t red = std::max<int64_t>(ntiles, static_cast<int64_t>(kMaxRed) * ctx->num_sms * 8);
         ensure_workspace(ctx, n, k, max_iter, red, ngroups, smp ? smp->m : 1);
