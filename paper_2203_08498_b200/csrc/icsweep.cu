@@ -115,30 +115,6 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
                 for (int j = 0; j < kDepChunk; ++j)
                     if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
                 unsigned spins = 0;
-                if (cnt > 0) {
-                    // spin on the critical parent only (the one of highest level, chosen on the
-                    // host); the others are almost always ready by then.  Polling one address per
-                    // row instead of all parents keeps L2 free for the rows being computed.
-                    const int c = a.pcrit ? __ldg(a.pcrit + pos) : 0;
-                    double cv = 0.0;
-                    int32_t cc = 0;
-#pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
-                        if (j == c) {
-                            cv = dep[j];
-                            cc = col[j];
-                        }
-                    while (is_sentinel(cv)) {
-                        cv = ld_relaxed(a.out + cc);
-                        if (++spins == (1u << 24)) {
-                            atomicExch(&a.tickets[3], 1);
-                            cv = 0.0;
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
-                        if (j == c) dep[j] = cv;
-                }
                 while (true) {
                     bool missing = false;
 #pragma unroll
