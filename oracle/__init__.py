@@ -158,6 +158,22 @@ class Oracle:
         if st:
             raise _KIND.get(st, OracleError)(st, self.lib.orc_last_error().decode())
 
+    def reversed_dots(self, order: int = 1):
+        """Context manager: run the oracle with every dot product summed in another valid order
+        (1 = backwards, 2 = pairwise tree) -- the problem's own sensitivity to reduction order,
+        used as the parity rounding floor."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def cm():
+            self.lib.orc_set_dot_order(order)
+            try:
+                yield self
+            finally:
+                self.lib.orc_set_dot_order(0)
+
+        return cm()
+
     # ---- sparse core
     def spmv(self, a: Matrix, x):
         x = _arr(x, np.float64)

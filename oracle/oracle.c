@@ -120,9 +120,30 @@ void orc_spmv_dual(const orc_csr* a, const double* x1, const double* x2, double*
     }
 }
 
+/* Test-only probe of the problem's sensitivity to reduction order: 0 = the reference's forward
+ * sequential sum (default, the pinned oracle); 1 = the same sum taken backwards.  Parity tests
+ * use the oracle's response to order 1 as the rounding floor a parallel reduction must meet. */
+static int g_dot_order = 0;
+void orc_set_dot_order(int order) { g_dot_order = order; }
+
+static double dot_pairwise(int64_t n, const double* a, const double* b) {
+    if (n <= 8) {
+        double acc = 0.0;
+        for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
+        return acc;
+    }
+    const int64_t h = n / 2;
+    return dot_pairwise(h, a, b) + dot_pairwise(n - h, a + h, b + h);
+}
+
 /* src/pcg.cpp:10-16 (same helper in dense.cpp:12-18, condest.cpp:13-19) */
 double orc_dot(int64_t n, const double* a, const double* b) {
     double acc = 0.0;
+    if (g_dot_order == 1) {
+        for (int64_t i = n - 1; i >= 0; --i) acc += a[i] * b[i];
+        return acc;
+    }
+    if (g_dot_order == 2) return dot_pairwise(n, a, b);
     for (int64_t i = 0; i < n; ++i) acc += a[i] * b[i];
     return acc;
 }

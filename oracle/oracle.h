@@ -48,6 +48,9 @@ void orc_uniform_pm1_fill(uint64_t seed, uint64_t skip, int64_t n, double* out);
 void orc_spmv(const orc_csr* a, const double* x, double* y);
 void orc_spmv_dual(const orc_csr* a, const double* x1, const double* x2, double* y1, double* y2);
 double orc_dot(int64_t n, const double* a, const double* b);
+/* test-only: 0 = reference forward summation (default), 1 = reversed, 2 = pairwise tree
+ * (rounding-floor probes of the problem's sensitivity to reduction order) */
+void orc_set_dot_order(int order);
 int orc_diagonal_scale(const orc_csr* a, double* va_out, double* d_inv_sqrt);
 
 /* ---- IC(0) (src/ic_preconditioner.cpp) ---- */

@@ -133,7 +133,13 @@ def test_pcg_matches_oracle(ctx, oracle, probs, name, prec):
                                                   ic=of if kind else None, max_iter=4000).iterations - ro.iterations))
     assert abs(rg.iterations - ro.iterations) <= max(2, 2 * spread)
     if rg.iterations == ro.iterations:
-        tol = _sol_tol(_rel(xp, xo)) if rp.iterations == ro.iterations else 1e-6
+        runs = [(rp, xp)]
+        for order in (1, 2):
+            with oracle.reversed_dots(order):
+                xrv = np.zeros(h.n)
+                runs.append((oracle.pcg_solve(sa, b, xrv, kind=kind, ic=of if kind else None, max_iter=4000), xrv))
+        floors = [_rel(x_, xo) for r_, x_ in runs if r_.iterations == ro.iterations]
+        tol = _sol_tol(max(floors)) if floors else 1e-6
         assert _rel(xg, xo) <= tol, (_rel(xg, xo), tol)
         # relres history drifts with the reduction order; bound it by the oracle's own drift
         # under a rounding-level perturbation of b
@@ -267,17 +273,27 @@ def test_accelerated_solves_given_oracle_basis(ctx, oracle, problems, probs, nam
 
 
 def _oracle_floor(oracle, cfg, h, ores, k):
+    """The oracle's own response to rounding-level changes: b moved by one ulp, and every dot
+    product summed in the opposite order (what a parallel reduction changes)."""
     sa, _ = oracle.diagonal_scale(Matrix.of(h))
     of = oracle.ic0_factorize(sa)
-    b = _ulp_perturb(ores["scaled_rhs"][k])
-    x = np.zeros(h.n)
-    if k == 0:
-        oracle.pcg_solve(sa, b, x, kind=1, ic=of, max_iter=cfg.max_iter)
-    elif cfg.method == "sc":
-        oracle.pcg_solve(sa, b, x, kind=2, ic=of, sc=oracle.basis(sa, ores["w"], 1), max_iter=cfg.max_iter)
-    else:
-        oracle.deflated_pcg_solve(sa, b, x, oracle.basis(sa, ores["w"], 0), kind=1, ic=of, max_iter=cfg.max_iter)
-    return _rel(x, ores["solutions"][k])
+
+    def solve(b):
+        x = np.zeros(h.n)
+        if k == 0:
+            oracle.pcg_solve(sa, b, x, kind=1, ic=of, max_iter=cfg.max_iter)
+        elif cfg.method == "sc":
+            oracle.pcg_solve(sa, b, x, kind=2, ic=of, sc=oracle.basis(sa, ores["w"], 1), max_iter=cfg.max_iter)
+        else:
+            oracle.deflated_pcg_solve(sa, b, x, oracle.basis(sa, ores["w"], 0), kind=1, ic=of,
+                                      max_iter=cfg.max_iter)
+        return x
+
+    floor = _rel(solve(_ulp_perturb(ores["scaled_rhs"][k])), ores["solutions"][k])
+    for order in (1, 2):
+        with oracle.reversed_dots(order):
+            floor = max(floor, _rel(solve(ores["scaled_rhs"][k]), ores["solutions"][k]))
+    return floor
 
 
 def test_c1_full_sequence_golden(ctx, problems):
