@@ -169,12 +169,12 @@ def run_ours(args, rank, world, local_rank):
     m_t = cfg.keep
     # algorithmic bytes per launch
     per_launch = {
-        0: 12 * n_nnz + 20 * n,                       # SpMV q = A p (+ (p,q))
-        1: 12 * nnz_l + 32 * n,                       # forward sweep: L entries, perm+prs, r in, y out
-        2: 12 * nnz_l + 48 * n + 8 * m_t * n,         # backward sweep: U, perm+prs, y, d, z out, W u, r
+        0: 12 * n_nnz + 20 * n,                       # SpMV q = A p (+ (p,q)): PAPER.md:276
+        1: 12 * nnz_l + 24 * n,                       # forward sweep: L entries, perm+prs, r in, y out
+        2: 12 * nnz_l + 48 * n,                       # backward sweep: U, perm+prs, y in+reset, d, z out, r
         4: 8 * m_t * n + 8 * n,                       # W^T r projection
     }
-    names = {0: "spmv (k_spmv_pq)", 1: "ic fwd sweep (k_sweep<false>)", 2: "ic bwd sweep + SC (k_sweep<true>)",
+    names = {0: "spmv (k_spmv_pq)", 1: "ic fwd sweep (k_sweep<false>)", 2: "ic bwd sweep (k_sweep<true>)",
              3: "vector ops", 4: "W^T r (k_tallt)"}
     dom = max((c for c in stats if stats[c][1] > 0), key=lambda c: stats[c][0])
     kernels = {}
@@ -190,10 +190,15 @@ def run_ours(args, rank, world, local_rank):
     roof_c = dom if dom in per_launch else 0
     avg_roof = stats[roof_c][0] / stats[roof_c][1]
     achieved = per_launch[roof_c] / (avg_roof * 1e-3) / 1e9
-    traffic = None
+    traffic = None  # dram bytes per launch from the committed ncu --set full capture (profiles/)
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(names[roof_c])
+    for c, entry_name in names.items():
+        if entry_name in kernels and os.path.exists(tp):
+            t = json.load(open(tp)).get(entry_name)
+            if t:
+                kernels[entry_name]["ncu_dram_bytes"] = t
     line = {
         "metric": METRIC,
         "value": round(iters / (ms / 1e3), 2),
