@@ -227,9 +227,50 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if not args.no_variants:
+        line["variants"] = {"multicolour": measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak)}
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, host, threads=1, reps=1)
     print(json.dumps(line), flush=True)
+
+
+def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
+    """The multicolour-reordered variant (a DIFFERENT operator: IC(0) of P A P^T, SURVEY 8(a)
+    a20), reported separately: same sequence, same timing rules."""
+    import torch
+
+    m, perm, ncolors = problems.multicolour(host)
+    prep = sequence.prepare(ctx, cfg, m, validate=False, new_of_old=perm)
+    dev = torch.device("cuda", ctx.device)
+    b_dev = [torch.from_numpy(sequence.rhs(prep, k)[1]).to(dev) for k in range(cfg.n_rhs)]
+
+    def step():
+        xs = [torch.zeros(m.n, dtype=torch.float64, device=dev) for _ in range(cfg.n_rhs)]
+        return _sequence(api, ctx, prep, cfg, b_dev, xs)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    ctx.synchronize()
+    ctx.set_profiling(True)
+    ctx.reset_stats()
+    ctx.record(4)
+    iters = sum(step() for _ in range(args.steps))
+    ctx.record(5)
+    ms = ctx.elapsed_ms(4, 5)
+    stats = {c: ctx.kernel_stats(c) for c in range(5)}
+    ctx.set_profiling(False)
+    nnz_l = prep.ic.nnz_l
+    sweep = {}
+    for c, b in ((1, 12 * nnz_l + 24 * m.n), (2, 12 * nnz_l + 48 * m.n)):
+        if stats[c][1]:
+            avg = stats[c][0] / stats[c][1]
+            sweep["fwd" if c == 1 else "bwd"] = {"avg_us": round(avg * 1e3, 2),
+                                                 "achieved_gbs": round(b / (avg * 1e-3) / 1e9, 1),
+                                                 "frac": round(b / (avg * 1e-3) / 1e9 / peak, 4)}
+    return {"operator": f"IC(0) of P A P^T, greedy colouring ({ncolors} colours -> {ncolors} sweep levels)",
+            "value": round(iters / (ms / 1e3), 2), "unit": UNIT,
+            "iterations_per_step": iters / args.steps, "ms_per_step": round(ms / args.steps, 3),
+            "time_to_solution_ms_per_rhs": round(ms / args.steps / cfg.n_rhs, 3), "sweeps": sweep}
 
 
 def _sequence(api, ctx, prep, cfg, bs, xs):
@@ -373,6 +414,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the multicolour variant line")
     ap.add_argument("--ref-threads", type=int, default=0)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -234,6 +234,14 @@ void rcg_normal(uint64_t seed, uint64_t skip, int64_t n, double* out);
 void rcg_host_free(void* p);
 /* IC(0) level depth of the natural ordering (diagnostics) */
 int rcg_level_depth(int32_t n, const int32_t* row_start, const int32_t* col_idx, int32_t* depth);
+/* Multicolour variant (a different operator, reported separately): greedy
+ * colouring in natural order (red-black for 7-point, 8 colours for 27-point) and the symmetric
+ * permutation P A P^T with ascending columns.  IC(0) of the permuted matrix has ncolors levels. */
+int rcg_multicolor_order(int32_t n, const int32_t* row_start, const int32_t* col_idx, int32_t* new_of_old,
+                         int32_t* ncolors);
+int rcg_permute_symmetric(int32_t n, const int32_t* row_start, const int32_t* col_idx, const double* values,
+                          const int32_t* new_of_old, int32_t** row_start_out, int32_t** col_idx_out,
+                          double** values_out);
 
 #ifdef __cplusplus
 }

@@ -12,19 +12,26 @@ import numpy as np
 from . import Matrix, Oracle
 
 
-def rhs_set(o: Oracle, cfg, host, a_orig: Matrix, dis):
+def rhs_set(o: Oracle, cfg, host, a_orig: Matrix, dis, new_of_old=None):
     from paper_2203_08498_b200.problems import solution_stream
 
     xs = [solution_stream(cfg, host.n, k) for k in range(cfg.n_rhs)]
+    if new_of_old is not None:  # multicolour variant: the solver sees P A P^T and P x
+        perm = []
+        for x in xs:
+            xp = np.empty_like(x)
+            xp[new_of_old] = x
+            perm.append(xp)
+        xs = perm
     b_orig = [o.spmv(a_orig, x) for x in xs]
     return b_orig, [dis * b for b in b_orig]
 
 
-def run_sequence(o: Oracle, cfg, host, blocks: int = 1, n_solves: int | None = None) -> dict:
+def run_sequence(o: Oracle, cfg, host, blocks: int = 1, n_solves: int | None = None, new_of_old=None) -> dict:
     a_orig = Matrix.of(host)
     a, dis = o.diagonal_scale(a_orig)
     ic = o.ic0_factorize(a, 0.0, blocks)
-    b_orig, bs = rhs_set(o, cfg, host, a_orig, dis)
+    b_orig, bs = rhs_set(o, cfg, host, a_orig, dis, new_of_old)
     n = host.n
     k_t = cfg.n_rhs if n_solves is None else n_solves
     out = {"iterations": [], "converged": [], "histories": [], "solutions": [], "true_relres": [],

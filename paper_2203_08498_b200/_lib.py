@@ -150,6 +150,9 @@ SIGNATURES = {
     "rcg_normal": (None, C.c_uint64, C.c_uint64, C.c_int64, vp),
     "rcg_host_free": (None, vp),
     "rcg_level_depth": (C.c_int, C.c_int32, vp, vp, i32p),
+    "rcg_multicolor_order": (C.c_int, C.c_int32, vp, vp, vp, i32p),
+    "rcg_permute_symmetric": (C.c_int, C.c_int32, vp, vp, vp, vp, C.POINTER(i32p), C.POINTER(i32p),
+                              C.POINTER(dp)),
 }
 
 for _name, (_res, *_args) in SIGNATURES.items():

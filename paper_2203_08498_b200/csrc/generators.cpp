@@ -434,6 +434,67 @@ void rcg_normal(uint64_t seed, uint64_t skip, int64_t n, double* out) {
 
 void rcg_host_free(void* p) { std::free(p); }
 
+// Greedy colouring in natural order (smallest colour unused by earlier neighbours): red-black
+// for the 7-point stencil, 8 colours for the 27-point.  new_of_old[i] = position of row i after
+// sorting by (colour, index).  Returns the colour count.
+int rcg_multicolor_order(int32_t n, const int32_t* row_start, const int32_t* col_idx, int32_t* new_of_old,
+                         int32_t* ncolors) {
+    return guard([&] {
+        std::vector<int32_t> color(n, -1);
+        std::vector<int32_t> mark;
+        int32_t nc = 0;
+        for (int32_t i = 0; i < n; ++i) {
+            for (int32_t p = row_start[i]; p < row_start[i + 1]; ++p) {
+                const int32_t j = col_idx[p];
+                if (j != i && color[j] >= 0) {
+                    if (static_cast<int32_t>(mark.size()) <= color[j]) mark.resize(color[j] + 1, -1);
+                    mark[color[j]] = i;
+                }
+            }
+            int32_t c = 0;
+            while (c < static_cast<int32_t>(mark.size()) && mark[c] == i) ++c;
+            color[i] = c;
+            nc = std::max(nc, c + 1);
+        }
+        std::vector<int64_t> start(nc + 1, 0);
+        for (int32_t i = 0; i < n; ++i) start[color[i] + 1]++;
+        for (int32_t c = 0; c < nc; ++c) start[c + 1] += start[c];
+        for (int32_t i = 0; i < n; ++i) new_of_old[i] = static_cast<int32_t>(start[color[i]]++);
+        *ncolors = nc;
+    });
+}
+
+// B = P A P^T with B[new_of_old[i], new_of_old[j]] = A[i, j]; columns of each row ascending.
+// Output arrays are malloc'ed (free with rcg_host_free).
+int rcg_permute_symmetric(int32_t n, const int32_t* row_start, const int32_t* col_idx, const double* values,
+                          const int32_t* new_of_old, int32_t** rs_out, int32_t** ci_out, double** va_out) {
+    return guard([&] {
+        std::vector<int32_t> old_of_new(n);
+        for (int32_t i = 0; i < n; ++i) old_of_new[new_of_old[i]] = i;
+        const int64_t nnz = row_start[n];
+        std::vector<int32_t> rs(static_cast<size_t>(n) + 1, 0), ci(nnz);
+        std::vector<double> va(nnz);
+        for (int32_t r = 0; r < n; ++r) {
+            const int32_t i = old_of_new[r];
+            rs[r + 1] = rs[r] + (row_start[i + 1] - row_start[i]);
+        }
+        std::vector<std::pair<int32_t, double>> row;
+        for (int32_t r = 0; r < n; ++r) {
+            const int32_t i = old_of_new[r];
+            row.clear();
+            for (int32_t p = row_start[i]; p < row_start[i + 1]; ++p) row.emplace_back(new_of_old[col_idx[p]], values[p]);
+            std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+            for (size_t t = 0; t < row.size(); ++t) {
+                ci[rs[r] + t] = row[t].first;
+                va[rs[r] + t] = row[t].second;
+            }
+        }
+        *rs_out = to_malloc(rs);
+        *ci_out = to_malloc(ci);
+        *va_out = to_malloc(va);
+    });
+}
+
 int rcg_level_depth(int32_t n, const int32_t* row_start, const int32_t* col_idx, int32_t* depth) {
     return guard([&] {
         std::vector<int32_t> lev(n, 0);

@@ -131,6 +131,21 @@ def solution_stream(cfg: Config, n: int, k: int) -> np.ndarray:
     raise ValueError(cfg.rhs)
 
 
+def multicolour(a: HostCsr):
+    """(P A P^T, new_of_old, ncolors) for the multicolour variant (greedy colouring)."""
+    new_of_old = np.empty(a.n, np.int32)
+    nc = C.c_int32()
+    check(lib.rcg_multicolor_order(a.n, a.row_start.ctypes.data, a.col_idx.ctypes.data, new_of_old.ctypes.data,
+                                   C.byref(nc)))
+    rs, ci, va = L.i32p(), L.i32p(), L.dp()
+    check(lib.rcg_permute_symmetric(a.n, a.row_start.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data,
+                                    new_of_old.ctypes.data, C.byref(rs), C.byref(ci), C.byref(va)))
+    nnz = a.nnz
+    b = HostCsr(a.n, _adopt(rs, a.n + 1, C.c_int32, np.int32), _adopt(ci, nnz, C.c_int32, np.int32),
+                _adopt(va, nnz, C.c_double, np.float64))
+    return b, new_of_old, nc.value
+
+
 def level_depth(a: HostCsr) -> int:
     d = C.c_int32()
     check(lib.rcg_level_depth(a.n, a.row_start.ctypes.data, a.col_idx.ctypes.data, C.byref(d)))

@@ -25,21 +25,29 @@ class Prepared:
     dis: np.ndarray
     ic: api.IcFactor
     setup_s: float = 0.0
+    new_of_old: np.ndarray | None = None   # multicolour variant: rows of P A P^T
 
 
-def prepare(ctx: api.Context, cfg: Config, host: HostCsr, validate: bool = True, blocks: int | None = None) -> Prepared:
+def prepare(ctx: api.Context, cfg: Config, host: HostCsr, validate: bool = True, blocks: int | None = None,
+            new_of_old: np.ndarray | None = None) -> Prepared:
+    """`host` is the matrix the solver sees (P A P^T for the multicolour variant, with
+    `new_of_old` the permutation applied to the generator's solution streams)."""
     t0 = time.perf_counter()
     a_orig = api.CsrMatrix(ctx, host.n, host.row_start, host.col_idx, host.values, validate=validate)
     a, dis = api.diagonal_scale(ctx, a_orig)
     scaled = a.values()
     ic = api.IcFactor.factorize(ctx, host.n, host.row_start, host.col_idx, scaled, 0.0,
                                 cfg.blocks if blocks is None else blocks)
-    return Prepared(ctx, cfg, host, a_orig, a, dis, ic, time.perf_counter() - t0)
+    return Prepared(ctx, cfg, host, a_orig, a, dis, ic, time.perf_counter() - t0, new_of_old)
 
 
 def rhs(p: Prepared, k: int) -> tuple[np.ndarray, np.ndarray]:
     """(b_orig, b_scaled) of solve k (0-based): b = A x_k, scaled by D^-1/2 (scaling.cpp:8-12)."""
     x = solution_stream(p.cfg, p.host.n, k)
+    if p.new_of_old is not None:
+        xp = np.empty_like(x)
+        xp[p.new_of_old] = x
+        x = xp
     b = p.a_orig.spmv(x)
     return b, p.dis * b
 

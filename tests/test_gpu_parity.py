@@ -392,3 +392,33 @@ def test_residual_sampling_and_method_b(ctx, oracle, probs):
     assert np.array_equal(oo, og) and np.array_equal(io, ig)
     for s in np.nonzero(oo)[0]:
         assert _rel(sg.slot(s), so.slot(s)) <= SOL_TOL
+
+
+# ---------------------------------------------------------------- multicolour variant (a20)
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_multicolour_sweeps_bitwise(ctx, oracle, problems, probs, name):
+    from paper_2203_08498_b200 import api
+
+    m, perm, nc = problems.multicolour(probs[name])
+    sa, _ = oracle.diagonal_scale(Matrix.of(m))
+    of = oracle.ic0_factorize(sa)
+    gf = api.IcFactor.factorize(ctx, m.n, m.row_start, m.col_idx, sa.va)
+    assert gf.fwd_levels == nc and gf.bwd_levels == nc
+    r = oracle.uniform_pm1(5, 0, m.n)
+    assert np.array_equal(gf.apply(r), oracle.ic_apply(of, r))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_multicolour_sequence_matches_oracle(ctx, oracle, problems, probs, name):
+    from oracle.sequence import run_sequence as oracle_sequence
+    from paper_2203_08498_b200 import sequence
+
+    cfg = problems.SMALL[name]
+    m, perm, nc = problems.multicolour(probs[name])
+    ores = oracle_sequence(oracle, cfg, m, new_of_old=perm)
+    p = sequence.prepare(ctx, cfg, m, new_of_old=perm)
+    gres = sequence.run_sequence(p, ores["scaled_rhs"])
+    assert gres.m_bar == ores["m_bar"] and gres.sampled_iterations == ores["sampled_iterations"]
+    assert np.max(np.abs(gres.ritz_values - ores["ritz_values"]) / np.abs(ores["ritz_values"])) <= RITZ_TOL
+    for gi, oi in zip(gres.iterations, ores["iterations"]):
+        assert abs(gi - oi) <= 2, (gres.iterations, ores["iterations"])
