@@ -28,7 +28,7 @@
 
 namespace rcg {
 
-constexpr int kDepChunk = 16;
+constexpr int kDepChunk = 8;
 
 // Sum of one value per thread over the block; then a two-level deterministic grid reduction
 // keyed by tile: tiles -> groups of kGroup -> total.  Returns true in the block that owns the
@@ -75,7 +75,7 @@ __device__ bool tile_reduce(double v, int tile, int ntiles, SweepArgs& a, double
 // level-sorted order from an atomic ticket until none is left.  Bounding the resident CTAs
 // bounds how many future-level rows spin at once.
 template <bool BWD>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
     __shared__ int s_tile;
     __shared__ double red[32];
     __shared__ double tot;
@@ -99,22 +99,25 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
             } else {
                 s = a.in[row];
             }
-            if (end - beg <= kDepChunk) {
-                // common case: one chunk; the row is published from inside the wait loop, so a
-                // lane never waits for slower lanes of its warp before releasing its dependants
-                const int cnt = end - beg;
+            // Entries in chunks of kDepChunk: all parents of a chunk are loaded together and
+            // the missing ones re-polled together (one L2 round trip after the last parent is
+            // published).  On the last chunk the row is published from inside the wait loop, so
+            // a lane never waits for slower lanes of its warp before releasing its dependants.
+            unsigned spins = 0;
+            for (int32_t e0 = beg;; e0 += kDepChunk) {
+                const int cnt = min(kDepChunk, end - e0);
+                const bool last = e0 + kDepChunk >= end;
                 int32_t col[kDepChunk];
                 double val[kDepChunk], dep[kDepChunk];
 #pragma unroll
                 for (int j = 0; j < kDepChunk; ++j)
                     if (j < cnt) {
-                        col[j] = __ldcs(a.pcol + beg + j);
-                        val[j] = __ldcs(a.pval + beg + j);
+                        col[j] = __ldcs(a.pcol + e0 + j);
+                        val[j] = __ldcs(a.pval + e0 + j);
                     }
 #pragma unroll
                 for (int j = 0; j < kDepChunk; ++j)
                     if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
-                unsigned spins = 0;
                 while (true) {
                     bool missing = false;
 #pragma unroll
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
 #pragma unroll
                         for (int j = 0; j < kDepChunk; ++j)
                             if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
-                        st_relaxed(a.out + row, publishable(s));
+                        if (last) st_relaxed(a.out + row, publishable(s));
                         break;
                     }
                     if (a.backoff_ns) __nanosleep(a.backoff_ns);
@@ -138,48 +141,9 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
                             if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
                     }
                 }
-                if (BWD && a.r) contrib = __dmul_rn(a.r[row], s);
-            } else {
-            for (int32_t e0 = beg; e0 < end; e0 += kDepChunk) {
-                const int cnt = min(kDepChunk, end - e0);
-                int32_t col[kDepChunk];
-                double val[kDepChunk], dep[kDepChunk];
-#pragma unroll
-                for (int j = 0; j < kDepChunk; ++j)
-                    if (j < cnt) {
-                        col[j] = __ldcs(a.pcol + e0 + j);
-                        val[j] = __ldcs(a.pval + e0 + j);
-                    }
-#pragma unroll
-                for (int j = 0; j < kDepChunk; ++j)
-                    if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
-                // re-poll every still-missing dependency of the row together, so the row pays
-                // one L2 round trip after its last parent is published (not one per parent)
-                unsigned spins = 0;
-                while (true) {
-                    bool missing = false;
-#pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
-                        if (j < cnt && is_sentinel(dep[j])) missing = true;
-                    if (!missing) break;
-                    if (a.backoff_ns) __nanosleep(a.backoff_ns);
-#pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
-                        if (j < cnt && is_sentinel(dep[j])) dep[j] = ld_relaxed(a.out + col[j]);
-                    if (++spins == (1u << 24)) {  // bounded: a schedule fault is an error, never a hang
-                        atomicExch(&a.tickets[3], 1);
-#pragma unroll
-                        for (int j = 0; j < kDepChunk; ++j)
-                            if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < kDepChunk; ++j)
-                    if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
+                if (last) break;
             }
-            st_relaxed(a.out + row, publishable(s));
             if (BWD && a.r) contrib = __dmul_rn(a.r[row], s);
-            }
         }
         if (BWD && a.r) {
             if (tile_reduce(contrib, tile, ntiles, a, red, &tot) && threadIdx.x == 0) {

@@ -23,7 +23,7 @@
 
 namespace rcg {
 
-constexpr int kTallKC = 32;   // W^T y columns accumulated per pass in registers
+constexpr int kTallKC = 16;   // W^T y columns accumulated per pass in registers
 
 // ------------------------------------------------------------------ kernels
 // p = z (first iteration) or z + beta p  (src/pcg.cpp:67-71); optionally resets the sweep buffer
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv_pq(SpmvArgs a, DevState* 
 
 // f = B^T y for the k columns of B (k <= kMaxRed), one deterministic grid reduction; the
 // finaliser either solves (L L^T) u = f into `u` (mode 1) or stores f (mode 0).
-__global__ void __launch_bounds__(kStreamThreads) k_tallt(const double* __restrict__ B, int64_t ldb, int k,
+__global__ void __launch_bounds__(kStreamThreads, 4) k_tallt(const double* __restrict__ B, int64_t ldb, int k,
                                                           const double* __restrict__ y, int32_t n,
                                                           double* partials, const double* __restrict__ L,
                                                           double* __restrict__ out, int mode, DevState* st,

@@ -17,8 +17,12 @@ def main():
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     import torch
 
+    mc = name.endswith("mc")
+    name = name[:-2] if mc else name
     cfg = problems.CONFIGS.get(name) or problems.SMALL[name.replace("s_", "")]
     h = problems.generate(cfg)
+    if mc:  # multicolour variant: sweeps have ncolors levels
+        h = problems.multicolour(h)[0]
     ctx = api.Context(0)
     a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values, validate=False)
     sa, dis = api.diagonal_scale(ctx, a)
