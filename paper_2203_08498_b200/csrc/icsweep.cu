@@ -190,7 +190,13 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
-    const int grid = std::max(1, std::min(ntiles, ctx->num_sms * ctx->sweep_bps));
+    // Resident CTAs per SM: a deep DAG (few rows per level) is latency-bound and every extra
+    // spinning CTA only adds L2 polling traffic -> 2; a shallow one (multicolour) is
+    // bandwidth-bound and wants full occupancy -> 8.  RCG_SWEEP_BPS overrides.
+    const int levels = backward ? f->bwd_levels : f->fwd_levels;
+    const int64_t rows_per_level = levels > 0 ? a.npos / levels : a.npos;
+    const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : (rows_per_level >= 65536 ? 8 : 2);
+    const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
     a.backoff_ns = ctx->sweep_backoff_ns;
     KTimer t(ctx, backward ? 2 : 1);
     if (backward)

@@ -158,7 +158,7 @@ struct rcg_ctx {
     std::vector<TimedLaunch> ev_pending;
     std::vector<cudaEvent_t> ev_free;
     cudaEvent_t user_ev[16] = {};
-    int sweep_bps = 4;          // resident sweep CTAs per SM (RCG_SWEEP_BPS)
+    int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
 };
 

@@ -67,8 +67,43 @@ class SequenceResult:
     basis_build_s: float = 0.0
 
 
+def context_pool(p: Prepared, size: int) -> list:
+    """Extra contexts (each its own CUDA stream and workspace) on the same GPU, for running
+    independent solves concurrently; cached on the Prepared problem."""
+    pool = getattr(p, "_pool", None)
+    if pool is None or len(pool) < size:
+        pool = [api.Context(p.ctx.device) for _ in range(size)]
+        p._pool = pool
+    return pool[:size]
+
+
+def run_accelerated(p: Prepared, basis, bs: list, xs: list, concurrency: int = 1) -> list:
+    """Solves 2..k of the sequence (independent given W): SC-PCG or deflated PCG for each
+    (b, x) pair.  With concurrency > 1 the solves run on separate contexts/streams from a thread
+    pool (the C-ABI releases the GIL), so their latency-bound sweeps overlap on the GPU; each
+    solve's arithmetic is unchanged."""
+    cfg = p.cfg
+
+    def one(ctx, b, x):
+        if basis is None:
+            return api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x, cfg.eps, cfg.max_iter)
+        if cfg.method == "sc":
+            return api.pcg_solve(ctx, p.a, b, api.Sc(basis, p.ic), x, cfg.eps, cfg.max_iter)
+        return api.deflated_pcg_solve(ctx, p.a, b, api.Ic(p.ic), basis, x, cfg.eps, cfg.max_iter)
+
+    if concurrency <= 1:
+        return [one(p.ctx, b, x) for b, x in zip(bs, xs)]
+    from concurrent.futures import ThreadPoolExecutor
+
+    pool = context_pool(p, min(concurrency, len(bs)))
+    p.ctx.synchronize()
+    with ThreadPoolExecutor(max_workers=len(pool)) as ex:
+        futs = [ex.submit(one, pool[i % len(pool)], b, x) for i, (b, x) in enumerate(zip(bs, xs))]
+        return [f.result() for f in futs]
+
+
 def run_sequence(p: Prepared, rhs_scaled: list, rhs_orig: list | None = None, n_solves: int | None = None,
-                 keep_solutions: bool = True) -> SequenceResult:
+                 keep_solutions: bool = True, concurrency: int = 1) -> SequenceResult:
     ctx, cfg, n = p.ctx, p.cfg, p.host.n
     k_t = len(rhs_scaled) if n_solves is None else n_solves
     res = SequenceResult()
@@ -84,14 +119,9 @@ def run_sequence(p: Prepared, rhs_scaled: list, rhs_orig: list | None = None, n_
     res.m_bar, res.m_tilde, res.ritz_values = m_bar, w.k, vals
     basis = api.Basis(ctx, p.a, w, "sc" if cfg.method == "sc" else "deflation") if w.k > 0 else None
     res.basis_build_s = time.perf_counter() - t0
-    for k in range(1, k_t):
-        xk = np.zeros(n)
-        if basis is None:
-            rk = api.pcg_solve(ctx, p.a, rhs_scaled[k], api.Ic(p.ic), xk, cfg.eps, cfg.max_iter)
-        elif cfg.method == "sc":
-            rk = api.pcg_solve(ctx, p.a, rhs_scaled[k], api.Sc(basis, p.ic), xk, cfg.eps, cfg.max_iter)
-        else:
-            rk = api.deflated_pcg_solve(ctx, p.a, rhs_scaled[k], api.Ic(p.ic), basis, xk, cfg.eps, cfg.max_iter)
+    xs = [np.zeros(n) for _ in range(1, k_t)]
+    reps = run_accelerated(p, basis, rhs_scaled[1:k_t], xs, concurrency)
+    for k, (rk, xk) in enumerate(zip(reps, xs), start=1):
         _record(p, res, rk, xk, rhs_orig[k] if rhs_orig else None, keep_solutions)
     return res
 
