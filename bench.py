@@ -152,6 +152,10 @@ def run_ours(args, rank, world, local_rank):
         stats[c] = (sum(t for t, _ in per), sum(n_ for _, n_ in per))
     for c_ in ctxs:
         c_.set_profiling(False)
+    # phase breakdown of one extra (untimed) step
+    phases = {}
+    _sequence(api, ctx, prep, cfg, b_dev, [torch.zeros(n, dtype=torch.float64, device=dev) for _ in b_dev],
+              phases=phases)
     # e2e through the public API with host buffers
     for _ in range(max(1, args.warmup // 2)):
         step_e2e()
@@ -232,6 +236,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": names[roof_c], "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src},
         "kernels": kernels,
+        "phases_ms_untimed_step": phases,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -288,22 +293,31 @@ def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
             "time_to_solution_ms_per_rhs": round(ms / args.steps / cfg.n_rhs, 3), "sweeps": sweep}
 
 
-CONCURRENCY = 9  # solves 2..10 of C2 run on their own streams (sequence.run_accelerated)
+CONCURRENCY = int(os.environ.get("RCG_CONCURRENCY", "9"))  # solves 2..10 on their own streams
 
 
-def _sequence(api, ctx, prep, cfg, bs, xs, concurrency=None):
-    """One full sequence; returns its PCG iteration count."""
+def _sequence(api, ctx, prep, cfg, bs, xs, concurrency=None, phases=None):
+    """One full sequence; returns its PCG iteration count (phases: optional dict of wall ms)."""
     from paper_2203_08498_b200 import sequence
 
     n = prep.host.n
+    t0 = time.perf_counter()
     sampler = api.SamplerState.method_a(ctx, cfg.sampler_m, cfg.max_iter, n)
     r = api.pcg_solve(ctx, prep.a, bs[0], api.Ic(prep.ic), xs[0], cfg.eps, cfg.max_iter, observer=sampler)
     total = r.iterations
+    t1 = time.perf_counter()
     errors = api.harvest_errors(ctx, xs[0], sampler)
     _, _, _, w = api.build_aux_matrix(ctx, prep.a, errors, 1e-3, keep_count=cfg.keep)
     basis = api.Basis(ctx, prep.a, w, "sc" if cfg.method == "sc" else "deflation")
+    ctx.synchronize()
+    t2 = time.perf_counter()
     reps = sequence.run_accelerated(prep, basis, bs[1:], xs[1:], CONCURRENCY if concurrency is None else concurrency)
     ctx.synchronize()
+    t3 = time.perf_counter()
+    if phases is not None:
+        phases.update(solve1_ms=round((t1 - t0) * 1e3, 2), solve1_iterations=total,
+                      rr_basis_ms=round((t2 - t1) * 1e3, 2), accelerated_ms=round((t3 - t2) * 1e3, 2),
+                      accelerated_iterations=[r.iterations for r in reps])
     return total + sum(r.iterations for r in reps)
 
 

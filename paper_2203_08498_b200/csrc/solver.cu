@@ -30,7 +30,7 @@ constexpr int kTallKC = 16;   // W^T y columns accumulated per pass in registers
 // With W != null (IC inner + subspace correction) z_i = z_ic,i + sum_j u_j W_ij first, in the
 // reference's accumulation order (src/subspace_correction.cpp:53-56).
 __global__ void __launch_bounds__(kStreamThreads) k_pupdate(const double* __restrict__ z, double* __restrict__ p,
-                                                            double* __restrict__ zs_reset, int32_t n, DevState* st,
+                                                            double* __restrict__ zs_reset, double* __restrict__ y_reset, int32_t n, DevState* st,
                                                             const double* __restrict__ W, int64_t ldw, int k,
                                                             const double* __restrict__ u) {
     if (st->done) return;
@@ -41,7 +41,10 @@ __global__ void __launch_bounds__(kStreamThreads) k_pupdate(const double* __rest
         if (W)
             for (int j = 0; j < k; ++j) zi = fadd_mul(zi, __ldg(u + j), __ldg(W + j * ldw + i));
         p[i] = first ? zi : fadd_mul(zi, beta, p[i]);
-        if (zs_reset) zs_reset[i] = sentinel();
+        if (zs_reset) {  // both sweep buffers back to the sentinel for the next iteration
+            zs_reset[i] = sentinel();
+            y_reset[i] = sentinel();
+        }
     }
 }
 
@@ -518,7 +521,7 @@ struct Solve {
             launch_sweep(ctx, m->ic, false, fa);
             SweepArgs ba = sweep_args(ctx, m->ic, true);
             ba.in = w.ybuf;
-            ba.in_reset = w.ybuf;
+
             ba.out = w.zs;
             ba.r = w.r;
             ba.add_sc = sc ? 1 : 0;
@@ -534,7 +537,7 @@ struct Solve {
             // IC + SC: z = z_ic + W u is formed here, coalesced, instead of inside the sweep
             KTimer t(ctx, 3);
             const bool fold = ic && sc;
-            k_pupdate<<<sg, kStreamThreads, 0, ctx->stream>>>(z, w.p, ic ? w.zs : nullptr, n, st,
+            k_pupdate<<<sg, kStreamThreads, 0, ctx->stream>>>(z, w.p, ic ? w.zs : nullptr, w.ybuf, n, st,
                                                                fold ? scb->w : nullptr, fold ? scb->ld : 0,
                                                                fold ? scb->k : 0, w.u2);
             RCG_LAUNCHED(ctx);

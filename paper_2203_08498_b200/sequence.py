@@ -93,12 +93,24 @@ def run_accelerated(p: Prepared, basis, bs: list, xs: list, concurrency: int = 1
 
     if concurrency <= 1:
         return [one(p.ctx, b, x) for b, x in zip(bs, xs)]
+    import queue
     from concurrent.futures import ThreadPoolExecutor
 
     pool = context_pool(p, min(concurrency, len(bs)))
+    free = queue.Queue()
+    for c in pool:
+        free.put(c)
+
+    def checked_out(b, x):
+        ctx = free.get()  # a context (stream + workspace) is owned by one solve at a time
+        try:
+            return one(ctx, b, x)
+        finally:
+            free.put(ctx)
+
     p.ctx.synchronize()
     with ThreadPoolExecutor(max_workers=len(pool)) as ex:
-        futs = [ex.submit(one, pool[i % len(pool)], b, x) for i, (b, x) in enumerate(zip(bs, xs))]
+        futs = [ex.submit(checked_out, b, x) for b, x in zip(bs, xs)]
         return [f.result() for f in futs]
 
 
