@@ -217,9 +217,8 @@ int rcg_ctx_create(int device, rcg_ctx** out) {
         auto* c = new rcg_ctx();
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
-        if (const char* e = std::getenv("RCG_SWEEP_BPS")) c->sweep_bps = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("RCG_SWEEP_BPS")) c->sweep_bps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("RCG_SWEEP_BACKOFF_NS")) c->sweep_backoff_ns = std::max(0, std::atoi(e));
-        if (const char* e = std::getenv("RCG_SWEEP_SKIP")) c->sweep_skip = std::atoi(e) != 0;
         RCG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         RCG_CK(cudaEventCreate(&c->ev0));
         RCG_CK(cudaEventCreate(&c->ev1));

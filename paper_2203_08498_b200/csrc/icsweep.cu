@@ -29,8 +29,6 @@
 namespace rcg {
 
 constexpr int kDepChunk = 8;
-constexpr int kSkipOwn = 8;    // level skipping: max entries of a row and of each recomputed parent
-constexpr int kSkipPoll = 16;  // level skipping: max values a skipping row polls
 
 // Sum of one value per thread over the block; then a two-level deterministic grid reduction
 // keyed by tile: tiles -> groups of kGroup -> total.  Returns true in the block that owns the
@@ -73,63 +71,6 @@ __device__ bool tile_reduce(double v, int tile, int ntiles, SweepArgs& a, double
     return true;
 }
 
-// Level skipping.  The row recomputes each parent flagged in `mask` (all on level l-1) from
-// that parent's own entries and start value -- the exact arithmetic the parent's lane performs,
-// so the value is bitwise identical -- and therefore waits only on rows of level <= l-2.  The
-// values it needs (grandparents and its unflagged parents) are polled together.
-template <bool BWD>
-__device__ __noinline__ double row_skip(const SweepArgs& a, int32_t beg, int32_t end, uint8_t mask, double s) {
-    const int cnt = end - beg;  // <= kSkipOwn (host-checked)
-    int32_t ocol[kSkipOwn];
-    double oval[kSkipOwn], part[kSkipOwn];
-    int dix[kSkipOwn];
-    int32_t pc[kSkipPoll];
-    double pv[kSkipPoll], pd[kSkipPoll];
-    int owner[kSkipPoll];
-    int np = 0;
-    for (int j = 0; j < cnt; ++j) {
-        ocol[j] = __ldcs(a.pcol + beg + j);
-        oval[j] = __ldcs(a.pval + beg + j);
-    }
-    for (int j = 0; j < cnt; ++j) {
-        const int32_t c = ocol[j];
-        if (mask & (1u << j)) {
-            const int32_t pp = __ldg(a.ipos + c);
-            const int32_t pb = __ldg(a.prs + pp), pe = __ldg(a.prs + pp + 1);
-            part[j] = BWD ? __ddiv_rn(a.in[c], __ldg(a.d + c)) : a.in[c];
-            for (int32_t m = pb; m < pe; ++m, ++np) {
-                pc[np] = __ldcs(a.pcol + m);
-                pv[np] = __ldcs(a.pval + m);
-                owner[np] = j;
-            }
-        } else {
-            pc[np] = c;
-            owner[np] = -1;
-            dix[j] = np++;
-        }
-    }
-    for (int e = 0; e < np; ++e) pd[e] = ld_relaxed(a.out + pc[e]);
-    unsigned spins = 0;
-    while (true) {
-        bool missing = false;
-        for (int e = 0; e < np; ++e) missing |= is_sentinel(pd[e]);
-        if (!missing) break;
-        for (int e = 0; e < np; ++e)
-            if (is_sentinel(pd[e])) pd[e] = ld_relaxed(a.out + pc[e]);
-        if (++spins == (1u << 24)) {  // bounded: a schedule fault is an error, never a hang
-            atomicExch(&a.tickets[3], 1);
-            for (int e = 0; e < np; ++e)
-                if (is_sentinel(pd[e])) pd[e] = 0.0;
-        }
-    }
-    // parents first (entries of each parent are contiguous and in its reference order) ...
-    for (int e = 0; e < np; ++e)
-        if (owner[e] >= 0) part[owner[e]] = fsub_mul(part[owner[e]], pv[e], pd[e]);
-    // ... then the row itself, in its own entry order
-    for (int j = 0; j < cnt; ++j) s = fsub_mul(s, oval[j], (mask & (1u << j)) ? part[j] : pd[dix[j]]);
-    return s;
-}
-
 // Persistent sweep: a grid of at most (SMs x blocks_per_sm) CTAs pulls 128-row tiles of the
 // level-sorted order from an atomic ticket until none is left.  Bounding the resident CTAs
 // bounds how many future-level rows spin at once.
@@ -157,11 +98,6 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
             } else {
                 s = a.in[row];
             }
-            const uint8_t mask = a.pskip ? __ldg(a.pskip + pos) : 0;
-            if (mask) {
-                s = row_skip<BWD>(a, beg, end, mask, s);
-                st_relaxed(a.out + row, publishable(s));
-            } else {
             // Entries in chunks of kDepChunk: all parents of a chunk are loaded together and
             // the missing ones re-polled together (one L2 round trip after the last parent is
             // published).  On the last chunk the row is published from inside the wait loop, so
@@ -206,7 +142,6 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
                 }
                 if (last) break;
             }
-            }
             if (BWD && a.r) contrib = __dmul_rn(a.r[row], s);
         }
         if (BWD && a.r) {
@@ -239,8 +174,7 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
     a.prs = backward ? f->b_prs : f->f_prs;
     a.pcol = backward ? f->b_col : f->f_col;
     a.pval = backward ? f->b_val : f->f_val;
-    a.pskip = backward ? f->b_skip : f->f_skip;
-    a.ipos = backward ? f->b_ipos : f->f_ipos;
+    a.pcrit = backward ? f->b_crit : f->f_crit;
     a.d = f->d;
     a.n = f->n;
     a.npos = backward ? f->b_npos : f->f_npos;
@@ -263,7 +197,6 @@ void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : (rows_per_level >= 65536 ? 8 : 2);
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
     a.backoff_ns = ctx->sweep_backoff_ns;
-    if (!ctx->sweep_skip) a.pskip = nullptr;  // RCG_SWEEP_SKIP=0: plain level order (A/B runs)
     KTimer t(ctx, backward ? 2 : 1);
     if (backward)
         k_sweep<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
@@ -328,7 +261,7 @@ static T* upload(rcg_ctx* ctx, const std::vector<T>& h) {
 static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vector<int32_t>& col,
                               const std::vector<double>& val, bool descending, std::vector<int32_t>& perm,
                               std::vector<int32_t>& prs, std::vector<int32_t>& pcol, std::vector<double>& pval,
-                              std::vector<uint8_t>& skip, std::vector<int32_t>& ipos, int32_t& npos) {
+                              std::vector<uint8_t>& crit, int32_t& npos) {
     std::vector<int32_t> level(n, 0);
     int32_t nlev = 0;
     for (int32_t t = 0; t < n; ++t) {
@@ -358,63 +291,41 @@ static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const s
     }
     pcol.resize(col.size());
     pval.resize(val.size());
-    ipos.assign(n, 0);
+    crit.assign(total, 0);
     for (int64_t pos = 0; pos < total; ++pos) {
         const int32_t i = perm[pos];
         if (i < 0) continue;
-        ipos[i] = static_cast<int32_t>(pos);
         std::copy(col.begin() + rs[i], col.begin() + rs[i + 1], pcol.begin() + prs[pos]);
         std::copy(val.begin() + rs[i], val.begin() + rs[i + 1], pval.begin() + prs[pos]);
-    }
-    // Level skipping: a row whose parents on level l-1 are all small recomputes them itself
-    // from their own parents (levels <= l-2), so it no longer waits for level l-1.  mask bit j
-    // = recompute the parent of entry j.  Rows that cannot skip keep mask 0.
-    skip.assign(total, 0);
-    for (int64_t pos = 0; pos < total; ++pos) {
-        const int32_t i = perm[pos];
-        if (i < 0) continue;
-        const int32_t cnt = rs[i + 1] - rs[i];
-        if (cnt == 0 || cnt > kSkipOwn) continue;
-        uint8_t mask = 0;
-        int polls = 0;
-        bool ok = true;
-        for (int32_t p = rs[i]; p < rs[i + 1] && ok; ++p) {
-            const int32_t c = col[p];
-            if (level[c] == level[i] - 1) {
-                const int32_t pc = rs[c + 1] - rs[c];
-                if (pc > kSkipOwn) ok = false;
-                mask |= static_cast<uint8_t>(1u << (p - rs[i]));
-                polls += pc;
-            } else {
-                polls += 1;
+        int32_t best = -1;
+        for (int32_t p = rs[i]; p < rs[i + 1]; ++p)
+            if (p - rs[i] < 255 && level[col[p]] >= best) {
+                best = level[col[p]];
+                crit[pos] = static_cast<uint8_t>(p - rs[i]);
             }
-        }
-        if (ok && mask && polls <= kSkipPoll) skip[pos] = mask;
     }
     return nlev;
 }
 
 static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
-    std::vector<int32_t> perm, prs, pcol, ipos;
+    std::vector<int32_t> perm, prs, pcol;
     std::vector<double> pval;
-    std::vector<uint8_t> skip;
-    f->fwd_levels = build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval, skip, ipos,
-                                   f->f_npos);
+    std::vector<uint8_t> crit;
+    f->fwd_levels =
+        build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval, crit, f->f_npos);
     f->f_perm = upload(ctx, perm);
     f->f_prs = upload(ctx, prs);
     f->f_col = upload(ctx, pcol);
     f->f_val = upload(ctx, pval);
-    f->f_skip = upload(ctx, skip);
-    f->f_ipos = upload(ctx, ipos);
+    f->f_crit = upload(ctx, crit);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    f->bwd_levels = build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval, skip, ipos,
-                                   f->b_npos);
+    f->bwd_levels =
+        build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval, crit, f->b_npos);
     f->b_perm = upload(ctx, perm);
     f->b_prs = upload(ctx, prs);
     f->b_col = upload(ctx, pcol);
     f->b_val = upload(ctx, pval);
-    f->b_skip = upload(ctx, skip);
-    f->b_ipos = upload(ctx, ipos);
+    f->b_crit = upload(ctx, crit);
     f->d = upload(ctx, f->h_d);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
 }
@@ -577,8 +488,8 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
-                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->f_skip,
-                    (void*)f->b_skip, (void*)f->f_ipos, (void*)f->b_ipos})
+                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->f_crit,
+                    (void*)f->b_crit})
         dev_free(p);
     delete f;
 }

@@ -160,7 +160,6 @@ struct rcg_ctx {
     cudaEvent_t user_ev[16] = {};
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
-    int sweep_skip = 1;         // level skipping on (RCG_SWEEP_SKIP)
 };
 
 struct rcg_matrix {
@@ -182,8 +181,7 @@ struct rcg_ic {
     // device schedules
     int32_t fwd_levels = 0, bwd_levels = 0;
     int32_t f_npos = 0, b_npos = 0;   // schedule lengths with each level padded to a warp multiple
-    uint8_t *f_skip = nullptr, *b_skip = nullptr;   // level-skip masks per position
-    int32_t *f_ipos = nullptr, *b_ipos = nullptr;   // schedule position of each row
+    uint8_t *f_crit = nullptr, *b_crit = nullptr;
     int32_t *f_perm = nullptr, *f_prs = nullptr, *f_col = nullptr;
     double* f_val = nullptr;
     int32_t *b_perm = nullptr, *b_prs = nullptr, *b_col = nullptr;

@@ -21,8 +21,7 @@ struct SweepArgs {
     const int32_t* prs;    // position-indexed row starts
     const int32_t* pcol;   // original column indices, reference entry order
     const double* pval;
-    const uint8_t* pskip;  // per position: bit j = recompute the level-(l-1) parent of entry j
-    const int32_t* ipos;   // schedule position of each row
+    const uint8_t* pcrit;  // per position: entry index of the highest-level parent (spin target)
     const double* d;       // pivots (backward)
     int32_t n;
     int32_t npos;          // level-padded length of the schedule (multiple of 32 per level)
