@@ -70,6 +70,7 @@ constexpr int kSpmvThreads = 256;     // 8 warps, one 32-row tile per warp at a 
 constexpr int kSpmvChunk = 256;       // smem staging entries per warp
 constexpr int kMaxRed = 160;          // max values reduced by one kernel (2*128 tall + scalars)
 constexpr int kGroup = 64;            // sweep tiles per first-level reduction group
+constexpr int kCsrPad = 8;            // zero entries after the CSR arrays (aligned bulk copies)
 constexpr unsigned long long kSentinelBits = 0x7FF4DEADBEEF0001ULL;  // "not yet computed"
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
@@ -168,7 +169,7 @@ struct rcg_matrix {
     int32_t* rs = nullptr;
     int32_t* ci = nullptr;
     double* va = nullptr;
-    double max_row_nnz = 0;
+    int cap = 256;  // pipelined SpMV stage capacity (entries)
 };
 
 struct rcg_ic {

@@ -40,6 +40,9 @@ struct SweepArgs {
 
 int spmv_grid(const rcg_ctx* ctx, int32_t n);
 int stream_grid(const rcg_ctx* ctx, int64_t n);
+size_t spmv_smem(const rcg_matrix* a);
+void spmv_prepare_kernels();
+int tile_capacity(int32_t n, const int32_t* rs);
 void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const double* x, double* r);
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
 SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward);

@@ -19,6 +19,7 @@
 
 #include "internal.cuh"
 #include "kernels.cuh"
+#include "spmv_pipe.cuh"
 #include "vec.cuh"
 
 namespace rcg {
@@ -51,51 +52,20 @@ __global__ void __launch_bounds__(kStreamThreads) k_pupdate(const double* __rest
 // q = A p [, v' = A v]  with (p,q) [, (v,v'), (v',v')] partials; finaliser: alpha (or only
 // records the dots when the deflated path still has to project q)
 template <int NV>
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv_pq(SpmvArgs a, DevState* st, int project_later) {
-    __shared__ double sv[kSpmvThreads / 32][kSpmvChunk];
-    __shared__ int32_t sc[kSpmvThreads / 32][kSpmvChunk];
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv_pq(SpmvArgs a, int cap, DevState* st, int project_later) {
     __shared__ double red[3 * 32];
     __shared__ double tot[3];
     if (st->done) return;
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = (a.n + 31) / 32;
-    const int nw = gridDim.x * (kSpmvThreads / 32);
     double acc3[3] = {0.0, 0.0, 0.0};
-    for (int t = blockIdx.x * (kSpmvThreads / 32) + wid; t < ntiles; t += nw) {
-        const int32_t r0 = t * 32, row = r0 + lane, rend = min(r0 + 32, a.n);
-        const int32_t e0 = __ldg(a.rs + r0), e1 = __ldg(a.rs + rend);
-        const int32_t my_b = row < a.n ? __ldg(a.rs + row) : e1;
-        const int32_t my_e = row < a.n ? __ldg(a.rs + row + 1) : e1;
-        double s[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) s[v] = 0.0;
-        for (int32_t c0 = e0; c0 < e1; c0 += kSpmvChunk) {
-            const int32_t c1 = min(c0 + kSpmvChunk, e1);
-            __syncwarp();
-#pragma unroll 8
-            for (int32_t e = c0 + lane; e < c1; e += 32) {
-                sv[wid][e - c0] = __ldcs(a.va + e);
-                sc[wid][e - c0] = __ldcs(a.ci + e);
-            }
-            __syncwarp();
-            const int32_t bb = max(my_b, c0), en = min(my_e, c1);
-            for (int32_t e = bb; e < en; ++e) {
-                const double av = sv[wid][e - c0];
-                const int32_t c = sc[wid][e - c0];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) s[v] = fadd_mul(s[v], av, __ldg(a.x[v] + c));
-            }
+    spmv_pipeline<NV>(a, cap, [&](int32_t row, const double (&s)[NV]) {
+        a.y[0][row] = s[0];
+        if (!project_later) acc3[0] = fadd_mul(acc3[0], a.x[0][row], s[0]);
+        if (NV == 2) {
+            a.y[1][row] = s[NV - 1];
+            acc3[1] = fadd_mul(acc3[1], a.x[NV - 1][row], s[NV - 1]);
+            acc3[2] = fadd_mul(acc3[2], s[NV - 1], s[NV - 1]);
         }
-        if (row < a.n) {
-            a.y[0][row] = s[0];
-            if (!project_later) acc3[0] = fadd_mul(acc3[0], a.x[0][row], s[0]);
-            if (NV == 2) {
-                a.y[1][row] = s[NV - 1];
-                acc3[1] = fadd_mul(acc3[1], a.x[NV - 1][row], s[NV - 1]);
-                acc3[2] = fadd_mul(acc3[2], s[NV - 1], s[NV - 1]);
-            }
-        }
-    }
+    });
     block_sum<3>(acc3, red);
     if (grid_reduce<3>(acc3, a.partials, blockIdx.x, gridDim.x, &st->tick[1], tot, red) && threadIdx.x == 0) {
         if (NV == 2) {  // power step (src/condest.cpp:86-92): quotient, then ||v'||
@@ -429,6 +399,13 @@ struct Solve {
         ensure_workspace(ctx, n, k, max_iter, red, ngroups, smp ? smp->m : 1);
         sg = stream_grid(ctx, n);
         pg = spmv_grid(ctx, n);
+        static bool smem_ok = false;
+        if (!smem_ok) {
+            spmv_prepare_kernels();
+            allow_smem(reinterpret_cast<const void*>(k_spmv_pq<1>));
+            allow_smem(reinterpret_cast<const void*>(k_spmv_pq<2>));
+            smem_ok = true;
+        }
     }
 
     XrArgs xr_args() {
@@ -556,9 +533,9 @@ struct Solve {
             if (condest) {
                 sa.x[1] = w.v;
                 sa.y[1] = w.vnext;
-                k_spmv_pq<2><<<pg, kSpmvThreads, 0, ctx->stream>>>(sa, st, dfl ? 1 : 0);
+                k_spmv_pq<2><<<pg, kSpmvThreads, spmv_smem(a), ctx->stream>>>(sa, a->cap, st, dfl ? 1 : 0);
             } else {
-                k_spmv_pq<1><<<pg, kSpmvThreads, 0, ctx->stream>>>(sa, st, dfl ? 1 : 0);
+                k_spmv_pq<1><<<pg, kSpmvThreads, spmv_smem(a), ctx->stream>>>(sa, a->cap, st, dfl ? 1 : 0);
             }
             RCG_LAUNCHED(ctx);
         }

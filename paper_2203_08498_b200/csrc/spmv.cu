@@ -13,92 +13,32 @@
 
 #include "internal.cuh"
 #include "kernels.cuh"
+#include "spmv_pipe.cuh"
 
 namespace rcg {
 
-// ------------------------------------------------------------------ generic row-tile engine
-// NV right-hand sides processed together (each output bitwise equal to a single spmv).
-template <int NV>
-struct RowAcc {
-    double s[NV];
-};
-
-template <int NV>
-__device__ __forceinline__ void tile_rows(const int32_t* __restrict__ rs, const int32_t* __restrict__ ci,
-                                          const double* __restrict__ va, int32_t n, int tile,
-                                          const double* const* __restrict__ x, int64_t ldx_unused,
-                                          double* sv, int32_t* sc, RowAcc<NV>& acc, int32_t& row) {
-    (void)ldx_unused;
-    const int lane = threadIdx.x & 31;
-    const int32_t r0 = tile * 32;
-    row = r0 + lane;
-    const int32_t rend = min(r0 + 32, n);
-    const int32_t e0 = __ldg(rs + r0), e1 = __ldg(rs + rend);
-    const int32_t my_b = row < n ? __ldg(rs + row) : e1;
-    const int32_t my_e = row < n ? __ldg(rs + row + 1) : e1;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) acc.s[v] = 0.0;
-    for (int32_t c0 = e0; c0 < e1; c0 += kSpmvChunk) {
-        const int32_t c1 = min(c0 + kSpmvChunk, e1);
-        __syncwarp();
-#pragma unroll 8
-        for (int32_t e = c0 + lane; e < c1; e += 32) {
-            sv[e - c0] = __ldcs(va + e);
-            sc[e - c0] = __ldcs(ci + e);
-        }
-        __syncwarp();
-        const int32_t b = max(my_b, c0), en = min(my_e, c1);
-        for (int32_t e = b; e < en; ++e) {
-            const double a = sv[e - c0];
-            const int32_t c = sc[e - c0];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc.s[v] = fadd_mul(acc.s[v], a, __ldg(x[v] + c));
-        }
-    }
-}
-
 // y_v = A x_v for NV vectors (plain spmv / spmv_dual)
 template <int NV>
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv(SpmvArgs a) {
-    __shared__ double sv[kSpmvThreads / 32][kSpmvChunk];
-    __shared__ int32_t sc[kSpmvThreads / 32][kSpmvChunk];
-    const int wid = threadIdx.x >> 5;
-    const int ntiles = (a.n + 31) / 32;
-    const int nw = gridDim.x * (kSpmvThreads / 32);
-    for (int t = blockIdx.x * (kSpmvThreads / 32) + wid; t < ntiles; t += nw) {
-        RowAcc<NV> acc;
-        int32_t row;
-        tile_rows<NV>(a.rs, a.ci, a.va, a.n, t, a.x, 0, sv[wid], sc[wid], acc, row);
-        if (row < a.n) {
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv(SpmvArgs a, int cap) {
+    spmv_pipeline<NV>(a, cap, [&](int32_t row, const double (&acc)[NV]) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) a.y[v][row] = acc.s[v];
-        }
-    }
+        for (int v = 0; v < NV; ++v) a.y[v][row] = acc[v];
+    });
 }
 
 // r = b - A x (src/pcg.cpp:50-52: spmv then r[i] = b[i] - r[i]); partials of (b,b) and (r,r)
-__global__ void __launch_bounds__(kSpmvThreads) k_residual(SpmvArgs a, const double* __restrict__ b,
+__global__ void __launch_bounds__(kSpmvThreads) k_residual(SpmvArgs a, int cap, const double* __restrict__ b,
                                                            DevState* st) {
-    __shared__ double sv[kSpmvThreads / 32][kSpmvChunk];
-    __shared__ int32_t sc[kSpmvThreads / 32][kSpmvChunk];
     __shared__ double red[2 * 32];
     __shared__ double tot[2];
-    const int wid = threadIdx.x >> 5;
-    const int ntiles = (a.n + 31) / 32;
-    const int nw = gridDim.x * (kSpmvThreads / 32);
     double acc2[2] = {0.0, 0.0};
-    for (int t = blockIdx.x * (kSpmvThreads / 32) + wid; t < ntiles; t += nw) {
-        RowAcc<1> acc;
-        int32_t row;
-        tile_rows<1>(a.rs, a.ci, a.va, a.n, t, a.x, 0, sv[wid], sc[wid], acc, row);
-        if (row < a.n) {
-            const double bi = b[row];
-            const double ri = __dsub_rn(bi, acc.s[0]);
-            a.y[0][row] = ri;
-            acc2[0] = fadd_mul(acc2[0], bi, bi);
-            acc2[1] = fadd_mul(acc2[1], ri, ri);
-        }
-    }
+    spmv_pipeline<1>(a, cap, [&](int32_t row, const double (&acc)[1]) {
+        const double bi = b[row];
+        const double ri = __dsub_rn(bi, acc[0]);
+        a.y[0][row] = ri;
+        acc2[0] = fadd_mul(acc2[0], bi, bi);
+        acc2[1] = fadd_mul(acc2[1], ri, ri);
+    });
     block_sum<2>(acc2, red);
     if (grid_reduce<2>(acc2, a.partials, blockIdx.x, gridDim.x, &st->tick[0], tot, red)) {
         if (threadIdx.x == 0) {
@@ -189,8 +129,31 @@ __global__ void k_fill_bits(double* p, int64_t n, unsigned long long bits) {
 // ------------------------------------------------------------------ launchers
 int spmv_grid(const rcg_ctx* ctx, int32_t n) {
     const int tiles = (n + 31) / 32;
-    const int blocks = (tiles + 7) / 8;
+    const int blocks = (tiles + kPipeWarps - 1) / kPipeWarps;
     return std::max(1, std::min(blocks, ctx->num_sms * 8));
+}
+
+// dynamic shared memory of the pipelined SpMV kernels (raises the opt-in limit once per kernel)
+size_t spmv_smem(const rcg_matrix* a) { return pipe_smem_bytes(a->cap); }
+
+// opt-in dynamic shared memory up to the per-block limit minus the kernel's static usage
+void allow_smem(const void* kernel) {
+    int dev = 0, optin = 0;
+    RCG_CK(cudaGetDevice(&dev));
+    RCG_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    RCG_CK(cudaFuncGetAttributes(&fa, kernel));
+    RCG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - static_cast<int>(fa.sharedSizeBytes)));
+}
+
+void spmv_prepare_kernels() {
+    static bool done = false;
+    if (done) return;
+    allow_smem(reinterpret_cast<const void*>(k_spmv<1>));
+    allow_smem(reinterpret_cast<const void*>(k_spmv<2>));
+    allow_smem(reinterpret_cast<const void*>(k_residual));
+    done = true;
 }
 
 int stream_grid(const rcg_ctx* ctx, int64_t n) {
@@ -213,7 +176,8 @@ void launch_spmv(rcg_ctx* ctx, const rcg_matrix* a, const double* x, double* y) 
     s.x[0] = x;
     s.y[0] = y;
     KTimer t(ctx, 0);
-    k_spmv<1><<<spmv_grid(ctx, a->n), kSpmvThreads, 0, ctx->stream>>>(s);
+    spmv_prepare_kernels();
+    k_spmv<1><<<spmv_grid(ctx, a->n), kSpmvThreads, spmv_smem(a), ctx->stream>>>(s, a->cap);
     RCG_LAUNCHED(ctx);
 }
 
@@ -226,7 +190,8 @@ void launch_spmv_dual(rcg_ctx* ctx, const rcg_matrix* a, const double* x1, const
     s.y[0] = y1;
     s.y[1] = y2;
     KTimer t(ctx, 0);
-    k_spmv<2><<<spmv_grid(ctx, a->n), kSpmvThreads, 0, ctx->stream>>>(s);
+    spmv_prepare_kernels();
+    k_spmv<2><<<spmv_grid(ctx, a->n), kSpmvThreads, spmv_smem(a), ctx->stream>>>(s, a->cap);
     RCG_LAUNCHED(ctx);
 }
 
@@ -236,7 +201,8 @@ void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const d
     s.y[0] = r;
     const int g = spmv_grid(ctx, a->n);
     s.partials = ctx->ws.partials;
-    k_residual<<<g, kSpmvThreads, 0, ctx->stream>>>(s, b, ctx->ws.st);
+    spmv_prepare_kernels();
+    k_residual<<<g, kSpmvThreads, spmv_smem(a), ctx->stream>>>(s, a->cap, b, ctx->ws.st);
     RCG_LAUNCHED(ctx);
 }
 
@@ -261,6 +227,17 @@ void launch_fill_bits(rcg_ctx* ctx, double* p, int64_t n, unsigned long long bit
     if (n <= 0) return;
     k_fill_bits<<<stream_grid(ctx, n), kStreamThreads, 0, ctx->stream>>>(p, n, bits);
     RCG_LAUNCHED(ctx);
+}
+
+// Stage capacity of the pipelined SpMV: the widest 16-byte-aligned entry range of a 32-row tile
+// (rounded to 32 entries, at most 1024; wider tiles take the direct path).
+int tile_capacity(int32_t n, const int32_t* rs) {
+    int32_t widest = 0;
+    for (int32_t r0 = 0; r0 < n; r0 += 32) {
+        const int32_t rend = std::min(r0 + 32, n);
+        widest = std::max(widest, ((rs[rend] + 3) & ~3) - (rs[r0] & ~3));
+    }
+    return static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, round_up(widest, 32))));
 }
 
 // ------------------------------------------------------------------ host validation
@@ -329,9 +306,13 @@ int rcg_matrix_create(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const i
             void* p = nullptr;
             RCG_CK(cudaMalloc(&p, sizeof(int32_t) * (n + 1)));
             m->rs = static_cast<int32_t*>(p);
-            RCG_CK(cudaMalloc(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+            // 8 zero padding entries: the pipelined SpMV widens tile ranges to 16-byte alignment
+            RCG_CK(cudaMalloc(&p, sizeof(int32_t) * (nnz + kCsrPad)));
             m->ci = static_cast<int32_t*>(p);
-            m->va = dev_alloc(nnz);
+            m->va = dev_alloc(nnz + kCsrPad);
+            RCG_CK(cudaMemsetAsync(m->ci + nnz, 0, sizeof(int32_t) * kCsrPad, ctx->stream));
+            RCG_CK(cudaMemsetAsync(m->va + nnz, 0, sizeof(double) * kCsrPad, ctx->stream));
+            m->cap = tile_capacity(n, rs_host);
             const cudaMemcpyKind kind = dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
             RCG_CK(cudaMemcpyAsync(m->rs, row_start, sizeof(int32_t) * (n + 1), kind, ctx->stream));
             if (nnz > 0) {
@@ -402,9 +383,12 @@ int rcg_diagonal_scale(rcg_ctx* ctx, const rcg_matrix* a, rcg_matrix** scaled, d
             void* p = nullptr;
             RCG_CK(cudaMalloc(&p, sizeof(int32_t) * (a->n + 1)));
             m->rs = static_cast<int32_t*>(p);
-            RCG_CK(cudaMalloc(&p, sizeof(int32_t) * std::max<int64_t>(a->nnz, 1)));
+            RCG_CK(cudaMalloc(&p, sizeof(int32_t) * (a->nnz + kCsrPad)));
             m->ci = static_cast<int32_t*>(p);
-            m->va = dev_alloc(a->nnz);
+            m->va = dev_alloc(a->nnz + kCsrPad);
+            RCG_CK(cudaMemsetAsync(m->ci + a->nnz, 0, sizeof(int32_t) * kCsrPad, ctx->stream));
+            RCG_CK(cudaMemsetAsync(m->va + a->nnz, 0, sizeof(double) * kCsrPad, ctx->stream));
+            m->cap = a->cap;
             RCG_CK(cudaMemcpyAsync(m->rs, a->rs, sizeof(int32_t) * (a->n + 1), cudaMemcpyDeviceToDevice, ctx->stream));
             if (a->nnz > 0)
                 RCG_CK(cudaMemcpyAsync(m->ci, a->ci, sizeof(int32_t) * a->nnz, cudaMemcpyDeviceToDevice, ctx->stream));
