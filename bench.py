@@ -293,7 +293,10 @@ def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
             "time_to_solution_ms_per_rhs": round(ms / args.steps / cfg.n_rhs, 3), "sweeps": sweep}
 
 
-CONCURRENCY = int(os.environ.get("RCG_CONCURRENCY", "9"))  # solves 2..10 on their own streams
+# solves 2..10: "batch" = one multi-RHS kernel sequence (default); an integer = that many
+# concurrent single solves on their own streams
+_conc = os.environ.get("RCG_CONCURRENCY", "batch")
+CONCURRENCY = _conc if _conc == "batch" else int(_conc)
 
 
 def _sequence(api, ctx, prep, cfg, bs, xs, concurrency=None, phases=None):

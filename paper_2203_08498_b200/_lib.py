@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librcg_b200.so")
+LIB_PATH = os.environ.get("RCG_LIB_PATH") or os.path.join(_HERE, "librcg_b200.so")  # override: dev A/B only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -142,6 +142,10 @@ SIGNATURES = {
                       C.POINTER(SolveReport)),
     "rcg_deflated_pcg_solve": (C.c_int, vp, vp, vp, C.POINTER(Prec), vp, vp, C.POINTER(SolverConfig),
                                C.POINTER(SolveReport)),
+    "rcg_pcg_solve_batch": (C.c_int, vp, vp, vp, C.POINTER(Prec), vp, C.POINTER(SolverConfig), C.c_int,
+                            C.POINTER(SolveReport)),
+    "rcg_deflated_pcg_solve_batch": (C.c_int, vp, vp, vp, C.POINTER(Prec), vp, vp, C.POINTER(SolverConfig), C.c_int,
+                                     C.POINTER(SolveReport)),
     "rcg_pcg_with_condest": (C.c_int, vp, vp, vp, C.POINTER(Prec), vp, C.POINTER(SolverConfig), C.c_int,
                              C.c_uint64, C.POINTER(SolveReport), C.POINTER(CondEstimate)),
     "rcg_lanczos_extremes": (C.c_int, C.c_int, vp, vp, dp, dp),

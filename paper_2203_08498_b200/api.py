@@ -465,6 +465,46 @@ def deflated_pcg_solve(ctx: Context, a: CsrMatrix, b, m, defl: Optional[Basis], 
     return _finish(rep, bufs)
 
 
+def _batch(fn, ctx, a, B, m, X, eps, max_iter, defl=None):
+    R = len(B)
+    if not (1 <= R <= 16):
+        raise InvalidArgument("batch solve: 1..16 right-hand sides")
+    if isinstance(B, np.ndarray) or isinstance(B, list) and isinstance(B[0], np.ndarray):
+        Bm = np.ascontiguousarray(np.stack(list(B)) if isinstance(B, list) else B, dtype=np.float64)
+    else:
+        import torch
+
+        Bm = torch.stack(list(B)).contiguous() if isinstance(B, list) else B.contiguous()
+    if Bm.shape[-1] != a.n:
+        raise InvalidArgument("batch solve: right-hand side length does not match matrix")
+    cfg = _cfg(eps, max_iter)
+    reps = (L.SolveReport * R)()
+    bufs = []
+    for r in reps:
+        rb = _report(max(1, int(max_iter)))
+        r.cap, r.history, r.alphas, r.betas = rb[0].cap, rb[0].history, None, None
+        bufs.append(rb[1])
+    p = _prec(m)
+    args = [ctx.h, a.h, _ptr(Bm), C.byref(p)]
+    if defl is not False:
+        args.append(defl.h if defl is not None else None)
+    args += [_ptr(X), C.byref(cfg), R, reps]
+    check(fn(*args))
+    return [_finish(r, b) for r, b in zip(reps, bufs)]
+
+
+def pcg_solve_batch(ctx: Context, a: CsrMatrix, B, m, X, eps: float = 1e-8, max_iter: int = 1000):
+    """R <= 16 independent pcg_solve calls of one matrix in one kernel sequence.  B, X: (R, n)
+    contiguous (numpy host or CUDA torch); X is updated in place.  Returns R SolveReports."""
+    return _batch(lib.rcg_pcg_solve_batch, ctx, a, B, m, X, eps, max_iter, defl=False)
+
+
+def deflated_pcg_solve_batch(ctx: Context, a: CsrMatrix, B, m, defl: Optional[Basis], X, eps: float = 1e-8,
+                             max_iter: int = 1000):
+    """R <= 16 independent deflated_pcg_solve calls in one kernel sequence (see pcg_solve_batch)."""
+    return _batch(lib.rcg_deflated_pcg_solve_batch, ctx, a, B, m, X, eps, max_iter, defl=defl)
+
+
 def pcg_with_condest(ctx: Context, a: CsrMatrix, b, m, x, eps: float = 1e-8, max_iter: int = 1000,
                      m_samples: int = 20, v0_seed: int = 42):
     """pcg_with_condest (condest.hpp:46-48) plus the Lanczos estimate; returns (report, estimate)."""

@@ -1,0 +1,964 @@
+// batch.cu -- batched multi-RHS PCG / SC-PCG / deflated PCG: R independent right-hand sides of
+// one matrix solved by ONE kernel sequence (the sequence protocol's solves 2..k are independent
+// given W, driver.cpp:181-195).  Vectors are stored interleaved, v[i*RT + k] (RT = R rounded up
+// to a power of two; padding columns are zero right-hand sides, done before the first
+// iteration).  Every RHS keeps its own alpha, beta, rho, relres, convergence flag and
+// iteration count; converged RHS are frozen while the others continue.
+//
+// Why: the natural-ordering IC sweeps are bound by dependency latency (one L2 round trip per
+// level), not bandwidth.  A batch carries RT values per row through the same waits, so a level
+// costs about the same time and moves RT times the bytes; A, the IC schedule and W/AW are read
+// once per iteration for all RHS.
+//
+// Arithmetic per RHS is the reference's (pcg.cpp:63-89, deflation.cpp:17-23,
+// subspace_correction.cpp:47-57); SpMV and sweep rows are bitwise the single-RHS values; the
+// dot products are deterministic tree reductions (run to run identical).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+#include "spmv_pipe.cuh"
+#include "vec.cuh"
+
+namespace rcg {
+
+constexpr int kRMax = 16;
+constexpr int kMaxRedB = 512;
+
+struct BState {
+    int iter;      // global iteration being executed (1-based)
+    int nrun;      // right-hand sides still running
+    int max_iter;
+    int pad;
+    double eps;
+    int done[kRMax];
+    int iters[kRMax];
+    int status[kRMax];
+    double bnorm[kRMax], rho[kRMax], rho_prev[kRMax], beta[kRMax], alpha[kRMax], pq[kRMax], rr[kRMax],
+        relres[kRMax], scal2[kRMax];
+    unsigned int tick[8];
+};
+
+struct BatchWs {
+    int64_t cap = 0;  // n * RT
+    double *b = nullptr, *x = nullptr, *r = nullptr, *zs = nullptr, *p = nullptr, *q = nullptr, *y = nullptr;
+    BState* st = nullptr;
+    double* hist = nullptr;
+    int64_t cap_hist = 0;
+    double *u = nullptr, *u2 = nullptr;  // [m][RT]
+    double* partials = nullptr;
+    int64_t cap_part = 0;
+    double* gpart = nullptr;
+    unsigned int* gcount = nullptr;
+    int64_t cap_groups = 0;
+    int* tickets = nullptr;
+};
+
+void batch_ws_free(rcg_ctx* ctx) {
+    BatchWs* w = ctx->bws;
+    if (!w) return;
+    for (void* p : {(void*)w->b, (void*)w->x, (void*)w->r, (void*)w->zs, (void*)w->p, (void*)w->q, (void*)w->y,
+                    (void*)w->st, (void*)w->hist, (void*)w->u, (void*)w->u2, (void*)w->partials, (void*)w->gpart,
+                    (void*)w->gcount, (void*)w->tickets})
+        dev_free(p);
+    delete w;
+    ctx->bws = nullptr;
+}
+
+static BatchWs& batch_ws(rcg_ctx* ctx, int64_t nrt, int64_t hist, int64_t m_rt, int64_t part, int64_t groups) {
+    if (!ctx->bws) ctx->bws = new BatchWs();
+    BatchWs& w = *ctx->bws;
+    if (!w.st) {
+        void* p = nullptr;
+        RCG_CK(cudaMalloc(&p, sizeof(BState)));
+        w.st = static_cast<BState*>(p);
+        RCG_CK(cudaMalloc(&p, 16 * sizeof(int)));
+        w.tickets = static_cast<int*>(p);
+        RCG_CK(cudaMemset(w.tickets, 0, 16 * sizeof(int)));
+        RCG_CK(cudaMemset(w.st, 0, sizeof(BState)));
+    }
+    if (nrt > w.cap) {
+        for (double** v : {&w.b, &w.x, &w.r, &w.zs, &w.p, &w.q, &w.y}) {
+            dev_free(*v);
+            *v = dev_alloc(nrt);
+        }
+        w.cap = nrt;
+    }
+    if (hist > w.cap_hist) {
+        dev_free(w.hist);
+        w.hist = dev_alloc(hist);
+        w.cap_hist = hist;
+    }
+    if (!w.u || m_rt > 0) {
+        dev_free(w.u);
+        dev_free(w.u2);
+        w.u = dev_alloc(std::max<int64_t>(m_rt, kRMax));
+        w.u2 = dev_alloc(std::max<int64_t>(m_rt, kRMax));
+    }
+    if (part > w.cap_part) {
+        dev_free(w.partials);
+        w.partials = dev_alloc(part);
+        w.cap_part = part;
+    }
+    if (groups > w.cap_groups) {
+        dev_free(w.gpart);
+        dev_free(w.gcount);
+        w.gpart = dev_alloc(groups * kRMax);
+        void* p = nullptr;
+        RCG_CK(cudaMalloc(&p, sizeof(unsigned int) * groups));
+        w.gcount = static_cast<unsigned int*>(p);
+        RCG_CK(cudaMemset(w.gcount, 0, sizeof(unsigned int) * groups));
+        w.cap_groups = groups;
+    }
+    return w;
+}
+
+// ------------------------------------------------------------------ device helpers
+// Sum of v over the threads of the block that share k = threadIdx.x % RT; out[k] (smem).
+template <int RT>
+__device__ __forceinline__ void block_sum_k(double v, double* scratch /* 32*RT */, double* out) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o >= RT; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane < RT) scratch[lane * 32 + wid] = v;
+    __syncthreads();
+    if (threadIdx.x < RT) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s = __dadd_rn(s, scratch[threadIdx.x * 32 + w]);
+        out[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ kernels
+template <int RT>
+__global__ void k_b_gather(const double* __restrict__ cols, int R, int64_t ldc, double* __restrict__ out, int32_t n) {
+    const int64_t total = static_cast<int64_t>(n) * RT;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / RT;
+        const int k = static_cast<int>(e % RT);
+        out[e] = k < R ? cols[k * ldc + i] : 0.0;
+    }
+}
+
+template <int RT>
+__global__ void k_b_scatter(const double* __restrict__ in, int R, int64_t ldc, double* __restrict__ cols, int32_t n) {
+    const int64_t total = static_cast<int64_t>(n) * RT;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = static_cast<int>(e % RT);
+        if (k < R) cols[k * ldc + e / RT] = in[e];
+    }
+}
+
+// lane per row, RT interleaved vectors (each result bitwise the single-vector spmv)
+template <int RT, class Body>
+__device__ __forceinline__ void bspmv_rows(const SpmvArgs& a, const double* __restrict__ x, int cap, Body&& body) {
+    extern __shared__ __align__(16) unsigned char pipe_smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned char* base = pipe_smem + static_cast<size_t>(wid) * (16 + 2 * cap * 12);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base);
+    double* sv = reinterpret_cast<double*>(base + 16);
+    int32_t* sc = reinterpret_cast<int32_t*>(base + 16 + 2 * cap * 8);
+    if (lane == 0) {
+        mbar_init(&bar[0]);
+        mbar_init(&bar[1]);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const int ntiles = (a.n + 31) / 32;
+    const int nw = gridDim.x * kPipeWarps;
+    unsigned phase[2] = {0u, 0u};
+    auto issue = [&](int t, int stg) -> bool {
+        const int32_t r0 = t * 32, rend = min(r0 + 32, a.n);
+        const int32_t e0a = __ldg(a.rs + r0) & ~3;
+        const int32_t e1a = (__ldg(a.rs + rend) + 3) & ~3;
+        const int cnt = e1a - e0a;
+        if (cnt > cap) return false;
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&bar[stg], static_cast<unsigned>(cnt) * 12u);
+            if (cnt > 0) {
+                bulk_g2s(sv + stg * cap, a.va + e0a, static_cast<unsigned>(cnt) * 8u, &bar[stg]);
+                bulk_g2s(sc + stg * cap, a.ci + e0a, static_cast<unsigned>(cnt) * 4u, &bar[stg]);
+            }
+        }
+        return true;
+    };
+    int t = blockIdx.x * kPipeWarps + wid;
+    int stg = 0;
+    bool bulk_cur = t < ntiles ? issue(t, 0) : false;
+    for (; t < ntiles; t += nw) {
+        const int tn = t + nw;
+        const bool bulk_next = tn < ntiles ? issue(tn, stg ^ 1) : false;
+        const int32_t r0 = t * 32, row = r0 + lane, rend = min(r0 + 32, a.n);
+        const int32_t e1 = __ldg(a.rs + rend);
+        const int32_t my_b = row < a.n ? __ldg(a.rs + row) : e1;
+        const int32_t my_e = row < a.n ? __ldg(a.rs + row + 1) : e1;
+        double acc[RT];
+#pragma unroll
+        for (int v = 0; v < RT; ++v) acc[v] = 0.0;
+        const double* vsrc = a.va;
+        const int32_t* csrc = a.ci;
+        int32_t off = 0;
+        if (bulk_cur) {
+            while (!mbar_try_wait(&bar[stg], phase[stg])) {
+            }
+            phase[stg] ^= 1u;
+            vsrc = sv + stg * cap;
+            csrc = sc + stg * cap;
+            off = __ldg(a.rs + r0) & ~3;
+        }
+        for (int32_t e = my_b; e < my_e; ++e) {
+            const double av = vsrc[e - off];
+            const double2* xv = reinterpret_cast<const double2*>(x + static_cast<int64_t>(csrc[e - off]) * RT);
+#pragma unroll
+            for (int v = 0; v < RT / 2; ++v) {
+                const double2 xx = __ldg(xv + v);
+                acc[2 * v] = fadd_mul(acc[2 * v], av, xx.x);
+                acc[2 * v + 1] = fadd_mul(acc[2 * v + 1], av, xx.y);
+            }
+        }
+        if (row < a.n) body(row, acc);
+        __syncwarp();
+        stg ^= 1;
+        bulk_cur = bulk_next;
+    }
+}
+
+// r = b - A x for all RT; finaliser: bnorm, rho = rr, already-converged / zero-rhs flags
+template <int RT>
+__global__ void __launch_bounds__(kSpmvThreads) k_b_residual(SpmvArgs a, int cap, const double* __restrict__ b,
+                                                             const double* __restrict__ x, double* __restrict__ r,
+                                                             BState* st, double* partials, int defer_check) {
+    __shared__ double scratch[2 * RT * 32];
+    __shared__ double vals[2 * RT];
+    __shared__ double tot[2 * RT];
+    double bb[RT], rr[RT];
+#pragma unroll
+    for (int v = 0; v < RT; ++v) bb[v] = rr[v] = 0.0;
+    bspmv_rows<RT>(a, x, cap, [&](int32_t row, const double (&acc)[RT]) {
+#pragma unroll
+        for (int v = 0; v < RT; ++v) {
+            const double bi = b[static_cast<int64_t>(row) * RT + v];
+            const double ri = __dsub_rn(bi, acc[v]);
+            r[static_cast<int64_t>(row) * RT + v] = ri;
+            bb[v] = fadd_mul(bb[v], bi, bi);
+            rr[v] = fadd_mul(rr[v], ri, ri);
+        }
+    });
+    // block reduction of 2*RT per-thread values
+    double accs[2 * RT];
+#pragma unroll
+    for (int v = 0; v < RT; ++v) {
+        accs[v] = bb[v];
+        accs[RT + v] = rr[v];
+    }
+    block_sum_dyn<2 * RT>(accs, 2 * RT, scratch, vals);
+    if (grid_reduce_dyn(vals, 2 * RT, partials, &st->tick[0], tot) && threadIdx.x < RT) {
+        const int k = threadIdx.x;
+        st->bnorm[k] = sqrt(tot[k]);
+        st->rr[k] = tot[RT + k];
+        st->rho[k] = tot[RT + k];
+        if (st->bnorm[k] == 0.0)
+            st->done[k] = kZeroRhs;
+        else if (!defer_check && sqrt(tot[RT + k]) <= st->eps * st->bnorm[k])
+            st->done[k] = kConverged;
+        else
+            st->done[k] = kRunning;
+    }
+}
+
+__global__ void k_b_count(BState* st, int RT) {
+    int c = 0;
+    for (int k = 0; k < RT; ++k) c += st->done[k] == kRunning;
+    st->nrun = c;
+}
+
+// one sweep, thread per (row, rhs); rho partials per rhs in the backward sweep
+template <bool BWD, int RT>
+__global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
+    __shared__ int s_tile;
+    __shared__ double scratch[RT * 32];
+    __shared__ double part[RT];
+    __shared__ bool s_last_group, s_last;
+    if (st->nrun == 0) return;
+    constexpr int kRows = 128 / RT;  // rows per tile
+    const int ntiles = (a.npos + kRows - 1) / kRows;
+    const int k = threadIdx.x % RT;
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
+        __syncthreads();
+        const int tile = s_tile;
+        __syncthreads();
+        if (tile >= ntiles) break;
+        const int pos = tile * kRows + threadIdx.x / RT;
+        double contrib = 0.0;
+        const int32_t row = pos < a.npos ? __ldg(a.perm + pos) : -1;
+        if (row >= 0) {
+            const int64_t me = static_cast<int64_t>(row) * RT + k;
+            const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
+            double s = BWD ? __ddiv_rn(a.in[me], __ldg(a.d + row)) : a.in[me];
+            unsigned spins = 0;
+            for (int32_t e0 = beg;; e0 += 8) {
+                const int cnt = min(8, end - e0);
+                const bool last = e0 + 8 >= end;
+                int32_t col[8];
+                double val[8], dep[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < cnt) {
+                        col[j] = __ldg(a.pcol + e0 + j);
+                        val[j] = __ldg(a.pval + e0 + j);
+                    }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < cnt) dep[j] = ld_relaxed(a.out + static_cast<int64_t>(col[j]) * RT + k);
+                while (true) {
+                    bool missing = false;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (j < cnt && is_sentinel(dep[j])) missing = true;
+                    if (!missing) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
+                        if (last) st_relaxed(a.out + me, publishable(s));
+                        break;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (j < cnt && is_sentinel(dep[j]))
+                            dep[j] = ld_relaxed(a.out + static_cast<int64_t>(col[j]) * RT + k);
+                    if (++spins == (1u << 24)) {
+                        atomicExch(&a.tickets[3], 1);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
+                    }
+                }
+                if (last) break;
+            }
+            if (BWD && a.r) contrib = __dmul_rn(a.r[me], s);
+        }
+        if (BWD && a.r) {
+            // per-tile partials (RT values) -> groups -> total, deterministic
+            block_sum_k<RT>(contrib, scratch, part);
+            const int g = tile / kGroup;
+            const int ngroups = (ntiles + kGroup - 1) / kGroup;
+            const int gsize = min(kGroup, ntiles - g * kGroup);
+            if (threadIdx.x < RT) a.partials[static_cast<int64_t>(tile) * RT + threadIdx.x] = part[threadIdx.x];
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) s_last_group = atomicAdd(&a.gcount[g], 1u) == static_cast<unsigned>(gsize) - 1u;
+            __syncthreads();
+            if (s_last_group) {
+                __threadfence();
+                if (threadIdx.x < RT) {
+                    double sg = 0.0;
+                    for (int q = 0; q < gsize; ++q)
+                        sg = __dadd_rn(sg, __ldcg(a.partials + static_cast<int64_t>(g * kGroup + q) * RT + threadIdx.x));
+                    a.gpart[static_cast<int64_t>(g) * RT + threadIdx.x] = sg;
+                }
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    a.gcount[g] = 0u;
+                    s_last = atomicAdd(reinterpret_cast<unsigned int*>(&a.tickets[2]), 1u) ==
+                             static_cast<unsigned>(ngroups) - 1u;
+                }
+                __syncthreads();
+                if (s_last) {
+                    __threadfence();
+                    if (threadIdx.x < RT) {
+                        const int kk = threadIdx.x;
+                        double rho = 0.0;
+                        for (int q = 0; q < ngroups; ++q)
+                            rho = __dadd_rn(rho, __ldcg(a.gpart + static_cast<int64_t>(q) * RT + kk));
+                        if (st->done[kk] == kRunning) {
+                            if (a.add_sc) rho = __dadd_rn(rho, st->scal2[kk]);
+                            st->rho[kk] = rho;
+                            if (rho <= 0.0) {
+                                st->done[kk] = kBroken;
+                                st->status[kk] = kBrkRz;
+                            }
+                            st->beta[kk] = st->iter > 1 ? rho / st->rho_prev[kk] : 0.0;
+                        }
+                    }
+                    if (threadIdx.x == 0) a.tickets[2] = 0;
+                }
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x) - 1) {
+            a.tickets[0] = 0;
+            a.tickets[1] = 0;
+        }
+    }
+}
+
+// p = z (+ W u) (+ beta p) for running rhs; sweep buffers back to the sentinel
+template <int RT>
+__global__ void __launch_bounds__(kStreamThreads) k_b_pupdate(const double* __restrict__ z, double* __restrict__ p,
+                                                              double* __restrict__ zs_reset, double* __restrict__ y_reset,
+                                                              int64_t total, BState* st, const double* __restrict__ W,
+                                                              int64_t ldw, int m, const double* __restrict__ u) {
+    __shared__ double beta[RT];
+    __shared__ int run[RT];
+    __shared__ int first;
+    if (st->nrun == 0) return;
+    if (threadIdx.x < RT) {
+        beta[threadIdx.x] = st->beta[threadIdx.x];
+        run[threadIdx.x] = st->done[threadIdx.x] == kRunning;
+    }
+    if (threadIdx.x == 0) first = st->iter == 1;
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = static_cast<int>(e % RT);
+        if (run[k]) {
+            double zi = z[e];
+            if (W) {
+                const int64_t i = e / RT;
+                for (int j = 0; j < m; ++j) zi = fadd_mul(zi, u[j * RT + k], __ldg(W + j * ldw + i));
+            }
+            p[e] = first ? zi : fadd_mul(zi, beta[k], p[e]);
+        }
+        if (zs_reset) {
+            zs_reset[e] = sentinel();
+            y_reset[e] = sentinel();
+        }
+    }
+}
+
+// q = A p (all RT), (p, q) per rhs -> alpha (unless the deflated path projects q first)
+template <int RT>
+__global__ void __launch_bounds__(kSpmvThreads) k_b_spmv_pq(SpmvArgs a, int cap, const double* __restrict__ p,
+                                                            double* __restrict__ q, BState* st, double* partials,
+                                                            int project_later) {
+    __shared__ double scratch[RT * 32];
+    __shared__ double vals[RT];
+    __shared__ double tot[RT];
+    if (st->nrun == 0) return;
+    double pq[RT];
+#pragma unroll
+    for (int v = 0; v < RT; ++v) pq[v] = 0.0;
+    bspmv_rows<RT>(a, p, cap, [&](int32_t row, const double (&acc)[RT]) {
+#pragma unroll
+        for (int v = 0; v < RT; ++v) {
+            q[static_cast<int64_t>(row) * RT + v] = acc[v];
+            pq[v] = fadd_mul(pq[v], p[static_cast<int64_t>(row) * RT + v], acc[v]);
+        }
+    });
+    if (project_later) return;
+    block_sum_dyn<RT>(pq, RT, scratch, vals);
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[1], tot) && threadIdx.x < RT) {
+        const int k = threadIdx.x;
+        if (st->done[k] == kRunning) {
+            st->pq[k] = tot[k];
+            if (tot[k] <= 0.0) {
+                st->done[k] = kBroken;
+                st->status[k] = kBrkPAp;
+            }
+            st->alpha[k] = st->rho[k] / tot[k];
+        }
+    }
+}
+
+// f[j][k] = W_j . y_k ; finaliser: u[:,k] = (W^T A W)^-1 f[:,k] (mode 1) and f.u (mode 2)
+template <int RT>
+__global__ void __launch_bounds__(kStreamThreads) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
+                                                            const double* __restrict__ y, int32_t n, double* partials,
+                                                            const double* __restrict__ L, double* __restrict__ u,
+                                                            int mode, BState* st, int respect_done) {
+    __shared__ double scratch[RT * 32];
+    __shared__ double part[RT];
+    __shared__ double bvals[kMaxRedB];
+    __shared__ double tot[kMaxRedB];
+    __shared__ double fk[8][128];
+    __shared__ double sol[8][128];
+    if (respect_done && st->nrun == 0) return;
+    const int64_t total = static_cast<int64_t>(n) * RT;
+    for (int j0 = 0; j0 < m; j0 += 8) {
+        const int mc = min(8, m - j0);
+        double acc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+            const double ye = y[e];
+            const int64_t i = e / RT;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < mc) acc[c] = fadd_mul(acc[c], __ldg(W + (j0 + c) * ldw + i), ye);
+        }
+        for (int c = 0; c < mc; ++c) {
+            block_sum_k<RT>(acc[c], scratch, part);
+            if (threadIdx.x < RT) bvals[(j0 + c) * RT + threadIdx.x] = part[threadIdx.x];
+        }
+    }
+    __syncthreads();
+    if (grid_reduce_dyn(bvals, m * RT, partials, &st->tick[2], tot)) {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int k = wid; k < RT; k += blockDim.x >> 5) {
+            for (int j = lane; j < m; j += 32) fk[wid][j] = tot[j * RT + k];
+            __syncwarp();
+            double* uk = sol[wid];
+            warp_chol_solve(L, m, fk[wid], uk, uk);  // solution lands in uk (scratch == output)
+            __syncwarp();
+            for (int j = lane; j < m; j += 32) u[j * RT + k] = uk[j];
+            if (mode == 2 && lane == 0) {
+                double fu = 0.0;
+                for (int j = 0; j < m; ++j) fu = fadd_mul(fu, fk[wid][j], uk[j]);
+                st->scal2[k] = fu;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// y -= sum_j u[j][k] C_j (running rhs) with (p, y) -> alpha (mode 0) or (y, y) initial check (1)
+template <int RT>
+__global__ void __launch_bounds__(kStreamThreads) k_b_deflate(double* __restrict__ y, const double* __restrict__ C,
+                                                              int64_t ldc, int m, const double* __restrict__ u,
+                                                              const double* __restrict__ p, int32_t n, double* partials,
+                                                              BState* st, int mode) {
+    __shared__ double scratch[RT * 32];
+    __shared__ double vals[RT];
+    __shared__ double tot[RT];
+    __shared__ int run[RT];
+    if (st->nrun == 0 && mode == 0) return;
+    if (threadIdx.x < RT) run[threadIdx.x] = mode == 1 || st->done[threadIdx.x] == kRunning;
+    __syncthreads();
+    const int64_t total = static_cast<int64_t>(n) * RT;
+    double acc = 0.0;  // every thread keeps one rhs: k = threadIdx.x % RT for all its elements
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = static_cast<int>(e % RT);
+        if (!run[k]) continue;
+        const int64_t i = e / RT;
+        double v = y[e];
+        for (int j = 0; j < m; ++j) v = fsub_mul(v, u[j * RT + k], __ldg(C + j * ldc + i));
+        y[e] = v;
+        acc = mode == 0 ? fadd_mul(acc, p[e], v) : fadd_mul(acc, v, v);
+    }
+    block_sum_k<RT>(acc, scratch, vals);
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[3], tot) && threadIdx.x < RT) {
+        const int k = threadIdx.x;
+        if (mode == 0) {
+            if (st->done[k] == kRunning) {
+                st->pq[k] = tot[k];
+                if (tot[k] <= 0.0) {
+                    st->done[k] = kBroken;
+                    st->status[k] = kBrkPAp;
+                }
+                st->alpha[k] = st->rho[k] / tot[k];
+            }
+        } else if (st->done[k] == kRunning) {
+            st->rr[k] = tot[k];
+            st->rho[k] = tot[k];
+            if (sqrt(tot[k]) <= st->eps * st->bnorm[k]) st->done[k] = kConverged;
+        }
+    }
+}
+
+// x += alpha p, r -= alpha q for running rhs; relres, history, convergence per rhs
+template <int RT>
+__global__ void __launch_bounds__(kStreamThreads) k_b_xr(double* __restrict__ x, double* __restrict__ r,
+                                                         const double* __restrict__ p, const double* __restrict__ q,
+                                                         int32_t n, double* partials, BState* st,
+                                                         double* __restrict__ hist, int64_t hist_ld, int identity) {
+    __shared__ double scratch[RT * 32];
+    __shared__ double vals[RT];
+    __shared__ double tot[RT];
+    __shared__ double alpha[RT];
+    __shared__ int run[RT];
+    if (st->nrun == 0) return;
+    if (threadIdx.x < RT) {
+        alpha[threadIdx.x] = st->alpha[threadIdx.x];
+        run[threadIdx.x] = st->done[threadIdx.x] == kRunning;
+    }
+    __syncthreads();
+    const int64_t total = static_cast<int64_t>(n) * RT;
+    double acc = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = static_cast<int>(e % RT);
+        if (!run[k]) continue;
+        x[e] = fadd_mul(x[e], alpha[k], p[e]);
+        const double ri = fsub_mul(r[e], alpha[k], q[e]);
+        r[e] = ri;
+        acc = fadd_mul(acc, ri, ri);
+    }
+    block_sum_k<RT>(acc, scratch, vals);
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[4], tot)) {
+        if (threadIdx.x < RT) {
+            const int k = threadIdx.x;
+            const int i = st->iter;
+            if (run[k]) {
+                const double relres = sqrt(tot[k]) / st->bnorm[k];
+                st->rr[k] = tot[k];
+                st->relres[k] = relres;
+                st->iters[k] = i;
+                hist[k * hist_ld + (i - 1)] = relres;
+                st->rho_prev[k] = st->rho[k];
+                if (relres <= st->eps) {
+                    st->done[k] = kConverged;
+                } else if (i >= st->max_iter) {
+                    st->done[k] = kCapped;
+                } else if (identity) {
+                    st->rho[k] = tot[k];
+                    if (tot[k] <= 0.0) {
+                        st->done[k] = kBroken;
+                        st->status[k] = kBrkRz;
+                    }
+                    st->beta[k] = tot[k] / st->rho_prev[k];
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int c = 0;
+            for (int k = 0; k < RT; ++k) c += st->done[k] == kRunning;
+            st->nrun = c;
+            st->iter = st->iter + 1;
+        }
+    }
+}
+
+// zero-rhs solutions; deflated recombination x = P x + W (W^T A W)^-1 W^T b per rhs
+template <int RT>
+__global__ void k_b_finish_combine(double* __restrict__ x, const double* __restrict__ Cm, int64_t ldc, int m,
+                                   const double* __restrict__ u, int32_t n, const BState* st, int mode) {
+    const int64_t total = static_cast<int64_t>(n) * RT;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = static_cast<int>(e % RT);
+        const int d = st->done[k];
+        if (mode == 2) {  // zero rhs -> x = 0
+            if (d == kZeroRhs) x[e] = 0.0;
+            continue;
+        }
+        if (d == kBroken || d == kZeroRhs) continue;
+        const int64_t i = e / RT;
+        if (mode == 0) {  // x -= W u (project_p)
+            double v = x[e];
+            for (int j = 0; j < m; ++j) v = fsub_mul(v, u[j * RT + k], __ldg(Cm + j * ldc + i));
+            x[e] = v;
+        } else {  // x += 0 + sum_j u_j W_j (direct_component)
+            double t = 0.0;
+            for (int j = 0; j < m; ++j) t = fadd_mul(t, u[j * RT + k], __ldg(Cm + j * ldc + i));
+            x[e] = __dadd_rn(x[e], t);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host driver
+template <int RT>
+struct BatchSolve {
+    rcg_ctx* ctx;
+    const rcg_matrix* a;
+    const rcg_prec* m;
+    const rcg_basis* defl;
+    int32_t n;
+    int R;
+    int max_iter;
+    double eps;
+    bool ic = false, sc = false;
+    const rcg_basis* scb = nullptr;
+    BatchWs* w = nullptr;
+    int sg = 1, pg = 1;
+
+    void setup() {
+        ic = m->kind == RCG_PREC_IC || (m->kind == RCG_PREC_SC && m->ic);
+        sc = m->kind == RCG_PREC_SC && m->sc && m->sc->k > 0;
+        scb = sc ? m->sc : nullptr;
+        int mm = 1;
+        if (sc) mm = std::max(mm, scb->k);
+        if (defl) mm = std::max(mm, defl->k);
+        require(mm * RT <= kMaxRedB, "batch: basis columns x right-hand sides exceed the reduction capacity");
+        const int64_t nrt = static_cast<int64_t>(n) * RT;
+        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 128 / RT - 1) / (128 / RT)
+                            : 1;
+        const int64_t groups = (ntiles + kGroup - 1) / kGroup;
+        const int64_t part = std::max<int64_t>(ntiles * RT, static_cast<int64_t>(kMaxRedB) * ctx->num_sms * 8);
+        w = &batch_ws(ctx, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
+        sg = stream_grid(ctx, nrt);
+        pg = spmv_grid(ctx, n);
+        static bool prepared = false;
+        if (!prepared) {
+            allow_smem(reinterpret_cast<const void*>(k_b_residual<RT>));
+            allow_smem(reinterpret_cast<const void*>(k_b_spmv_pq<RT>));
+            prepared = true;
+        }
+    }
+
+    SpmvArgs sargs() const {
+        SpmvArgs s{};
+        s.rs = a->rs;
+        s.ci = a->ci;
+        s.va = a->va;
+        s.n = n;
+        s.partials = w->partials;
+        return s;
+    }
+
+    SweepArgs swargs(bool backward) {
+        SweepArgs s = sweep_args(ctx, m->ic, backward);
+        s.tickets = w->tickets + (backward ? 4 : 0);
+        s.partials = w->partials;
+        s.gpart = w->gpart;
+        s.gcount = w->gcount;
+        return s;
+    }
+
+    void initial() {
+        BState h{};
+        h.iter = 1;
+        h.max_iter = max_iter;
+        h.eps = eps;
+        std::memcpy(ctx->host_pinned, &h, sizeof(h));
+        RCG_CK(cudaMemcpyAsync(w->st, ctx->host_pinned, sizeof(BState), cudaMemcpyHostToDevice, ctx->stream));
+        const int64_t nrt = static_cast<int64_t>(n) * RT;
+        if (ic) {
+            launch_fill_bits(ctx, w->y, nrt, kSentinelBits);
+            launch_fill_bits(ctx, w->zs, nrt, kSentinelBits);
+        }
+        const bool dfl = defl && defl->k > 0;
+        k_b_residual<RT><<<pg, kSpmvThreads, spmv_smem(a), ctx->stream>>>(sargs(), a->cap, w->b, w->x, w->r, w->st,
+                                                                          w->partials, dfl ? 1 : 0);
+        RCG_LAUNCHED(ctx);
+        if (dfl) {
+            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->r, n, w->partials,
+                                                                  defl->l, w->u, 1, w->st, 0);
+            RCG_LAUNCHED(ctx);
+            k_b_deflate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr,
+                                                                    n, w->partials, w->st, 1);
+            RCG_LAUNCHED(ctx);
+        }
+        if (sc) {
+            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
+                                                                  scb->l, w->u2, 2, w->st, 0);
+            RCG_LAUNCHED(ctx);
+        }
+        k_b_count<<<1, 1, 0, ctx->stream>>>(w->st, RT);
+        RCG_LAUNCHED(ctx);
+    }
+
+    void iteration() {
+        const int64_t nrt = static_cast<int64_t>(n) * RT;
+        const double* z = w->r;
+        if (ic) {
+            SweepArgs fa = swargs(false);
+            fa.in = w->r;
+            fa.out = w->y;
+            launch_b_sweep(false, fa);
+            SweepArgs ba = swargs(true);
+            ba.in = w->y;
+            ba.out = w->zs;
+            ba.r = w->r;
+            ba.add_sc = sc ? 1 : 0;
+            launch_b_sweep(true, ba);
+            z = w->zs;
+        }
+        require(ic || !sc, "batch: subspace correction needs the IC inner preconditioner");
+        {
+            KTimer t(ctx, 3);
+            k_b_pupdate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(z, w->p, ic ? w->zs : nullptr, w->y, nrt, w->st,
+                                                                    sc ? scb->w : nullptr, sc ? scb->ld : 0,
+                                                                    sc ? scb->k : 0, w->u2);
+            RCG_LAUNCHED(ctx);
+        }
+        const bool dfl = defl && defl->k > 0;
+        {
+            KTimer t(ctx, 0);
+            k_b_spmv_pq<RT><<<pg, kSpmvThreads, spmv_smem(a), ctx->stream>>>(sargs(), a->cap, w->p, w->q, w->st,
+                                                                             w->partials, dfl ? 1 : 0);
+            RCG_LAUNCHED(ctx);
+        }
+        if (dfl) {
+            KTimer t(ctx, 4);
+            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n, w->partials,
+                                                                  defl->l, w->u, 1, w->st, 1);
+            RCG_LAUNCHED(ctx);
+            k_b_deflate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, n,
+                                                                    w->partials, w->st, 0);
+            RCG_LAUNCHED(ctx);
+        }
+        {
+            KTimer t(ctx, 3);
+            k_b_xr<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, w->r, w->p, w->q, n, w->partials, w->st, w->hist,
+                                                               max_iter + 1, (!ic && !sc) ? 1 : 0);
+            RCG_LAUNCHED(ctx);
+        }
+        if (sc) {
+            KTimer t(ctx, 4);
+            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
+                                                                  scb->l, w->u2, 2, w->st, 1);
+            RCG_LAUNCHED(ctx);
+        }
+    }
+
+    void launch_b_sweep(bool backward, SweepArgs& s) {
+        const rcg_ic* f = m->ic;
+        const int rows = 128 / RT;
+        const int ntiles = (s.npos + rows - 1) / rows;
+        const int levels = backward ? f->bwd_levels : f->fwd_levels;
+        const int64_t rows_per_level = levels > 0 ? s.npos / levels : s.npos;
+        const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : (rows_per_level >= 65536 ? 8 : 2);
+        const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
+        KTimer t(ctx, backward ? 2 : 1);
+        if (backward)
+            k_b_sweep<true, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+        else
+            k_b_sweep<false, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+        RCG_LAUNCHED(ctx);
+    }
+
+    void finish() {
+        k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, nullptr, 0, 0, nullptr, n, w->st, 2);
+        RCG_LAUNCHED(ctx);
+        if (defl && defl->k > 0) {  // x = P x + W (W^T A W)^-1 W^T b (pcg.cpp:152-157)
+            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->aw, defl->ld, defl->k, w->x, n, w->partials,
+                                                                  defl->l, w->u, 1, w->st, 0);
+            RCG_LAUNCHED(ctx);
+            k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
+                                                                           w->st, 0);
+            RCG_LAUNCHED(ctx);
+            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->b, n, w->partials,
+                                                                  defl->l, w->u2, 1, w->st, 0);
+            RCG_LAUNCHED(ctx);
+            k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u2, n,
+                                                                           w->st, 1);
+            RCG_LAUNCHED(ctx);
+        }
+    }
+
+    void run(double* wall) {
+        cudaEvent_t evs[2], t0, t1;
+        RCG_CK(cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming));
+        RCG_CK(cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming));
+        RCG_CK(cudaEventCreate(&t0));
+        RCG_CK(cudaEventCreate(&t1));
+        RCG_CK(cudaEventRecord(t0, ctx->stream));
+        volatile int* flags = reinterpret_cast<volatile int*>(ctx->host_pinned + 256);
+        int enq = 0, batch = 2, slot = 0, prev = 0;
+        bool have_prev = false;
+        while (true) {
+            for (int j = 0; j < batch && enq < max_iter; ++j, ++enq) iteration();
+            RCG_CK(cudaMemcpyAsync((void*)(flags + slot), &w->st->nrun, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            RCG_CK(cudaEventRecord(evs[slot], ctx->stream));
+            if (enq >= max_iter) {
+                RCG_CK(cudaEventSynchronize(evs[slot]));
+                break;
+            }
+            if (have_prev) {
+                RCG_CK(cudaEventSynchronize(evs[prev]));
+                if (flags[prev] == 0) break;
+            }
+            have_prev = true;
+            prev = slot;
+            slot ^= 1;
+            batch = std::min(batch * 2, 16);
+        }
+        RCG_CK(cudaEventRecord(t1, ctx->stream));
+        RCG_CK(cudaEventSynchronize(t1));
+        float ms = 0.f;
+        RCG_CK(cudaEventElapsedTime(&ms, t0, t1));
+        *wall = ms * 1e-3;
+        for (auto e : {evs[0], evs[1], t0, t1}) cudaEventDestroy(e);
+    }
+};
+
+template <int RT>
+static void batch_solve(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const rcg_prec* m, const rcg_basis* defl,
+                        double* X, const rcg_solver_config* cfg, int R, rcg_solve_report* reps) {
+    BatchSolve<RT> s{};
+    s.ctx = ctx;
+    s.a = a;
+    s.m = m;
+    s.defl = defl;
+    s.n = a->n;
+    s.R = R;
+    s.max_iter = cfg->max_iter;
+    s.eps = cfg->eps;
+    s.setup();
+    const int32_t n = a->n;
+    Staged bs, xs;
+    stage_in(ctx, B, static_cast<int64_t>(n) * R, bs);
+    stage_in(ctx, X, static_cast<int64_t>(n) * R, xs);
+    const int g = stream_grid(ctx, static_cast<int64_t>(n) * RT);
+    k_b_gather<RT><<<g, kStreamThreads, 0, ctx->stream>>>(bs.dev, R, n, s.w->b, n);
+    RCG_LAUNCHED(ctx);
+    k_b_gather<RT><<<g, kStreamThreads, 0, ctx->stream>>>(xs.dev, R, n, s.w->x, n);
+    RCG_LAUNCHED(ctx);
+    s.initial();
+    double wall = 0.0;
+    s.run(&wall);
+    s.finish();
+    Staged xo;
+    stage_out_begin(ctx, X, static_cast<int64_t>(n) * R, xo);
+    k_b_scatter<RT><<<g, kStreamThreads, 0, ctx->stream>>>(s.w->x, R, n, xo.dev, n);
+    RCG_LAUNCHED(ctx);
+    stage_out_end(ctx, X, static_cast<int64_t>(n) * R, xo);
+    RCG_CK(cudaStreamSynchronize(ctx->stream));
+    check_sweep_watchdog(ctx);
+    BState h{};
+    RCG_CK(cudaMemcpy(&h, s.w->st, sizeof(BState), cudaMemcpyDeviceToHost));
+    std::vector<double> hist(static_cast<size_t>(RT) * (s.max_iter + 1));
+    RCG_CK(cudaMemcpy(hist.data(), s.w->hist, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost));
+    int broken = -1;
+    for (int k = 0; k < R; ++k) {
+        rcg_solve_report& r = reps[k];
+        r.iterations = (h.done[k] == kZeroRhs) ? 0 : h.iters[k];
+        r.converged = (h.done[k] == kConverged || h.done[k] == kZeroRhs) ? 1 : 0;
+        r.wall_time = wall;
+        const int cnt = std::min(r.iterations, r.cap);
+        if (r.history && cnt > 0)
+            std::memcpy(r.history, hist.data() + static_cast<size_t>(k) * (s.max_iter + 1), sizeof(double) * cnt);
+        if (h.done[k] == kBroken && broken < 0) broken = k;
+    }
+    if (broken >= 0) {
+        const bool dfl = defl && defl->k > 0;
+        throw Error(RCG_E_BREAKDOWN, std::string(dfl ? "deflated pcg" : "pcg") + ": breakdown in right-hand side " +
+                                         std::to_string(broken) +
+                                         (h.status[broken] == kBrkRz ? " ((r, z) <= 0)" : " ((p, A p) <= 0)"));
+    }
+}
+
+}  // namespace rcg
+
+using namespace rcg;
+
+static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const rcg_prec* m, const rcg_basis* defl,
+                       double* X, const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps) {
+    return guard([&] {
+        require(ctx && a && reps && B && X, "batch solve: null argument");
+        require(nrhs >= 1 && nrhs <= kRMax, "batch solve: nrhs must be in [1, 16]");
+        check_cfg(cfg);
+        check_prec(m, a->n);
+        if (defl && defl->k > 0) require(defl->n == a->n, "deflated_pcg_solve: W row count does not match A");
+        if (nrhs <= 2)
+            batch_solve<2>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
+        else if (nrhs <= 4)
+            batch_solve<4>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
+        else if (nrhs <= 8)
+            batch_solve<8>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
+        else
+            batch_solve<16>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
+    });
+}
+
+extern "C" {
+
+int rcg_pcg_solve_batch(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const rcg_prec* m, double* X,
+                        const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps) {
+    return batch_entry(ctx, a, B, m, nullptr, X, cfg, nrhs, reps);
+}
+
+int rcg_deflated_pcg_solve_batch(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const rcg_prec* m,
+                                 const rcg_basis* defl, double* X, const rcg_solver_config* cfg, int nrhs,
+                                 rcg_solve_report* reps) {
+    return batch_entry(ctx, a, B, m, defl, X, cfg, nrhs, reps);
+}
+
+}  // extern "C"

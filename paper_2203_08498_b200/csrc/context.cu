@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "internal.cuh"
+#include "kernels.cuh"
 
 namespace rcg {
 
@@ -219,6 +220,7 @@ int rcg_ctx_create(int device, rcg_ctx** out) {
         c->num_sms = prop.multiProcessorCount;
         if (const char* e = std::getenv("RCG_SWEEP_BPS")) c->sweep_bps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("RCG_SWEEP_BACKOFF_NS")) c->sweep_backoff_ns = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("RCG_SPMV_BPS")) c->spmv_bps = std::max(1, std::atoi(e));
         RCG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         RCG_CK(cudaEventCreate(&c->ev0));
         RCG_CK(cudaEventCreate(&c->ev1));
@@ -233,6 +235,7 @@ void rcg_ctx_destroy(rcg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    batch_ws_free(ctx);
     Workspace& w = ctx->ws;
     for (void* p : {(void*)w.r, (void*)w.z, (void*)w.p, (void*)w.q, (void*)w.ybuf, (void*)w.zs,
                     (void*)w.v, (void*)w.vnext, (void*)w.bw, (void*)w.xw, (void*)w.hist,

@@ -168,6 +168,14 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
     }
 }
 
+void sweep_prepare_kernels() {
+    static bool done = false;
+    if (done) return;
+    set_carveout(reinterpret_cast<const void*>(k_sweep<false>));
+    set_carveout(reinterpret_cast<const void*>(k_sweep<true>));
+    done = true;
+}
+
 SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
     SweepArgs a{};
     a.perm = backward ? f->b_perm : f->f_perm;

@@ -138,6 +138,8 @@ struct Workspace {
     int cap_pending = 0;
 };
 
+struct BatchWs;  // batch.cu
+
 }  // namespace rcg
 
 // ------------------------------------------------------------------ handle structs
@@ -161,6 +163,8 @@ struct rcg_ctx {
     cudaEvent_t user_ev[16] = {};
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
+    int spmv_bps = 2;           // SpMV CTAs per SM (RCG_SPMV_BPS): leaves room for concurrent solves
+    rcg::BatchWs* bws = nullptr;  // multi-RHS workspace (batch.cu)
 };
 
 struct rcg_matrix {

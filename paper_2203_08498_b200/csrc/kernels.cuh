@@ -42,11 +42,17 @@ int spmv_grid(const rcg_ctx* ctx, int32_t n);
 int stream_grid(const rcg_ctx* ctx, int64_t n);
 size_t spmv_smem(const rcg_matrix* a);
 void spmv_prepare_kernels();
+void sweep_prepare_kernels();
+void set_carveout(const void* kernel);
+void allow_smem(const void* kernel);
 int tile_capacity(int32_t n, const int32_t* rs);
 void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const double* x, double* r);
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
 SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward);
 void check_sweep_watchdog(rcg_ctx* ctx);
 int64_t sweep_tiles(const rcg_ic* f);
+void check_cfg(const rcg_solver_config* cfg);
+void batch_ws_free(rcg_ctx* ctx);
+void check_prec(const rcg_prec* m, int32_t n);
 
 }  // namespace rcg

@@ -404,6 +404,15 @@ struct Solve {
             spmv_prepare_kernels();
             allow_smem(reinterpret_cast<const void*>(k_spmv_pq<1>));
             allow_smem(reinterpret_cast<const void*>(k_spmv_pq<2>));
+            // one shared-memory carveout for every kernel of the loop: an SM must drain before
+            // it switches carveout, so mixed preferences serialise concurrent solves
+            for (const void* k : {reinterpret_cast<const void*>(k_pupdate), reinterpret_cast<const void*>(k_xr),
+                                  reinterpret_cast<const void*>(k_tallt), reinterpret_cast<const void*>(k_deflate),
+                                  reinterpret_cast<const void*>(k_sc_identity),
+                                  reinterpret_cast<const void*>(k_spmv_pq<1>),
+                                  reinterpret_cast<const void*>(k_spmv_pq<2>)})
+                set_carveout(k);
+            sweep_prepare_kernels();
             smem_ok = true;
         }
     }
@@ -649,13 +658,13 @@ static void run_loop(Solve& s, double* wall_s) {
     cudaEventDestroy(t1);
 }
 
-static void check_cfg(const rcg_solver_config* cfg) {
+void check_cfg(const rcg_solver_config* cfg) {
     require(cfg != nullptr, "SolverConfig: null");
     if (!(cfg->eps > 0.0 && cfg->eps < 1.0)) throw Error(RCG_E_INVALID, "SolverConfig: eps must be in (0, 1)");
     if (cfg->max_iter < 1) throw Error(RCG_E_INVALID, "SolverConfig: max_iter must be >= 1");
 }
 
-static void check_prec(const rcg_prec* m, int32_t n) {
+void check_prec(const rcg_prec* m, int32_t n) {
     require(m != nullptr, "preconditioner: null");
     switch (m->kind) {
         case RCG_PREC_IDENTITY:

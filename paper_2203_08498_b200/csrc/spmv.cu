@@ -9,6 +9,7 @@
 // Gathers of x go through the read-only path (L1/L2; x is L2-resident for C1-C3).
 // Algorithmic bytes per launch: 12 nnz + 20 n.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -130,7 +131,7 @@ __global__ void k_fill_bits(double* p, int64_t n, unsigned long long bits) {
 int spmv_grid(const rcg_ctx* ctx, int32_t n) {
     const int tiles = (n + 31) / 32;
     const int blocks = (tiles + kPipeWarps - 1) / kPipeWarps;
-    return std::max(1, std::min(blocks, ctx->num_sms * 8));
+    return std::max(1, std::min(blocks, ctx->num_sms * ctx->spmv_bps));
 }
 
 // dynamic shared memory of the pipelined SpMV kernels (raises the opt-in limit once per kernel)
@@ -147,9 +148,21 @@ void allow_smem(const void* kernel) {
                                 optin - static_cast<int>(fa.sharedSizeBytes)));
 }
 
+// same preferred carveout for all hot kernels (RCG_CARVEOUT percent of the maximum smem)
+void set_carveout(const void* kernel) {
+    static int pct = [] {
+        const char* e = std::getenv("RCG_CARVEOUT");
+        return e ? std::atoi(e) : 50;
+    }();
+    if (pct >= 0) RCG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+}
+
 void spmv_prepare_kernels() {
     static bool done = false;
     if (done) return;
+    set_carveout(reinterpret_cast<const void*>(k_spmv<1>));
+    set_carveout(reinterpret_cast<const void*>(k_spmv<2>));
+    set_carveout(reinterpret_cast<const void*>(k_residual));
     allow_smem(reinterpret_cast<const void*>(k_spmv<1>));
     allow_smem(reinterpret_cast<const void*>(k_spmv<2>));
     allow_smem(reinterpret_cast<const void*>(k_residual));

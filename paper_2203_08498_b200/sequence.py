@@ -91,6 +91,8 @@ def run_accelerated(p: Prepared, basis, bs: list, xs: list, concurrency: int = 1
             return api.pcg_solve(ctx, p.a, b, api.Sc(basis, p.ic), x, cfg.eps, cfg.max_iter)
         return api.deflated_pcg_solve(ctx, p.a, b, api.Ic(p.ic), basis, x, cfg.eps, cfg.max_iter)
 
+    if concurrency == "batch":
+        return run_batched(p, basis, bs, xs)
     if concurrency <= 1:
         return [one(p.ctx, b, x) for b, x in zip(bs, xs)]
     import queue
@@ -112,6 +114,33 @@ def run_accelerated(p: Prepared, basis, bs: list, xs: list, concurrency: int = 1
     with ThreadPoolExecutor(max_workers=len(pool)) as ex:
         futs = [ex.submit(checked_out, b, x) for b, x in zip(bs, xs)]
         return [f.result() for f in futs]
+
+
+def run_batched(p: Prepared, basis, bs: list, xs: list) -> list:
+    """Solves 2..k as batched multi-RHS solves (up to 16 right-hand sides per kernel sequence):
+    one pass over A, the IC schedules and W per iteration serves every right-hand side."""
+    cfg = p.cfg
+    reps = []
+    for c0 in range(0, len(bs), 16):
+        chunk_b, chunk_x = bs[c0:c0 + 16], xs[c0:c0 + 16]
+        if isinstance(chunk_b[0], np.ndarray):
+            B = np.ascontiguousarray(np.stack(chunk_b))
+            X = np.ascontiguousarray(np.stack(chunk_x))
+        else:
+            import torch
+
+            B = torch.stack(chunk_b).contiguous()
+            X = torch.stack(chunk_x).contiguous()
+        if basis is None:
+            r = api.pcg_solve_batch(p.ctx, p.a, B, api.Ic(p.ic), X, cfg.eps, cfg.max_iter)
+        elif cfg.method == "sc":
+            r = api.pcg_solve_batch(p.ctx, p.a, B, api.Sc(basis, p.ic), X, cfg.eps, cfg.max_iter)
+        else:
+            r = api.deflated_pcg_solve_batch(p.ctx, p.a, B, api.Ic(p.ic), basis, X, cfg.eps, cfg.max_iter)
+        for x_dst, x_src in zip(chunk_x, X):
+            x_dst[:] = x_src
+        reps += r
+    return reps
 
 
 def run_sequence(p: Prepared, rhs_scaled: list, rhs_orig: list | None = None, n_solves: int | None = None,
