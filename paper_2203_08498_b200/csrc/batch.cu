@@ -116,23 +116,6 @@ static BatchWs& batch_ws(rcg_ctx* ctx, int64_t nrt, int64_t hist, int64_t m_rt, 
 }
 
 // ------------------------------------------------------------------ device helpers
-// Sum of v over the threads of the block that share k = threadIdx.x % RT; out[k] (smem).
-template <int RT>
-__device__ __forceinline__ void block_sum_k(double v, double* scratch /* 32*RT */, double* out) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int o = 16; o >= RT; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-    __syncthreads();
-    if (lane < RT) scratch[lane * 32 + wid] = v;
-    __syncthreads();
-    if (threadIdx.x < RT) {
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s = __dadd_rn(s, scratch[threadIdx.x * 32 + w]);
-        out[threadIdx.x] = s;
-    }
-    __syncthreads();
-}
-
 // ------------------------------------------------------------------ kernels
 template <int RT>
 __global__ void k_b_gather(const double* __restrict__ cols, int R, int64_t ldc, double* __restrict__ out, int32_t n) {
@@ -277,75 +260,132 @@ __global__ void k_b_count(BState* st, int RT) {
     st->nrun = c;
 }
 
-// one sweep, thread per (row, rhs); rho partials per rhs in the backward sweep
+// 16-byte relaxed accesses of two interleaved values (each value its own ready flag)
+__device__ __forceinline__ double2 ld_relaxed2(const double* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed2(double* p, double a, double b) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+// One sweep, lane per row carrying all RT values: the same 128-row tiles, the same number of
+// polling lanes and the same dependency waits as the single-RHS sweep, RT times the bytes.
+// Parents are loaded in chunks of CH entries (every value of a chunk in flight together) and
+// the missing entries re-polled together; the row is published from inside the wait loop.
 template <bool BWD, int RT>
 __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
+    constexpr int CH = RT <= 4 ? 8 : (RT <= 8 ? 4 : 3);
     __shared__ int s_tile;
-    __shared__ double scratch[RT * 32];
+    __shared__ double scratch[32 * RT];
     __shared__ double part[RT];
     __shared__ bool s_last_group, s_last;
     if (st->nrun == 0) return;
-    constexpr int kRows = 128 / RT;  // rows per tile
-    const int ntiles = (a.npos + kRows - 1) / kRows;
-    const int k = threadIdx.x % RT;
+    const int ntiles = (a.npos + 127) / 128;
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
         __syncthreads();
         const int tile = s_tile;
         __syncthreads();
         if (tile >= ntiles) break;
-        const int pos = tile * kRows + threadIdx.x / RT;
-        double contrib = 0.0;
+        const int pos = tile * 128 + threadIdx.x;
+        double contrib[RT];
+#pragma unroll
+        for (int v = 0; v < RT; ++v) contrib[v] = 0.0;
         const int32_t row = pos < a.npos ? __ldg(a.perm + pos) : -1;
         if (row >= 0) {
-            const int64_t me = static_cast<int64_t>(row) * RT + k;
+            const int64_t me = static_cast<int64_t>(row) * RT;
             const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
-            double s = BWD ? __ddiv_rn(a.in[me], __ldg(a.d + row)) : a.in[me];
-            unsigned spins = 0;
-            for (int32_t e0 = beg;; e0 += 8) {
-                const int cnt = min(8, end - e0);
-                const bool last = e0 + 8 >= end;
-                int32_t col[8];
-                double val[8], dep[8];
+            double s[RT];
+            const double2* in2 = reinterpret_cast<const double2*>(a.in + me);
+            const double dr = BWD ? __ldg(a.d + row) : 1.0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+            for (int v = 0; v < RT / 2; ++v) {
+                const double2 t = in2[v];
+                s[2 * v] = BWD ? __ddiv_rn(t.x, dr) : t.x;
+                s[2 * v + 1] = BWD ? __ddiv_rn(t.y, dr) : t.y;
+            }
+            unsigned spins = 0;
+            for (int32_t e0 = beg;; e0 += CH) {
+                const int cnt = min(CH, end - e0);
+                const bool last = e0 + CH >= end;
+                int32_t col[CH];
+                double val[CH];
+                double dep[CH][RT];
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
                     if (j < cnt) {
                         col[j] = __ldg(a.pcol + e0 + j);
                         val[j] = __ldg(a.pval + e0 + j);
                     }
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < cnt) dep[j] = ld_relaxed(a.out + static_cast<int64_t>(col[j]) * RT + k);
+                for (int j = 0; j < CH; ++j)
+                    if (j < cnt)
+#pragma unroll
+                        for (int v = 0; v < RT / 2; ++v) {
+                            const double2 t = ld_relaxed2(a.out + static_cast<int64_t>(col[j]) * RT + 2 * v);
+                            dep[j][2 * v] = t.x;
+                            dep[j][2 * v + 1] = t.y;
+                        }
                 while (true) {
-                    bool missing = false;
+                    bool miss[CH];
+                    bool any = false;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (j < cnt && is_sentinel(dep[j])) missing = true;
-                    if (!missing) {
+                    for (int j = 0; j < CH; ++j) {
+                        miss[j] = false;
+                        if (j < cnt)
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
-                        if (last) st_relaxed(a.out + me, publishable(s));
+                            for (int v = 0; v < RT; ++v) miss[j] |= is_sentinel(dep[j][v]);
+                        any |= miss[j];
+                    }
+                    if (!any) {
+#pragma unroll
+                        for (int j = 0; j < CH; ++j)
+                            if (j < cnt)
+#pragma unroll
+                                for (int v = 0; v < RT; ++v) s[v] = fsub_mul(s[v], val[j], dep[j][v]);
+                        if (last) {
+                            double* o = a.out + me;
+#pragma unroll
+                            for (int v = 0; v < RT / 2; ++v)
+                                st_relaxed2(o + 2 * v, publishable(s[2 * v]), publishable(s[2 * v + 1]));
+                        }
                         break;
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (j < cnt && is_sentinel(dep[j]))
-                            dep[j] = ld_relaxed(a.out + static_cast<int64_t>(col[j]) * RT + k);
+                    for (int j = 0; j < CH; ++j)
+                        if (miss[j])
+#pragma unroll
+                            for (int v = 0; v < RT / 2; ++v) {
+                                const double2 t = ld_relaxed2(a.out + static_cast<int64_t>(col[j]) * RT + 2 * v);
+                                dep[j][2 * v] = t.x;
+                                dep[j][2 * v + 1] = t.y;
+                            }
                     if (++spins == (1u << 24)) {
                         atomicExch(&a.tickets[3], 1);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
+                        for (int j = 0; j < CH; ++j)
+#pragma unroll
+                            for (int v = 0; v < RT; ++v)
+                                if (is_sentinel(dep[j][v])) dep[j][v] = 0.0;
                     }
                 }
                 if (last) break;
             }
-            if (BWD && a.r) contrib = __dmul_rn(a.r[me], s);
+            if (BWD && a.r) {
+                const double2* r2 = reinterpret_cast<const double2*>(a.r + me);
+#pragma unroll
+                for (int v = 0; v < RT / 2; ++v) {
+                    const double2 t = r2[v];
+                    contrib[2 * v] = __dmul_rn(t.x, s[2 * v]);
+                    contrib[2 * v + 1] = __dmul_rn(t.y, s[2 * v + 1]);
+                }
+            }
         }
         if (BWD && a.r) {
             // per-tile partials (RT values) -> groups -> total, deterministic
-            block_sum_k<RT>(contrib, scratch, part);
+            block_sum_dyn<RT>(contrib, RT, scratch, part);
             const int g = tile / kGroup;
             const int ngroups = (ntiles + kGroup - 1) / kGroup;
             const int gsize = min(kGroup, ntiles - g * kGroup);
@@ -401,11 +441,12 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
     }
 }
 
-// p = z (+ W u) (+ beta p) for running rhs; sweep buffers back to the sentinel
+// p = z (+ W u) (+ beta p) for running rhs, lane per row (W read once for all rhs); sweep
+// buffers back to the sentinel
 template <int RT>
 __global__ void __launch_bounds__(kStreamThreads) k_b_pupdate(const double* __restrict__ z, double* __restrict__ p,
                                                               double* __restrict__ zs_reset, double* __restrict__ y_reset,
-                                                              int64_t total, BState* st, const double* __restrict__ W,
+                                                              int32_t n, BState* st, const double* __restrict__ W,
                                                               int64_t ldw, int m, const double* __restrict__ u) {
     __shared__ double beta[RT];
     __shared__ int run[RT];
@@ -417,19 +458,33 @@ __global__ void __launch_bounds__(kStreamThreads) k_b_pupdate(const double* __re
     }
     if (threadIdx.x == 0) first = st->iter == 1;
     __syncthreads();
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int k = static_cast<int>(e % RT);
-        if (run[k]) {
-            double zi = z[e];
-            if (W) {
-                const int64_t i = e / RT;
-                for (int j = 0; j < m; ++j) zi = fadd_mul(zi, u[j * RT + k], __ldg(W + j * ldw + i));
-            }
-            p[e] = first ? zi : fadd_mul(zi, beta[k], p[e]);
+    const double sent = sentinel();
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t me = static_cast<int64_t>(i) * RT;
+        double zi[RT];
+#pragma unroll
+        for (int v = 0; v < RT / 2; ++v) {
+            const double2 t = reinterpret_cast<const double2*>(z + me)[v];
+            zi[2 * v] = t.x;
+            zi[2 * v + 1] = t.y;
         }
+        if (W)
+            for (int j = 0; j < m; ++j) {
+                const double wj = __ldg(W + j * ldw + i);
+#pragma unroll
+                for (int v = 0; v < RT; ++v) zi[v] = fadd_mul(zi[v], u[j * RT + v], wj);
+            }
+#pragma unroll
+        for (int v = 0; v < RT; ++v)
+            if (run[v]) p[me + v] = first ? zi[v] : fadd_mul(zi[v], beta[v], p[me + v]);
         if (zs_reset) {
-            zs_reset[e] = sentinel();
-            y_reset[e] = sentinel();
+            double2* zr = reinterpret_cast<double2*>(zs_reset + me);
+            double2* yr = reinterpret_cast<double2*>(y_reset + me);
+#pragma unroll
+            for (int v = 0; v < RT / 2; ++v) {
+                zr[v] = make_double2(sent, sent);
+                yr[v] = make_double2(sent, sent);
+            }
         }
     }
 }
@@ -468,36 +523,42 @@ __global__ void __launch_bounds__(kSpmvThreads) k_b_spmv_pq(SpmvArgs a, int cap,
     }
 }
 
-// f[j][k] = W_j . y_k ; finaliser: u[:,k] = (W^T A W)^-1 f[:,k] (mode 1) and f.u (mode 2)
+// f[j][k] = W_j . y_k, lane per row (W_j[i] read once for all rhs); finaliser per rhs:
+// u[:,k] = (W^T A W)^-1 f[:,k] (mode 1) and f.u (mode 2)
 template <int RT>
 __global__ void __launch_bounds__(kStreamThreads) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
                                                             const double* __restrict__ y, int32_t n, double* partials,
                                                             const double* __restrict__ L, double* __restrict__ u,
                                                             int mode, BState* st, int respect_done) {
-    __shared__ double scratch[RT * 32];
-    __shared__ double part[RT];
+    constexpr int JC = RT <= 4 ? 8 : (RT <= 8 ? 4 : 2);
+    __shared__ double scratch[32 * JC * RT];
     __shared__ double bvals[kMaxRedB];
     __shared__ double tot[kMaxRedB];
     __shared__ double fk[8][128];
     __shared__ double sol[8][128];
     if (respect_done && st->nrun == 0) return;
-    const int64_t total = static_cast<int64_t>(n) * RT;
-    for (int j0 = 0; j0 < m; j0 += 8) {
-        const int mc = min(8, m - j0);
-        double acc[8];
+    for (int j0 = 0; j0 < m; j0 += JC) {
+        const int mc = min(JC, m - j0);
+        double acc[JC * RT];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-            const double ye = y[e];
-            const int64_t i = e / RT;
+        for (int c = 0; c < JC * RT; ++c) acc[c] = 0.0;
+        for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            double yi[RT];
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (c < mc) acc[c] = fadd_mul(acc[c], __ldg(W + (j0 + c) * ldw + i), ye);
+            for (int v = 0; v < RT / 2; ++v) {
+                const double2 t = reinterpret_cast<const double2*>(y + static_cast<int64_t>(i) * RT)[v];
+                yi[2 * v] = t.x;
+                yi[2 * v + 1] = t.y;
+            }
+#pragma unroll
+            for (int c = 0; c < JC; ++c)
+                if (c < mc) {
+                    const double wj = __ldg(W + (j0 + c) * ldw + i);
+#pragma unroll
+                    for (int v = 0; v < RT; ++v) acc[c * RT + v] = fadd_mul(acc[c * RT + v], wj, yi[v]);
+                }
         }
-        for (int c = 0; c < mc; ++c) {
-            block_sum_k<RT>(acc[c], scratch, part);
-            if (threadIdx.x < RT) bvals[(j0 + c) * RT + threadIdx.x] = part[threadIdx.x];
-        }
+        block_sum_dyn<JC * RT>(acc, mc * RT, scratch, bvals + j0 * RT);
     }
     __syncthreads();
     if (grid_reduce_dyn(bvals, m * RT, partials, &st->tick[2], tot)) {
@@ -506,7 +567,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_b_tallt(const double* __rest
             for (int j = lane; j < m; j += 32) fk[wid][j] = tot[j * RT + k];
             __syncwarp();
             double* uk = sol[wid];
-            warp_chol_solve(L, m, fk[wid], uk, uk);  // solution lands in uk (scratch == output)
+            warp_chol_solve(L, m, fk[wid], uk, uk);
             __syncwarp();
             for (int j = lane; j < m; j += 32) u[j * RT + k] = uk[j];
             if (mode == 2 && lane == 0) {
@@ -519,31 +580,41 @@ __global__ void __launch_bounds__(kStreamThreads) k_b_tallt(const double* __rest
     }
 }
 
-// y -= sum_j u[j][k] C_j (running rhs) with (p, y) -> alpha (mode 0) or (y, y) initial check (1)
+// y -= sum_j u[j][k] C_j (running rhs, lane per row) with (p, y) -> alpha (mode 0) or the
+// projected initial residual check (mode 1)
 template <int RT>
-__global__ void __launch_bounds__(kStreamThreads) k_b_deflate(double* __restrict__ y, const double* __restrict__ C,
+__global__ void __launch_bounds__(kStreamThreads) k_b_deflate(double* __restrict__ y, const double* __restrict__ Cm,
                                                               int64_t ldc, int m, const double* __restrict__ u,
                                                               const double* __restrict__ p, int32_t n, double* partials,
                                                               BState* st, int mode) {
-    __shared__ double scratch[RT * 32];
+    __shared__ double scratch[32 * RT];
     __shared__ double vals[RT];
     __shared__ double tot[RT];
     __shared__ int run[RT];
     if (st->nrun == 0 && mode == 0) return;
     if (threadIdx.x < RT) run[threadIdx.x] = mode == 1 || st->done[threadIdx.x] == kRunning;
     __syncthreads();
-    const int64_t total = static_cast<int64_t>(n) * RT;
-    double acc = 0.0;  // every thread keeps one rhs: k = threadIdx.x % RT for all its elements
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int k = static_cast<int>(e % RT);
-        if (!run[k]) continue;
-        const int64_t i = e / RT;
-        double v = y[e];
-        for (int j = 0; j < m; ++j) v = fsub_mul(v, u[j * RT + k], __ldg(C + j * ldc + i));
-        y[e] = v;
-        acc = mode == 0 ? fadd_mul(acc, p[e], v) : fadd_mul(acc, v, v);
+    double acc[RT];
+#pragma unroll
+    for (int v = 0; v < RT; ++v) acc[v] = 0.0;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t me = static_cast<int64_t>(i) * RT;
+        double yv[RT];
+#pragma unroll
+        for (int v = 0; v < RT; ++v) yv[v] = y[me + v];
+        for (int j = 0; j < m; ++j) {
+            const double cj = __ldg(Cm + j * ldc + i);
+#pragma unroll
+            for (int v = 0; v < RT; ++v) yv[v] = fsub_mul(yv[v], u[j * RT + v], cj);
+        }
+#pragma unroll
+        for (int v = 0; v < RT; ++v)
+            if (run[v]) {
+                y[me + v] = yv[v];
+                acc[v] = mode == 0 ? fadd_mul(acc[v], p[me + v], yv[v]) : fadd_mul(acc[v], yv[v], yv[v]);
+            }
     }
-    block_sum_k<RT>(acc, scratch, vals);
+    block_sum_dyn<RT>(acc, RT, scratch, vals);
     if (grid_reduce_dyn(vals, RT, partials, &st->tick[3], tot) && threadIdx.x < RT) {
         const int k = threadIdx.x;
         if (mode == 0) {
@@ -563,13 +634,13 @@ __global__ void __launch_bounds__(kStreamThreads) k_b_deflate(double* __restrict
     }
 }
 
-// x += alpha p, r -= alpha q for running rhs; relres, history, convergence per rhs
+// x += alpha p, r -= alpha q for running rhs (lane per row); relres, history, convergence
 template <int RT>
 __global__ void __launch_bounds__(kStreamThreads) k_b_xr(double* __restrict__ x, double* __restrict__ r,
                                                          const double* __restrict__ p, const double* __restrict__ q,
                                                          int32_t n, double* partials, BState* st,
                                                          double* __restrict__ hist, int64_t hist_ld, int identity) {
-    __shared__ double scratch[RT * 32];
+    __shared__ double scratch[32 * RT];
     __shared__ double vals[RT];
     __shared__ double tot[RT];
     __shared__ double alpha[RT];
@@ -580,17 +651,21 @@ __global__ void __launch_bounds__(kStreamThreads) k_b_xr(double* __restrict__ x,
         run[threadIdx.x] = st->done[threadIdx.x] == kRunning;
     }
     __syncthreads();
-    const int64_t total = static_cast<int64_t>(n) * RT;
-    double acc = 0.0;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int k = static_cast<int>(e % RT);
-        if (!run[k]) continue;
-        x[e] = fadd_mul(x[e], alpha[k], p[e]);
-        const double ri = fsub_mul(r[e], alpha[k], q[e]);
-        r[e] = ri;
-        acc = fadd_mul(acc, ri, ri);
+    double acc[RT];
+#pragma unroll
+    for (int v = 0; v < RT; ++v) acc[v] = 0.0;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t me = static_cast<int64_t>(i) * RT;
+#pragma unroll
+        for (int v = 0; v < RT; ++v)
+            if (run[v]) {
+                x[me + v] = fadd_mul(x[me + v], alpha[v], p[me + v]);
+                const double ri = fsub_mul(r[me + v], alpha[v], q[me + v]);
+                r[me + v] = ri;
+                acc[v] = fadd_mul(acc[v], ri, ri);
+            }
     }
-    block_sum_k<RT>(acc, scratch, vals);
+    block_sum_dyn<RT>(acc, RT, scratch, vals);
     if (grid_reduce_dyn(vals, RT, partials, &st->tick[4], tot)) {
         if (threadIdx.x < RT) {
             const int k = threadIdx.x;
@@ -677,12 +752,11 @@ struct BatchSolve {
         if (defl) mm = std::max(mm, defl->k);
         require(mm * RT <= kMaxRedB, "batch: basis columns x right-hand sides exceed the reduction capacity");
         const int64_t nrt = static_cast<int64_t>(n) * RT;
-        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 128 / RT - 1) / (128 / RT)
-                            : 1;
+        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 127) / 128 : 1;
         const int64_t groups = (ntiles + kGroup - 1) / kGroup;
         const int64_t part = std::max<int64_t>(ntiles * RT, static_cast<int64_t>(kMaxRedB) * ctx->num_sms * 8);
         w = &batch_ws(ctx, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
-        sg = stream_grid(ctx, nrt);
+        sg = stream_grid(ctx, n);
         pg = spmv_grid(ctx, n);
         static bool prepared = false;
         if (!prepared) {
@@ -763,7 +837,7 @@ struct BatchSolve {
         require(ic || !sc, "batch: subspace correction needs the IC inner preconditioner");
         {
             KTimer t(ctx, 3);
-            k_b_pupdate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(z, w->p, ic ? w->zs : nullptr, w->y, nrt, w->st,
+            k_b_pupdate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(z, w->p, ic ? w->zs : nullptr, w->y, n, w->st,
                                                                     sc ? scb->w : nullptr, sc ? scb->ld : 0,
                                                                     sc ? scb->k : 0, w->u2);
             RCG_LAUNCHED(ctx);
@@ -800,8 +874,7 @@ struct BatchSolve {
 
     void launch_b_sweep(bool backward, SweepArgs& s) {
         const rcg_ic* f = m->ic;
-        const int rows = 128 / RT;
-        const int ntiles = (s.npos + rows - 1) / rows;
+        const int ntiles = (s.npos + 127) / 128;
         const int levels = backward ? f->bwd_levels : f->fwd_levels;
         const int64_t rows_per_level = levels > 0 ? s.npos / levels : s.npos;
         const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : (rows_per_level >= 65536 ? 8 : 2);
@@ -937,14 +1010,16 @@ static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const
         check_cfg(cfg);
         check_prec(m, a->n);
         if (defl && defl->k > 0) require(defl->n == a->n, "deflated_pcg_solve: W row count does not match A");
-        if (nrhs <= 2)
-            batch_solve<2>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
-        else if (nrhs <= 4)
-            batch_solve<4>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
-        else if (nrhs <= 8)
-            batch_solve<8>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
-        else
-            batch_solve<16>(ctx, a, B, m, defl, X, cfg, nrhs, reps);
+        switch ((nrhs + 1) / 2 * 2) {  // RT: nrhs rounded up to even (16-byte row accesses)
+            case 2: batch_solve<2>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+            case 4: batch_solve<4>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+            case 6: batch_solve<6>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+            case 8: batch_solve<8>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+            case 10: batch_solve<10>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+            case 12: batch_solve<12>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+            case 14: batch_solve<14>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+            default: batch_solve<16>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+        }
     });
 }
 
