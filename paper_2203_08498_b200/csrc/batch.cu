@@ -1,7 +1,7 @@
 // batch.cu -- batched multi-RHS PCG / SC-PCG / deflated PCG: R independent right-hand sides of
 // one matrix solved by ONE kernel sequence (the sequence protocol's solves 2..k are independent
-// given W, driver.cpp:181-195).  Vectors are stored interleaved, v[i*RT + k] (RT = R rounded up
-// to a power of two; padding columns are zero right-hand sides, done before the first
+// given W, driver.cpp:181-195).  Vectors are stored interleaved, v[i*RT + k] (RT = 2 for R <= 2,
+// else R rounded up to a multiple of 4; padding columns are zero right-hand sides, done before the first
 // iteration).  Every RHS keeps its own alpha, beta, rho, relres, convergence flag and
 // iteration count; converged RHS are frozen while the others continue.
 //
@@ -211,6 +211,110 @@ __device__ __forceinline__ void bspmv_rows(const SpmvArgs& a, const double* __re
     }
 }
 
+__device__ __forceinline__ void ldg4(const double* p, double* v) {
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+
+// RT % 4 == 0: G = RT/4 lanes per row, each carrying one 32-byte chunk of the row's values, so
+// a warp's gather instruction reads whole chunks of consecutive rows (for stencil rows: one
+// contiguous run) instead of one 16-byte piece per row.  Items of a 32-row tile are (row,
+// chunk) pairs, row-major; every value's sum runs over the row's entries in CSR order, so each
+// result is bitwise the single-vector spmv.  body(row, chunk, acc[4]).
+template <int RT, class Body>
+__device__ __forceinline__ void bspmv_chunks(const SpmvArgs& a, const double* __restrict__ x, int cap, Body&& body) {
+    constexpr int G = RT / 4;
+    extern __shared__ __align__(16) unsigned char pipe_smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned char* base = pipe_smem + static_cast<size_t>(wid) * (16 + 2 * cap * 12);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base);
+    double* sv = reinterpret_cast<double*>(base + 16);
+    int32_t* sc = reinterpret_cast<int32_t*>(base + 16 + 2 * cap * 8);
+    if (lane == 0) {
+        mbar_init(&bar[0]);
+        mbar_init(&bar[1]);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const int ntiles = (a.n + 31) / 32;
+    const int nw = gridDim.x * kPipeWarps;
+    unsigned phase[2] = {0u, 0u};
+    auto issue = [&](int t, int stg) -> bool {
+        const int32_t r0 = t * 32, rend = min(r0 + 32, a.n);
+        const int32_t e0a = __ldg(a.rs + r0) & ~3;
+        const int32_t e1a = (__ldg(a.rs + rend) + 3) & ~3;
+        const int cnt = e1a - e0a;
+        if (cnt > cap) return false;
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&bar[stg], static_cast<unsigned>(cnt) * 12u);
+            if (cnt > 0) {
+                bulk_g2s(sv + stg * cap, a.va + e0a, static_cast<unsigned>(cnt) * 8u, &bar[stg]);
+                bulk_g2s(sc + stg * cap, a.ci + e0a, static_cast<unsigned>(cnt) * 4u, &bar[stg]);
+            }
+        }
+        return true;
+    };
+    int t = blockIdx.x * kPipeWarps + wid;
+    int stg = 0;
+    bool bulk_cur = t < ntiles ? issue(t, 0) : false;
+    for (; t < ntiles; t += nw) {
+        const int tn = t + nw;
+        const bool bulk_next = tn < ntiles ? issue(tn, stg ^ 1) : false;
+        const int32_t r0 = t * 32;
+        const double* vsrc = a.va;
+        const int32_t* csrc = a.ci;
+        int32_t off = 0;
+        if (bulk_cur) {
+            while (!mbar_try_wait(&bar[stg], phase[stg])) {
+            }
+            phase[stg] ^= 1u;
+            vsrc = sv + stg * cap;
+            csrc = sc + stg * cap;
+            off = __ldg(a.rs + r0) & ~3;
+        }
+#pragma unroll
+        for (int pass = 0; pass < G; ++pass) {
+            const int item = pass * 32 + lane;
+            const int32_t row = r0 + item / G;
+            const int c = item % G;
+            if (row < a.n) {
+                const int32_t b = __ldg(a.rs + row), e = __ldg(a.rs + row + 1);
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                int32_t k = b;
+                for (; k + 1 < e; k += 2) {
+                    const double a0 = vsrc[k - off], a1 = vsrc[k + 1 - off];
+                    double x0[4], x1[4];
+                    ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
+                    ldg4(x + static_cast<int64_t>(csrc[k + 1 - off]) * RT + 4 * c, x1);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(fadd_mul(acc[i], a0, x0[i]), a1, x1[i]);
+                }
+                if (k < e) {
+                    const double a0 = vsrc[k - off];
+                    double x0[4];
+                    ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(acc[i], a0, x0[i]);
+                }
+                body(row, c, acc);
+            }
+        }
+        __syncwarp();
+        stg ^= 1;
+        bulk_cur = bulk_next;
+    }
+}
+
+// per-thread per-rhs accumulator update for chunk c (c is lane-dependent; unrolled select)
+template <int RT, class F>
+__device__ __forceinline__ void chunk_acc(double (&accs)[RT], int c, F&& f) {
+#pragma unroll
+    for (int cc = 0; cc < RT / 4; ++cc)
+        if (cc == c)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) accs[4 * cc + i] = f(accs[4 * cc + i], i);
+}
+
 // r = b - A x for all RT; finaliser: bnorm, rho = rr, already-converged / zero-rhs flags
 template <int RT>
 __global__ void __launch_bounds__(kSpmvThreads) k_b_residual(SpmvArgs a, int cap, const double* __restrict__ b,
@@ -222,16 +326,31 @@ __global__ void __launch_bounds__(kSpmvThreads) k_b_residual(SpmvArgs a, int cap
     double bb[RT], rr[RT];
 #pragma unroll
     for (int v = 0; v < RT; ++v) bb[v] = rr[v] = 0.0;
-    bspmv_rows<RT>(a, x, cap, [&](int32_t row, const double (&acc)[RT]) {
+    if constexpr (RT % 4 == 0) {
+        bspmv_chunks<RT>(a, x, cap, [&](int32_t row, int c, const double (&acc)[4]) {
+            const int64_t o = static_cast<int64_t>(row) * RT + 4 * c;
+            double bi[4], ri[4];
 #pragma unroll
-        for (int v = 0; v < RT; ++v) {
-            const double bi = b[static_cast<int64_t>(row) * RT + v];
-            const double ri = __dsub_rn(bi, acc[v]);
-            r[static_cast<int64_t>(row) * RT + v] = ri;
-            bb[v] = fadd_mul(bb[v], bi, bi);
-            rr[v] = fadd_mul(rr[v], ri, ri);
-        }
-    });
+            for (int i = 0; i < 4; ++i) {
+                bi[i] = b[o + i];
+                ri[i] = __dsub_rn(bi[i], acc[i]);
+                r[o + i] = ri[i];
+            }
+            chunk_acc<RT>(bb, c, [&](double s, int i) { return fadd_mul(s, bi[i], bi[i]); });
+            chunk_acc<RT>(rr, c, [&](double s, int i) { return fadd_mul(s, ri[i], ri[i]); });
+        });
+    } else {
+        bspmv_rows<RT>(a, x, cap, [&](int32_t row, const double (&acc)[RT]) {
+#pragma unroll
+            for (int v = 0; v < RT; ++v) {
+                const double bi = b[static_cast<int64_t>(row) * RT + v];
+                const double ri = __dsub_rn(bi, acc[v]);
+                r[static_cast<int64_t>(row) * RT + v] = ri;
+                bb[v] = fadd_mul(bb[v], bi, bi);
+                rr[v] = fadd_mul(rr[v], ri, ri);
+            }
+        });
+    }
     // block reduction of 2*RT per-thread values
     double accs[2 * RT];
 #pragma unroll
@@ -260,36 +379,54 @@ __global__ void k_b_count(BState* st, int RT) {
     st->nrun = c;
 }
 
-// 16-byte relaxed accesses of two interleaved values (each value its own ready flag)
-__device__ __forceinline__ double2 ld_relaxed2(const double* p) {
-    double2 v;
-    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed2(double* p, double a, double b) {
-    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
-}
+// 16- / 32-byte relaxed accesses of interleaved values (each value its own ready flag; a
+// 32-byte access is one LDG/STG.E.ENL2.256 on sm_100a)
+template <int VW>
+struct RelVec;
+template <>
+struct RelVec<2> {
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+        asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p) : "memory");
+    }
+    static __device__ __forceinline__ void st(double* p, const double* v) {
+        asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v[0]), "d"(v[1]) : "memory");
+    }
+};
+template <>
+struct RelVec<4> {
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+        asm volatile("ld.relaxed.gpu.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(p)
+                     : "memory");
+    }
+    static __device__ __forceinline__ void st(double* p, const double* v) {
+        asm volatile("st.relaxed.gpu.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]),
+                     "d"(v[3])
+                     : "memory");
+    }
+};
 
-// One sweep, lane per row carrying all RT values: the same 128-row tiles, the same number of
-// polling lanes and the same dependency waits as the single-RHS sweep, RT times the bytes.
+// One sweep, lane per row carrying all RT values.  Tiles are 32 positions taken by a WARP from
+// the ticket counter (not 128 per CTA as in the single sweep): a level's rows then spread over
+// ~4x more SMs, so the burst of RT-wide reloads and stores when a level's parents publish is
+// not concentrated on a few SMs' L2 ports.  Monotone tickets keep the schedule deadlock-free.
 // Parents are loaded in chunks of CH entries (every value of a chunk in flight together) and
 // the missing entries re-polled together; the row is published from inside the wait loop.
 template <bool BWD, int RT>
 __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
     constexpr int CH = RT <= 4 ? 8 : (RT <= 8 ? 4 : 3);
-    __shared__ int s_tile;
-    __shared__ double scratch[32 * RT];
-    __shared__ double part[RT];
-    __shared__ bool s_last_group, s_last;
+    constexpr int VW = RT % 4 == 0 ? 4 : 2;  // doubles per relaxed access (32 B beats 2 x 16 B)
+    constexpr int NC = RT / VW;
     if (st->nrun == 0) return;
-    const int ntiles = (a.npos + 127) / 128;
+    const int lane = threadIdx.x & 31;
+    const int ntiles = (a.npos + 31) / 32;
     while (true) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
-        __syncthreads();
-        const int tile = s_tile;
-        __syncthreads();
+        int tile = 0;
+        if (lane == 0) tile = atomicAdd(&a.tickets[0], 1);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= ntiles) break;
-        const int pos = tile * 128 + threadIdx.x;
+        const int pos = tile * 32 + lane;
         double contrib[RT];
 #pragma unroll
         for (int v = 0; v < RT; ++v) contrib[v] = 0.0;
@@ -323,11 +460,7 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
                 for (int j = 0; j < CH; ++j)
                     if (j < cnt)
 #pragma unroll
-                        for (int v = 0; v < RT / 2; ++v) {
-                            const double2 t = ld_relaxed2(a.out + static_cast<int64_t>(col[j]) * RT + 2 * v);
-                            dep[j][2 * v] = t.x;
-                            dep[j][2 * v + 1] = t.y;
-                        }
+                        for (int c = 0; c < NC; ++c) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + c * VW, &dep[j][c * VW]);
                 while (true) {
                     bool miss[CH];
                     bool any = false;
@@ -348,20 +481,30 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
                         if (last) {
                             double* o = a.out + me;
 #pragma unroll
-                            for (int v = 0; v < RT / 2; ++v)
-                                st_relaxed2(o + 2 * v, publishable(s[2 * v]), publishable(s[2 * v + 1]));
+                            for (int c = 0; c < NC; ++c) {
+                                double t[VW];
+#pragma unroll
+                                for (int i = 0; i < VW; ++i) t[i] = publishable(s[c * VW + i]);
+                                RelVec<VW>::st(o + c * VW, t);
+                            }
                         }
                         break;
                     }
+                    if (a.backoff_ns) __nanosleep(a.backoff_ns);
+                    // re-poll every chunk still missing (polling only a parent's last-published
+                    // chunk first costs a second round trip per level once it arrives)
 #pragma unroll
                     for (int j = 0; j < CH; ++j)
-                        if (miss[j])
+                        if (miss[j]) {
+                            const double* pj = a.out + static_cast<int64_t>(col[j]) * RT;
 #pragma unroll
-                            for (int v = 0; v < RT / 2; ++v) {
-                                const double2 t = ld_relaxed2(a.out + static_cast<int64_t>(col[j]) * RT + 2 * v);
-                                dep[j][2 * v] = t.x;
-                                dep[j][2 * v + 1] = t.y;
+                            for (int c = 0; c < NC; ++c) {
+                                bool m = false;
+#pragma unroll
+                                for (int i = 0; i < VW; ++i) m |= is_sentinel(dep[j][c * VW + i]);
+                                if (m) RelVec<VW>::ld(pj + c * VW, &dep[j][c * VW]);
                             }
+                        }
                     if (++spins == (1u << 24)) {
                         atomicExch(&a.tickets[3], 1);
 #pragma unroll
@@ -384,57 +527,59 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
             }
         }
         if (BWD && a.r) {
-            // per-tile partials (RT values) -> groups -> total, deterministic
-            block_sum_dyn<RT>(contrib, RT, scratch, part);
+            // per-tile partials (RT values) -> groups of kGroup tiles -> total, fixed order
+#pragma unroll
+            for (int v = 0; v < RT; ++v) {
+                const double t = warp_sum(contrib[v]);
+                if (lane == v) a.partials[static_cast<int64_t>(tile) * RT + v] = t;
+            }
             const int g = tile / kGroup;
             const int ngroups = (ntiles + kGroup - 1) / kGroup;
             const int gsize = min(kGroup, ntiles - g * kGroup);
-            if (threadIdx.x < RT) a.partials[static_cast<int64_t>(tile) * RT + threadIdx.x] = part[threadIdx.x];
             __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0) s_last_group = atomicAdd(&a.gcount[g], 1u) == static_cast<unsigned>(gsize) - 1u;
-            __syncthreads();
-            if (s_last_group) {
+            __syncwarp();
+            int last_group = 0;
+            if (lane == 0) last_group = atomicAdd(&a.gcount[g], 1u) == static_cast<unsigned>(gsize) - 1u;
+            if (__shfl_sync(0xffffffffu, last_group, 0)) {
                 __threadfence();
-                if (threadIdx.x < RT) {
+                if (lane < RT) {
                     double sg = 0.0;
                     for (int q = 0; q < gsize; ++q)
-                        sg = __dadd_rn(sg, __ldcg(a.partials + static_cast<int64_t>(g * kGroup + q) * RT + threadIdx.x));
-                    a.gpart[static_cast<int64_t>(g) * RT + threadIdx.x] = sg;
+                        sg = __dadd_rn(sg, __ldcg(a.partials + static_cast<int64_t>(g * kGroup + q) * RT + lane));
+                    a.gpart[static_cast<int64_t>(g) * RT + lane] = sg;
                 }
                 __threadfence();
-                __syncthreads();
-                if (threadIdx.x == 0) {
+                __syncwarp();
+                int last = 0;
+                if (lane == 0) {
                     a.gcount[g] = 0u;
-                    s_last = atomicAdd(reinterpret_cast<unsigned int*>(&a.tickets[2]), 1u) ==
-                             static_cast<unsigned>(ngroups) - 1u;
+                    last = atomicAdd(reinterpret_cast<unsigned int*>(&a.tickets[2]), 1u) ==
+                           static_cast<unsigned>(ngroups) - 1u;
                 }
-                __syncthreads();
-                if (s_last) {
+                if (__shfl_sync(0xffffffffu, last, 0)) {
                     __threadfence();
-                    if (threadIdx.x < RT) {
-                        const int kk = threadIdx.x;
+                    if (lane < RT) {
                         double rho = 0.0;
                         for (int q = 0; q < ngroups; ++q)
-                            rho = __dadd_rn(rho, __ldcg(a.gpart + static_cast<int64_t>(q) * RT + kk));
-                        if (st->done[kk] == kRunning) {
-                            if (a.add_sc) rho = __dadd_rn(rho, st->scal2[kk]);
-                            st->rho[kk] = rho;
+                            rho = __dadd_rn(rho, __ldcg(a.gpart + static_cast<int64_t>(q) * RT + lane));
+                        if (st->done[lane] == kRunning) {
+                            if (a.add_sc) rho = __dadd_rn(rho, st->scal2[lane]);
+                            st->rho[lane] = rho;
                             if (rho <= 0.0) {
-                                st->done[kk] = kBroken;
-                                st->status[kk] = kBrkRz;
+                                st->done[lane] = kBroken;
+                                st->status[lane] = kBrkRz;
                             }
-                            st->beta[kk] = st->iter > 1 ? rho / st->rho_prev[kk] : 0.0;
+                            st->beta[lane] = st->iter > 1 ? rho / st->rho_prev[lane] : 0.0;
                         }
                     }
-                    if (threadIdx.x == 0) a.tickets[2] = 0;
+                    if (lane == 0) a.tickets[2] = 0;
                 }
             }
         }
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         __threadfence();
-        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x) - 1) {
+        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x * (blockDim.x / 32)) - 1) {
             a.tickets[0] = 0;
             a.tickets[1] = 0;
         }
@@ -501,13 +646,26 @@ __global__ void __launch_bounds__(kSpmvThreads) k_b_spmv_pq(SpmvArgs a, int cap,
     double pq[RT];
 #pragma unroll
     for (int v = 0; v < RT; ++v) pq[v] = 0.0;
-    bspmv_rows<RT>(a, p, cap, [&](int32_t row, const double (&acc)[RT]) {
+    if constexpr (RT % 4 == 0) {
+        bspmv_chunks<RT>(a, p, cap, [&](int32_t row, int c, const double (&acc)[4]) {
+            const int64_t o = static_cast<int64_t>(row) * RT + 4 * c;
+            double pi[4];
 #pragma unroll
-        for (int v = 0; v < RT; ++v) {
-            q[static_cast<int64_t>(row) * RT + v] = acc[v];
-            pq[v] = fadd_mul(pq[v], p[static_cast<int64_t>(row) * RT + v], acc[v]);
-        }
-    });
+            for (int i = 0; i < 4; ++i) {
+                q[o + i] = acc[i];
+                pi[i] = p[o + i];
+            }
+            chunk_acc<RT>(pq, c, [&](double s, int i) { return fadd_mul(s, pi[i], acc[i]); });
+        });
+    } else {
+        bspmv_rows<RT>(a, p, cap, [&](int32_t row, const double (&acc)[RT]) {
+#pragma unroll
+            for (int v = 0; v < RT; ++v) {
+                q[static_cast<int64_t>(row) * RT + v] = acc[v];
+                pq[v] = fadd_mul(pq[v], p[static_cast<int64_t>(row) * RT + v], acc[v]);
+            }
+        });
+    }
     if (project_later) return;
     block_sum_dyn<RT>(pq, RT, scratch, vals);
     if (grid_reduce_dyn(vals, RT, partials, &st->tick[1], tot) && threadIdx.x < RT) {
@@ -752,7 +910,7 @@ struct BatchSolve {
         if (defl) mm = std::max(mm, defl->k);
         require(mm * RT <= kMaxRedB, "batch: basis columns x right-hand sides exceed the reduction capacity");
         const int64_t nrt = static_cast<int64_t>(n) * RT;
-        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 127) / 128 : 1;
+        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 31) / 32 : 1;
         const int64_t groups = (ntiles + kGroup - 1) / kGroup;
         const int64_t part = std::max<int64_t>(ntiles * RT, static_cast<int64_t>(kMaxRedB) * ctx->num_sms * 8);
         w = &batch_ws(ctx, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
@@ -819,7 +977,6 @@ struct BatchSolve {
     }
 
     void iteration() {
-        const int64_t nrt = static_cast<int64_t>(n) * RT;
         const double* z = w->r;
         if (ic) {
             SweepArgs fa = swargs(false);
@@ -874,11 +1031,12 @@ struct BatchSolve {
 
     void launch_b_sweep(bool backward, SweepArgs& s) {
         const rcg_ic* f = m->ic;
-        const int ntiles = (s.npos + 127) / 128;
+        const int ntiles = (s.npos + 127) / 128;  // in CTAs of 4 warp tiles
         const int levels = backward ? f->bwd_levels : f->fwd_levels;
         const int64_t rows_per_level = levels > 0 ? s.npos / levels : s.npos;
         const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : (rows_per_level >= 65536 ? 8 : 2);
         const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
+        s.backoff_ns = ctx->sweep_backoff_ns;
         KTimer t(ctx, backward ? 2 : 1);
         if (backward)
             k_b_sweep<true, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
@@ -1010,14 +1168,13 @@ static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const
         check_cfg(cfg);
         check_prec(m, a->n);
         if (defl && defl->k > 0) require(defl->n == a->n, "deflated_pcg_solve: W row count does not match A");
-        switch ((nrhs + 1) / 2 * 2) {  // RT: nrhs rounded up to even (16-byte row accesses)
+        // RT: 2 for one or two right-hand sides, else nrhs rounded up to a multiple of 4 (32-byte
+        // chunks: one 256-bit access per chunk in the sweeps and spmv gathers)
+        switch (nrhs <= 2 ? 2 : (nrhs + 3) / 4 * 4) {
             case 2: batch_solve<2>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
             case 4: batch_solve<4>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
-            case 6: batch_solve<6>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
             case 8: batch_solve<8>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
-            case 10: batch_solve<10>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
             case 12: batch_solve<12>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
-            case 14: batch_solve<14>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
             default: batch_solve<16>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
         }
     });
