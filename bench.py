@@ -135,7 +135,7 @@ def run_ours(args, rank, world, local_rank):
     ctxs = _all_contexts(prep)
     for c_ in ctxs:
         c_.synchronize()
-        c_.set_profiling(True)
+        c_.set_profiling(PROFILE_TIMED)
         c_.reset_stats()
     launches0 = sum(c_.launches for c_ in ctxs)
     iters = 0
@@ -146,6 +146,12 @@ def run_ours(args, rank, world, local_rank):
         ctx.record(1)
         ms = ctx.elapsed_ms(0, 1)
     launches = sum(c_.launches for c_ in ctxs) - launches0
+    if not PROFILE_TIMED:  # kernel statistics from separate profiled steps
+        for c_ in ctxs:
+            c_.set_profiling(True)
+        for _ in range(args.steps):
+            step_device()
+        ctxs = _all_contexts(prep)
     stats = {}
     for c in range(5):
         per = [c_.kernel_stats(c) for c_ in ctxs]
@@ -296,6 +302,7 @@ def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
 # solves 2..10: "batch" = one multi-RHS kernel sequence (default); an integer = that many
 # concurrent single solves on their own streams
 _conc = os.environ.get("RCG_CONCURRENCY", "batch")
+PROFILE_TIMED = os.environ.get("RCG_BENCH_PROFILE_TIMED", "1") == "1"
 CONCURRENCY = _conc if _conc == "batch" else int(_conc)
 
 

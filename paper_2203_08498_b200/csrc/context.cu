@@ -1,5 +1,8 @@
 // context.cu -- context, workspaces, host/device staging, error strings, timing.
+#include <algorithm>
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 #include <cstdlib>
 #include <cstring>
 
@@ -20,22 +23,154 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
     throw Error(RCG_E_CUDA, buf);
 }
 
-double* dev_alloc(int64_t count) {
+// ------------------------------------------------------------------ device allocations
+// A block cache in front of cudaMalloc/cudaFree.  The sequence allocates and frees hundreds of
+// MB per step (sampler slots, the error block, W / AW, staging buffers); cudaMalloc/cudaFree of
+// such blocks are slow and erratic (cudaFree synchronises the device; a process's first large
+// allocations on a fresh GPU cost far more), so freed blocks are kept and reused.  A freed
+// block is fenced with one event per live context stream on its device and handed out again
+// only once every fence has completed -- the ordering cudaFree's implicit sync gave, without
+// the sync.  The cache is capped; an allocation failure releases it and retries.
+namespace {
+struct FreeBlock {
+    void* p;
+    size_t bytes;
+    int dev;
+    std::vector<cudaEvent_t> fences;
+};
+std::mutex g_mx;
+std::vector<rcg_ctx*> g_ctxs;
+std::unordered_map<void*, std::pair<size_t, int>> g_live;
+std::vector<FreeBlock> g_free;
+std::vector<cudaEvent_t> g_fence_pool;
+size_t g_cached = 0;
+constexpr size_t kCacheCap = size_t(48) << 30;
+
+size_t round_bytes(size_t b) {
+    if (b < 256) b = 256;
+    if (b < (size_t(1) << 20)) return (b + 511) & ~size_t(511);
+    return (b + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+}
+
+bool fences_done(FreeBlock& f) {
+    for (auto e : f.fences)
+        if (cudaEventQuery(e) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+    return true;
+}
+
+void recycle_fences(FreeBlock& f) {
+    for (auto e : f.fences) g_fence_pool.push_back(e);
+    f.fences.clear();
+}
+
+// caller holds g_mx
+void release_cached(int dev) {
+    cudaDeviceSynchronize();
+    for (size_t i = 0; i < g_free.size();) {
+        if (g_free[i].dev == dev) {
+            cudaFree(g_free[i].p);
+            g_cached -= g_free[i].bytes;
+            recycle_fences(g_free[i]);
+            g_free[i] = std::move(g_free.back());
+            g_free.pop_back();
+        } else {
+            ++i;
+        }
+    }
+}
+}  // namespace
+
+void register_ctx(rcg_ctx* c, bool add) {
+    std::lock_guard<std::mutex> lk(g_mx);
+    if (add) {
+        g_ctxs.push_back(c);
+    } else {
+        g_ctxs.erase(std::remove(g_ctxs.begin(), g_ctxs.end(), c), g_ctxs.end());
+    }
+}
+
+void* dev_alloc_bytes(size_t bytes) {
+    int dev = 0;
+    RCG_CK(cudaGetDevice(&dev));
+    const size_t rb = round_bytes(bytes);
+    std::lock_guard<std::mutex> lk(g_mx);
+    int best = -1;
+    for (size_t i = 0; i < g_free.size(); ++i) {
+        FreeBlock& f = g_free[i];
+        if (f.dev != dev || f.bytes < rb || f.bytes > rb + rb / 4) continue;
+        if (best >= 0 && f.bytes >= g_free[best].bytes) continue;
+        if (!fences_done(f)) continue;
+        best = static_cast<int>(i);
+        if (f.bytes == rb) break;
+    }
+    if (best >= 0) {
+        FreeBlock f = std::move(g_free[best]);
+        g_free[best] = std::move(g_free.back());
+        g_free.pop_back();
+        g_cached -= f.bytes;
+        recycle_fences(f);
+        g_live[f.p] = {f.bytes, dev};
+        return f.p;
+    }
     void* p = nullptr;
-    if (count <= 0) count = 1;
-    const cudaError_t e = cudaMalloc(&p, static_cast<size_t>(count) * sizeof(double));
+    cudaError_t e = cudaMalloc(&p, rb);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        release_cached(dev);
+        e = cudaMalloc(&p, rb);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         char buf[256];
-        std::snprintf(buf, sizeof buf, "device allocation of %lld bytes failed: %s",
-                      static_cast<long long>(count * 8), cudaGetErrorString(e));
+        std::snprintf(buf, sizeof buf, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
         throw Error(RCG_E_CUDA, buf);
     }
-    return static_cast<double*>(p);
+    g_live[p] = {rb, dev};
+    return p;
+}
+
+double* dev_alloc(int64_t count) {
+    if (count <= 0) count = 1;
+    return static_cast<double*>(dev_alloc_bytes(static_cast<size_t>(count) * sizeof(double)));
 }
 
 void dev_free(void* p) {
-    if (p) cudaFree(p);
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_mx);
+    auto it = g_live.find(p);
+    if (it == g_live.end()) {  // not from this allocator
+        cudaFree(p);
+        return;
+    }
+    FreeBlock f{p, it->second.first, it->second.second, {}};
+    g_live.erase(it);
+    if (g_cached + f.bytes > kCacheCap) {
+        cudaFree(p);
+        return;
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != f.dev) cudaSetDevice(f.dev);
+    for (rcg_ctx* c : g_ctxs) {
+        if (c->device != f.dev) continue;
+        cudaEvent_t e;
+        if (!g_fence_pool.empty()) {
+            e = g_fence_pool.back();
+            g_fence_pool.pop_back();
+        } else if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            cudaDeviceSynchronize();  // no event: fall back to a full fence
+            continue;
+        }
+        cudaEventRecord(e, c->stream);
+        f.fences.push_back(e);
+    }
+    if (cur != f.dev) cudaSetDevice(cur);
+    g_cached += f.bytes;
+    g_free.push_back(std::move(f));
 }
 
 bool is_device_ptr(const void* p) {
@@ -50,7 +185,7 @@ bool is_device_ptr(const void* p) {
 }
 
 Staged::~Staged() {
-    if (owned && dev) cudaFree(dev);
+    if (owned && dev) dev_free(dev);
 }
 
 void stage_in(rcg_ctx* ctx, const double* src, int64_t count, Staged& out) {
@@ -147,13 +282,34 @@ void ensure_workspace(rcg_ctx* ctx, int64_t n, int k, int64_t max_iter, int64_t 
     }
 }
 
-// Event pairs are recorded around each timed launch without synchronising; they are resolved
-// (and recycled) when the statistics are read, so timing does not serialise the stream.
-static cudaEvent_t pooled_event(rcg_ctx* ctx) {
-    if (ctx->ev_free.empty()) {
+// Event pairs are recorded around each timed launch without synchronising; completed pairs are
+// folded into the statistics and recycled as new events are needed (cudaEventQuery, no stream
+// sync), and the pool is pre-filled when profiling is switched on, so timing neither creates
+// events on the enqueue path nor serialises the stream.
+static void fold(rcg_ctx* ctx, const rcg_ctx::TimedLaunch& t) {
+    float ms = 0.f;
+    RCG_CK(cudaEventElapsedTime(&ms, t.start, t.stop));
+    ctx->stat_ms[t.cls] += ms;
+    ctx->stat_n[t.cls] += 1;
+    ctx->ev_free.push_back(t.start);
+    ctx->ev_free.push_back(t.stop);
+}
+
+static void grow_pool(rcg_ctx* ctx, int count) {
+    for (int i = 0; i < count; ++i) {
         cudaEvent_t e;
         RCG_CK(cudaEventCreate(&e));
-        return e;
+        ctx->ev_free.push_back(e);
+    }
+}
+
+static cudaEvent_t pooled_event(rcg_ctx* ctx) {
+    if (ctx->ev_free.empty()) {
+        while (!ctx->ev_pending.empty() && cudaEventQuery(ctx->ev_pending.front().stop) == cudaSuccess) {
+            fold(ctx, ctx->ev_pending.front());
+            ctx->ev_pending.pop_front();
+        }
+        if (ctx->ev_free.empty()) grow_pool(ctx, 512);
     }
     cudaEvent_t e = ctx->ev_free.back();
     ctx->ev_free.pop_back();
@@ -176,14 +332,7 @@ KTimer::~KTimer() {
 void resolve_timers(rcg_ctx* ctx) {
     if (ctx->ev_pending.empty()) return;
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    for (auto& t : ctx->ev_pending) {
-        float ms = 0.f;
-        RCG_CK(cudaEventElapsedTime(&ms, t.start, t.stop));
-        ctx->stat_ms[t.cls] += ms;
-        ctx->stat_n[t.cls] += 1;
-        ctx->ev_free.push_back(t.start);
-        ctx->ev_free.push_back(t.stop);
-    }
+    for (auto& t : ctx->ev_pending) fold(ctx, t);
     ctx->ev_pending.clear();
 }
 
@@ -222,6 +371,7 @@ int rcg_ctx_create(int device, rcg_ctx** out) {
         if (const char* e = std::getenv("RCG_SWEEP_BACKOFF_NS")) c->sweep_backoff_ns = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("RCG_SPMV_BPS")) c->spmv_bps = std::max(1, std::atoi(e));
         RCG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        register_ctx(c, true);
         RCG_CK(cudaEventCreate(&c->ev0));
         RCG_CK(cudaEventCreate(&c->ev1));
         void* hp = nullptr;
@@ -235,6 +385,7 @@ void rcg_ctx_destroy(rcg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    register_ctx(ctx, false);
     batch_ws_free(ctx);
     Workspace& w = ctx->ws;
     for (void* p : {(void*)w.r, (void*)w.z, (void*)w.p, (void*)w.q, (void*)w.ybuf, (void*)w.zs,
@@ -264,7 +415,11 @@ int rcg_ctx_synchronize(rcg_ctx* ctx) {
 int64_t rcg_ctx_launch_count(const rcg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable) {
-    return guard([&] { ctx->profiling = enable != 0; });
+    return guard([&] {
+        ctx->profiling = enable != 0;
+        const size_t want = 8192;
+        if (ctx->profiling && ctx->ev_free.size() < want) grow_pool(ctx, static_cast<int>(want - ctx->ev_free.size()));
+    });
 }
 
 int rcg_ctx_event_record(rcg_ctx* ctx, int slot) {

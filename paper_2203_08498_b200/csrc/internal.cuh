@@ -13,6 +13,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <deque>
 #include <vector>
 
 #include "rcg_b200.h"
@@ -158,7 +159,7 @@ struct rcg_ctx {
         int cls;
         cudaEvent_t start, stop;
     };
-    std::vector<TimedLaunch> ev_pending;
+    std::deque<TimedLaunch> ev_pending;
     std::vector<cudaEvent_t> ev_free;
     cudaEvent_t user_ev[16] = {};
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
@@ -244,7 +245,9 @@ void stage_in(rcg_ctx* ctx, const double* src, int64_t count, Staged& out);
 void stage_out_begin(rcg_ctx* ctx, double* dst, int64_t count, Staged& tmp);
 void stage_out_end(rcg_ctx* ctx, double* dst, int64_t count, Staged& tmp);
 double* dev_alloc(int64_t count);
-void dev_free(void* p);
+void* dev_alloc_bytes(size_t bytes);
+void dev_free(void* p);  // cached: see context.cu
+void register_ctx(rcg_ctx* c, bool add);
 
 // kernel timing (bench roofline): brackets a launch with events when profiling is on
 struct KTimer {

@@ -334,11 +334,8 @@ static rcg_tall* harvest(rcg_ctx* ctx, const double* x_dev, const rcg_sampler* s
     int* dl = nullptr;
     int* nz = nullptr;
     try {
-        void* p = nullptr;
-        RCG_CK(cudaMalloc(&p, sizeof(int) * list.size()));
-        dl = static_cast<int*>(p);
-        RCG_CK(cudaMalloc(&p, sizeof(int) * list.size()));
-        nz = static_cast<int*>(p);
+        dl = static_cast<int*>(dev_alloc_bytes(sizeof(int) * list.size()));
+        nz = static_cast<int*>(dev_alloc_bytes(sizeof(int) * list.size()));
         RCG_CK(cudaMemcpyAsync(dl, list.data(), sizeof(int) * list.size(), cudaMemcpyHostToDevice, ctx->stream));
         RCG_CK(cudaMemsetAsync(nz, 0, sizeof(int) * list.size(), ctx->stream));
         dim3 grid(stream_grid(ctx, s->n), std::min<int>(static_cast<int>(list.size()), 64));
@@ -467,11 +464,8 @@ int rcg_sampler_create(rcg_ctx* ctx, int method, int m, int iteration_cap, doubl
             s->n = n;
             s->ld = ld_of(n);
             s->slots = dev_alloc(s->ld * m);
-            void* p = nullptr;
-            RCG_CK(cudaMalloc(&p, sizeof(int) * m));
-            s->occupied = static_cast<int*>(p);
-            RCG_CK(cudaMalloc(&p, sizeof(int) * m));
-            s->stored_iter = static_cast<int*>(p);
+            s->occupied = static_cast<int*>(dev_alloc_bytes(sizeof(int) * m));
+            s->stored_iter = static_cast<int*>(dev_alloc_bytes(sizeof(int) * m));
             RCG_CK(cudaMemsetAsync(s->occupied, 0, sizeof(int) * m, ctx->stream));
             RCG_CK(cudaMemsetAsync(s->stored_iter, 0, sizeof(int) * m, ctx->stream));
             s->thresholds = dev_alloc(m);
