@@ -48,6 +48,7 @@ struct BatchWs {
     double* hist = nullptr;
     int64_t cap_hist = 0;
     double *u = nullptr, *u2 = nullptr;  // [m][RT]
+    int64_t cap_u = 0;
     double* partials = nullptr;
     int64_t cap_part = 0;
     double* gpart = nullptr;
@@ -56,26 +57,28 @@ struct BatchWs {
     int* tickets = nullptr;
 };
 
-void batch_ws_free(rcg_ctx* ctx) {
-    BatchWs* w = ctx->bws;
+static void free_ws(BatchWs*& w) {
     if (!w) return;
     for (void* p : {(void*)w->b, (void*)w->x, (void*)w->r, (void*)w->zs, (void*)w->p, (void*)w->q, (void*)w->y,
                     (void*)w->st, (void*)w->hist, (void*)w->u, (void*)w->u2, (void*)w->partials, (void*)w->gpart,
                     (void*)w->gcount, (void*)w->tickets})
         dev_free(p);
     delete w;
-    ctx->bws = nullptr;
+    w = nullptr;
 }
 
-static BatchWs& batch_ws(rcg_ctx* ctx, int64_t nrt, int64_t hist, int64_t m_rt, int64_t part, int64_t groups) {
-    if (!ctx->bws) ctx->bws = new BatchWs();
-    BatchWs& w = *ctx->bws;
+void batch_ws_free(rcg_ctx* ctx) {
+    free_ws(ctx->bws);
+    free_ws(ctx->bws2);
+}
+
+// the workspace in `slot` (ctx->bws or ctx->bws2: a compacted phase reads one and writes the other)
+static BatchWs& batch_ws(BatchWs*& slot, int64_t nrt, int64_t hist, int64_t m_rt, int64_t part, int64_t groups) {
+    if (!slot) slot = new BatchWs();
+    BatchWs& w = *slot;
     if (!w.st) {
-        void* p = nullptr;
-        RCG_CK(cudaMalloc(&p, sizeof(BState)));
-        w.st = static_cast<BState*>(p);
-        RCG_CK(cudaMalloc(&p, 16 * sizeof(int)));
-        w.tickets = static_cast<int*>(p);
+        w.st = static_cast<BState*>(dev_alloc_bytes(sizeof(BState)));
+        w.tickets = static_cast<int*>(dev_alloc_bytes(16 * sizeof(int)));
         RCG_CK(cudaMemset(w.tickets, 0, 16 * sizeof(int)));
         RCG_CK(cudaMemset(w.st, 0, sizeof(BState)));
     }
@@ -91,11 +94,13 @@ static BatchWs& batch_ws(rcg_ctx* ctx, int64_t nrt, int64_t hist, int64_t m_rt, 
         w.hist = dev_alloc(hist);
         w.cap_hist = hist;
     }
-    if (!w.u || m_rt > 0) {
+    m_rt = std::max<int64_t>(m_rt, kRMax);
+    if (m_rt > w.cap_u) {
         dev_free(w.u);
         dev_free(w.u2);
-        w.u = dev_alloc(std::max<int64_t>(m_rt, kRMax));
-        w.u2 = dev_alloc(std::max<int64_t>(m_rt, kRMax));
+        w.u = dev_alloc(m_rt);
+        w.u2 = dev_alloc(m_rt);
+        w.cap_u = m_rt;
     }
     if (part > w.cap_part) {
         dev_free(w.partials);
@@ -106,14 +111,19 @@ static BatchWs& batch_ws(rcg_ctx* ctx, int64_t nrt, int64_t hist, int64_t m_rt, 
         dev_free(w.gpart);
         dev_free(w.gcount);
         w.gpart = dev_alloc(groups * kRMax);
-        void* p = nullptr;
-        RCG_CK(cudaMalloc(&p, sizeof(unsigned int) * groups));
-        w.gcount = static_cast<unsigned int*>(p);
+        w.gcount = static_cast<unsigned int*>(dev_alloc_bytes(sizeof(unsigned int) * groups));
         RCG_CK(cudaMemset(w.gcount, 0, sizeof(unsigned int) * groups));
         w.cap_groups = groups;
     }
     return w;
 }
+
+// slot k of a phase <-> slot[k] of the previous phase / original right-hand side col[k]
+struct SlotMap {
+    int cnt = 0;
+    int slot[kRMax];
+    int col[kRMax];
+};
 
 // ------------------------------------------------------------------ device helpers
 // ------------------------------------------------------------------ kernels
@@ -871,7 +881,7 @@ __global__ void k_b_finish_combine(double* __restrict__ x, const double* __restr
             if (d == kZeroRhs) x[e] = 0.0;
             continue;
         }
-        if (d == kBroken || d == kZeroRhs) continue;
+        if (d == kBroken || d == kZeroRhs || d == kRunning) continue;
         const int64_t i = e / RT;
         if (mode == 0) {  // x -= W u (project_p)
             double v = x[e];
@@ -885,9 +895,81 @@ __global__ void k_b_finish_combine(double* __restrict__ x, const double* __restr
     }
 }
 
+// ------------------------------------------------------------------ compaction
+// Running right-hand sides of a wider phase continue in a narrower one: vectors x, r, p, b and
+// the per-rhs state (scalars, residual history, the subspace-correction coefficients u2) move
+// to slots 0..cnt-1; the remaining slots are inert zero right-hand sides.
+__global__ void k_b_carry_vec(const double* __restrict__ in, int rt_in, double* __restrict__ out, int rt_out,
+                              SlotMap sel, int32_t n) {
+    const int64_t total = static_cast<int64_t>(n) * rt_out;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / rt_out;
+        const int k = static_cast<int>(e % rt_out);
+        out[e] = k < sel.cnt ? in[i * rt_in + sel.slot[k]] : 0.0;
+    }
+}
+
+__global__ void k_b_carry_state(const BState* __restrict__ a, BState* __restrict__ b, SlotMap sel, int rt_out,
+                                const double* __restrict__ hist_a, double* __restrict__ hist_b, int64_t hist_ld,
+                                const double* __restrict__ u2a, int rt_in, double* __restrict__ u2b, int m) {
+    const int t = threadIdx.x;
+    if (t == 0) {
+        b->iter = a->iter;
+        b->max_iter = a->max_iter;
+        b->eps = a->eps;
+        b->nrun = sel.cnt;
+        for (int j = 0; j < 8; ++j) b->tick[j] = 0u;
+    }
+    if (t < rt_out) {
+        if (t < sel.cnt) {
+            const int s = sel.slot[t];
+            b->done[t] = a->done[s];
+            b->iters[t] = a->iters[s];
+            b->status[t] = a->status[s];
+            b->bnorm[t] = a->bnorm[s];
+            b->rho[t] = a->rho[s];
+            b->rho_prev[t] = a->rho_prev[s];
+            b->beta[t] = a->beta[s];
+            b->alpha[t] = a->alpha[s];
+            b->pq[t] = a->pq[s];
+            b->rr[t] = a->rr[s];
+            b->relres[t] = a->relres[s];
+            b->scal2[t] = a->scal2[s];
+        } else {
+            b->done[t] = kZeroRhs;
+            b->iters[t] = 0;
+            b->status[t] = 0;
+            b->bnorm[t] = 0.0;
+            b->rho[t] = b->rho_prev[t] = b->beta[t] = b->alpha[t] = b->pq[t] = b->rr[t] = b->relres[t] = 0.0;
+            b->scal2[t] = 0.0;
+        }
+    }
+    const int done_iters = a->iter - 1;
+    for (int k = 0; k < sel.cnt; ++k)
+        for (int i = t; i < done_iters; i += blockDim.x) hist_b[k * hist_ld + i] = hist_a[sel.slot[k] * hist_ld + i];
+    for (int e = t; e < m * rt_out; e += blockDim.x) {
+        const int j = e / rt_out, k = e % rt_out;
+        u2b[e] = k < sel.cnt ? u2a[j * rt_in + sel.slot[k]] : 0.0;
+    }
+}
+
+// x columns of the listed slots -> the caller's column-major X
+__global__ void k_b_scatter_map(const double* __restrict__ in, int rt, SlotMap map, int64_t ldc,
+                                double* __restrict__ cols, int32_t n) {
+    const int64_t total = static_cast<int64_t>(n) * map.cnt;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = static_cast<int>(e % map.cnt);
+        const int64_t i = e / map.cnt;
+        cols[map.col[k] * ldc + i] = in[i * rt + map.slot[k]];
+    }
+}
+
 // ------------------------------------------------------------------ host driver
-template <int RT>
-struct BatchSolve {
+// One solve of up to 16 right-hand sides, run in phases: a phase of width RT iterates until
+// every slot is done or the running slots fit a narrower width (the converged ones stay frozen
+// but still cost RT-wide passes), then retires its finished slots (deflated recombination,
+// scatter to X, reports) and hands the running ones to the next, narrower phase.
+struct BatchJob {
     rcg_ctx* ctx;
     const rcg_matrix* a;
     const rcg_prec* m;
@@ -896,12 +978,38 @@ struct BatchSolve {
     int R;
     int max_iter;
     double eps;
+    const double* b_cols;  // device, column-major (ld n)
+    double* x_cols;        // device, column-major (ld n)
+    rcg_solve_report* reps;
+    double wall = 0.0;
+    int broken = -1;
+    int broken_status = 0;
+    int phases = 0;
+};
+
+static int pick_rt(int nrhs) { return nrhs <= 2 ? 2 : (nrhs + 3) / 4 * 4; }
+
+template <int RT>
+struct BatchSolve {
+    BatchJob& job;
+    rcg_ctx* ctx;
+    const rcg_matrix* a;
+    const rcg_prec* m;
+    const rcg_basis* defl;
+    int32_t n;
+    int max_iter;
+    double eps;
     bool ic = false, sc = false;
     const rcg_basis* scb = nullptr;
     BatchWs* w = nullptr;
     int sg = 1, pg = 1;
+    int start_iter = 1;
+    SlotMap map;  // slot k <-> original right-hand side map.col[k]
 
-    void setup() {
+    explicit BatchSolve(BatchJob& j)
+        : job(j), ctx(j.ctx), a(j.a), m(j.m), defl(j.defl), n(j.n), max_iter(j.max_iter), eps(j.eps) {}
+
+    void setup(BatchWs*& slot) {
         ic = m->kind == RCG_PREC_IC || (m->kind == RCG_PREC_SC && m->ic);
         sc = m->kind == RCG_PREC_SC && m->sc && m->sc->k > 0;
         scb = sc ? m->sc : nullptr;
@@ -913,7 +1021,7 @@ struct BatchSolve {
         int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 31) / 32 : 1;
         const int64_t groups = (ntiles + kGroup - 1) / kGroup;
         const int64_t part = std::max<int64_t>(ntiles * RT, static_cast<int64_t>(kMaxRedB) * ctx->num_sms * 8);
-        w = &batch_ws(ctx, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
+        w = &batch_ws(slot, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
         sg = stream_grid(ctx, n);
         pg = spmv_grid(ctx, n);
         static bool prepared = false;
@@ -922,6 +1030,43 @@ struct BatchSolve {
             allow_smem(reinterpret_cast<const void*>(k_b_spmv_pq<RT>));
             prepared = true;
         }
+    }
+
+    // first phase: right-hand sides 0..R-1 in slots 0..R-1
+    void fresh() {
+        map.cnt = job.R;
+        for (int k = 0; k < job.R; ++k) map.slot[k] = map.col[k] = k;
+        const int g = stream_grid(ctx, static_cast<int64_t>(n) * RT);
+        k_b_gather<RT><<<g, kStreamThreads, 0, ctx->stream>>>(job.b_cols, job.R, n, w->b, n);
+        RCG_LAUNCHED(ctx);
+        k_b_gather<RT><<<g, kStreamThreads, 0, ctx->stream>>>(job.x_cols, job.R, n, w->x, n);
+        RCG_LAUNCHED(ctx);
+        initial();
+        start_iter = 1;
+    }
+
+    // later phase: the running slots `sel` of a wider phase (state after a whole iteration)
+    void resume(const BatchWs* from, int rt_from, const SlotMap& sel, int iter) {
+        map.cnt = sel.cnt;
+        for (int k = 0; k < sel.cnt; ++k) {
+            map.slot[k] = k;
+            map.col[k] = sel.col[k];
+        }
+        const int64_t nrt = static_cast<int64_t>(n) * RT;
+        if (ic) {
+            launch_fill_bits(ctx, w->y, nrt, kSentinelBits);
+            launch_fill_bits(ctx, w->zs, nrt, kSentinelBits);
+        }
+        const int g = stream_grid(ctx, nrt);
+        for (auto pr : {std::make_pair(from->b, w->b), std::make_pair(from->x, w->x), std::make_pair(from->r, w->r),
+                        std::make_pair(from->p, w->p)}) {
+            k_b_carry_vec<<<g, kStreamThreads, 0, ctx->stream>>>(pr.first, rt_from, pr.second, RT, sel, n);
+            RCG_LAUNCHED(ctx);
+        }
+        k_b_carry_state<<<1, 256, 0, ctx->stream>>>(from->st, w->st, sel, RT, from->hist, w->hist, max_iter + 1,
+                                                    from->u2, rt_from, w->u2, sc ? scb->k : 0);
+        RCG_LAUNCHED(ctx);
+        start_iter = iter;
     }
 
     SpmvArgs sargs() const {
@@ -1048,7 +1193,7 @@ struct BatchSolve {
     void finish() {
         k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, nullptr, 0, 0, nullptr, n, w->st, 2);
         RCG_LAUNCHED(ctx);
-        if (defl && defl->k > 0) {  // x = P x + W (W^T A W)^-1 W^T b (pcg.cpp:152-157)
+        if (defl && defl->k > 0) {  // x = P x + W (W^T A W)^-1 W^T b (pcg.cpp:152-157), finished slots
             k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->aw, defl->ld, defl->k, w->x, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
@@ -1056,15 +1201,16 @@ struct BatchSolve {
                                                                            w->st, 0);
             RCG_LAUNCHED(ctx);
             k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->b, n, w->partials,
-                                                                  defl->l, w->u2, 1, w->st, 0);
+                                                                  defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
-            k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u2, n,
+            k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
                                                                            w->st, 1);
             RCG_LAUNCHED(ctx);
         }
     }
 
-    void run(double* wall) {
+    // iterate; returns early (allow_shrink) once the running slots fit a narrower phase
+    void run(bool allow_shrink) {
         cudaEvent_t evs[2], t0, t1;
         RCG_CK(cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming));
         RCG_CK(cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming));
@@ -1072,19 +1218,17 @@ struct BatchSolve {
         RCG_CK(cudaEventCreate(&t1));
         RCG_CK(cudaEventRecord(t0, ctx->stream));
         volatile int* flags = reinterpret_cast<volatile int*>(ctx->host_pinned + 256);
-        int enq = 0, batch = 2, slot = 0, prev = 0;
+        int enq = start_iter - 1, batch = 2, slot = 0, prev = 0;
         bool have_prev = false;
-        while (true) {
+        while (enq < max_iter) {
             for (int j = 0; j < batch && enq < max_iter; ++j, ++enq) iteration();
             RCG_CK(cudaMemcpyAsync((void*)(flags + slot), &w->st->nrun, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
             RCG_CK(cudaEventRecord(evs[slot], ctx->stream));
-            if (enq >= max_iter) {
-                RCG_CK(cudaEventSynchronize(evs[slot]));
-                break;
-            }
+            if (enq >= max_iter) break;
             if (have_prev) {
                 RCG_CK(cudaEventSynchronize(evs[prev]));
-                if (flags[prev] == 0) break;
+                const int nr = flags[prev];
+                if (nr == 0 || (allow_shrink && pick_rt(nr) < RT)) break;
             }
             have_prev = true;
             prev = slot;
@@ -1095,64 +1239,78 @@ struct BatchSolve {
         RCG_CK(cudaEventSynchronize(t1));
         float ms = 0.f;
         RCG_CK(cudaEventElapsedTime(&ms, t0, t1));
-        *wall = ms * 1e-3;
+        job.wall += ms * 1e-3;
         for (auto e : {evs[0], evs[1], t0, t1}) cudaEventDestroy(e);
+    }
+
+    // finish, scatter and report the slots that are done; returns the running ones (slot ->
+    // original column) and their iteration
+    SlotMap retire(int* iter) {
+        finish();
+        BState h{};
+        RCG_CK(cudaMemcpyAsync(ctx->host_pinned + 1024, w->st, sizeof(BState), cudaMemcpyDeviceToHost, ctx->stream));
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+        std::memcpy(&h, ctx->host_pinned + 1024, sizeof(BState));
+        SlotMap out, carry;
+        for (int k = 0; k < map.cnt; ++k) {
+            if (h.done[k] == kRunning) {
+                carry.slot[carry.cnt] = k;
+                carry.col[carry.cnt++] = map.col[k];
+            } else {
+                out.slot[out.cnt] = k;
+                out.col[out.cnt++] = map.col[k];
+            }
+        }
+        if (out.cnt > 0) {
+            const int g = stream_grid(ctx, static_cast<int64_t>(n) * out.cnt);
+            k_b_scatter_map<<<g, kStreamThreads, 0, ctx->stream>>>(w->x, RT, out, n, job.x_cols, n);
+            RCG_LAUNCHED(ctx);
+            std::vector<double> hist(static_cast<size_t>(max_iter + 1));
+            for (int q = 0; q < out.cnt; ++q) {
+                const int k = out.slot[q];
+                rcg_solve_report& r = job.reps[out.col[q]];
+                r.iterations = (h.done[k] == kZeroRhs) ? 0 : h.iters[k];
+                r.converged = (h.done[k] == kConverged || h.done[k] == kZeroRhs) ? 1 : 0;
+                const int cnt = std::min(r.iterations, r.cap);
+                if (r.history && cnt > 0) {
+                    RCG_CK(cudaMemcpy(r.history, w->hist + static_cast<int64_t>(k) * (max_iter + 1), sizeof(double) * cnt,
+                                      cudaMemcpyDeviceToHost));
+                }
+                if (h.done[k] == kBroken && (job.broken < 0 || out.col[q] < job.broken)) {
+                    job.broken = out.col[q];
+                    job.broken_status = h.status[k];
+                }
+            }
+        }
+        *iter = h.iter;
+        return carry;
     }
 };
 
+static void run_phase(int rt, BatchJob& job, int wsi, const BatchWs* from, int rt_from, const SlotMap* sel, int iter);
+
 template <int RT>
-static void batch_solve(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const rcg_prec* m, const rcg_basis* defl,
-                        double* X, const rcg_solver_config* cfg, int R, rcg_solve_report* reps) {
-    BatchSolve<RT> s{};
-    s.ctx = ctx;
-    s.a = a;
-    s.m = m;
-    s.defl = defl;
-    s.n = a->n;
-    s.R = R;
-    s.max_iter = cfg->max_iter;
-    s.eps = cfg->eps;
-    s.setup();
-    const int32_t n = a->n;
-    Staged bs, xs;
-    stage_in(ctx, B, static_cast<int64_t>(n) * R, bs);
-    stage_in(ctx, X, static_cast<int64_t>(n) * R, xs);
-    const int g = stream_grid(ctx, static_cast<int64_t>(n) * RT);
-    k_b_gather<RT><<<g, kStreamThreads, 0, ctx->stream>>>(bs.dev, R, n, s.w->b, n);
-    RCG_LAUNCHED(ctx);
-    k_b_gather<RT><<<g, kStreamThreads, 0, ctx->stream>>>(xs.dev, R, n, s.w->x, n);
-    RCG_LAUNCHED(ctx);
-    s.initial();
-    double wall = 0.0;
-    s.run(&wall);
-    s.finish();
-    Staged xo;
-    stage_out_begin(ctx, X, static_cast<int64_t>(n) * R, xo);
-    k_b_scatter<RT><<<g, kStreamThreads, 0, ctx->stream>>>(s.w->x, R, n, xo.dev, n);
-    RCG_LAUNCHED(ctx);
-    stage_out_end(ctx, X, static_cast<int64_t>(n) * R, xo);
-    RCG_CK(cudaStreamSynchronize(ctx->stream));
-    check_sweep_watchdog(ctx);
-    BState h{};
-    RCG_CK(cudaMemcpy(&h, s.w->st, sizeof(BState), cudaMemcpyDeviceToHost));
-    std::vector<double> hist(static_cast<size_t>(RT) * (s.max_iter + 1));
-    RCG_CK(cudaMemcpy(hist.data(), s.w->hist, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost));
-    int broken = -1;
-    for (int k = 0; k < R; ++k) {
-        rcg_solve_report& r = reps[k];
-        r.iterations = (h.done[k] == kZeroRhs) ? 0 : h.iters[k];
-        r.converged = (h.done[k] == kConverged || h.done[k] == kZeroRhs) ? 1 : 0;
-        r.wall_time = wall;
-        const int cnt = std::min(r.iterations, r.cap);
-        if (r.history && cnt > 0)
-            std::memcpy(r.history, hist.data() + static_cast<size_t>(k) * (s.max_iter + 1), sizeof(double) * cnt);
-        if (h.done[k] == kBroken && broken < 0) broken = k;
-    }
-    if (broken >= 0) {
-        const bool dfl = defl && defl->k > 0;
-        throw Error(RCG_E_BREAKDOWN, std::string(dfl ? "deflated pcg" : "pcg") + ": breakdown in right-hand side " +
-                                         std::to_string(broken) +
-                                         (h.status[broken] == kBrkRz ? " ((r, z) <= 0)" : " ((p, A p) <= 0)"));
+static void phase(BatchJob& job, int wsi, const BatchWs* from, int rt_from, const SlotMap* sel, int iter) {
+    BatchSolve<RT> s(job);
+    s.setup(wsi == 0 ? job.ctx->bws : job.ctx->bws2);
+    if (from)
+        s.resume(from, rt_from, *sel, iter);
+    else
+        s.fresh();
+    ++job.phases;
+    s.run(RT > 2);
+    int it = 0;
+    const SlotMap carry = s.retire(&it);
+    if (carry.cnt > 0) run_phase(pick_rt(carry.cnt), job, wsi ^ 1, s.w, RT, &carry, it);
+}
+
+static void run_phase(int rt, BatchJob& job, int wsi, const BatchWs* from, int rt_from, const SlotMap* sel, int iter) {
+    switch (rt) {
+        case 2: phase<2>(job, wsi, from, rt_from, sel, iter); break;
+        case 4: phase<4>(job, wsi, from, rt_from, sel, iter); break;
+        case 8: phase<8>(job, wsi, from, rt_from, sel, iter); break;
+        case 12: phase<12>(job, wsi, from, rt_from, sel, iter); break;
+        default: phase<16>(job, wsi, from, rt_from, sel, iter); break;
     }
 }
 
@@ -1168,14 +1326,27 @@ static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const
         check_cfg(cfg);
         check_prec(m, a->n);
         if (defl && defl->k > 0) require(defl->n == a->n, "deflated_pcg_solve: W row count does not match A");
-        // RT: 2 for one or two right-hand sides, else nrhs rounded up to a multiple of 4 (32-byte
-        // chunks: one 256-bit access per chunk in the sweeps and spmv gathers)
-        switch (nrhs <= 2 ? 2 : (nrhs + 3) / 4 * 4) {
-            case 2: batch_solve<2>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
-            case 4: batch_solve<4>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
-            case 8: batch_solve<8>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
-            case 12: batch_solve<12>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
-            default: batch_solve<16>(ctx, a, B, m, defl, X, cfg, nrhs, reps); break;
+        const int32_t n = a->n;
+        Staged bs, xs;
+        stage_in(ctx, B, static_cast<int64_t>(n) * nrhs, bs);
+        stage_in(ctx, X, static_cast<int64_t>(n) * nrhs, xs);
+        Staged xo;
+        stage_out_begin(ctx, X, static_cast<int64_t>(n) * nrhs, xo);
+        if (xo.dev != xs.dev && nrhs > 0)
+            RCG_CK(cudaMemcpyAsync(xo.dev, xs.dev, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, ctx->stream));
+        BatchJob job{ctx, a, m, defl, n, nrhs, cfg->max_iter, cfg->eps, bs.dev, xo.dev, reps};
+        // RT: 2 for one or two right-hand sides, else a multiple of 4 (32-byte chunks: one
+        // 256-bit access per chunk in the sweeps and spmv gathers)
+        run_phase(pick_rt(nrhs), job, 0, nullptr, 0, nullptr, 1);
+        stage_out_end(ctx, X, static_cast<int64_t>(n) * nrhs, xo);
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+        check_sweep_watchdog(ctx);
+        for (int k = 0; k < nrhs; ++k) reps[k].wall_time = job.wall;
+        if (job.broken >= 0) {
+            const bool dfl = defl && defl->k > 0;
+            throw Error(RCG_E_BREAKDOWN, std::string(dfl ? "deflated pcg" : "pcg") + ": breakdown in right-hand side " +
+                                             std::to_string(job.broken) +
+                                             (job.broken_status == kBrkRz ? " ((r, z) <= 0)" : " ((p, A p) <= 0)"));
         }
     });
 }

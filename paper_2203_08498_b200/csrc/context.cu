@@ -375,7 +375,7 @@ int rcg_ctx_create(int device, rcg_ctx** out) {
         RCG_CK(cudaEventCreate(&c->ev0));
         RCG_CK(cudaEventCreate(&c->ev1));
         void* hp = nullptr;
-        RCG_CK(cudaMallocHost(&hp, 4096));
+        RCG_CK(cudaMallocHost(&hp, 16384));  // [0,2K) state staging, [2K,4K) done flags, [8K,16K) batch retire
         c->host_pinned = static_cast<double*>(hp);
         *out = c;
     });

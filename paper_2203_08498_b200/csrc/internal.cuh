@@ -165,7 +165,8 @@ struct rcg_ctx {
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
     int spmv_bps = 2;           // SpMV CTAs per SM (RCG_SPMV_BPS): leaves room for concurrent solves
-    rcg::BatchWs* bws = nullptr;  // multi-RHS workspace (batch.cu)
+    rcg::BatchWs* bws = nullptr;   // multi-RHS workspaces (batch.cu): a compacted phase
+    rcg::BatchWs* bws2 = nullptr;  // reads one and writes the other
 };
 
 struct rcg_matrix {
