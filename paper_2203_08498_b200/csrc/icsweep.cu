@@ -30,64 +30,59 @@ namespace rcg {
 
 constexpr int kDepChunk = 8;
 
-// Sum of one value per thread over the block; then a two-level deterministic grid reduction
-// keyed by tile: tiles -> groups of kGroup -> total.  Returns true in the block that owns the
-// final total (written to *tot).
-__device__ bool tile_reduce(double v, int tile, int ntiles, SweepArgs& a, double* red, double* tot) {
-    __shared__ bool s_last_group, s_last;
-    double acc[1] = {v};
-    block_sum<1>(acc, red);
+constexpr int kTile = 32;  // positions per ticket: one warp
+
+// (r, z) partial of one warp tile -> groups of kGroup tiles -> total, fixed order (run-to-run
+// deterministic).  Returns true in the one warp that owns the final total (*tot, all lanes).
+__device__ __forceinline__ bool tile_reduce(double v, int tile, int ntiles, SweepArgs& a, double* tot) {
+    const int lane = threadIdx.x & 31;
+    v = warp_sum(v);
     const int g = tile / kGroup;
     const int ngroups = (ntiles + kGroup - 1) / kGroup;
     const int gsize = min(kGroup, ntiles - g * kGroup);
-    if (threadIdx.x == 0) {
-        a.partials[tile] = acc[0];
+    int last_group = 0;
+    if (lane == 0) {
+        a.partials[tile] = v;
         __threadfence();
-        s_last_group = atomicAdd(&a.gcount[g], 1u) == static_cast<unsigned>(gsize) - 1u;
+        last_group = atomicAdd(&a.gcount[g], 1u) == static_cast<unsigned>(gsize) - 1u;
     }
-    __syncthreads();
-    if (!s_last_group) return false;
+    if (!__shfl_sync(0xffffffffu, last_group, 0)) return false;
     __threadfence();
-    double gs[1] = {threadIdx.x < gsize ? __ldcg(a.partials + g * kGroup + threadIdx.x) : 0.0};
-    block_sum<1>(gs, red);
-    if (threadIdx.x == 0) {
-        a.gpart[g] = gs[0];
+    double gs = 0.0;
+    for (int q = lane; q < gsize; q += 32) gs = __dadd_rn(gs, __ldcg(a.partials + g * kGroup + q));
+    gs = warp_sum(gs);
+    int last = 0;
+    if (lane == 0) {
+        a.gpart[g] = gs;
         a.gcount[g] = 0u;
         __threadfence();
-        s_last = atomicAdd(reinterpret_cast<unsigned int*>(&a.tickets[2]), 1u) ==
-                 static_cast<unsigned>(ngroups) - 1u;
+        last = atomicAdd(reinterpret_cast<unsigned int*>(&a.tickets[2]), 1u) == static_cast<unsigned>(ngroups) - 1u;
     }
-    __syncthreads();
-    if (!s_last) return false;
+    if (!__shfl_sync(0xffffffffu, last, 0)) return false;
     __threadfence();
-    double ts[1] = {0.0};
-    for (int i = threadIdx.x; i < ngroups; i += blockDim.x) ts[0] = __dadd_rn(ts[0], __ldcg(a.gpart + i));
-    block_sum<1>(ts, red);
-    if (threadIdx.x == 0) {
-        *tot = ts[0];
-        a.tickets[2] = 0;
-    }
-    __syncthreads();
+    double ts = 0.0;
+    for (int q = lane; q < ngroups; q += 32) ts = __dadd_rn(ts, __ldcg(a.gpart + q));
+    ts = warp_sum(ts);
+    if (lane == 0) a.tickets[2] = 0;
+    *tot = ts;
     return true;
 }
 
-// Persistent sweep: a grid of at most (SMs x blocks_per_sm) CTAs pulls 128-row tiles of the
-// level-sorted order from an atomic ticket until none is left.  Bounding the resident CTAs
-// bounds how many future-level rows spin at once.
+// Persistent sweep: a grid of at most (SMs x blocks_per_sm) CTAs whose warps each pull 32-row
+// tiles of the level-sorted order from an atomic ticket until none is left (tickets are
+// monotone, so every row a warp can wait on belongs to a running warp: no deadlock).  Bounding
+// the resident CTAs bounds how many future-level rows spin at once.
 template <bool BWD>
 __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
-    __shared__ int s_tile;
-    __shared__ double red[32];
-    __shared__ double tot;
     if (a.st->done) return;
-    const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
+    const int lane = threadIdx.x & 31;
+    const int ntiles = (a.npos + kTile - 1) / kTile;
     while (true) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&a.tickets[0], 1);
-        __syncthreads();
-        const int tile = s_tile;
-        __syncthreads();
+        int tile = 0;
+        if (lane == 0) tile = atomicAdd(&a.tickets[0], 1);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= ntiles) break;
-        const int pos = tile * kSweepThreads + threadIdx.x;
+        const int pos = tile * kTile + lane;
         double contrib = 0.0;
         const int32_t row = pos < a.npos ? __ldg(a.perm + pos) : -1;  // -1: level padding
         if (row >= 0) {
@@ -111,8 +106,8 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
 #pragma unroll
                 for (int j = 0; j < kDepChunk; ++j)
                     if (j < cnt) {
-                        col[j] = __ldcs(a.pcol + e0 + j);
-                        val[j] = __ldcs(a.pval + e0 + j);
+                        col[j] = __ldg(a.pcol + e0 + j);
+                        val[j] = __ldg(a.pval + e0 + j);
                     }
 #pragma unroll
                 for (int j = 0; j < kDepChunk; ++j)
@@ -145,7 +140,8 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
             if (BWD && a.r) contrib = __dmul_rn(a.r[row], s);
         }
         if (BWD && a.r) {
-            if (tile_reduce(contrib, tile, ntiles, a, red, &tot) && threadIdx.x == 0) {
+            double tot;
+            if (tile_reduce(contrib, tile, ntiles, a, &tot) && lane == 0) {
                 // (r, z) complete: breakdown test and beta of src/pcg.cpp:65-71.  With subspace
                 // correction z = z_ic + W u, so (r, z) = (r, z_ic) + (W^T r) . u (st->scal[2])
                 DevState* st = a.st;
@@ -159,9 +155,9 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
             }
         }
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         __threadfence();
-        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x) - 1) {
+        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x * (blockDim.x / 32)) - 1) {
             a.tickets[0] = 0;
             a.tickets[1] = 0;
         }
@@ -229,7 +225,7 @@ void check_sweep_watchdog(rcg_ctx* ctx) {
 // workspace needed by the sweeps of an n-row factor
 int64_t sweep_tiles(const rcg_ic* f) {
     const int64_t npos = std::max<int64_t>(std::max(f->f_npos, f->b_npos), f->n);
-    return (npos + kSweepThreads - 1) / kSweepThreads;
+    return (npos + kTile - 1) / kTile;
 }
 
 static void ensure_sweep_ws(rcg_ctx* ctx, const rcg_ic* f, int k, int64_t max_iter, int pending) {
