@@ -1177,9 +1177,7 @@ struct BatchSolve {
     void launch_b_sweep(bool backward, SweepArgs& s) {
         const rcg_ic* f = m->ic;
         const int ntiles = (s.npos + 127) / 128;  // in CTAs of 4 warp tiles
-        const int levels = backward ? f->bwd_levels : f->fwd_levels;
-        const int64_t rows_per_level = levels > 0 ? s.npos / levels : s.npos;
-        const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : (rows_per_level >= 65536 ? 8 : 2);
+        const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, s.npos);
         const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
         s.backoff_ns = ctx->sweep_backoff_ns;
         KTimer t(ctx, backward ? 2 : 1);

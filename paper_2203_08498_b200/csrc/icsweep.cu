@@ -190,15 +190,25 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
     return a;
 }
 
+// Resident CTAs per SM (RCG_SWEEP_BPS overrides).  Rows in flight beyond what the current
+// levels can use only spin and add L2 polling traffic, and too few leave a wide level's rows
+// waiting on their load chains.  Measured on B200 with 32-row warp tiles:
+//   rows/level   5.5K (C2)  9.4K (C3, 27-pt)  87K (C4)  262K (C2 multicolour)
+//   best         2          fwd 2 / bwd 1     3         8
+// A backward row with more than one chunk of parents (kDepChunk) spins on more lines per poll.
+int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos) {
+    const int levels = backward ? f->bwd_levels : f->fwd_levels;
+    const int64_t rows_per_level = levels > 0 ? npos / levels : npos;
+    if (rows_per_level >= 200000) return 8;
+    if (rows_per_level >= 32768) return 3;
+    const double entries_per_row = f->n > 0 ? static_cast<double>(f->nnz_l) / f->n : 0.0;
+    return backward && entries_per_row > kDepChunk ? 1 : 2;
+}
+
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
-    // Resident CTAs per SM: a deep DAG (few rows per level) is latency-bound and every extra
-    // spinning CTA only adds L2 polling traffic -> 2; a shallow one (multicolour) is
-    // bandwidth-bound and wants full occupancy -> 8.  RCG_SWEEP_BPS overrides.
-    const int levels = backward ? f->bwd_levels : f->fwd_levels;
-    const int64_t rows_per_level = levels > 0 ? a.npos / levels : a.npos;
-    const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : (rows_per_level >= 65536 ? 8 : 2);
+    const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
     a.backoff_ns = ctx->sweep_backoff_ns;
     KTimer t(ctx, backward ? 2 : 1);

@@ -39,6 +39,7 @@ struct SweepArgs {
 };
 
 int spmv_grid(const rcg_ctx* ctx, int32_t n);
+int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos);
 int stream_grid(const rcg_ctx* ctx, int64_t n);
 size_t spmv_smem(const rcg_matrix* a);
 void spmv_prepare_kernels();
