@@ -152,10 +152,7 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(args.steps):
             step_device()
         ctxs = _all_contexts(prep)
-    stats = {}
-    for c in range(5):
-        per = [c_.kernel_stats(c) for c_ in ctxs]
-        stats[c] = (sum(t for t, _ in per), sum(n_ for _, n_ in per))
+    stats = kernel_stats(ctxs)
     for c_ in ctxs:
         c_.set_profiling(False)
     # phase breakdown of one extra (untimed) step
@@ -183,39 +180,7 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_src = peaks()
-    m_t = cfg.keep
-    # algorithmic bytes per launch
-    per_launch = {
-        0: 12 * n_nnz + 20 * n,                       # SpMV q = A p (+ (p,q)): PAPER.md:276
-        1: 12 * nnz_l + 24 * n,                       # forward sweep: L entries, perm+prs, r in, y out
-        2: 12 * nnz_l + 48 * n,                       # backward sweep: U, perm+prs, y in+reset, d, z out, r
-        4: 8 * m_t * n + 8 * n,                       # W^T r projection
-    }
-    names = {0: "spmv (k_spmv_pq)", 1: "ic fwd sweep (k_sweep<false>)", 2: "ic bwd sweep (k_sweep<true>)",
-             3: "vector ops", 4: "W^T r (k_tallt)"}
-    dom = max((c for c in stats if stats[c][1] > 0), key=lambda c: stats[c][0])
-    kernels = {}
-    for c, (tot_ms, cnt) in stats.items():
-        if cnt == 0:
-            continue
-        avg = tot_ms / cnt
-        entry = {"launches": cnt, "avg_us": round(avg * 1e3, 3), "busy_ms_per_step": round(tot_ms / args.steps, 2)}
-        if c in per_launch:
-            entry["algorithmic_bytes"] = per_launch[c]
-            entry["achieved_gbs"] = round(per_launch[c] / (avg * 1e-3) / 1e9, 1)
-        kernels[names[c]] = entry
-    roof_c = dom if dom in per_launch else 0
-    avg_roof = stats[roof_c][0] / stats[roof_c][1]
-    achieved = per_launch[roof_c] / (avg_roof * 1e-3) / 1e9
-    traffic = None  # dram bytes per launch from the committed ncu --set full capture (profiles/)
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(names[roof_c])
-    for c, entry_name in names.items():
-        if entry_name in kernels and os.path.exists(tp):
-            t = json.load(open(tp)).get(entry_name)
-            if t:
-                kernels[entry_name]["ncu_dram_bytes"] = t
+    kernels, roof = kernel_report(stats, n, n_nnz, nnz_l, cfg.keep, args.steps, peak, peak_src)
     line = {
         "metric": METRIC,
         "value": round(iters / (ms / 1e3), 2),
@@ -239,8 +204,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_iters / (e2e_ms / 1e3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": 8 * n * cfg.n_rhs, "d2h_bytes_per_step": 8 * n * cfg.n_rhs,
                 "time_to_solution_ms_per_rhs": round(e2e_ms / args.steps / cfg.n_rhs, 3)},
-        "roofline": {"bound": "hbm", "kernel": names[roof_c], "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src},
+        "roofline": roof,
         "kernels": kernels,
         "phases_ms_untimed_step": phases,
         "gpu_launches": int(launches),
@@ -251,6 +215,68 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, host, threads=1, reps=1)
     print(json.dumps(line), flush=True)
+
+
+# Kernel classes (rcg_b200.h rcg_ctx_kernel_stats): 0-4 single right-hand side, 5-9 batched.
+CLASS_NAMES = {0: "spmv (k_spmv_pq)", 1: "ic fwd sweep (k_sweep<false>)", 2: "ic bwd sweep (k_sweep<true>)",
+               3: "vector ops", 4: "W^T r (k_tallt)",
+               5: "batched spmv (k_b_spmv_pq)", 6: "batched ic fwd sweep (k_b_sweep<false>)",
+               7: "batched ic bwd sweep (k_b_sweep<true>)", 8: "batched vector ops", 9: "batched W^T r (k_b_tallt)"}
+
+
+def kernel_stats(ctxs):
+    """{class: (total ms, launches, right-hand-side units)} summed over the contexts."""
+    out = {}
+    for c in CLASS_NAMES:
+        per = [c_.kernel_stats(c) for c_ in ctxs]
+        out[c] = (sum(t for t, _ in per), sum(k for _, k in per), sum(c_.kernel_units(c) for c_ in ctxs))
+    return out
+
+
+def algorithmic_bytes(c, n, nnz, nnz_l, m):
+    """(bytes per launch, bytes per carried right-hand side) of class c -- DESIGN.md "Roofline
+    accounting": matrix / factor / schedule / basis bytes are read once per
+    launch; vector bytes scale with the right-hand sides a launch carries."""
+    return {
+        0: (12 * nnz + 4 * n, 16 * n),      # A (val+col), row starts | p in, q out
+        1: (12 * nnz_l + 8 * n, 16 * n),    # L entries, perm+row starts | r in, y out
+        2: (12 * nnz_l + 16 * n, 24 * n),   # U entries, perm+row starts, d | y in, z out, r
+        4: (8 * m * n, 8 * n),              # W | the projected vector
+    }.get(c % 5)
+
+
+def kernel_report(stats, n, nnz, nnz_l, m, steps, peak, peak_src):
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic = json.load(open(tp)) if os.path.exists(tp) else {}
+    kernels, best = {}, None
+    for c, (tot_ms, cnt, units) in stats.items():
+        if cnt == 0:
+            continue
+        entry = {"launches": cnt, "avg_us": round(tot_ms / cnt * 1e3, 3), "busy_ms_per_step": round(tot_ms / steps, 2)}
+        if c >= 5:
+            entry["rhs_per_launch"] = round(units / cnt, 2)
+        ab = algorithmic_bytes(c, n, nnz, nnz_l, m)
+        if ab:
+            per_launch = (ab[0] * cnt + ab[1] * units) / cnt
+            entry["algorithmic_bytes"] = int(per_launch)
+            entry["achieved_gbs"] = round(per_launch / (tot_ms / cnt * 1e-3) / 1e9, 1)
+            t = traffic.get(CLASS_NAMES[c])
+            if isinstance(t, dict):  # batched: measured at a given right-hand-side count
+                entry["ncu_dram_bytes"] = t
+            elif t:
+                entry["ncu_dram_bytes"] = t
+            if best is None or tot_ms > stats[best][0]:
+                best = c
+        kernels[CLASS_NAMES[c]] = entry
+    e = kernels[CLASS_NAMES[best]]
+    t = traffic.get(CLASS_NAMES[best])
+    roof = {"bound": "hbm", "kernel": CLASS_NAMES[best], "achieved": e["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": round(e["achieved_gbs"] / peak, 4), "traffic": t["dram_bytes"] if isinstance(t, dict) else t,
+            "peak_source": peak_src}
+    if isinstance(t, dict):  # the ncu capture's launch carried rhs_per_launch right-hand sides
+        roof["traffic_rhs_per_launch"] = t["rhs_per_launch"]
+        roof["traffic_algorithmic_bytes"] = t["algorithmic_bytes"]
+    return kernels, roof
 
 
 def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
@@ -279,20 +305,20 @@ def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
     iters = sum(step() for _ in range(args.steps))
     ctx.record(5)
     ms = ctx.elapsed_ms(4, 5)
-    stats = {}
-    for c in range(5):
-        per = [c_.kernel_stats(c) for c_ in ctxs]
-        stats[c] = (sum(t for t, _ in per), sum(n_ for _, n_ in per))
+    stats = kernel_stats(ctxs)
     for c_ in ctxs:
         c_.set_profiling(False)
     nnz_l = prep.ic.nnz_l
     sweep = {}
-    for c, b in ((1, 12 * nnz_l + 24 * m.n), (2, 12 * nnz_l + 48 * m.n)):
-        if stats[c][1]:
-            avg = stats[c][0] / stats[c][1]
-            sweep["fwd" if c == 1 else "bwd"] = {"avg_us": round(avg * 1e3, 2),
-                                                 "achieved_gbs": round(b / (avg * 1e-3) / 1e9, 1),
-                                                 "frac": round(b / (avg * 1e-3) / 1e9 / peak, 4)}
+    for c in (1, 2, 6, 7):
+        tot_ms, cnt, units = stats[c]
+        if cnt:
+            fixed, per_rhs = algorithmic_bytes(c, m.n, m.nnz, nnz_l, cfg.keep)
+            b = (fixed * cnt + per_rhs * units) / cnt
+            avg = tot_ms / cnt
+            sweep[CLASS_NAMES[c]] = {"avg_us": round(avg * 1e3, 2), "rhs_per_launch": round(units / cnt, 2),
+                                     "achieved_gbs": round(b / (avg * 1e-3) / 1e9, 1),
+                                     "frac": round(b / (avg * 1e-3) / 1e9 / peak, 4)}
     return {"operator": f"IC(0) of P A P^T, greedy colouring ({ncolors} colours -> {ncolors} sweep levels)",
             "value": round(iters / (ms / 1e3), 2), "unit": UNIT,
             "iterations_per_step": iters / args.steps, "ms_per_step": round(ms / args.steps, 3),

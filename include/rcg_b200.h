@@ -48,12 +48,15 @@ int rcg_ctx_synchronize(rcg_ctx* ctx);
 int64_t rcg_ctx_launch_count(const rcg_ctx* ctx);
 /* device time (ms) accumulated by the named kernel class since the last reset, measured with
  * CUDA events on the context stream when profiling is enabled (class: 0 spmv, 1 fwd sweep,
- * 2 bwd sweep, 3 vector ops, 4 projection).  Used by bench.py for the roofline. */
+ * 2 bwd sweep, 3 vector ops, 4 projection; 5-9 the same for batched multi-RHS solves, whose
+ * launches each carry RT right-hand sides -- rcg_ctx_kernel_units returns the sum of RT over a
+ * class's launches).  Used by bench.py for the roofline. */
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable);
 /* CUDA events on the context stream (slots 0..15) for device-side timing by callers */
 int rcg_ctx_event_record(rcg_ctx* ctx, int slot);
 int rcg_ctx_event_elapsed(rcg_ctx* ctx, int slot_a, int slot_b, double* ms);
 int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launches);
+int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units);
 void rcg_ctx_reset_stats(rcg_ctx* ctx);
 
 /* ------------------------------------------------------------------ CSR (csr_matrix.hpp) */

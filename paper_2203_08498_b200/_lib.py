@@ -102,6 +102,7 @@ SIGNATURES = {
     "rcg_ctx_event_record": (C.c_int, vp, C.c_int),
     "rcg_ctx_event_elapsed": (C.c_int, vp, C.c_int, C.c_int, dp),
     "rcg_ctx_kernel_stats": (C.c_int, vp, C.c_int, dp, i64p),
+    "rcg_ctx_kernel_units": (C.c_int, vp, C.c_int, i64p),
     "rcg_ctx_reset_stats": (None, vp),
     "rcg_matrix_create": (C.c_int, vp, C.c_int32, vp, vp, vp, C.c_int, C.POINTER(vp)),
     "rcg_matrix_destroy": (None, vp),

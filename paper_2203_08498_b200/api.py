@@ -102,6 +102,12 @@ class Context:
         check(lib.rcg_ctx_kernel_stats(self.h, cls, C.byref(ms), C.byref(cnt)))
         return ms.value, cnt.value
 
+    def kernel_units(self, cls: int) -> int:
+        """Right-hand sides carried by a class's launches (batched classes 5-9: RT each)."""
+        u = C.c_int64()
+        check(lib.rcg_ctx_kernel_units(self.h, cls, C.byref(u)))
+        return u.value
+
     def reset_stats(self):
         lib.rcg_ctx_reset_stats(self.h)
 

@@ -1138,7 +1138,7 @@ struct BatchSolve {
         }
         require(ic || !sc, "batch: subspace correction needs the IC inner preconditioner");
         {
-            KTimer t(ctx, 3);
+            KTimer t(ctx, 8, RT);
             k_b_pupdate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(z, w->p, ic ? w->zs : nullptr, w->y, n, w->st,
                                                                     sc ? scb->w : nullptr, sc ? scb->ld : 0,
                                                                     sc ? scb->k : 0, w->u2);
@@ -1146,13 +1146,13 @@ struct BatchSolve {
         }
         const bool dfl = defl && defl->k > 0;
         {
-            KTimer t(ctx, 0);
+            KTimer t(ctx, 5, RT);
             k_b_spmv_pq<RT><<<pg, kSpmvThreads, spmv_smem(a), ctx->stream>>>(sargs(), a->cap, w->p, w->q, w->st,
                                                                              w->partials, dfl ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
         if (dfl) {
-            KTimer t(ctx, 4);
+            KTimer t(ctx, 9, RT);
             k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 1);
             RCG_LAUNCHED(ctx);
@@ -1161,13 +1161,13 @@ struct BatchSolve {
             RCG_LAUNCHED(ctx);
         }
         {
-            KTimer t(ctx, 3);
+            KTimer t(ctx, 8, RT);
             k_b_xr<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, w->r, w->p, w->q, n, w->partials, w->st, w->hist,
                                                                max_iter + 1, (!ic && !sc) ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
         if (sc) {
-            KTimer t(ctx, 4);
+            KTimer t(ctx, 9, RT);
             k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
                                                                   scb->l, w->u2, 2, w->st, 1);
             RCG_LAUNCHED(ctx);
@@ -1180,7 +1180,7 @@ struct BatchSolve {
         const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, s.npos);
         const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
         s.backoff_ns = ctx->sweep_backoff_ns;
-        KTimer t(ctx, backward ? 2 : 1);
+        KTimer t(ctx, backward ? 7 : 6, RT);
         if (backward)
             k_b_sweep<true, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
         else

@@ -291,6 +291,7 @@ static void fold(rcg_ctx* ctx, const rcg_ctx::TimedLaunch& t) {
     RCG_CK(cudaEventElapsedTime(&ms, t.start, t.stop));
     ctx->stat_ms[t.cls] += ms;
     ctx->stat_n[t.cls] += 1;
+    ctx->stat_units[t.cls] += t.units;
     ctx->ev_free.push_back(t.start);
     ctx->ev_free.push_back(t.stop);
 }
@@ -316,7 +317,7 @@ static cudaEvent_t pooled_event(rcg_ctx* ctx) {
     return e;
 }
 
-KTimer::KTimer(rcg_ctx* c, int k) : ctx(c), cls(k) {
+KTimer::KTimer(rcg_ctx* c, int k, int u) : ctx(c), cls(k), units(u) {
     if (!ctx->profiling) return;
     start = pooled_event(ctx);
     RCG_CK(cudaEventRecord(start, ctx->stream));
@@ -326,7 +327,7 @@ KTimer::~KTimer() {
     if (!ctx->profiling) return;
     cudaEvent_t stop = pooled_event(ctx);
     cudaEventRecord(stop, ctx->stream);
-    ctx->ev_pending.push_back({cls, start, stop});
+    ctx->ev_pending.push_back({cls, units, start, stop});
 }
 
 void resolve_timers(rcg_ctx* ctx) {
@@ -444,10 +445,18 @@ int rcg_ctx_event_elapsed(rcg_ctx* ctx, int slot_a, int slot_b, double* ms) {
 
 int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launches) {
     return guard([&] {
-        require(cls >= 0 && cls < 5, "rcg_ctx_kernel_stats: class out of range");
+        require(cls >= 0 && cls < kStatClasses, "rcg_ctx_kernel_stats: class out of range");
         resolve_timers(ctx);
         *total_ms = ctx->stat_ms[cls];
         *launches = ctx->stat_n[cls];
+    });
+}
+
+int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units) {
+    return guard([&] {
+        require(cls >= 0 && cls < kStatClasses, "rcg_ctx_kernel_units: class out of range");
+        resolve_timers(ctx);
+        *units = ctx->stat_units[cls];
     });
 }
 
@@ -456,9 +465,10 @@ void rcg_ctx_reset_stats(rcg_ctx* ctx) {
         resolve_timers(ctx);
     } catch (...) {
     }
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < kStatClasses; ++i) {
         ctx->stat_ms[i] = 0;
         ctx->stat_n[i] = 0;
+        ctx->stat_units[i] = 0;
     }
 }
 

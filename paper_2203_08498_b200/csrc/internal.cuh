@@ -144,6 +144,8 @@ struct BatchWs;  // batch.cu
 }  // namespace rcg
 
 // ------------------------------------------------------------------ handle structs
+constexpr int kStatClasses = 10;  // 0-4 single right-hand side, 5-9 batched (rcg_b200.h)
+
 struct rcg_ctx {
     int device = 0;
     int num_sms = 148;
@@ -152,11 +154,13 @@ struct rcg_ctx {
     rcg::Workspace ws;
     double* host_pinned = nullptr;   // small pinned scratch for scalar readbacks
     bool profiling = false;
-    double stat_ms[5] = {0, 0, 0, 0, 0};
-    int64_t stat_n[5] = {0, 0, 0, 0, 0};
+    double stat_ms[kStatClasses] = {};
+    int64_t stat_n[kStatClasses] = {};
+    int64_t stat_units[kStatClasses] = {};  // right-hand sides carried (batched: RT per launch)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     struct TimedLaunch {
         int cls;
+        int units;
         cudaEvent_t start, stop;
     };
     std::deque<TimedLaunch> ev_pending;
@@ -254,8 +258,9 @@ void register_ctx(rcg_ctx* c, bool add);
 struct KTimer {
     rcg_ctx* ctx;
     int cls;
+    int units;
     cudaEvent_t start = nullptr;
-    KTimer(rcg_ctx* c, int k);
+    KTimer(rcg_ctx* c, int k, int units = 1);
     ~KTimer();
 };
 void resolve_timers(rcg_ctx* ctx);
