@@ -26,6 +26,7 @@ namespace rcg {
 
 constexpr int kRMax = 16;
 constexpr int kMaxRedB = 512;
+constexpr int kElemThreads = 192;  // a multiple of every RT (2, 4, 8, 12, 16): a thread keeps one rhs
 
 struct BState {
     int iter;      // global iteration being executed (1-based)
@@ -596,30 +597,39 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
     }
 }
 
-// p = z (+ W u) (+ beta p) for running rhs, lane per row (W read once for all rhs); sweep
-// buffers back to the sentinel
+// p = z (+ W u) (+ beta p) for running rhs; sweep buffers back to the sentinel.  G = RT/VW
+// threads per row, each on one VW-value chunk: a warp's accesses are contiguous and each W_j[i]
+// load serves VW values.  Per value the arithmetic of the single-rhs k_pupdate.
 template <int RT>
-__global__ void __launch_bounds__(kStreamThreads) k_b_pupdate(const double* __restrict__ z, double* __restrict__ p,
-                                                              double* __restrict__ zs_reset, double* __restrict__ y_reset,
-                                                              int32_t n, BState* st, const double* __restrict__ W,
-                                                              int64_t ldw, int m, const double* __restrict__ u) {
+__global__ void __launch_bounds__(256) k_b_pupdate(const double* __restrict__ z, double* __restrict__ p,
+                                                   double* __restrict__ zs_reset, double* __restrict__ y_reset,
+                                                   int32_t n, BState* st, const double* __restrict__ W, int64_t ldw,
+                                                   int m, const double* __restrict__ u) {
+    constexpr int VW = RT % 4 == 0 ? 4 : 2;
+    constexpr int G = RT / VW;
+    __shared__ double us[kMaxRedB];
     __shared__ double beta[RT];
     __shared__ int run[RT];
-    __shared__ int first;
     if (st->nrun == 0) return;
+    if (W)
+        for (int t = threadIdx.x; t < m * RT; t += blockDim.x) us[t] = u[t];
     if (threadIdx.x < RT) {
         beta[threadIdx.x] = st->beta[threadIdx.x];
         run[threadIdx.x] = st->done[threadIdx.x] == kRunning;
     }
-    if (threadIdx.x == 0) first = st->iter == 1;
+    const bool first = st->iter == 1;
     __syncthreads();
     const double sent = sentinel();
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int64_t me = static_cast<int64_t>(i) * RT;
-        double zi[RT];
+    const int64_t items = static_cast<int64_t>(n) * G;
+    for (int64_t it = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; it < items;
+         it += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = it / G;
+        const int k0 = static_cast<int>(it % G) * VW;
+        const int64_t e0 = it * VW;
+        double zi[VW];
 #pragma unroll
-        for (int v = 0; v < RT / 2; ++v) {
-            const double2 t = reinterpret_cast<const double2*>(z + me)[v];
+        for (int v = 0; v < VW / 2; ++v) {
+            const double2 t = reinterpret_cast<const double2*>(z + e0)[v];
             zi[2 * v] = t.x;
             zi[2 * v + 1] = t.y;
         }
@@ -627,18 +637,16 @@ __global__ void __launch_bounds__(kStreamThreads) k_b_pupdate(const double* __re
             for (int j = 0; j < m; ++j) {
                 const double wj = __ldg(W + j * ldw + i);
 #pragma unroll
-                for (int v = 0; v < RT; ++v) zi[v] = fadd_mul(zi[v], u[j * RT + v], wj);
+                for (int v = 0; v < VW; ++v) zi[v] = fadd_mul(zi[v], us[j * RT + k0 + v], wj);
             }
 #pragma unroll
-        for (int v = 0; v < RT; ++v)
-            if (run[v]) p[me + v] = first ? zi[v] : fadd_mul(zi[v], beta[v], p[me + v]);
+        for (int v = 0; v < VW; ++v)
+            if (run[k0 + v]) p[e0 + v] = first ? zi[v] : fadd_mul(zi[v], beta[k0 + v], p[e0 + v]);
         if (zs_reset) {
-            double2* zr = reinterpret_cast<double2*>(zs_reset + me);
-            double2* yr = reinterpret_cast<double2*>(y_reset + me);
 #pragma unroll
-            for (int v = 0; v < RT / 2; ++v) {
-                zr[v] = make_double2(sent, sent);
-                yr[v] = make_double2(sent, sent);
+            for (int v = 0; v < VW / 2; ++v) {
+                reinterpret_cast<double2*>(zs_reset + e0)[v] = make_double2(sent, sent);
+                reinterpret_cast<double2*>(y_reset + e0)[v] = make_double2(sent, sent);
             }
         }
     }
@@ -691,45 +699,98 @@ __global__ void __launch_bounds__(kSpmvThreads) k_b_spmv_pq(SpmvArgs a, int cap,
     }
 }
 
-// f[j][k] = W_j . y_k, lane per row (W_j[i] read once for all rhs); finaliser per rhs:
-// u[:,k] = (W^T A W)^-1 f[:,k] (mode 1) and f.u (mode 2)
+// f[j][k] = W_j . y_k for every (j, k).  Lane per row (each y row read as RT/2 16-byte loads,
+// W_j[i] loads coalesced), JC columns x RT values in registers.  The m/JC column passes run as
+// SIBLING CTAs over the same contiguous row range (consecutive block ids, so they are resident
+// together and read the same y rows at about the same time: y comes from HBM about once, from L2
+// for the siblings; W once).  Per output: thread partials, a fixed-order block sum, then the
+// last CTA sums the row ranges in order.  Finaliser per rhs: u[:,k] = (W^T A W)^-1 f[:,k]
+// (mode 1) and f.u (mode 2).  Host grid: X x P (BatchSolve::tgrid).
 template <int RT>
-__global__ void __launch_bounds__(kStreamThreads) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
-                                                            const double* __restrict__ y, int32_t n, double* partials,
-                                                            const double* __restrict__ L, double* __restrict__ u,
-                                                            int mode, BState* st, int respect_done) {
-    constexpr int JC = RT <= 4 ? 8 : (RT <= 8 ? 4 : 2);
+__device__ __host__ constexpr int tallt_jc() {
+    return RT <= 4 ? 8 : (RT <= 8 ? 4 : 2);
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kElemThreads, 6) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
+                                                            const double* __restrict__ y, int32_t n,
+                                                            double* partials, const double* __restrict__ L,
+                                                            double* __restrict__ u, int mode, BState* st,
+                                                            int respect_done) {
+    constexpr int JC = tallt_jc<RT>();
+    constexpr int VW = RT % 4 == 0 ? 4 : 2;  // values per thread: G = RT/VW threads per row
+    constexpr int G = RT / VW;
     __shared__ double scratch[32 * JC * RT];
-    __shared__ double bvals[kMaxRedB];
+    __shared__ double bvals[JC * RT];
     __shared__ double tot[kMaxRedB];
-    __shared__ double fk[8][128];
-    __shared__ double sol[8][128];
+    __shared__ double fk[6][128];
+    __shared__ double sol[6][128];
+    __shared__ bool s_last;
     if (respect_done && st->nrun == 0) return;
-    for (int j0 = 0; j0 < m; j0 += JC) {
-        const int mc = min(JC, m - j0);
-        double acc[JC * RT];
+    const int P = (m + JC - 1) / JC;
+    const int X = gridDim.x / P;
+    const int pc = blockIdx.x % P, x = blockIdx.x / P;
+    const int j0 = pc * JC, mc = min(JC, m - j0);
+    if (x < X) {
+        const int32_t per = (n + X - 1) / X;
+        const int32_t i0 = x * per, i1 = min(n, i0 + per);
+        const int c = threadIdx.x % G;  // kElemThreads % G == 0: fixed chunk
+        double acc[JC][VW];
 #pragma unroll
-        for (int c = 0; c < JC * RT; ++c) acc[c] = 0.0;
-        for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-            double yi[RT];
+        for (int jc = 0; jc < JC; ++jc)
 #pragma unroll
-            for (int v = 0; v < RT / 2; ++v) {
-                const double2 t = reinterpret_cast<const double2*>(y + static_cast<int64_t>(i) * RT)[v];
-                yi[2 * v] = t.x;
-                yi[2 * v + 1] = t.y;
+            for (int v = 0; v < VW; ++v) acc[jc][v] = 0.0;
+        const int64_t it1 = static_cast<int64_t>(i1) * G;
+#pragma unroll 4
+        for (int64_t it = static_cast<int64_t>(i0) * G + threadIdx.x; it < it1; it += kElemThreads) {
+            const int64_t i = it / G;
+            double yv[VW];
+#pragma unroll
+            for (int v = 0; v < VW / 2; ++v) {
+                const double2 t = reinterpret_cast<const double2*>(y + it * VW)[v];
+                yv[2 * v] = t.x;
+                yv[2 * v + 1] = t.y;
             }
 #pragma unroll
-            for (int c = 0; c < JC; ++c)
-                if (c < mc) {
-                    const double wj = __ldg(W + (j0 + c) * ldw + i);
+            for (int jc = 0; jc < JC; ++jc)
+                if (jc < mc) {
+                    const double wj = __ldg(W + (j0 + jc) * ldw + i);
 #pragma unroll
-                    for (int v = 0; v < RT; ++v) acc[c * RT + v] = fadd_mul(acc[c * RT + v], wj, yi[v]);
+                    for (int v = 0; v < VW; ++v) acc[jc][v] = fadd_mul(acc[jc][v], wj, yv[v]);
                 }
         }
-        block_sum_dyn<JC * RT>(acc, mc * RT, scratch, bvals + j0 * RT);
+        double full[JC * RT];  // this thread's chunk, zeros elsewhere (adding 0.0 is exact)
+#pragma unroll
+        for (int t = 0; t < JC * RT; ++t) full[t] = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < G; ++cc)
+            if (cc == c)
+#pragma unroll
+                for (int jc = 0; jc < JC; ++jc)
+#pragma unroll
+                    for (int v = 0; v < VW; ++v) full[jc * RT + cc * VW + v] = acc[jc][v];
+        block_sum_dyn<JC * RT>(full, mc * RT, scratch, bvals);
+        for (int t = threadIdx.x; t < mc * RT; t += blockDim.x)
+            partials[static_cast<int64_t>(j0 * RT + t) * X + x] = bvals[t];
     }
+    __threadfence();
     __syncthreads();
-    if (grid_reduce_dyn(bvals, m * RT, partials, &st->tick[2], tot)) {
+    if (threadIdx.x == 0) s_last = atomicAdd(&st->tick[2], 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int o = wid; o < m * RT; o += nw) {
+            double sv = 0.0;
+            for (int xx = lane; xx < X; xx += 32) sv = __dadd_rn(sv, __ldcg(partials + static_cast<int64_t>(o) * X + xx));
+            sv = warp_sum(sv);
+            if (lane == 0) tot[o] = sv;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) st->tick[2] = 0u;
+    }
+    {
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         for (int k = wid; k < RT; k += blockDim.x >> 5) {
             for (int j = lane; j < m; j += 32) fk[wid][j] = tot[j * RT + k];
@@ -802,43 +863,44 @@ __global__ void __launch_bounds__(kStreamThreads) k_b_deflate(double* __restrict
     }
 }
 
-// x += alpha p, r -= alpha q for running rhs (lane per row); relres, history, convergence
+// x += alpha p, r -= alpha q for running rhs; relres, history, convergence.  Element-parallel
+// (coalesced), each thread on one rhs; per-rhs sums over the block's threads in a fixed order.
 template <int RT>
-__global__ void __launch_bounds__(kStreamThreads) k_b_xr(double* __restrict__ x, double* __restrict__ r,
-                                                         const double* __restrict__ p, const double* __restrict__ q,
-                                                         int32_t n, double* partials, BState* st,
-                                                         double* __restrict__ hist, int64_t hist_ld, int identity) {
-    __shared__ double scratch[32 * RT];
+__global__ void __launch_bounds__(kElemThreads) k_b_xr(double* __restrict__ x, double* __restrict__ r,
+                                                       const double* __restrict__ p, const double* __restrict__ q,
+                                                       int32_t n, double* partials, BState* st,
+                                                       double* __restrict__ hist, int64_t hist_ld, int identity) {
+    __shared__ double sred[kElemThreads];
     __shared__ double vals[RT];
     __shared__ double tot[RT];
-    __shared__ double alpha[RT];
-    __shared__ int run[RT];
     if (st->nrun == 0) return;
+    const int kk = threadIdx.x % RT;
+    const bool run_k = st->done[kk] == kRunning;
+    const double alpha = st->alpha[kk];
+    double acc = 0.0;
+    if (run_k) {
+        const int64_t total = static_cast<int64_t>(n) * RT;
+        for (int64_t e = blockIdx.x * static_cast<int64_t>(kElemThreads) + threadIdx.x; e < total;
+             e += static_cast<int64_t>(gridDim.x) * kElemThreads) {
+            x[e] = fadd_mul(x[e], alpha, p[e]);
+            const double ri = fsub_mul(r[e], alpha, q[e]);
+            r[e] = ri;
+            acc = fadd_mul(acc, ri, ri);
+        }
+    }
+    sred[threadIdx.x] = acc;
+    __syncthreads();
     if (threadIdx.x < RT) {
-        alpha[threadIdx.x] = st->alpha[threadIdx.x];
-        run[threadIdx.x] = st->done[threadIdx.x] == kRunning;
+        double v = 0.0;
+        for (int t = threadIdx.x; t < kElemThreads; t += RT) v = __dadd_rn(v, sred[t]);
+        vals[threadIdx.x] = v;
     }
     __syncthreads();
-    double acc[RT];
-#pragma unroll
-    for (int v = 0; v < RT; ++v) acc[v] = 0.0;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int64_t me = static_cast<int64_t>(i) * RT;
-#pragma unroll
-        for (int v = 0; v < RT; ++v)
-            if (run[v]) {
-                x[me + v] = fadd_mul(x[me + v], alpha[v], p[me + v]);
-                const double ri = fsub_mul(r[me + v], alpha[v], q[me + v]);
-                r[me + v] = ri;
-                acc[v] = fadd_mul(acc[v], ri, ri);
-            }
-    }
-    block_sum_dyn<RT>(acc, RT, scratch, vals);
     if (grid_reduce_dyn(vals, RT, partials, &st->tick[4], tot)) {
         if (threadIdx.x < RT) {
             const int k = threadIdx.x;
             const int i = st->iter;
-            if (run[k]) {
+            if (st->done[k] == kRunning) {
                 const double relres = sqrt(tot[k]) / st->bnorm[k];
                 st->rr[k] = tot[k];
                 st->relres[k] = relres;
@@ -1003,6 +1065,7 @@ struct BatchSolve {
     const rcg_basis* scb = nullptr;
     BatchWs* w = nullptr;
     int sg = 1, pg = 1;
+    int eg = 1;  // element-parallel grid (kElemThreads)
     int start_iter = 1;
     SlotMap map;  // slot k <-> original right-hand side map.col[k]
 
@@ -1017,6 +1080,7 @@ struct BatchSolve {
         if (sc) mm = std::max(mm, scb->k);
         if (defl) mm = std::max(mm, defl->k);
         require(mm * RT <= kMaxRedB, "batch: basis columns x right-hand sides exceed the reduction capacity");
+        require(mm <= 128, "batch: at most 128 basis columns");
         const int64_t nrt = static_cast<int64_t>(n) * RT;
         int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 31) / 32 : 1;
         const int64_t groups = (ntiles + kGroup - 1) / kGroup;
@@ -1024,6 +1088,8 @@ struct BatchSolve {
         w = &batch_ws(slot, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
         sg = stream_grid(ctx, n);
         pg = spmv_grid(ctx, n);
+        eg = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>((nrt + kElemThreads * 4 - 1) / (kElemThreads * 4), ctx->num_sms * 8)));
         static bool prepared = false;
         if (!prepared) {
             allow_smem(reinterpret_cast<const void*>(k_b_residual<RT>));
@@ -1069,6 +1135,13 @@ struct BatchSolve {
         start_iter = iter;
     }
 
+    // k_b_tallt grid: X row ranges x P sibling column passes, about 4 CTAs per SM
+    int tgrid(int mcols) const {
+        const int P = std::max(1, (mcols + tallt_jc<RT>() - 1) / tallt_jc<RT>());
+        const int X = std::max(1, std::min((n + 255) / 256, ctx->num_sms * 6 / P));  // one wave
+        return X * P;
+    }  // (kElemThreads threads per CTA)
+
     SpmvArgs sargs() const {
         SpmvArgs s{};
         s.rs = a->rs;
@@ -1105,7 +1178,7 @@ struct BatchSolve {
                                                                           w->partials, dfl ? 1 : 0);
         RCG_LAUNCHED(ctx);
         if (dfl) {
-            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->r, n, w->partials,
+            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->r, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
             k_b_deflate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr,
@@ -1113,7 +1186,7 @@ struct BatchSolve {
             RCG_LAUNCHED(ctx);
         }
         if (sc) {
-            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
+            k_b_tallt<RT><<<tgrid(scb->k), kElemThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
                                                                   scb->l, w->u2, 2, w->st, 0);
             RCG_LAUNCHED(ctx);
         }
@@ -1139,7 +1212,7 @@ struct BatchSolve {
         require(ic || !sc, "batch: subspace correction needs the IC inner preconditioner");
         {
             KTimer t(ctx, 8, RT);
-            k_b_pupdate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(z, w->p, ic ? w->zs : nullptr, w->y, n, w->st,
+            k_b_pupdate<RT><<<sg, 256, 0, ctx->stream>>>(z, w->p, ic ? w->zs : nullptr, w->y, n, w->st,
                                                                     sc ? scb->w : nullptr, sc ? scb->ld : 0,
                                                                     sc ? scb->k : 0, w->u2);
             RCG_LAUNCHED(ctx);
@@ -1153,7 +1226,7 @@ struct BatchSolve {
         }
         if (dfl) {
             KTimer t(ctx, 9, RT);
-            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n, w->partials,
+            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 1);
             RCG_LAUNCHED(ctx);
             k_b_deflate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, n,
@@ -1162,13 +1235,13 @@ struct BatchSolve {
         }
         {
             KTimer t(ctx, 8, RT);
-            k_b_xr<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, w->r, w->p, w->q, n, w->partials, w->st, w->hist,
+            k_b_xr<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->x, w->r, w->p, w->q, n, w->partials, w->st, w->hist,
                                                                max_iter + 1, (!ic && !sc) ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
         if (sc) {
             KTimer t(ctx, 9, RT);
-            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
+            k_b_tallt<RT><<<tgrid(scb->k), kElemThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
                                                                   scb->l, w->u2, 2, w->st, 1);
             RCG_LAUNCHED(ctx);
         }
@@ -1192,13 +1265,13 @@ struct BatchSolve {
         k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, nullptr, 0, 0, nullptr, n, w->st, 2);
         RCG_LAUNCHED(ctx);
         if (defl && defl->k > 0) {  // x = P x + W (W^T A W)^-1 W^T b (pcg.cpp:152-157), finished slots
-            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->aw, defl->ld, defl->k, w->x, n, w->partials,
+            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->aw, defl->ld, defl->k, w->x, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
             k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
                                                                            w->st, 0);
             RCG_LAUNCHED(ctx);
-            k_b_tallt<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->b, n, w->partials,
+            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->b, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
             k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
