@@ -35,6 +35,8 @@ typedef struct rcg_ic rcg_ic;           /* device IC(0) factor + sweep schedules
 typedef struct rcg_tall rcg_tall;       /* device n x k column block (TallDense) */
 typedef struct rcg_basis rcg_basis;     /* W, AW, chol(W^T A W) (DeflationOperator / SC state) */
 typedef struct rcg_sampler rcg_sampler; /* device snapshot slots (SamplerState) */
+typedef struct rcg_dslab rcg_dslab;     /* one GPU's row slab of a multi-GPU solve */
+typedef struct rcg_comm rcg_comm;       /* slab transport: NCCL (one slab per process) or loopback */
 
 /* message of the last failing call on this thread; "" after success */
 const char* rcg_last_error(void);
@@ -255,6 +257,50 @@ int rcg_multicolor_order(int32_t n, const int32_t* row_start, const int32_t* col
 int rcg_permute_symmetric(int32_t n, const int32_t* row_start, const int32_t* col_idx, const double* values,
                           const int32_t* new_of_old, int32_t** row_start_out, int32_t** col_idx_out,
                           double** values_out);
+
+/* ------------------------------------------------------------------ multi-GPU row slabs
+ * The reference has no distributed solver; its block-Jacobi IC(0) (ic0_factorize(a, s, G),
+ * ic_preconditioner.cpp:97-121, bounds floor(b n / G)) is the operator the slabs apply: rank b
+ * owns rows [floor(b n/G), floor((b+1) n/G)), factorises its diagonal block (no communication in
+ * the preconditioner), and exchanges halo values of p (and of x once) before each SpMV; the three
+ * dot products of an iteration are summed over ranks (NCCL allreduce), so every rank holds the
+ * same scalars and stops at the same iteration.  A symmetric sparsity pattern is assumed (the
+ * reference matrices are SPD): what rank q needs from rank b is b's rows with a column in q's
+ * range. */
+typedef struct {
+    int32_t row_begin, row_end;  /* global rows of this slab */
+    int32_t nloc, nhalo;         /* local rows, halo columns */
+    int64_t nnz;                 /* local entries */
+    int32_t* row_start;          /* nloc + 1 */
+    int32_t* col_idx;            /* local columns: [0, nloc) own rows, nloc + h = halo_global[h] */
+    double* values;
+    int32_t* halo_global;        /* nhalo, ascending (so grouped by owning slab) */
+    int32_t* recv_count;         /* nparts: halo values received from each slab */
+    int32_t* send_count;         /* nparts: values sent to each slab */
+    int32_t* send_idx;           /* sum(send_count) local rows, grouped by destination, ascending */
+    int nparts, part;
+} rcg_slab_plan;
+/* host: the slab `part` of `nparts` of a global CSR (arrays malloc'ed; rcg_slab_plan_free) */
+int rcg_slab_plan_create(int32_t n, const int32_t* row_start, const int32_t* col_idx, const double* values,
+                         int nparts, int part, rcg_slab_plan* out);
+void rcg_slab_plan_free(rcg_slab_plan* plan);
+/* device slab on ctx's GPU/stream; ic (the slab's diagonal-block factor) may be null = identity */
+int rcg_dslab_create(rcg_ctx* ctx, const rcg_slab_plan* plan, const rcg_ic* ic, rcg_dslab** out);
+void rcg_dslab_destroy(rcg_dslab* s);
+/* NCCL transport, one slab per process: id = 128-byte ncclUniqueId made by rank 0
+ * (rcg_comm_nccl_unique_id) and broadcast by the caller.  libnccl is resolved at run time (the
+ * copy the process already loaded, else libnccl.so.2). */
+int rcg_comm_nccl_unique_id(void* id128);
+int rcg_comm_create_nccl(const void* id128, int nranks, int rank, rcg_comm** out);
+/* loopback transport: all nparts slabs in this process on one GPU (stream-ordered device copies
+ * and a fixed-order sum; slabs never wait on each other inside a kernel) -- tests the distributed
+ * iteration on one GPU */
+int rcg_comm_create_loopback(int nparts, rcg_comm** out);
+void rcg_comm_destroy(rcg_comm* c);
+/* distributed PCG (pcg.cpp:37-92 per rank with block-Jacobi IC or identity): nslabs = 1 with
+ * NCCL, = nparts with loopback; b[s], x[s] are slab s's local rows (host or device) */
+int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* b,
+                       double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,14 @@ class GenParams(C.Structure):
     ]
 
 
+class SlabPlanC(C.Structure):
+    _fields_ = [
+        ("row_begin", C.c_int32), ("row_end", C.c_int32), ("nloc", C.c_int32), ("nhalo", C.c_int32),
+        ("nnz", C.c_int64), ("row_start", i32p), ("col_idx", i32p), ("values", dp), ("halo_global", i32p),
+        ("recv_count", i32p), ("send_count", i32p), ("send_idx", i32p), ("nparts", C.c_int), ("part", C.c_int),
+    ]
+
+
 def _sig(name, restype, *args):
     f = getattr(lib, name)
     f.restype = restype
@@ -158,6 +166,16 @@ SIGNATURES = {
     "rcg_multicolor_order": (C.c_int, C.c_int32, vp, vp, vp, i32p),
     "rcg_permute_symmetric": (C.c_int, C.c_int32, vp, vp, vp, vp, C.POINTER(i32p), C.POINTER(i32p),
                               C.POINTER(dp)),
+    "rcg_slab_plan_create": (C.c_int, C.c_int32, vp, vp, vp, C.c_int, C.c_int, C.POINTER(SlabPlanC)),
+    "rcg_slab_plan_free": (None, C.POINTER(SlabPlanC)),
+    "rcg_dslab_create": (C.c_int, vp, C.POINTER(SlabPlanC), vp, C.POINTER(vp)),
+    "rcg_dslab_destroy": (None, vp),
+    "rcg_comm_nccl_unique_id": (C.c_int, vp),
+    "rcg_comm_create_nccl": (C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)),
+    "rcg_comm_create_loopback": (C.c_int, C.c_int, C.POINTER(vp)),
+    "rcg_comm_destroy": (None, vp),
+    "rcg_dist_pcg_solve": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                           C.POINTER(SolverConfig), C.POINTER(SolveReport)),
 }
 
 for _name, (_res, *_args) in SIGNATURES.items():

@@ -572,3 +572,108 @@ def lanczos_extremes(alphas, betas):
     lo, hi = C.c_double(), C.c_double()
     check(lib.rcg_lanczos_extremes(len(a), _ptr(a), _ptr(b), C.byref(lo), C.byref(hi)))
     return lo.value, hi.value
+
+
+# --------------------------------------------------------------------------- multi-GPU row slabs
+class SlabPlan:
+    """Host plan of slab `part` of `nparts` (rcg_slab_plan_create): the reference's block bounds
+    floor(b n / G), the local CSR with halo columns numbered after the owned rows, and the halo
+    send / receive lists.  Arrays are numpy copies; the C plan is kept for rcg_dslab_create."""
+
+    def __init__(self, n, row_start, col_idx, values, nparts: int, part: int):
+        rs = np.ascontiguousarray(row_start, dtype=np.int32)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        va = np.ascontiguousarray(values, dtype=np.float64)
+        self._c = L.SlabPlanC()
+        check(lib.rcg_slab_plan_create(int(n), _ptr(rs), _ptr(ci), _ptr(va), int(nparts), int(part), C.byref(self._c)))
+        c = self._c
+        self.nparts, self.part = c.nparts, c.part
+        self.row_begin, self.row_end, self.nloc, self.nhalo, self.nnz = c.row_begin, c.row_end, c.nloc, c.nhalo, c.nnz
+
+        def arr(ptr, k, dt):
+            return np.ctypeslib.as_array(ptr, shape=(k,)).astype(dt, copy=True) if k > 0 else np.zeros(0, dt)
+
+        self.row_start = arr(c.row_start, self.nloc + 1, np.int32)
+        self.col_idx = arr(c.col_idx, self.nnz, np.int32)
+        self.values = arr(c.values, self.nnz, np.float64)
+        self.halo_global = arr(c.halo_global, self.nhalo, np.int32)
+        self.recv_count = arr(c.recv_count, self.nparts, np.int32)
+        self.send_count = arr(c.send_count, self.nparts, np.int32)
+        self.send_idx = arr(c.send_idx, int(self.send_count.sum()), np.int32)
+
+    def diagonal_block(self):
+        """CSR of the slab's diagonal block (columns < nloc): the block-Jacobi IC(0) input."""
+        keep = self.col_idx < self.nloc
+        rows = np.repeat(np.arange(self.nloc), np.diff(self.row_start))
+        counts = np.bincount(rows[keep], minlength=self.nloc)
+        rs = np.zeros(self.nloc + 1, np.int32)
+        rs[1:] = np.cumsum(counts)
+        return rs, self.col_idx[keep].copy(), self.values[keep].copy()
+
+    def __del__(self):
+        try:
+            lib.rcg_slab_plan_free(C.byref(self._c))
+        except Exception:
+            pass
+
+
+class DSlab:
+    """One GPU's row slab (rcg_dslab_create): local matrix with halo columns, exchange lists,
+    extended x / p buffers; `ic` is the slab's diagonal-block IcFactor (None = identity)."""
+
+    def __init__(self, ctx: Context, plan: SlabPlan, ic: Optional[IcFactor] = None):
+        h = C.c_void_p()
+        check(lib.rcg_dslab_create(ctx.h, C.byref(plan._c), ic.h if ic is not None else None, C.byref(h)))
+        self.h, self.ctx, self.plan, self.ic = h, ctx, plan, ic
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.rcg_dslab_destroy(self.h)
+            self.h = None
+
+
+class Comm:
+    """Slab transport: `Comm.nccl(id, nranks, rank)` (one slab per process, NCCL over NVLink) or
+    `Comm.loopback(nparts)` (all slabs in this process on one GPU; tests)."""
+
+    def __init__(self, h, nparts):
+        self.h, self.nparts = h, nparts
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        check(lib.rcg_comm_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, nranks: int, rank: int) -> "Comm":
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib.rcg_comm_create_nccl(buf, int(nranks), int(rank), C.byref(h)))
+        return cls(h, nranks)
+
+    @classmethod
+    def loopback(cls, nparts: int) -> "Comm":
+        h = C.c_void_p()
+        check(lib.rcg_comm_create_loopback(int(nparts), C.byref(h)))
+        return cls(h, nparts)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.rcg_comm_destroy(self.h)
+            self.h = None
+
+
+def dist_pcg_solve(comm: Comm, slabs, bs, xs, eps: float = 1e-8, max_iter: int = 1000) -> SolveReport:
+    """Distributed PCG over row slabs (rcg_dist_pcg_solve): block-Jacobi IC(0) when the slabs
+    carry factors, else identity.  bs[s], xs[s]: slab s's local rows; xs updated in place."""
+    slabs = list(slabs)
+    ns = len(slabs)
+    bs = [_f64(b, s.plan.nloc, "b") for b, s in zip(bs, slabs)]
+    hs = (C.c_void_p * ns)(*[s.h.value for s in slabs])
+    bp = (C.c_void_p * ns)(*[_ptr(b) for b in bs])
+    xp = (C.c_void_p * ns)(*[_ptr(x) for x in xs])
+    cfg = _cfg(eps, max_iter)
+    rep, bufs = _report(max(1, int(max_iter)))
+    check(lib.rcg_dist_pcg_solve(comm.h, ns, hs, bp, xp, C.byref(cfg), C.byref(rep)))
+    return _finish(rep, bufs)

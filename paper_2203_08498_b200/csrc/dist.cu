@@ -1,0 +1,795 @@
+// dist.cu -- multi-GPU row slabs: the host slab plan, device slabs, the two
+// slab transports (NCCL, one slab per process; loopback, all slabs in one process on one GPU)
+// and the distributed PCG.
+//
+// Operator: the reference's block-Jacobi IC(0) (ic0_factorize(a, s, G), ic_preconditioner.cpp:
+// 97-121, bounds floor(b n / G)).  Rank b owns rows [floor(b n/G), floor((b+1) n/G)); its
+// preconditioner is the IC(0) factor of its diagonal block, so the sweeps need no communication.
+// Per iteration (pcg.cpp:63-89 order): local sweeps -> allreduce (r,z) -> beta, p = z + beta p ->
+// halo exchange of p -> q = A p_ext -> allreduce (p,q) -> alpha, x, r -> allreduce (r,r) ->
+// relres / convergence.  Local partial sums are deterministic (fixed-order grid reductions);
+// every rank receives identical totals, so every rank's DevState evolves identically and all
+// ranks stop enqueueing at the same batch boundary (matching collectives, no host agreement).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+#include "spmv_pipe.cuh"
+
+namespace rcg {
+
+constexpr int kDistTick = 6;  // DevState::tick slot of the slab-local reductions
+
+// ------------------------------------------------------------------ host slab plan
+static int32_t bound_of(int b, int32_t n, int nparts) {
+    return static_cast<int32_t>((static_cast<int64_t>(b) * n) / nparts);  // ic_preconditioner.cpp:104-106
+}
+
+static void plan_create(int32_t n, const int32_t* rs, const int32_t* ci, const double* va, int nparts, int part,
+                        rcg_slab_plan* out) {
+    require(n >= 1 && rs && ci && va && out, "rcg_slab_plan_create: null argument");
+    require(nparts >= 1 && nparts <= n && part >= 0 && part < nparts, "rcg_slab_plan_create: bad partition");
+    std::memset(out, 0, sizeof(*out));
+    std::vector<int32_t> bounds(nparts + 1);
+    for (int b = 0; b <= nparts; ++b) bounds[b] = bound_of(b, n, nparts);
+    auto owner = [&](int32_t col) {
+        return static_cast<int>(std::upper_bound(bounds.begin(), bounds.end(), col) - bounds.begin()) - 1;
+    };
+    const int32_t r0 = bounds[part], r1 = bounds[part + 1], nloc = r1 - r0;
+    std::vector<int32_t> halo;
+    for (int64_t e = rs[r0]; e < rs[r1]; ++e)
+        if (ci[e] < r0 || ci[e] >= r1) halo.push_back(ci[e]);
+    std::sort(halo.begin(), halo.end());
+    halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+    const int64_t nnz = rs[r1] - rs[r0];
+    out->row_begin = r0;
+    out->row_end = r1;
+    out->nloc = nloc;
+    out->nhalo = static_cast<int32_t>(halo.size());
+    out->nnz = nnz;
+    out->nparts = nparts;
+    out->part = part;
+    auto alloc = [](size_t bytes) {
+        void* p = std::malloc(std::max<size_t>(bytes, 8));
+        if (!p) throw Error(RCG_E_INVALID, "rcg_slab_plan_create: out of host memory");
+        return p;
+    };
+    out->row_start = static_cast<int32_t*>(alloc(sizeof(int32_t) * (nloc + 1)));
+    out->col_idx = static_cast<int32_t*>(alloc(sizeof(int32_t) * nnz));
+    out->values = static_cast<double*>(alloc(sizeof(double) * nnz));
+    out->halo_global = static_cast<int32_t*>(alloc(sizeof(int32_t) * halo.size()));
+    out->recv_count = static_cast<int32_t*>(alloc(sizeof(int32_t) * nparts));
+    out->send_count = static_cast<int32_t*>(alloc(sizeof(int32_t) * nparts));
+    std::memcpy(out->halo_global, halo.data(), sizeof(int32_t) * halo.size());
+    for (int q = 0; q < nparts; ++q) out->recv_count[q] = out->send_count[q] = 0;
+    for (int32_t h : halo) out->recv_count[owner(h)]++;
+    // local CSR: own columns -> col - r0, halo columns -> nloc + position in halo
+    for (int32_t i = 0; i <= nloc; ++i) out->row_start[i] = static_cast<int32_t>(rs[r0 + i] - rs[r0]);
+    for (int64_t e = rs[r0]; e < rs[r1]; ++e) {
+        const int32_t c = ci[e];
+        const int64_t le = e - rs[r0];
+        out->col_idx[le] = (c >= r0 && c < r1)
+                               ? c - r0
+                               : nloc + static_cast<int32_t>(std::lower_bound(halo.begin(), halo.end(), c) - halo.begin());
+        out->values[le] = va[e];
+    }
+    // send lists (symmetric pattern): my rows with a column owned by q, ascending, grouped by q
+    std::vector<std::vector<int32_t>> send(nparts);
+    for (int32_t i = 0; i < nloc; ++i) {
+        int last = -1;
+        std::vector<int> qs;
+        for (int64_t e = rs[r0 + i]; e < rs[r0 + i + 1]; ++e) {
+            const int32_t c = ci[e];
+            if (c >= r0 && c < r1) continue;
+            qs.push_back(owner(c));
+        }
+        std::sort(qs.begin(), qs.end());
+        for (int q : qs)
+            if (q != last) {
+                send[q].push_back(i);
+                last = q;
+            }
+    }
+    int64_t nsend = 0;
+    for (int q = 0; q < nparts; ++q) nsend += static_cast<int64_t>(send[q].size());
+    out->send_idx = static_cast<int32_t*>(alloc(sizeof(int32_t) * nsend));
+    int64_t off = 0;
+    for (int q = 0; q < nparts; ++q) {
+        out->send_count[q] = static_cast<int32_t>(send[q].size());
+        std::memcpy(out->send_idx + off, send[q].data(), sizeof(int32_t) * send[q].size());
+        off += static_cast<int64_t>(send[q].size());
+    }
+}
+
+static void plan_free(rcg_slab_plan* p) {
+    if (!p) return;
+    for (void* a : {(void*)p->row_start, (void*)p->col_idx, (void*)p->values, (void*)p->halo_global,
+                    (void*)p->recv_count, (void*)p->send_count, (void*)p->send_idx})
+        std::free(a);
+    std::memset(p, 0, sizeof(*p));
+}
+
+}  // namespace rcg
+
+// ------------------------------------------------------------------ device slab
+struct rcg_dslab {
+    rcg_ctx* ctx = nullptr;       // borrowed: stream, workspace, DevState
+    rcg_matrix* a = nullptr;      // owned: nloc rows, columns [0, nloc + nhalo)
+    const rcg_ic* ic = nullptr;   // borrowed: diagonal-block factor (null = identity)
+    int nparts = 1, part = 0;
+    int32_t nloc = 0, nhalo = 0, row_begin = 0;
+    std::vector<int32_t> send_count, recv_count, send_off, recv_off;
+    int32_t nsend = 0;
+    int32_t* send_idx = nullptr;  // device
+    double* sendbuf = nullptr;    // device
+    double* xe = nullptr;         // device x_ext (nloc + nhalo)
+    double* pe = nullptr;         // device p_ext (nloc + nhalo)
+    double* dsum = nullptr;       // device: local partials in, global totals out
+};
+
+namespace rcg {
+
+// ------------------------------------------------------------------ kernels
+// r = b - A x_ext (local rows); partials (b, b), (r, r)
+__global__ void __launch_bounds__(kSpmvThreads) k_d_residual(SpmvArgs a, int cap, const double* __restrict__ b,
+                                                             double* __restrict__ r, DevState* st, double* dsum) {
+    __shared__ double red[2 * 32];
+    __shared__ double tot[2];
+    double acc[2] = {0.0, 0.0};
+    spmv_pipeline<1>(a, cap, [&](int32_t row, const double (&s)[1]) {
+        const double bi = b[row];
+        const double ri = __dsub_rn(bi, s[0]);
+        r[row] = ri;
+        acc[0] = fadd_mul(acc[0], bi, bi);
+        acc[1] = fadd_mul(acc[1], ri, ri);
+    });
+    block_sum<2>(acc, red);
+    if (grid_reduce<2>(acc, a.partials, blockIdx.x, gridDim.x, &st->tick[kDistTick], tot, red) && threadIdx.x == 0) {
+        dsum[0] = tot[0];
+        dsum[1] = tot[1];
+    }
+}
+
+// q = A p_ext (local rows); partial (p, q)
+__global__ void __launch_bounds__(kSpmvThreads) k_d_spmv(SpmvArgs a, int cap, DevState* st, double* dsum) {
+    __shared__ double red[32];
+    __shared__ double tot[1];
+    if (st->done) return;
+    double acc[1] = {0.0};
+    spmv_pipeline<1>(a, cap, [&](int32_t row, const double (&s)[1]) {
+        a.y[0][row] = s[0];
+        acc[0] = fadd_mul(acc[0], a.x[0][row], s[0]);
+    });
+    block_sum<1>(acc, red);
+    if (grid_reduce<1>(acc, a.partials, blockIdx.x, gridDim.x, &st->tick[kDistTick], tot, red) && threadIdx.x == 0)
+        dsum[0] = tot[0];
+}
+
+// partial (u, v)
+__global__ void __launch_bounds__(kStreamThreads) k_d_dot(const double* __restrict__ u, const double* __restrict__ v,
+                                                          int32_t n, double* partials, DevState* st, double* dsum) {
+    __shared__ double red[32];
+    __shared__ double tot[1];
+    if (st->done) return;
+    double acc[1] = {0.0};
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        acc[0] = fadd_mul(acc[0], u[i], v[i]);
+    block_sum<1>(acc, red);
+    if (grid_reduce<1>(acc, partials, blockIdx.x, gridDim.x, &st->tick[kDistTick], tot, red) && threadIdx.x == 0)
+        dsum[0] = tot[0];
+}
+
+// x += alpha p, r -= alpha q (local rows); partial (r, r)
+__global__ void __launch_bounds__(kStreamThreads) k_d_xr(double* __restrict__ x, double* __restrict__ r,
+                                                         const double* __restrict__ p, const double* __restrict__ q,
+                                                         int32_t n, double* partials, DevState* st, double* dsum) {
+    __shared__ double red[32];
+    __shared__ double tot[1];
+    if (st->done) return;
+    const double alpha = st->alpha;
+    double acc[1] = {0.0};
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        x[i] = fadd_mul(x[i], alpha, p[i]);
+        const double ri = fsub_mul(r[i], alpha, q[i]);
+        r[i] = ri;
+        acc[0] = fadd_mul(acc[0], ri, ri);
+    }
+    block_sum<1>(acc, red);
+    if (grid_reduce<1>(acc, partials, blockIdx.x, gridDim.x, &st->tick[kDistTick], tot, red) && threadIdx.x == 0)
+        dsum[0] = tot[0];
+}
+
+__global__ void k_d_pack(const double* __restrict__ v, const int32_t* __restrict__ idx, int32_t cnt,
+                         double* __restrict__ out) {
+    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) out[t] = v[idx[t]];
+}
+
+// scalar updates from the global totals g (pcg.cpp:43-89): 0 initial (b,b),(r,r); 1 (r,z);
+// 2 (p,q); 3 (r,r) after the x/r update
+__global__ void k_d_scalar(DevState* st, const double* __restrict__ g, int stage, double* hist, double* alph,
+                           double* bet, int identity) {
+    if (stage == 0) {
+        st->bnorm = sqrt(g[0]);
+        st->rr = g[1];
+        st->rho = g[1];
+        if (st->bnorm == 0.0)
+            st->done = kZeroRhs;
+        else if (sqrt(g[1]) <= st->eps * st->bnorm)
+            st->done = kConverged;
+        return;
+    }
+    if (st->done) return;
+    if (stage == 1) {
+        const double rho = g[0];
+        st->rho = rho;
+        if (rho <= 0.0) {
+            st->done = kBroken;
+            st->status = kBrkRz;
+        }
+        st->beta = st->iter > 1 ? rho / st->rho_prev : 0.0;
+    } else if (stage == 2) {
+        st->pq = g[0];
+        if (g[0] <= 0.0) {
+            st->done = kBroken;
+            st->status = kBrkPAp;
+        }
+        st->alpha = st->rho / g[0];
+    } else {
+        const int i = st->iter;
+        const double rr = g[0];
+        const double relres = sqrt(rr) / st->bnorm;
+        st->rr = rr;
+        st->relres = relres;
+        st->iters = i;
+        hist[i - 1] = relres;
+        alph[i - 1] = st->alpha;
+        bet[i - 1] = st->beta;
+        st->rho_prev = st->rho;
+        if (relres <= st->eps) {
+            st->done = kConverged;
+        } else if (i >= st->max_iter) {
+            st->done = kCapped;
+        } else {
+            st->iter = i + 1;
+            if (identity) {  // z = r: the next (r, z) is this (r, r)
+                st->rho = rr;
+                if (rr <= 0.0) {
+                    st->done = kBroken;
+                    st->status = kBrkRz;
+                }
+                st->beta = rr / st->rho_prev;
+            }
+        }
+    }
+}
+
+// loopback allreduce: every slab's partials summed in slab order, written back to all
+__global__ void k_lb_sum(double* const* d, int nslabs, int count) {
+    const int c = threadIdx.x;
+    if (c >= count) return;
+    double s = 0.0;
+    for (int b = 0; b < nslabs; ++b) s = __dadd_rn(s, d[b][c]);
+    for (int b = 0; b < nslabs; ++b) d[b][c] = s;
+}
+
+}  // namespace rcg
+
+// ------------------------------------------------------------------ transports
+struct rcg_comm {
+    virtual ~rcg_comm() {}
+    virtual int nparts() const = 0;
+    virtual int local_slabs() const = 0;
+    virtual void begin(rcg_dslab* const* s, int ns) { (void)s, (void)ns; }
+    // in-place sum over all slabs of dsum[0..count)
+    virtual void allreduce(rcg_dslab* const* s, int ns, int count) = 0;
+    // halo of the ext vector `which` (0: x_ext, 1: p_ext)
+    virtual void halo(rcg_dslab* const* s, int ns, int which) = 0;
+};
+
+namespace rcg {
+
+static double* ext_of(rcg_dslab* s, int which) { return which == 0 ? s->xe : s->pe; }
+
+static void pack(rcg_dslab* s, int which) {
+    if (s->nsend == 0) return;
+    const int g = std::max(1, std::min((s->nsend + 255) / 256, s->ctx->num_sms * 4));
+    k_d_pack<<<g, 256, 0, s->ctx->stream>>>(ext_of(s, which), s->send_idx, s->nsend, s->sendbuf);
+    RCG_LAUNCHED(s->ctx);
+}
+
+// --- NCCL, resolved at run time
+struct Nccl {
+    void* h = nullptr;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+
+    static Nccl& get() {
+        static Nccl n;
+        if (!n.h) {
+            // the copy the process already loaded (torch's), else the loader's libnccl.so.2
+            n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+            if (!n.h) n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!n.h) throw Error(RCG_E_CUDA, std::string("NCCL transport: cannot load libnccl.so.2: ") + dlerror());
+            auto sym = [&](const char* name) {
+                void* f = dlsym(n.h, name);
+                if (!f) throw Error(RCG_E_CUDA, std::string("NCCL transport: missing symbol ") + name);
+                return f;
+            };
+            n.get_unique_id = reinterpret_cast<decltype(n.get_unique_id)>(sym("ncclGetUniqueId"));
+            n.comm_init_rank = reinterpret_cast<decltype(n.comm_init_rank)>(sym("ncclCommInitRank"));
+            n.comm_destroy = reinterpret_cast<decltype(n.comm_destroy)>(sym("ncclCommDestroy"));
+            n.all_reduce = reinterpret_cast<decltype(n.all_reduce)>(sym("ncclAllReduce"));
+            n.send = reinterpret_cast<decltype(n.send)>(sym("ncclSend"));
+            n.recv = reinterpret_cast<decltype(n.recv)>(sym("ncclRecv"));
+            n.group_start = reinterpret_cast<decltype(n.group_start)>(sym("ncclGroupStart"));
+            n.group_end = reinterpret_cast<decltype(n.group_end)>(sym("ncclGroupEnd"));
+            n.error_string = reinterpret_cast<decltype(n.error_string)>(sym("ncclGetErrorString"));
+        }
+        return n;
+    }
+    void check(ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) throw Error(RCG_E_CUDA, std::string("NCCL ") + what + ": " + error_string(r));
+    }
+};
+
+struct NcclComm : rcg_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    int nparts() const override { return nranks; }
+    int local_slabs() const override { return 1; }
+    ~NcclComm() override {
+        if (comm) Nccl::get().comm_destroy(comm);
+    }
+    void allreduce(rcg_dslab* const* s, int ns, int count) override {
+        (void)ns;
+        Nccl& nc = Nccl::get();
+        nc.check(nc.all_reduce(s[0]->dsum, s[0]->dsum, count, ncclFloat64, ncclSum, comm, s[0]->ctx->stream),
+                 "allreduce");
+    }
+    void halo(rcg_dslab* const* s, int ns, int which) override {
+        (void)ns;
+        rcg_dslab* d = s[0];
+        pack(d, which);
+        Nccl& nc = Nccl::get();
+        double* ext = ext_of(d, which);
+        nc.check(nc.group_start(), "group start");
+        for (int q = 0; q < nranks; ++q) {
+            if (d->send_count[q])
+                nc.check(nc.send(d->sendbuf + d->send_off[q], d->send_count[q], ncclFloat64, q, comm, d->ctx->stream),
+                         "send");
+            if (d->recv_count[q])
+                nc.check(nc.recv(ext + d->nloc + d->recv_off[q], d->recv_count[q], ncclFloat64, q, comm, d->ctx->stream),
+                         "recv");
+        }
+        nc.check(nc.group_end(), "group end");
+    }
+};
+
+// --- loopback: all slabs in this process (one GPU); stream-ordered copies, fixed-order sums
+struct LoopComm : rcg_comm {
+    int np = 1;
+    int dev = 0;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev_join = nullptr;
+    std::vector<cudaEvent_t> ev;
+    double** dptrs = nullptr;  // device array of the slabs' dsum pointers
+    int nparts() const override { return np; }
+    int local_slabs() const override { return np; }
+    ~LoopComm() override {
+        if (dptrs) dev_free(dptrs);
+        for (auto e : ev) cudaEventDestroy(e);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (cs) cudaStreamDestroy(cs);
+    }
+    void begin(rcg_dslab* const* s, int ns) override {
+        std::vector<double*> h(ns);
+        for (int b = 0; b < ns; ++b) h[b] = s[b]->dsum;
+        RCG_CK(cudaMemcpy(dptrs, h.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice));
+    }
+    void allreduce(rcg_dslab* const* s, int ns, int count) override {
+        for (int b = 0; b < ns; ++b) {
+            RCG_CK(cudaEventRecord(ev[b], s[b]->ctx->stream));
+            RCG_CK(cudaStreamWaitEvent(cs, ev[b], 0));
+        }
+        k_lb_sum<<<1, 32, 0, cs>>>(dptrs, ns, count);
+        RCG_CK(cudaGetLastError());
+        RCG_CK(cudaEventRecord(ev_join, cs));
+        for (int b = 0; b < ns; ++b) RCG_CK(cudaStreamWaitEvent(s[b]->ctx->stream, ev_join, 0));
+    }
+    void halo(rcg_dslab* const* s, int ns, int which) override {
+        for (int q = 0; q < ns; ++q) {
+            pack(s[q], which);
+            RCG_CK(cudaEventRecord(ev[q], s[q]->ctx->stream));
+        }
+        for (int b = 0; b < ns; ++b) {
+            rcg_dslab* d = s[b];
+            double* ext = ext_of(d, which);
+            for (int q = 0; q < ns; ++q) {
+                if (!d->recv_count[q]) continue;
+                RCG_CK(cudaStreamWaitEvent(d->ctx->stream, ev[q], 0));
+                RCG_CK(cudaMemcpyAsync(ext + d->nloc + d->recv_off[q], s[q]->sendbuf + s[q]->send_off[b],
+                                       sizeof(double) * d->recv_count[q], cudaMemcpyDeviceToDevice, d->ctx->stream));
+            }
+        }
+    }
+};
+
+// ------------------------------------------------------------------ distributed PCG
+struct DistSolve {
+    rcg_comm* comm;
+    int ns;
+    rcg_dslab* const* sl;
+    int max_iter;
+    double eps;
+    bool ic = false;
+    std::vector<Staged> bst, xst;
+    std::vector<double*> bdev;
+
+    void setup(const double* const* b, double* const* x) {
+        static bool smem_ok = false;
+        if (!smem_ok) {
+            allow_smem(reinterpret_cast<const void*>(k_d_residual));
+            allow_smem(reinterpret_cast<const void*>(k_d_spmv));
+            smem_ok = true;
+        }
+        ic = sl[0]->ic != nullptr;
+        bst.resize(ns);
+        xst.resize(ns);
+        bdev.resize(ns);
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            const int32_t n = d->nloc;
+            require((d->ic != nullptr) == ic, "dist_pcg_solve: every slab needs the same preconditioner kind");
+            const int64_t ntiles = ic ? sweep_tiles(d->ic) : (n + kSweepThreads - 1) / kSweepThreads;
+            const int64_t ngroups = (ntiles + kGroup - 1) / kGroup;
+            const int64_t red = std::max<int64_t>(ntiles, static_cast<int64_t>(kMaxRed) * ctx->num_sms * 8);
+            ensure_workspace(ctx, std::max(n, 1), 1, max_iter, red, ngroups, 1);
+            stage_in(ctx, b[s], n, bst[s]);
+            bdev[s] = bst[s].dev;
+            stage_in(ctx, x[s], n, xst[s]);
+            if (n > 0)
+                RCG_CK(cudaMemcpyAsync(d->xe, xst[s].dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            DevState h{};
+            h.done = kRunning;
+            h.iter = 1;
+            h.max_iter = max_iter;
+            h.eps = eps;
+            h.smp_method = -1;
+            std::memcpy(ctx->host_pinned, &h, sizeof(h));
+            RCG_CK(cudaMemcpyAsync(ctx->ws.st, ctx->host_pinned, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
+            if (ic) {
+                launch_fill_bits(ctx, ctx->ws.ybuf, n, kSentinelBits);
+                launch_fill_bits(ctx, ctx->ws.zs, n, kSentinelBits);
+            }
+        }
+        comm->begin(sl, ns);
+    }
+
+    SpmvArgs sargs(rcg_dslab* d, const double* xin, double* yout) {
+        SpmvArgs a{};
+        a.rs = d->a->rs;
+        a.ci = d->a->ci;
+        a.va = d->a->va;
+        a.n = d->nloc;
+        a.partials = d->ctx->ws.partials;
+        a.x[0] = xin;
+        a.y[0] = yout;
+        return a;
+    }
+
+    void scalar(int stage) {
+        for (int s = 0; s < ns; ++s) {
+            rcg_ctx* ctx = sl[s]->ctx;
+            k_d_scalar<<<1, 1, 0, ctx->stream>>>(ctx->ws.st, sl[s]->dsum, stage, ctx->ws.hist, ctx->ws.alph,
+                                                 ctx->ws.bet, ic ? 0 : 1);
+            RCG_LAUNCHED(ctx);
+        }
+    }
+
+    void initial() {
+        comm->halo(sl, ns, 0);
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            k_d_residual<<<spmv_grid(ctx, d->nloc), kSpmvThreads, spmv_smem(d->a), ctx->stream>>>(
+                sargs(d, d->xe, nullptr), d->a->cap, bdev[s], ctx->ws.r, ctx->ws.st, d->dsum);
+            RCG_LAUNCHED(ctx);
+        }
+        comm->allreduce(sl, ns, 2);
+        scalar(0);
+    }
+
+    void iteration() {
+        if (ic) {
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                rcg_ctx* ctx = d->ctx;
+                SweepArgs fa = sweep_args(ctx, d->ic, false);
+                fa.in = ctx->ws.r;
+                fa.out = ctx->ws.ybuf;
+                launch_sweep(ctx, d->ic, false, fa);
+                SweepArgs ba = sweep_args(ctx, d->ic, true);
+                ba.in = ctx->ws.ybuf;
+                ba.out = ctx->ws.zs;
+                launch_sweep(ctx, d->ic, true, ba);
+                k_d_dot<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                    ctx->ws.r, ctx->ws.zs, d->nloc, ctx->ws.partials, ctx->ws.st, d->dsum);
+                RCG_LAUNCHED(ctx);
+            }
+            comm->allreduce(sl, ns, 1);
+            scalar(1);
+        }
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            KTimer t(ctx, 3);
+            k_pupdate<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                ic ? ctx->ws.zs : ctx->ws.r, d->pe, ic ? ctx->ws.zs : nullptr, ctx->ws.ybuf, d->nloc, ctx->ws.st,
+                nullptr, 0, 0, nullptr);
+            RCG_LAUNCHED(ctx);
+        }
+        comm->halo(sl, ns, 1);
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            KTimer t(ctx, 0);
+            k_d_spmv<<<spmv_grid(ctx, d->nloc), kSpmvThreads, spmv_smem(d->a), ctx->stream>>>(
+                sargs(d, d->pe, ctx->ws.q), d->a->cap, ctx->ws.st, d->dsum);
+            RCG_LAUNCHED(ctx);
+        }
+        comm->allreduce(sl, ns, 1);
+        scalar(2);
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            KTimer t(ctx, 3);
+            k_d_xr<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                d->xe, ctx->ws.r, d->pe, ctx->ws.q, d->nloc, ctx->ws.partials, ctx->ws.st, d->dsum);
+            RCG_LAUNCHED(ctx);
+        }
+        comm->allreduce(sl, ns, 1);
+        scalar(3);
+    }
+
+    // same batching as the single-GPU loop; every slab holds identical scalars, slab 0 is polled
+    double run() {
+        rcg_ctx* c0 = sl[0]->ctx;
+        cudaEvent_t evs[2], t0, t1;
+        RCG_CK(cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming));
+        RCG_CK(cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming));
+        RCG_CK(cudaEventCreate(&t0));
+        RCG_CK(cudaEventCreate(&t1));
+        RCG_CK(cudaEventRecord(t0, c0->stream));
+        volatile int* flags = reinterpret_cast<volatile int*>(c0->host_pinned + 256);
+        flags[0] = flags[1] = 0;
+        int enq = 0, batch = 2, slot = 0, prev = 0;
+        bool have_prev = false;
+        while (true) {
+            for (int j = 0; j < batch && enq < max_iter; ++j, ++enq) iteration();
+            RCG_CK(cudaMemcpyAsync((void*)(flags + slot), &c0->ws.st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                                   c0->stream));
+            RCG_CK(cudaEventRecord(evs[slot], c0->stream));
+            if (enq >= max_iter) {
+                RCG_CK(cudaEventSynchronize(evs[slot]));
+                break;
+            }
+            if (have_prev) {
+                RCG_CK(cudaEventSynchronize(evs[prev]));
+                if (flags[prev] != kRunning) break;
+            }
+            have_prev = true;
+            prev = slot;
+            slot ^= 1;
+            batch = std::min(batch * 2, 16);
+        }
+        for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+        RCG_CK(cudaEventRecord(t1, c0->stream));
+        RCG_CK(cudaEventSynchronize(t1));
+        float ms = 0.f;
+        RCG_CK(cudaEventElapsedTime(&ms, t0, t1));
+        for (auto e : {evs[0], evs[1], t0, t1}) cudaEventDestroy(e);
+        return ms * 1e-3;
+    }
+
+    DevState finish(double* const* x) {
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            const int32_t n = d->nloc;
+            k_zero_if<<<stream_grid(ctx, n), kStreamThreads, 0, ctx->stream>>>(d->xe, n, ctx->ws.st);
+            RCG_LAUNCHED(ctx);
+            Staged out;
+            stage_out_begin(ctx, x[s], n, out);
+            if (n > 0)
+                RCG_CK(cudaMemcpyAsync(out.dev, d->xe, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            stage_out_end(ctx, x[s], n, out);
+            RCG_CK(cudaStreamSynchronize(ctx->stream));
+            if (ic) check_sweep_watchdog(ctx);
+        }
+        rcg_ctx* c0 = sl[0]->ctx;
+        DevState h{};
+        RCG_CK(cudaMemcpy(&h, c0->ws.st, sizeof(DevState), cudaMemcpyDeviceToHost));
+        return h;
+    }
+};
+
+}  // namespace rcg
+
+using namespace rcg;
+
+extern "C" {
+
+int rcg_slab_plan_create(int32_t n, const int32_t* row_start, const int32_t* col_idx, const double* values,
+                         int nparts, int part, rcg_slab_plan* out) {
+    return guard([&] {
+        try {
+            plan_create(n, row_start, col_idx, values, nparts, part, out);
+        } catch (...) {
+            plan_free(out);
+            throw;
+        }
+    });
+}
+
+void rcg_slab_plan_free(rcg_slab_plan* plan) { plan_free(plan); }
+
+int rcg_dslab_create(rcg_ctx* ctx, const rcg_slab_plan* p, const rcg_ic* ic, rcg_dslab** out) {
+    return guard([&] {
+        require(ctx && p && out, "rcg_dslab_create: null argument");
+        *out = nullptr;
+        if (ic) require(ic->n == p->nloc, "rcg_dslab_create: factor size does not match the slab's rows");
+        RCG_CK(cudaSetDevice(ctx->device));
+        auto* d = new rcg_dslab();
+        try {
+            d->ctx = ctx;
+            d->ic = ic;
+            d->nparts = p->nparts;
+            d->part = p->part;
+            d->nloc = p->nloc;
+            d->nhalo = p->nhalo;
+            d->row_begin = p->row_begin;
+            rcg_matrix* a = nullptr;
+            const int rc = rcg_matrix_create(ctx, p->nloc, p->row_start, p->col_idx, p->values, 0, &a);
+            if (rc != RCG_OK) throw Error(rc, rcg_last_error());
+            d->a = a;
+            d->send_count.assign(p->send_count, p->send_count + p->nparts);
+            d->recv_count.assign(p->recv_count, p->recv_count + p->nparts);
+            d->send_off.assign(p->nparts, 0);
+            d->recv_off.assign(p->nparts, 0);
+            for (int q = 1; q < p->nparts; ++q) {
+                d->send_off[q] = d->send_off[q - 1] + d->send_count[q - 1];
+                d->recv_off[q] = d->recv_off[q - 1] + d->recv_count[q - 1];
+            }
+            d->nsend = p->nparts > 0 ? d->send_off[p->nparts - 1] + d->send_count[p->nparts - 1] : 0;
+            d->send_idx = static_cast<int32_t*>(dev_alloc_bytes(sizeof(int32_t) * std::max(d->nsend, 1)));
+            if (d->nsend)
+                RCG_CK(cudaMemcpy(d->send_idx, p->send_idx, sizeof(int32_t) * d->nsend, cudaMemcpyHostToDevice));
+            d->sendbuf = dev_alloc(std::max(d->nsend, 1));
+            d->xe = dev_alloc(static_cast<int64_t>(d->nloc) + d->nhalo);
+            d->pe = dev_alloc(static_cast<int64_t>(d->nloc) + d->nhalo);
+            d->dsum = dev_alloc(4);
+            RCG_CK(cudaMemset(d->xe, 0, sizeof(double) * (static_cast<int64_t>(d->nloc) + d->nhalo)));
+            RCG_CK(cudaMemset(d->pe, 0, sizeof(double) * (static_cast<int64_t>(d->nloc) + d->nhalo)));
+            RCG_CK(cudaMemset(d->dsum, 0, sizeof(double) * 4));
+        } catch (...) {
+            rcg_dslab_destroy(d);
+            throw;
+        }
+        *out = d;
+    });
+}
+
+void rcg_dslab_destroy(rcg_dslab* d) {
+    if (!d) return;
+    if (d->ctx) cudaStreamSynchronize(d->ctx->stream);
+    rcg_matrix_destroy(d->a);
+    for (void* p : {(void*)d->send_idx, (void*)d->sendbuf, (void*)d->xe, (void*)d->pe, (void*)d->dsum}) dev_free(p);
+    delete d;
+}
+
+int rcg_comm_nccl_unique_id(void* id128) {
+    return guard([&] {
+        require(id128 != nullptr, "rcg_comm_nccl_unique_id: null argument");
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+        Nccl& nc = Nccl::get();
+        ncclUniqueId id;
+        nc.check(nc.get_unique_id(&id), "get unique id");
+        std::memcpy(id128, &id, sizeof(id));
+    });
+}
+
+int rcg_comm_create_nccl(const void* id128, int nranks, int rank, rcg_comm** out) {
+    return guard([&] {
+        require(id128 && out && nranks >= 1 && rank >= 0 && rank < nranks, "rcg_comm_create_nccl: bad argument");
+        *out = nullptr;
+        Nccl& nc = Nccl::get();
+        auto* c = new NcclComm();
+        c->nranks = nranks;
+        c->rank = rank;
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        try {
+            nc.check(nc.comm_init_rank(&c->comm, nranks, id, rank), "comm init");
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int rcg_comm_create_loopback(int nparts, rcg_comm** out) {
+    return guard([&] {
+        require(out && nparts >= 1, "rcg_comm_create_loopback: bad argument");
+        *out = nullptr;
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            throw Error(RCG_E_CUDA, "no CUDA device available: librcg_b200 has no CPU fallback");
+        }
+        auto* c = new LoopComm();
+        c->np = nparts;
+        RCG_CK(cudaGetDevice(&c->dev));
+        RCG_CK(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+        RCG_CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        c->ev.resize(nparts);
+        for (auto& e : c->ev) RCG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->dptrs = static_cast<double**>(dev_alloc_bytes(sizeof(double*) * nparts));
+        *out = c;
+    });
+}
+
+void rcg_comm_destroy(rcg_comm* c) { delete c; }
+
+int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* b,
+                       double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
+    return guard([&] {
+        require(comm && slabs && b && x && report, "dist_pcg_solve: null argument");
+        require(nslabs == comm->local_slabs(), "dist_pcg_solve: slab count does not match the transport");
+        check_cfg(cfg);
+        for (int s = 0; s < nslabs; ++s) {
+            require(slabs[s] && b[s] && x[s], "dist_pcg_solve: null slab / vector");
+            require(slabs[s]->nparts == comm->nparts(), "dist_pcg_solve: slab partition does not match the transport");
+            if (nslabs > 1) require(slabs[s]->part == s, "dist_pcg_solve: loopback slabs must be given in part order");
+        }
+        DistSolve ds{comm, nslabs, slabs, cfg->max_iter, cfg->eps};
+        ds.setup(b, x);
+        ds.initial();
+        const double wall = ds.run();
+        const DevState h = ds.finish(x);
+        report->iterations = h.done == kZeroRhs ? 0 : h.iters;
+        report->converged = (h.done == kConverged || h.done == kZeroRhs) ? 1 : 0;
+        report->wall_time = wall;
+        const int cnt = std::min(report->iterations, report->cap);
+        if (cnt > 0) {
+            rcg_ctx* c0 = slabs[0]->ctx;
+            if (report->history)
+                RCG_CK(cudaMemcpy(report->history, c0->ws.hist, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+            if (report->alphas)
+                RCG_CK(cudaMemcpy(report->alphas, c0->ws.alph, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+            if (report->betas)
+                RCG_CK(cudaMemcpy(report->betas, c0->ws.bet, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+        }
+        if (h.done == kBroken)
+            throw Error(RCG_E_BREAKDOWN, h.status == kBrkRz ? "pcg: preconditioner not SPD ((r, z) <= 0)"
+                                                            : "pcg: matrix not SPD ((p, A p) <= 0)");
+    });
+}
+
+}  // extern "C"

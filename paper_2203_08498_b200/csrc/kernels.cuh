@@ -40,6 +40,15 @@ struct SweepArgs {
 
 int spmv_grid(const rcg_ctx* ctx, int32_t n);
 int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos);
+
+#ifdef __CUDACC__
+// solver.cu kernels reused by the multi-GPU slabs (dist.cu)
+__global__ void __launch_bounds__(kStreamThreads) k_pupdate(const double* __restrict__ z, double* __restrict__ p,
+                                                            double* __restrict__ zs_reset, double* __restrict__ y_reset,
+                                                            int32_t n, DevState* st, const double* __restrict__ W,
+                                                            int64_t ldw, int k, const double* __restrict__ u);
+__global__ void k_zero_if(double* x, int32_t n, const DevState* st);
+#endif
 int stream_grid(const rcg_ctx* ctx, int64_t n);
 size_t spmv_smem(const rcg_matrix* a);
 void spmv_prepare_kernels();

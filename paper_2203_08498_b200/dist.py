@@ -1,0 +1,87 @@
+"""Multi-GPU row slabs above the C-ABI: one process per GPU over NCCL, or all
+slabs in one process (loopback transport, for tests on one GPU).
+
+The operator is the reference's block-Jacobi IC(0) -- ic0_factorize(a, s, G) with block bounds
+floor(b n / G) (ic_preconditioner.cpp:97-121): slab b factorises its own diagonal block.  The
+reference's shift ladder is global (a failing block restarts EVERY block with the next shift),
+so the slabs agree on the largest shift any block needed and refactorise at it (the ladder's
+first shift at which all blocks succeed, success being monotone in the shift).
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import api
+
+
+def bounds(n: int, nparts: int) -> np.ndarray:
+    """Slab row bounds floor(b n / G), b = 0..G (ic_preconditioner.cpp:104-106)."""
+    return (np.arange(nparts + 1, dtype=np.int64) * n) // nparts
+
+
+def block_factor(ctx: api.Context, plan: api.SlabPlan, shift: float = 0.0) -> api.IcFactor:
+    rs, ci, va = plan.diagonal_block()
+    return api.IcFactor.factorize(ctx, plan.nloc, rs, ci, va, shift, 1)
+
+
+def agree_factors(ctxs, plans, allreduce_max: Callable[[float], float]):
+    """Block factors of the local slabs with the reference's global shift ladder: each block runs
+    the ladder, the ranks take the largest shift (allreduce_max), and blocks that stopped lower
+    are refactorised at it."""
+    fs = [block_factor(c, p) for c, p in zip(ctxs, plans)]
+    s = allreduce_max(max(f.shift_used for f in fs))
+    return [f if f.shift_used == s else block_factor(c, p, s) for f, c, p in zip(fs, ctxs, plans)]
+
+
+class LoopbackSystem:
+    """All G slabs of a matrix in this process on one GPU (one context / stream per slab)."""
+
+    def __init__(self, host, nparts: int, preconditioner: str = "ic", device: int = 0):
+        self.n, self.nparts = host.n, nparts
+        self.ctxs = [api.Context(device) for _ in range(nparts)]
+        self.plans = [api.SlabPlan(host.n, host.row_start, host.col_idx, host.values, nparts, b) for b in range(nparts)]
+        self.factors = agree_factors(self.ctxs, self.plans, lambda v: v) if preconditioner == "ic" else [None] * nparts
+        self.slabs = [api.DSlab(c, p, f) for c, p, f in zip(self.ctxs, self.plans, self.factors)]
+        self.comm = api.Comm.loopback(nparts)
+
+    def solve(self, b: np.ndarray, x: np.ndarray, eps: float = 1e-8, max_iter: int = 1000) -> api.SolveReport:
+        """Global b, x (x updated in place) split along the slab bounds."""
+        bs = [np.ascontiguousarray(b[p.row_begin:p.row_end]) for p in self.plans]
+        xs = [np.ascontiguousarray(x[p.row_begin:p.row_end]) for p in self.plans]
+        rep = api.dist_pcg_solve(self.comm, self.slabs, bs, xs, eps, max_iter)
+        for p, xl in zip(self.plans, xs):
+            x[p.row_begin:p.row_end] = xl
+        return rep
+
+
+class NcclRank:
+    """This process's slab of a G-GPU solve (rank = slab index), plumbing over torch.distributed
+    (NCCL backend): rank 0 creates the NCCL id, every rank builds its own plan / factor / slab."""
+
+    def __init__(self, host, ctx: Optional[api.Context] = None, preconditioner: str = "ic"):
+        import torch
+        import torch.distributed as dist
+
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.ctx = ctx or api.Context(torch.cuda.current_device())
+        self.plan = api.SlabPlan(host.n, host.row_start, host.col_idx, host.values, self.world, self.rank)
+
+        def allreduce_max(v: float) -> float:
+            t = torch.tensor([v], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        self.factor = agree_factors([self.ctx], [self.plan], allreduce_max)[0] if preconditioner == "ic" else None
+        self.slab = api.DSlab(self.ctx, self.plan, self.factor)
+        obj = [api.Comm.unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        self.comm = api.Comm.nccl(obj[0], self.world, self.rank)
+
+    def solve(self, b_local, x_local, eps: float = 1e-8, max_iter: int = 1000) -> api.SolveReport:
+        return api.dist_pcg_solve(self.comm, [self.slab], [b_local], [x_local], eps, max_iter)
+
+
+def scatter(v: np.ndarray, plans: Sequence[api.SlabPlan]):
+    return [np.ascontiguousarray(v[p.row_begin:p.row_end]) for p in plans]

@@ -1,0 +1,116 @@
+"""Multi-GPU row slabs on the device (rcg_dist_pcg_solve).  Only one GPU is available, so the
+distributed iteration runs with the loopback transport (all G slabs in one process, each on its
+own stream; exchanges are stream-ordered device copies, reductions a fixed-order sum -- no slab
+waits on another inside a kernel), and the NCCL transport at world size 1.  The bar is the
+oracle's single-process block-Jacobi PCG (ic0_factorize(a, 0, G), pinned to the reference):
+iterations +-2, solution within max(1e-8, 10 x the oracle's own reduction-order response).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import Matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _scaled(oracle, problems, name):
+    h = problems.generate(problems.SMALL[name])
+    sa, _ = oracle.diagonal_scale(Matrix.of(h))
+    return sa, problems.HostCsr(h.n, sa.rs, sa.ci, sa.va)
+
+
+def _oracle_block_jacobi(oracle, sa, b, nparts, kind=1, eps=1e-8, max_iter=5000):
+    f = oracle.ic0_factorize(sa, 0.0, nparts) if kind == 1 else None
+    xo = np.zeros(sa.n)
+    ro = oracle.pcg_solve(sa, b, xo, kind=kind, ic=f, eps=eps, max_iter=max_iter)
+    with oracle.reversed_dots(1):
+        x2 = np.zeros(sa.n)
+        oracle.pcg_solve(sa, b, x2, kind=kind, ic=f, eps=eps, max_iter=max_iter)
+    return ro, xo, max(1e-8, 10 * _rel(x2, xo))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("nparts", [1, 2, 3, 4])
+def test_loopback_matches_block_jacobi_pcg(oracle, problems, name, nparts):
+    from paper_2203_08498_b200 import dist
+
+    sa, host = _scaled(oracle, problems, name)
+    b = oracle.uniform_pm1(5, 0, sa.n)
+    system = dist.LoopbackSystem(host, nparts)
+    x = np.zeros(sa.n)
+    rep = system.solve(b, x, 1e-8, 5000)
+    ro, xo, tol = _oracle_block_jacobi(oracle, sa, b, nparts)
+    assert rep.converged and ro.converged
+    assert abs(rep.iterations - ro.iterations) <= 2, (rep.iterations, ro.iterations)
+    if rep.iterations == ro.iterations:
+        assert _rel(x, xo) <= tol, (_rel(x, xo), tol)
+    assert len(rep.history) == rep.iterations and rep.history[-1] <= 1e-8
+
+
+def test_loopback_identity_preconditioner(oracle, problems):
+    from paper_2203_08498_b200 import dist
+
+    sa, host = _scaled(oracle, problems, "c1")
+    b = oracle.uniform_pm1(9, 0, sa.n)
+    system = dist.LoopbackSystem(host, 3, preconditioner="identity")
+    x = np.zeros(sa.n)
+    rep = system.solve(b, x, 1e-8, 5000)
+    ro, xo, tol = _oracle_block_jacobi(oracle, sa, b, 3, kind=0)
+    assert rep.converged and abs(rep.iterations - ro.iterations) <= 2
+    if rep.iterations == ro.iterations:
+        assert _rel(x, xo) <= tol
+
+
+def test_loopback_zero_rhs_and_cap(oracle, problems):
+    from paper_2203_08498_b200 import dist
+
+    sa, host = _scaled(oracle, problems, "c1")
+    system = dist.LoopbackSystem(host, 2)
+    x = np.ones(sa.n)
+    rep = system.solve(np.zeros(sa.n), x)
+    assert rep.converged and rep.iterations == 0 and not x.any()
+    x = np.zeros(sa.n)
+    rep = system.solve(oracle.uniform_pm1(3, 0, sa.n), x, 1e-10, 7)
+    assert not rep.converged and rep.iterations == 7 and len(rep.history) == 7
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_nccl_transport_world_one_equals_loopback(oracle, problems):
+    """The NCCL transport (one slab per process) at world size 1: bitwise the loopback G = 1."""
+    import torch
+    import torch.distributed as dist_
+
+    from paper_2203_08498_b200 import dist
+
+    sa, host = _scaled(oracle, problems, "c2")
+    b = oracle.uniform_pm1(21, 0, sa.n)
+    lb = dist.LoopbackSystem(host, 1)
+    x1 = np.zeros(sa.n)
+    r1 = lb.solve(b, x1)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist_.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rank = dist.NcclRank(host)
+        x2 = np.zeros(sa.n)
+        r2 = rank.solve(b, x2)
+    finally:
+        dist_.destroy_process_group()
+    assert r2.iterations == r1.iterations
+    assert np.array_equal(r2.history, r1.history)
+    assert np.array_equal(x2, x1)
