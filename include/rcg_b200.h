@@ -85,6 +85,10 @@ int rcg_diagonal_scale(rcg_ctx* ctx, const rcg_matrix* a, rcg_matrix** scaled, d
  * uploaded with its level schedules. */
 int rcg_ic0_factorize(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const int32_t* col_idx,
                       const double* values, double shift, int num_blocks, rcg_ic** out);
+/* ic0_factorize on the device: pattern work (L / U patterns, level schedules)
+ * on the host from a's pattern, the numeric row merge + shift ladder by a level-ordered
+ * sync-free kernel from a's device values; the factor is bitwise rcg_ic0_factorize's. */
+int rcg_ic0_factorize_device(rcg_ctx* ctx, const rcg_matrix* a, double shift, int num_blocks, rcg_ic** out);
 /* upload an existing IcFactor (ic_preconditioner.hpp:18-37) so the operator is identical */
 int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_bounds,
                   const int32_t* l_row_start, const int32_t* l_col, const double* l_val,

@@ -193,6 +193,17 @@ class IcFactor:
         return f
 
     @classmethod
+    def factorize_device(cls, ctx: Context, a: "CsrMatrix", shift: float = 0.0, num_blocks: int = 1):
+        """ic0_factorize with the numeric row merge on the GPU (rcg_ic0_factorize_device) from the
+        device matrix's values; bitwise the host factorisation."""
+        h = C.c_void_p()
+        check(lib.rcg_ic0_factorize_device(ctx.h, a.h, float(shift), int(num_blocks), C.byref(h)))
+        f = cls(ctx, h)
+        f.n = int(a.n)
+        f.num_blocks = int(num_blocks)
+        return f
+
+    @classmethod
     def from_arrays(cls, ctx: Context, n, block_bounds, l_row_start, l_col, l_val, d, u_row_start, u_col, u_val,
                     shift_used=0.0):
         arrs = [np.ascontiguousarray(block_bounds, dtype=np.int32), np.ascontiguousarray(l_row_start, dtype=np.int32),

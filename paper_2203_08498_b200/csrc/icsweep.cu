@@ -272,10 +272,12 @@ static T* upload(rcg_ctx* ctx, const std::vector<T>& h) {
 }
 
 // Level-sorted copy of a row-wise triangular factor.  `descending` walks rows n-1..0 (U).
-static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vector<int32_t>& col,
+// `val` may be empty: then pval stays empty and only pidx (the source entry of every schedule
+// entry) is produced, for a device-side gather of values computed on the GPU.
+int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vector<int32_t>& col,
                               const std::vector<double>& val, bool descending, std::vector<int32_t>& perm,
                               std::vector<int32_t>& prs, std::vector<int32_t>& pcol, std::vector<double>& pval,
-                              std::vector<uint8_t>& crit, int32_t& npos) {
+                              std::vector<uint8_t>& crit, int32_t& npos, std::vector<int32_t>* pidx = nullptr) {
     std::vector<int32_t> level(n, 0);
     int32_t nlev = 0;
     for (int32_t t = 0; t < n; ++t) {
@@ -305,12 +307,15 @@ static int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const s
     }
     pcol.resize(col.size());
     pval.resize(val.size());
+    if (pidx) pidx->resize(col.size());
     crit.assign(total, 0);
     for (int64_t pos = 0; pos < total; ++pos) {
         const int32_t i = perm[pos];
         if (i < 0) continue;
         std::copy(col.begin() + rs[i], col.begin() + rs[i + 1], pcol.begin() + prs[pos]);
-        std::copy(val.begin() + rs[i], val.begin() + rs[i + 1], pval.begin() + prs[pos]);
+        if (!val.empty()) std::copy(val.begin() + rs[i], val.begin() + rs[i + 1], pval.begin() + prs[pos]);
+        if (pidx)
+            for (int32_t p = rs[i]; p < rs[i + 1]; ++p) (*pidx)[prs[pos] + (p - rs[i])] = p;
         int32_t best = -1;
         for (int32_t p = rs[i]; p < rs[i + 1]; ++p)
             if (p - rs[i] < 255 && level[col[p]] >= best) {
