@@ -15,6 +15,7 @@
 // dot products are deterministic tree reductions (run to run identical).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -55,6 +56,8 @@ struct BatchWs {
     double* gpart = nullptr;
     unsigned int* gcount = nullptr;
     int64_t cap_groups = 0;
+    double* tpart = nullptr;  // chunk-lane sweep tile partials
+    int64_t cap_tpart = 0;
     int* tickets = nullptr;
 };
 
@@ -62,7 +65,7 @@ static void free_ws(BatchWs*& w) {
     if (!w) return;
     for (void* p : {(void*)w->b, (void*)w->x, (void*)w->r, (void*)w->zs, (void*)w->p, (void*)w->q, (void*)w->y,
                     (void*)w->st, (void*)w->hist, (void*)w->u, (void*)w->u2, (void*)w->partials, (void*)w->gpart,
-                    (void*)w->gcount, (void*)w->tickets})
+                    (void*)w->gcount, (void*)w->tpart, (void*)w->tickets})
         dev_free(p);
     delete w;
     w = nullptr;
@@ -107,6 +110,11 @@ static BatchWs& batch_ws(BatchWs*& slot, int64_t nrt, int64_t hist, int64_t m_rt
         dev_free(w.partials);
         w.partials = dev_alloc(part);
         w.cap_part = part;
+    }
+    if (part > w.cap_tpart) {
+        dev_free(w.tpart);
+        w.tpart = dev_alloc(part);
+        w.cap_tpart = part;
     }
     if (groups > w.cap_groups) {
         dev_free(w.gpart);
@@ -597,6 +605,171 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
     }
 }
 
+// Chunk-lane sweep: right-hand sides are independent, so chunk c (values 2c, 2c+1) of a row
+// depends only on chunk c of its parents.  A warp covers RPW = 32/G rows x G = RT/2 chunks, each
+// lane sweeping its own 16-byte chunk exactly like the single-pair (RT = 2) sweep: per-lane work
+// and polling stay those of RT = 2 whatever RT is, the row's values are published chunk by chunk
+// with no coordination between lanes, and a level costs about what it costs at RT = 2.
+template <bool BWD, int RT, int VW, int CH>
+__global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
+    constexpr int G = RT / VW;
+    constexpr int RPW = 32 / G;
+    if (st->nrun == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int rl = lane / G, c = lane % G;
+    const bool lane_on = rl < RPW;
+    const int ntiles = (a.npos + RPW - 1) / RPW;
+    while (true) {
+        int tile = 0;
+        if (lane == 0) tile = atomicAdd(&a.tickets[0], 1);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile >= ntiles) break;
+        const int pos = tile * RPW + rl;
+        double contrib[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) contrib[v] = 0.0;
+        const int32_t row = (lane_on && pos < a.npos) ? __ldg(a.perm + pos) : -1;
+        if (row >= 0) {
+            const int64_t me = static_cast<int64_t>(row) * RT + VW * c;
+            const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
+            double s[VW];
+            {
+                const double dr = BWD ? __ldg(a.d + row) : 1.0;
+#pragma unroll
+                for (int v = 0; v < VW / 2; ++v) {
+                    const double2 t = reinterpret_cast<const double2*>(a.in + me)[v];
+                    s[2 * v] = BWD ? __ddiv_rn(t.x, dr) : t.x;
+                    s[2 * v + 1] = BWD ? __ddiv_rn(t.y, dr) : t.y;
+                }
+            }
+            unsigned spins = 0;
+            for (int32_t e0 = beg;; e0 += CH) {
+                const int cnt = min(CH, end - e0);
+                const bool last = e0 + CH >= end;
+                int32_t col[CH];
+                double val[CH];
+                double dep[CH][VW];
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    if (j < cnt) {
+                        col[j] = __ldg(a.pcol + e0 + j);
+                        val[j] = __ldg(a.pval + e0 + j);
+                    }
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    if (j < cnt) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + VW * c, dep[j]);
+                while (true) {
+                    bool any = false;
+#pragma unroll
+                    for (int j = 0; j < CH; ++j)
+                        if (j < cnt)
+#pragma unroll
+                            for (int v = 0; v < VW; ++v) any |= is_sentinel(dep[j][v]);
+                    if (!any) {
+#pragma unroll
+                        for (int j = 0; j < CH; ++j)
+                            if (j < cnt)
+#pragma unroll
+                                for (int v = 0; v < VW; ++v) s[v] = fsub_mul(s[v], val[j], dep[j][v]);
+                        if (last) {
+                            double t[VW];
+#pragma unroll
+                            for (int v = 0; v < VW; ++v) t[v] = publishable(s[v]);
+                            RelVec<VW>::st(a.out + me, t);
+                        }
+                        break;
+                    }
+                    if (a.backoff_ns) __nanosleep(a.backoff_ns);
+#pragma unroll
+                    for (int j = 0; j < CH; ++j)
+                        if (j < cnt) {
+                            bool m = false;
+#pragma unroll
+                            for (int v = 0; v < VW; ++v) m |= is_sentinel(dep[j][v]);
+                            if (m) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + VW * c, dep[j]);
+                        }
+                    if (++spins == (1u << 24)) {
+                        atomicExch(&a.tickets[3], 1);
+#pragma unroll
+                        for (int j = 0; j < CH; ++j)
+#pragma unroll
+                            for (int v = 0; v < VW; ++v)
+                                if (is_sentinel(dep[j][v])) dep[j][v] = 0.0;
+                    }
+                }
+                if (last) break;
+            }
+            if (BWD && a.r) {
+#pragma unroll
+                for (int v = 0; v < VW / 2; ++v) {
+                    const double2 t = reinterpret_cast<const double2*>(a.r + me)[v];
+                    contrib[2 * v] = __dmul_rn(t.x, s[2 * v]);
+                    contrib[2 * v + 1] = __dmul_rn(t.y, s[2 * v + 1]);
+                }
+            }
+        }
+        if (BWD && a.r) {
+            // per-tile partials: chunk c's RPW rows sit on lanes c, c+G, ..., summed in row order
+            // (RPW-1 strided shuffles per value); k_b_rho sums the tiles in a fixed order
+            double tot[VW];
+#pragma unroll
+            for (int v = 0; v < VW; ++v) tot[v] = contrib[v];
+#pragma unroll
+            for (int r = 1; r < RPW; ++r)
+#pragma unroll
+                for (int v = 0; v < VW; ++v) tot[v] = __dadd_rn(tot[v], __shfl_sync(0xffffffffu, contrib[v], c + r * G));
+            if (lane < G)
+#pragma unroll
+                for (int v = 0; v < VW; ++v) a.partials[static_cast<int64_t>(tile) * RT + lane * VW + v] = tot[v];
+        }
+    }
+    if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x * (blockDim.x / 32)) - 1) {
+            a.tickets[0] = 0;
+            a.tickets[1] = 0;
+        }
+    }
+}
+
+// (r, z) per rhs from the chunk-lane sweep's tile partials (tile-major, RT per tile): thread
+// sums in a fixed stride (kElemThreads is a multiple of RT: fixed rhs per thread), block and grid
+// reductions in a fixed order; finaliser as the sweep's: SC term, breakdown test, beta.
+template <int RT>
+__global__ void __launch_bounds__(kElemThreads) k_b_rho(const double* __restrict__ tpart, int64_t ntiles,
+                                                       double* partials, BState* st, int add_sc) {
+    __shared__ double sred[kElemThreads];
+    __shared__ double vals[RT];
+    __shared__ double tot[RT];
+    if (st->nrun == 0) return;
+    double acc = 0.0;
+    const int64_t total = ntiles * RT;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(kElemThreads) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * kElemThreads)
+        acc = __dadd_rn(acc, tpart[e]);
+    sred[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < RT) {
+        double v = 0.0;
+        for (int t = threadIdx.x; t < kElemThreads; t += RT) v = __dadd_rn(v, sred[t]);
+        vals[threadIdx.x] = v;
+    }
+    __syncthreads();
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[5], tot) && threadIdx.x < RT) {
+        const int k = threadIdx.x;
+        double rho = tot[k];
+        if (st->done[k] == kRunning) {
+            if (add_sc) rho = __dadd_rn(rho, st->scal2[k]);
+            st->rho[k] = rho;
+            if (rho <= 0.0) {
+                st->done[k] = kBroken;
+                st->status[k] = kBrkRz;
+            }
+            st->beta[k] = st->iter > 1 ? rho / st->rho_prev[k] : 0.0;
+        }
+    }
+}
+
 // p = z (+ W u) (+ beta p) for running rhs; sweep buffers back to the sentinel.  G = RT/VW
 // threads per row, each on one VW-value chunk: a warp's accesses are contiguous and each W_j[i]
 // load serves VW values.  Per value the arithmetic of the single-rhs k_pupdate.
@@ -1082,7 +1255,7 @@ struct BatchSolve {
         require(mm * RT <= kMaxRedB, "batch: basis columns x right-hand sides exceed the reduction capacity");
         require(mm <= 128, "batch: at most 128 basis columns");
         const int64_t nrt = static_cast<int64_t>(n) * RT;
-        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 31) / 32 : 1;
+        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 3) / 4 : 1;  // >= RPW 4
         const int64_t groups = (ntiles + kGroup - 1) / kGroup;
         const int64_t part = std::max<int64_t>(ntiles * RT, static_cast<int64_t>(kMaxRedB) * ctx->num_sms * 8);
         w = &batch_ws(slot, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
@@ -1249,15 +1422,41 @@ struct BatchSolve {
 
     void launch_b_sweep(bool backward, SweepArgs& s) {
         const rcg_ic* f = m->ic;
-        const int ntiles = (s.npos + 127) / 128;  // in CTAs of 4 warp tiles
-        const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, s.npos);
-        const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
+        // RCG_BSWEEP=0 selects the row-lane sweep (A/B only); default: chunk lanes
+        static const int mode = std::getenv("RCG_BSWEEP") ? std::atoi(std::getenv("RCG_BSWEEP")) : 1;
+        const int bps0 = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, s.npos);
         s.backoff_ns = ctx->sweep_backoff_ns;
         KTimer t(ctx, backward ? 7 : 6, RT);
-        if (backward)
-            k_b_sweep<true, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
-        else
-            k_b_sweep<false, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+        if (mode != 0) {
+            // chunk lanes: 16-byte chunks (measured faster than 32-byte), 4 parents per poll
+            // chunk (register budget -> residency); 3x the single-sweep CTAs from RT = 12 on
+            constexpr int rpw = 32 / (RT / 2);
+            const int cmul = RT >= 12 ? 3 : 2;
+            const int ntiles = (s.npos + rpw * 4 - 1) / (rpw * 4);  // CTAs of 4 warp tiles
+            const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps0 * cmul));
+            const bool rho = backward && s.r;
+            if (rho) s.partials = w->tpart;
+            if (backward)
+                k_b_sweepc<true, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+            else
+                k_b_sweepc<false, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+            RCG_LAUNCHED(ctx);
+            if (rho) {
+                const int64_t tiles = (s.npos + rpw - 1) / rpw;
+                const int g = static_cast<int>(std::max<int64_t>(
+                    1, std::min<int64_t>((tiles * RT + kElemThreads * 4 - 1) / (kElemThreads * 4), ctx->num_sms * 8)));
+                k_b_rho<RT><<<g, kElemThreads, 0, ctx->stream>>>(w->tpart, tiles, w->partials, w->st, s.add_sc);
+                RCG_LAUNCHED(ctx);
+            }
+            return;
+        } else {
+            const int ntiles = (s.npos + 127) / 128;  // in CTAs of 4 warp tiles
+            const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps0));
+            if (backward)
+                k_b_sweep<true, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+            else
+                k_b_sweep<false, RT><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+        }
         RCG_LAUNCHED(ctx);
     }
 

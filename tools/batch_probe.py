@@ -25,7 +25,7 @@ def main():
                 reps = [api.pcg_solve(ctx, p.a, B[0], api.Ic(p.ic), X[0], cfg.eps, 60)]
             else:
                 reps = api.pcg_solve_batch(ctx, p.a, B, api.Ic(p.ic), X, cfg.eps, 60)
-        stats = {c: ctx.kernel_stats(c) for c in range(5)}
+        stats = {c % 5: ctx.kernel_stats(c) for c in (range(5) if R == 1 else range(5, 10))}
         ctx.set_profiling(False)
         its = max(r.iterations for r in reps)
         print(json.dumps({"R": R, "iters": its, "ms_per_iter": round(reps[0].wall_time / its * 1e3, 3),
