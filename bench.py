@@ -223,8 +223,8 @@ def run_ours(args, rank, world, local_rank):
 # Kernel classes (rcg_b200.h rcg_ctx_kernel_stats): 0-4 single right-hand side, 5-9 batched.
 CLASS_NAMES = {0: "spmv (k_spmv_pq)", 1: "ic fwd sweep (k_sweep<false>)", 2: "ic bwd sweep (k_sweep<true>)",
                3: "vector ops", 4: "W^T r (k_tallt)",
-               5: "batched spmv (k_b_spmv_pq)", 6: "batched ic fwd sweep (k_b_sweep<false>)",
-               7: "batched ic bwd sweep (k_b_sweep<true>)", 8: "batched vector ops", 9: "batched W^T r (k_b_tallt)"}
+               5: "batched spmv (k_b_spmv_pq)", 6: "batched ic fwd sweep (k_b_sweepc<false>)",
+               7: "batched ic bwd sweep (k_b_sweepc<true> + k_b_rho)", 8: "batched vector ops", 9: "batched W^T r (k_b_tallt)"}
 
 
 def kernel_stats(ctxs):

@@ -10,8 +10,8 @@ import sys
 from collections import defaultdict
 
 CLASSES = [  # (regex on the demangled name, bench.py class)
-    (r"k_b_sweep<0", "batched ic fwd sweep (k_b_sweep<false>)"),
-    (r"k_b_sweep<1", "batched ic bwd sweep (k_b_sweep<true>)"),
+    (r"k_b_sweepc?<0", "batched ic fwd sweep (k_b_sweepc<false>)"),
+    (r"k_b_sweepc?<1|k_b_rho", "batched ic bwd sweep (k_b_sweepc<true> + k_b_rho)"),
     (r"k_b_spmv_pq|k_b_residual", "batched spmv (k_b_spmv_pq)"),
     (r"k_b_tallt", "batched W^T r (k_b_tallt)"),
     (r"k_b_", "batched vector ops"),
