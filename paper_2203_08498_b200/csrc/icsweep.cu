@@ -178,7 +178,6 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
     a.prs = backward ? f->b_prs : f->f_prs;
     a.pcol = backward ? f->b_col : f->f_col;
     a.pval = backward ? f->b_val : f->f_val;
-    a.pcrit = backward ? f->b_crit : f->f_crit;
     a.d = f->d;
     a.n = f->n;
     a.npos = backward ? f->b_npos : f->f_npos;
@@ -277,7 +276,7 @@ static T* upload(rcg_ctx* ctx, const std::vector<T>& h) {
 int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vector<int32_t>& col,
                               const std::vector<double>& val, bool descending, std::vector<int32_t>& perm,
                               std::vector<int32_t>& prs, std::vector<int32_t>& pcol, std::vector<double>& pval,
-                              std::vector<uint8_t>& crit, int32_t& npos, std::vector<int32_t>* pidx = nullptr) {
+                              int32_t& npos, std::vector<int32_t>* pidx = nullptr) {
     std::vector<int32_t> level(n, 0);
     int32_t nlev = 0;
     for (int32_t t = 0; t < n; ++t) {
@@ -308,7 +307,6 @@ int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vec
     pcol.resize(col.size());
     pval.resize(val.size());
     if (pidx) pidx->resize(col.size());
-    crit.assign(total, 0);
     for (int64_t pos = 0; pos < total; ++pos) {
         const int32_t i = perm[pos];
         if (i < 0) continue;
@@ -316,12 +314,6 @@ int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vec
         if (!val.empty()) std::copy(val.begin() + rs[i], val.begin() + rs[i + 1], pval.begin() + prs[pos]);
         if (pidx)
             for (int32_t p = rs[i]; p < rs[i + 1]; ++p) (*pidx)[prs[pos] + (p - rs[i])] = p;
-        int32_t best = -1;
-        for (int32_t p = rs[i]; p < rs[i + 1]; ++p)
-            if (p - rs[i] < 255 && level[col[p]] >= best) {
-                best = level[col[p]];
-                crit[pos] = static_cast<uint8_t>(p - rs[i]);
-            }
     }
     return nlev;
 }
@@ -329,22 +321,17 @@ int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vec
 static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
     std::vector<int32_t> perm, prs, pcol;
     std::vector<double> pval;
-    std::vector<uint8_t> crit;
-    f->fwd_levels =
-        build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval, crit, f->f_npos);
+    f->fwd_levels = build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval, f->f_npos);
     f->f_perm = upload(ctx, perm);
     f->f_prs = upload(ctx, prs);
     f->f_col = upload(ctx, pcol);
     f->f_val = upload(ctx, pval);
-    f->f_crit = upload(ctx, crit);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    f->bwd_levels =
-        build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval, crit, f->b_npos);
+    f->bwd_levels = build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval, f->b_npos);
     f->b_perm = upload(ctx, perm);
     f->b_prs = upload(ctx, prs);
     f->b_col = upload(ctx, pcol);
     f->b_val = upload(ctx, pval);
-    f->b_crit = upload(ctx, crit);
     f->d = upload(ctx, f->h_d);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
 }
@@ -507,8 +494,7 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
-                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->f_crit,
-                    (void*)f->b_crit})
+                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d})
         dev_free(p);
     delete f;
 }
@@ -525,6 +511,7 @@ int rcg_ic_info(const rcg_ic* f, int64_t* nnz_l, double* shift_used, int32_t* fw
 int rcg_ic_export(const rcg_ic* f, int32_t* block_bounds, int32_t* l_row_start, int32_t* l_col,
                   double* l_val, double* d, int32_t* u_row_start, int32_t* u_col, double* u_val) {
     return guard([&] {
+        ensure_host_image(f);
         auto cp = [](auto* dst, const auto& v) {
             if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(v[0]) * v.size());
         };

@@ -186,13 +186,13 @@ struct rcg_ic {
     int32_t n = 0;
     int64_t nnz_l = 0;
     double shift = 0.0;
+    bool host_image = true;  // h_* below filled (device-built factors: on demand, ensure_host_image)
     // host image (IcFactor fields)
     std::vector<int32_t> h_bounds, h_lrs, h_lcol, h_urs, h_ucol;
     std::vector<double> h_lval, h_d, h_uval;
     // device schedules
     int32_t fwd_levels = 0, bwd_levels = 0;
     int32_t f_npos = 0, b_npos = 0;   // schedule lengths with each level padded to a warp multiple
-    uint8_t *f_crit = nullptr, *b_crit = nullptr;
     int32_t *f_perm = nullptr, *f_prs = nullptr, *f_col = nullptr;
     double* f_val = nullptr;
     int32_t *b_perm = nullptr, *b_prs = nullptr, *b_col = nullptr;

@@ -21,7 +21,6 @@ struct SweepArgs {
     const int32_t* prs;    // position-indexed row starts
     const int32_t* pcol;   // original column indices, reference entry order
     const double* pval;
-    const uint8_t* pcrit;  // per position: entry index of the highest-level parent (spin target)
     const double* d;       // pivots (backward)
     int32_t n;
     int32_t npos;          // level-padded length of the schedule (multiple of 32 per level)
@@ -40,6 +39,7 @@ struct SweepArgs {
 
 int spmv_grid(const rcg_ctx* ctx, int32_t n);
 int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos);
+void ensure_host_image(const rcg_ic* f);  // icfactor.cu
 
 #ifdef __CUDACC__
 // solver.cu kernels reused by the multi-GPU slabs (dist.cu)

@@ -35,9 +35,8 @@ def prepare(ctx: api.Context, cfg: Config, host: HostCsr, validate: bool = True,
     t0 = time.perf_counter()
     a_orig = api.CsrMatrix(ctx, host.n, host.row_start, host.col_idx, host.values, validate=validate)
     a, dis = api.diagonal_scale(ctx, a_orig)
-    scaled = a.values()
-    ic = api.IcFactor.factorize(ctx, host.n, host.row_start, host.col_idx, scaled, 0.0,
-                                cfg.blocks if blocks is None else blocks)
+    # IC(0) on the device (pattern + numeric; bitwise the reference factor)
+    ic = api.IcFactor.factorize_device(ctx, a, 0.0, cfg.blocks if blocks is None else blocks)
     return Prepared(ctx, cfg, host, a_orig, a, dis, ic, time.perf_counter() - t0, new_of_old)
 
 
