@@ -115,14 +115,18 @@ def run_accelerated(p: Prepared, basis, bs: list, xs: list, concurrency: int = 1
         return [f.result() for f in futs]
 
 
-def run_batched(p: Prepared, basis, bs: list, xs: list) -> list:
+def run_batched(p: Prepared, basis, bs, xs) -> list:
     """Solves 2..k as batched multi-RHS solves (up to 16 right-hand sides per kernel sequence):
-    one pass over A, the IC schedules and W per iteration serves every right-hand side."""
+    one pass over A, the IC schedules and W per iteration serves every right-hand side.  bs / xs:
+    (k, n) arrays or tensors (row slices are passed as they are: no copies) or lists of vectors."""
     cfg = p.cfg
     reps = []
+    two_d = getattr(bs, "ndim", 1) == 2 and getattr(xs, "ndim", 1) == 2
     for c0 in range(0, len(bs), 16):
         chunk_b, chunk_x = bs[c0:c0 + 16], xs[c0:c0 + 16]
-        if isinstance(chunk_b[0], np.ndarray):
+        if two_d:
+            B, X = chunk_b, chunk_x
+        elif isinstance(chunk_b[0], np.ndarray):
             B = np.ascontiguousarray(np.stack(chunk_b))
             X = np.ascontiguousarray(np.stack(chunk_x))
         else:
@@ -136,8 +140,9 @@ def run_batched(p: Prepared, basis, bs: list, xs: list) -> list:
             r = api.pcg_solve_batch(p.ctx, p.a, B, api.Sc(basis, p.ic), X, cfg.eps, cfg.max_iter)
         else:
             r = api.deflated_pcg_solve_batch(p.ctx, p.a, B, api.Ic(p.ic), basis, X, cfg.eps, cfg.max_iter)
-        for x_dst, x_src in zip(chunk_x, X):
-            x_dst[:] = x_src
+        if not two_d:
+            for x_dst, x_src in zip(chunk_x, X):
+                x_dst[:] = x_src
         reps += r
     return reps
 
