@@ -37,6 +37,7 @@ typedef struct rcg_basis rcg_basis;     /* W, AW, chol(W^T A W) (DeflationOperat
 typedef struct rcg_sampler rcg_sampler; /* device snapshot slots (SamplerState) */
 typedef struct rcg_dslab rcg_dslab;     /* one GPU's row slab of a multi-GPU solve */
 typedef struct rcg_comm rcg_comm;       /* slab transport: NCCL (one slab per process) or loopback */
+typedef struct rcg_dbasis rcg_dbasis;   /* row-partitioned W, AW + replicated chol(W^T A W) */
 
 /* message of the last failing call on this thread; "" after success */
 const char* rcg_last_error(void);
@@ -305,6 +306,17 @@ void rcg_comm_destroy(rcg_comm* c);
  * NCCL, = nparts with loopback; b[s], x[s] are slab s's local rows (host or device) */
 int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* b,
                        double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report);
+/* build_deflation_operator / ScPreconditioner state over slabs (deflation.cpp:45-76): w[s] = slab
+ * s's rows of W (column-major nloc x m); AW by halo exchange + local SpMV, the Gram allreduced
+ * and factored identically on every rank.  kind: RCG_BASIS_DEFLATION or RCG_BASIS_SC. */
+int rcg_dbasis_create(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* w, int m, int kind,
+                      rcg_dbasis** out);
+void rcg_dbasis_destroy(rcg_dbasis* b);
+/* distributed deflated PCG (basis kind DEFLATION, pcg.cpp:94-160) or SC-PCG around the block
+ * IC(0) (kind SC, subspace_correction.cpp:27-57); basis null = rcg_dist_pcg_solve.  Per
+ * iteration the m-vector W^T q (or W^T r) is allreduced before the replicated Cholesky solve. */
+int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
+                   double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report);
 
 #ifdef __cplusplus
 }

@@ -177,6 +177,10 @@ SIGNATURES = {
     "rcg_comm_destroy": (None, vp),
     "rcg_dist_pcg_solve": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                            C.POINTER(SolverConfig), C.POINTER(SolveReport)),
+    "rcg_dbasis_create": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_int, C.c_int, C.POINTER(vp)),
+    "rcg_dbasis_destroy": (None, vp),
+    "rcg_dist_solve": (C.c_int, vp, C.c_int, C.POINTER(vp), vp, C.POINTER(vp), C.POINTER(vp),
+                       C.POINTER(SolverConfig), C.POINTER(SolveReport)),
 }
 
 for _name, (_res, *_args) in SIGNATURES.items():

@@ -688,3 +688,44 @@ def dist_pcg_solve(comm: Comm, slabs, bs, xs, eps: float = 1e-8, max_iter: int =
     rep, bufs = _report(max(1, int(max_iter)))
     check(lib.rcg_dist_pcg_solve(comm.h, ns, hs, bp, xp, C.byref(cfg), C.byref(rep)))
     return _finish(rep, bufs)
+
+
+class DBasis:
+    """Row-partitioned W / AW with the replicated chol(W^T A W) (rcg_dbasis_create): the
+    distributed DeflationOperator / ScPreconditioner state.  ws[s]: slab s's rows of W as an
+    (m, nloc) array (one basis vector per row)."""
+
+    def __init__(self, comm: Comm, slabs, ws, kind: str = "deflation"):
+        slabs = list(slabs)
+        ns = len(slabs)
+        self.m = int(ws[0].shape[0])
+        cols = [np.ascontiguousarray(w, dtype=np.float64) for w in ws]  # (m, nloc) row-major = column-major nloc x m
+        self._cols = cols
+        hs = (C.c_void_p * ns)(*[s_.h.value for s_ in slabs])
+        wp = (C.c_void_p * ns)(*[_ptr(c) for c in cols])
+        h = C.c_void_p()
+        check(lib.rcg_dbasis_create(comm.h, ns, hs, wp, self.m, L.RCG_BASIS_SC if kind == "sc" else L.RCG_BASIS_DEFLATION,
+                                    C.byref(h)))
+        self.h, self.kind, self.slabs = h, kind, slabs
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.rcg_dbasis_destroy(self.h)
+            self.h = None
+
+
+def dist_solve(comm: Comm, slabs, bs, xs, basis: Optional[DBasis] = None, eps: float = 1e-8,
+               max_iter: int = 1000) -> SolveReport:
+    """rcg_dist_solve: distributed block-Jacobi PCG, deflated PCG (basis kind 'deflation') or
+    SC-PCG (kind 'sc') over row slabs."""
+    slabs = list(slabs)
+    ns = len(slabs)
+    bs = [_f64(b, s_.plan.nloc, "b") for b, s_ in zip(bs, slabs)]
+    hs = (C.c_void_p * ns)(*[s_.h.value for s_ in slabs])
+    bp = (C.c_void_p * ns)(*[_ptr(b) for b in bs])
+    xp = (C.c_void_p * ns)(*[_ptr(x) for x in xs])
+    cfg = _cfg(eps, max_iter)
+    rep, bufs = _report(max(1, int(max_iter)))
+    check(lib.rcg_dist_solve(comm.h, ns, hs, basis.h if basis is not None else None, bp, xp, C.byref(cfg),
+                             C.byref(rep)))
+    return _finish(rep, bufs)

@@ -22,6 +22,7 @@
 #include "internal.cuh"
 #include "kernels.cuh"
 #include "spmv_pipe.cuh"
+#include "vec.cuh"
 
 namespace rcg {
 
@@ -131,7 +132,20 @@ struct rcg_dslab {
     double* sendbuf = nullptr;    // device
     double* xe = nullptr;         // device x_ext (nloc + nhalo)
     double* pe = nullptr;         // device p_ext (nloc + nhalo)
-    double* dsum = nullptr;       // device: local partials in, global totals out
+    double* dsum = nullptr;       // device: local partials in, global totals out (scalars)
+    double* gbuf = nullptr;       // device: m-vectors / the m x m Gram (allreduced the same way)
+    double* ubuf = nullptr;       // device: projection coefficients (m)
+    double* u2buf = nullptr;      // device: subspace-correction coefficients (m)
+    int64_t cap_g = 0;
+};
+
+// a row-partitioned basis: every slab holds its rows of W and AW, and the
+// replicated Cholesky factor of W^T A W (allreduced Gram, factored identically on every rank)
+struct rcg_dbasis {
+    int kind = 0;  // RCG_BASIS_DEFLATION / RCG_BASIS_SC
+    int m = 0;
+    std::vector<double*> w, aw, l;  // per local slab (W, AW: nloc x m column-major, ld nloc)
+    std::vector<double> h_l;        // the factor (row-major m x m), identical on every rank
 };
 
 namespace rcg {
@@ -213,21 +227,29 @@ __global__ void k_d_pack(const double* __restrict__ v, const int32_t* __restrict
 
 // scalar updates from the global totals g (pcg.cpp:43-89): 0 initial (b,b),(r,r); 1 (r,z);
 // 2 (p,q); 3 (r,r) after the x/r update
+// flags: 1 = defer the initial check to the projected residual (deflation; stage 4), 2 = add
+// the subspace-correction term st->scal[2] to (r, z)
 __global__ void k_d_scalar(DevState* st, const double* __restrict__ g, int stage, double* hist, double* alph,
-                           double* bet, int identity) {
+                           double* bet, int identity, int flags) {
     if (stage == 0) {
         st->bnorm = sqrt(g[0]);
         st->rr = g[1];
         st->rho = g[1];
         if (st->bnorm == 0.0)
             st->done = kZeroRhs;
-        else if (sqrt(g[1]) <= st->eps * st->bnorm)
+        else if (!(flags & 1) && sqrt(g[1]) <= st->eps * st->bnorm)
             st->done = kConverged;
         return;
     }
     if (st->done) return;
+    if (stage == 4) {  // projected initial residual (pcg.cpp:112-118)
+        st->rr = g[0];
+        st->rho = g[0];
+        if (sqrt(g[0]) <= st->eps * st->bnorm) st->done = kConverged;
+        return;
+    }
     if (stage == 1) {
-        const double rho = g[0];
+        const double rho = (flags & 2) ? __dadd_rn(g[0], st->scal[2]) : g[0];
         st->rho = rho;
         if (rho <= 0.0) {
             st->done = kBroken;
@@ -270,9 +292,48 @@ __global__ void k_d_scalar(DevState* st, const double* __restrict__ g, int stage
     }
 }
 
+// u = (W^T A W)^-1 f by one warp (replicated factor); mode 2 also stores f . u in st->scal[2]
+// (the subspace-correction term of (r, z), subspace_correction.cpp:47-57)
+__global__ void k_d_chol(const double* __restrict__ L, int m, const double* __restrict__ f, double* __restrict__ u,
+                         DevState* st, int mode, int respect_done) {
+    __shared__ double sf[128], ss[128];
+    if (respect_done && st->done) return;
+    const int lane = threadIdx.x & 31;
+    for (int j = lane; j < m; j += 32) sf[j] = f[j];
+    __syncwarp();
+    warp_chol_solve(L, m, sf, u, ss);
+    __syncwarp();
+    if (mode == 2 && lane == 0) {
+        double fu = 0.0;
+        for (int j = 0; j < m; ++j) fu = fadd_mul(fu, sf[j], ss[j]);
+        st->scal[2] = fu;
+    }
+}
+
+// y -= sum_j u_j C_j (subtract_combination, deflation.cpp:7-13) on the local rows, partial of
+// (p, y) (mode 0) or (y, y) (mode 1) into dsum[0]
+__global__ void __launch_bounds__(kStreamThreads) k_d_deflate(double* __restrict__ y, const double* __restrict__ C,
+                                                              int64_t ldc, int m, const double* __restrict__ u,
+                                                              const double* __restrict__ p, int32_t n, double* partials,
+                                                              DevState* st, double* dsum, int mode) {
+    __shared__ double red[32];
+    __shared__ double tot[1];
+    if (st->done) return;
+    double acc[1] = {0.0};
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double v = y[i];
+        for (int j = 0; j < m; ++j) v = fsub_mul(v, __ldg(u + j), __ldg(C + j * ldc + i));
+        y[i] = v;
+        acc[0] = mode == 0 ? fadd_mul(acc[0], p[i], v) : fadd_mul(acc[0], v, v);
+    }
+    block_sum<1>(acc, red);
+    if (grid_reduce<1>(acc, partials, blockIdx.x, gridDim.x, &st->tick[kDistTick], tot, red) && threadIdx.x == 0)
+        dsum[0] = tot[0];
+}
+
 // loopback allreduce: every slab's partials summed in slab order, written back to all
 __global__ void k_lb_sum(double* const* d, int nslabs, int count) {
-    const int c = threadIdx.x;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= count) return;
     double s = 0.0;
     for (int b = 0; b < nslabs; ++b) s = __dadd_rn(s, d[b][c]);
@@ -287,8 +348,8 @@ struct rcg_comm {
     virtual int nparts() const = 0;
     virtual int local_slabs() const = 0;
     virtual void begin(rcg_dslab* const* s, int ns) { (void)s, (void)ns; }
-    // in-place sum over all slabs of dsum[0..count)
-    virtual void allreduce(rcg_dslab* const* s, int ns, int count) = 0;
+    // in-place sum over all slabs of dsum[0..count) (sel 0) or gbuf[0..count) (sel 1)
+    virtual void allreduce(rcg_dslab* const* s, int ns, int count, int sel = 0) = 0;
     // halo of the ext vector `which` (0: x_ext, 1: p_ext)
     virtual void halo(rcg_dslab* const* s, int ns, int which) = 0;
 };
@@ -355,11 +416,11 @@ struct NcclComm : rcg_comm {
     ~NcclComm() override {
         if (comm) Nccl::get().comm_destroy(comm);
     }
-    void allreduce(rcg_dslab* const* s, int ns, int count) override {
+    void allreduce(rcg_dslab* const* s, int ns, int count, int sel) override {
         (void)ns;
         Nccl& nc = Nccl::get();
-        nc.check(nc.all_reduce(s[0]->dsum, s[0]->dsum, count, ncclFloat64, ncclSum, comm, s[0]->ctx->stream),
-                 "allreduce");
+        double* buf = sel ? s[0]->gbuf : s[0]->dsum;
+        nc.check(nc.all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm, s[0]->ctx->stream), "allreduce");
     }
     void halo(rcg_dslab* const* s, int ns, int which) override {
         (void)ns;
@@ -387,26 +448,41 @@ struct LoopComm : rcg_comm {
     cudaStream_t cs = nullptr;
     cudaEvent_t ev_join = nullptr;
     std::vector<cudaEvent_t> ev;
-    double** dptrs = nullptr;  // device array of the slabs' dsum pointers
+    double** dptrs = nullptr;  // device arrays of the slabs' dsum / gbuf pointers
+    double** gptrs = nullptr;
+    std::vector<double*> hd, hg;
     int nparts() const override { return np; }
     int local_slabs() const override { return np; }
     ~LoopComm() override {
         if (dptrs) dev_free(dptrs);
+        if (gptrs) dev_free(gptrs);
         for (auto e : ev) cudaEventDestroy(e);
         if (ev_join) cudaEventDestroy(ev_join);
         if (cs) cudaStreamDestroy(cs);
     }
-    void begin(rcg_dslab* const* s, int ns) override {
-        std::vector<double*> h(ns);
-        for (int b = 0; b < ns; ++b) h[b] = s[b]->dsum;
-        RCG_CK(cudaMemcpy(dptrs, h.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice));
+    void sync_ptrs(rcg_dslab* const* s, int ns) {
+        std::vector<double*> d(ns), g(ns);
+        for (int b = 0; b < ns; ++b) {
+            d[b] = s[b]->dsum;
+            g[b] = s[b]->gbuf;
+        }
+        if (d != hd) {
+            RCG_CK(cudaMemcpy(dptrs, d.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice));
+            hd = d;
+        }
+        if (g != hg) {
+            RCG_CK(cudaMemcpy(gptrs, g.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice));
+            hg = g;
+        }
     }
-    void allreduce(rcg_dslab* const* s, int ns, int count) override {
+    void begin(rcg_dslab* const* s, int ns) override { sync_ptrs(s, ns); }
+    void allreduce(rcg_dslab* const* s, int ns, int count, int sel) override {
+        sync_ptrs(s, ns);
         for (int b = 0; b < ns; ++b) {
             RCG_CK(cudaEventRecord(ev[b], s[b]->ctx->stream));
             RCG_CK(cudaStreamWaitEvent(cs, ev[b], 0));
         }
-        k_lb_sum<<<1, 32, 0, cs>>>(dptrs, ns, count);
+        k_lb_sum<<<(count + 255) / 256, 256, 0, cs>>>(sel ? gptrs : dptrs, ns, count);
         RCG_CK(cudaGetLastError());
         RCG_CK(cudaEventRecord(ev_join, cs));
         for (int b = 0; b < ns; ++b) RCG_CK(cudaStreamWaitEvent(s[b]->ctx->stream, ev_join, 0));
@@ -430,15 +506,30 @@ struct LoopComm : rcg_comm {
 };
 
 // ------------------------------------------------------------------ distributed PCG
+static void ensure_g(rcg_dslab* d, int64_t count) {
+    if (count <= d->cap_g) return;
+    dev_free(d->gbuf);
+    dev_free(d->ubuf);
+    dev_free(d->u2buf);
+    d->gbuf = dev_alloc(count);
+    d->ubuf = dev_alloc(std::max<int64_t>(count, 128));
+    d->u2buf = dev_alloc(std::max<int64_t>(count, 128));
+    d->cap_g = count;
+}
+
 struct DistSolve {
     rcg_comm* comm;
     int ns;
     rcg_dslab* const* sl;
     int max_iter;
     double eps;
+    const rcg_dbasis* defl = nullptr;  // deflated PCG (pcg.cpp:94-160)
+    const rcg_dbasis* sc = nullptr;    // subspace correction around the block IC (subspace_correction.cpp)
     bool ic = false;
     std::vector<Staged> bst, xst;
     std::vector<double*> bdev;
+
+    int flags() const { return (defl ? 1 : 0) | (sc ? 2 : 0); }
 
     void setup(const double* const* b, double* const* x) {
         static bool smem_ok = false;
@@ -448,6 +539,9 @@ struct DistSolve {
             smem_ok = true;
         }
         ic = sl[0]->ic != nullptr;
+        require(!(defl && sc), "dist_pcg_solve: deflation and subspace correction are exclusive");
+        require(!sc || ic, "dist_pcg_solve: subspace correction needs the block IC(0) inner preconditioner");
+        const int m = defl ? defl->m : (sc ? sc->m : 0);
         bst.resize(ns);
         xst.resize(ns);
         bdev.resize(ns);
@@ -459,7 +553,8 @@ struct DistSolve {
             const int64_t ntiles = ic ? sweep_tiles(d->ic) : (n + kSweepThreads - 1) / kSweepThreads;
             const int64_t ngroups = (ntiles + kGroup - 1) / kGroup;
             const int64_t red = std::max<int64_t>(ntiles, static_cast<int64_t>(kMaxRed) * ctx->num_sms * 8);
-            ensure_workspace(ctx, std::max(n, 1), 1, max_iter, red, ngroups, 1);
+            ensure_workspace(ctx, std::max(n, 1), std::max(m, 1), max_iter, red, ngroups, 1);
+            ensure_g(d, std::max(m * m, 128));
             stage_in(ctx, b[s], n, bst[s]);
             bdev[s] = bst[s].dev;
             stage_in(ctx, x[s], n, xst[s]);
@@ -497,8 +592,28 @@ struct DistSolve {
         for (int s = 0; s < ns; ++s) {
             rcg_ctx* ctx = sl[s]->ctx;
             k_d_scalar<<<1, 1, 0, ctx->stream>>>(ctx->ws.st, sl[s]->dsum, stage, ctx->ws.hist, ctx->ws.alph,
-                                                 ctx->ws.bet, ic ? 0 : 1);
+                                                 ctx->ws.bet, ic ? 0 : 1, flags());
             RCG_LAUNCHED(ctx);
+        }
+    }
+
+    // f = C^T y over the local rows -> allreduce (m values) -> out = (W^T A W)^-1 f on every slab
+    void project_coeffs(const rcg_dbasis* B, bool use_aw, double* const* ys, bool to_u2, int mode, int respect_done) {
+        const int m = B->m;
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            k_tallt<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                use_aw ? B->aw[s] : B->w[s], d->nloc, m, ys[s], d->nloc, ctx->ws.partials, nullptr, d->gbuf, 0,
+                ctx->ws.st, respect_done);
+            RCG_LAUNCHED(ctx);
+        }
+        comm->allreduce(sl, ns, m, 1);
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            k_d_chol<<<1, 32, 0, d->ctx->stream>>>(B->l[s], m, d->gbuf, to_u2 ? d->u2buf : d->ubuf, d->ctx->ws.st, mode,
+                                                   respect_done);
+            RCG_LAUNCHED(d->ctx);
         }
     }
 
@@ -513,6 +628,22 @@ struct DistSolve {
         }
         comm->allreduce(sl, ns, 2);
         scalar(0);
+        std::vector<double*> rs(ns);
+        for (int s = 0; s < ns; ++s) rs[s] = sl[s]->ctx->ws.r;
+        if (defl) {  // r = P^T r and the check on the projected residual (pcg.cpp:112-118)
+            project_coeffs(defl, false, rs.data(), false, 1, 1);
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                rcg_ctx* ctx = d->ctx;
+                k_d_deflate<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                    ctx->ws.r, defl->aw[s], d->nloc, defl->m, d->ubuf, nullptr, d->nloc, ctx->ws.partials, ctx->ws.st,
+                    d->dsum, 1);
+                RCG_LAUNCHED(ctx);
+            }
+            comm->allreduce(sl, ns, 1);
+            scalar(4);
+        }
+        if (sc) project_coeffs(sc, false, rs.data(), true, 2, 1);  // u2 = chol(W^T r), f . u
     }
 
     void iteration() {
@@ -533,7 +664,7 @@ struct DistSolve {
                 RCG_LAUNCHED(ctx);
             }
             comm->allreduce(sl, ns, 1);
-            scalar(1);
+            scalar(1);  // (+ f . u with subspace correction)
         }
         for (int s = 0; s < ns; ++s) {
             rcg_dslab* d = sl[s];
@@ -541,7 +672,7 @@ struct DistSolve {
             KTimer t(ctx, 3);
             k_pupdate<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
                 ic ? ctx->ws.zs : ctx->ws.r, d->pe, ic ? ctx->ws.zs : nullptr, ctx->ws.ybuf, d->nloc, ctx->ws.st,
-                nullptr, 0, 0, nullptr);
+                sc ? sc->w[s] : nullptr, d->nloc, sc ? sc->m : 0, d->u2buf);
             RCG_LAUNCHED(ctx);
         }
         comm->halo(sl, ns, 1);
@@ -552,6 +683,19 @@ struct DistSolve {
             k_d_spmv<<<spmv_grid(ctx, d->nloc), kSpmvThreads, spmv_smem(d->a), ctx->stream>>>(
                 sargs(d, d->pe, ctx->ws.q), d->a->cap, ctx->ws.st, d->dsum);
             RCG_LAUNCHED(ctx);
+        }
+        if (defl) {  // q = P^T q (pcg.cpp:131), then (p, q)
+            std::vector<double*> qs(ns);
+            for (int s = 0; s < ns; ++s) qs[s] = sl[s]->ctx->ws.q;
+            project_coeffs(defl, false, qs.data(), false, 1, 1);
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                rcg_ctx* ctx = d->ctx;
+                k_d_deflate<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                    ctx->ws.q, defl->aw[s], d->nloc, defl->m, d->ubuf, d->pe, d->nloc, ctx->ws.partials, ctx->ws.st,
+                    d->dsum, 0);
+                RCG_LAUNCHED(ctx);
+            }
         }
         comm->allreduce(sl, ns, 1);
         scalar(2);
@@ -565,6 +709,11 @@ struct DistSolve {
         }
         comm->allreduce(sl, ns, 1);
         scalar(3);
+        if (sc) {  // W^T r for the next apply (subspace_correction.cpp:50-51)
+            std::vector<double*> rs(ns);
+            for (int s = 0; s < ns; ++s) rs[s] = sl[s]->ctx->ws.r;
+            project_coeffs(sc, false, rs.data(), true, 2, 1);
+        }
     }
 
     // same batching as the single-GPU loop; every slab holds identical scalars, slab 0 is polled
@@ -576,13 +725,13 @@ struct DistSolve {
         RCG_CK(cudaEventCreate(&t0));
         RCG_CK(cudaEventCreate(&t1));
         RCG_CK(cudaEventRecord(t0, c0->stream));
-        volatile int* flags = reinterpret_cast<volatile int*>(c0->host_pinned + 256);
-        flags[0] = flags[1] = 0;
+        volatile int* flags_h = reinterpret_cast<volatile int*>(c0->host_pinned + 256);
+        flags_h[0] = flags_h[1] = 0;
         int enq = 0, batch = 2, slot = 0, prev = 0;
         bool have_prev = false;
         while (true) {
             for (int j = 0; j < batch && enq < max_iter; ++j, ++enq) iteration();
-            RCG_CK(cudaMemcpyAsync((void*)(flags + slot), &c0->ws.st->done, sizeof(int), cudaMemcpyDeviceToHost,
+            RCG_CK(cudaMemcpyAsync((void*)(flags_h + slot), &c0->ws.st->done, sizeof(int), cudaMemcpyDeviceToHost,
                                    c0->stream));
             RCG_CK(cudaEventRecord(evs[slot], c0->stream));
             if (enq >= max_iter) {
@@ -591,7 +740,7 @@ struct DistSolve {
             }
             if (have_prev) {
                 RCG_CK(cudaEventSynchronize(evs[prev]));
-                if (flags[prev] != kRunning) break;
+                if (flags_h[prev] != kRunning) break;
             }
             have_prev = true;
             prev = slot;
@@ -610,10 +759,35 @@ struct DistSolve {
     DevState finish(double* const* x) {
         for (int s = 0; s < ns; ++s) {
             rcg_dslab* d = sl[s];
+            k_zero_if<<<stream_grid(d->ctx, d->nloc), kStreamThreads, 0, d->ctx->stream>>>(d->xe, d->nloc,
+                                                                                          d->ctx->ws.st);
+            RCG_LAUNCHED(d->ctx);
+        }
+        if (defl) {  // x = P x + W (W^T A W)^-1 W^T b (pcg.cpp:152-157), skipped for breakdown / zero rhs
+            std::vector<double*> xs(ns), bs(ns);
+            for (int s = 0; s < ns; ++s) {
+                xs[s] = sl[s]->xe;
+                bs[s] = bdev[s];
+            }
+            project_coeffs(defl, true, xs.data(), false, 1, 0);
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                k_sub_combination_ok<<<stream_grid(d->ctx, d->nloc), kStreamThreads, 0, d->ctx->stream>>>(
+                    d->xe, defl->w[s], d->nloc, defl->m, d->ubuf, d->nloc, d->ctx->ws.st);
+                RCG_LAUNCHED(d->ctx);
+            }
+            project_coeffs(defl, false, bs.data(), true, 1, 0);
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                k_add_combination<<<stream_grid(d->ctx, d->nloc), kStreamThreads, 0, d->ctx->stream>>>(
+                    d->xe, defl->w[s], d->nloc, defl->m, d->u2buf, d->nloc, d->ctx->ws.st, 1);
+                RCG_LAUNCHED(d->ctx);
+            }
+        }
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
             rcg_ctx* ctx = d->ctx;
             const int32_t n = d->nloc;
-            k_zero_if<<<stream_grid(ctx, n), kStreamThreads, 0, ctx->stream>>>(d->xe, n, ctx->ws.st);
-            RCG_LAUNCHED(ctx);
             Staged out;
             stage_out_begin(ctx, x[s], n, out);
             if (n > 0)
@@ -628,6 +802,69 @@ struct DistSolve {
         return h;
     }
 };
+
+// W (local rows of every slab) -> AW by m halo exchanges + local SpMVs, the Gram W^T A W (lower
+// triangle mirrored, as rcg_basis_create) allreduced, factored once on the host from the
+// identical totals, the factor uploaded to every slab
+static rcg_dbasis* dbasis_create(rcg_comm* comm, int ns, rcg_dslab* const* sl, const double* const* wcols, int m,
+                                 int kind) {
+    auto* B = new rcg_dbasis();
+    B->kind = kind;
+    B->m = m;
+    try {
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            const int64_t sz = static_cast<int64_t>(d->nloc) * m;
+            B->w.push_back(dev_alloc(std::max<int64_t>(sz, 1)));
+            B->aw.push_back(dev_alloc(std::max<int64_t>(sz, 1)));
+            B->l.push_back(dev_alloc(static_cast<int64_t>(std::max(m, 1)) * std::max(m, 1)));
+            Staged wst;
+            stage_in(ctx, wcols[s], sz, wst);
+            if (sz) RCG_CK(cudaMemcpyAsync(B->w[s], wst.dev, sizeof(double) * sz, cudaMemcpyDeviceToDevice, ctx->stream));
+            RCG_CK(cudaStreamSynchronize(ctx->stream));
+            ensure_g(d, std::max(m * m, 128));
+        }
+        comm->begin(sl, ns);
+        for (int j = 0; j < m; ++j) {
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                if (d->nloc)
+                    RCG_CK(cudaMemcpyAsync(d->pe, B->w[s] + static_cast<int64_t>(j) * d->nloc, sizeof(double) * d->nloc,
+                                           cudaMemcpyDeviceToDevice, d->ctx->stream));
+            }
+            comm->halo(sl, ns, 1);
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                const int rc = rcg_spmv(d->ctx, d->a, d->pe, B->aw[s] + static_cast<int64_t>(j) * d->nloc);
+                if (rc != RCG_OK) throw Error(rc, rcg_last_error());
+            }
+        }
+        std::vector<double> g;
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            gram_host(d->ctx, B->w[s], d->nloc, m, B->aw[s], d->nloc, m, d->nloc, true, g);
+            RCG_CK(cudaMemcpy(d->gbuf, g.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice));
+        }
+        comm->allreduce(sl, ns, m * m, 1);
+        for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+        g.assign(static_cast<size_t>(m) * m, 0.0);
+        RCG_CK(cudaMemcpy(g.data(), sl[0]->gbuf, sizeof(double) * m * m, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < i; ++j) g[static_cast<size_t>(j) * m + i] = g[static_cast<size_t>(i) * m + j];
+        int bad = -1;
+        if (!chol_factor_host(m, g, B->h_l, &bad)) throw Error(RCG_E_BREAKDOWN, "distributed basis: W^T A W not SPD");
+        for (int s = 0; s < ns; ++s)
+            RCG_CK(cudaMemcpy(B->l[s], B->h_l.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice));
+    } catch (...) {
+        for (auto p : B->w) dev_free(p);
+        for (auto p : B->aw) dev_free(p);
+        for (auto p : B->l) dev_free(p);
+        delete B;
+        throw;
+    }
+    return B;
+}
 
 }  // namespace rcg
 
@@ -699,7 +936,9 @@ void rcg_dslab_destroy(rcg_dslab* d) {
     if (!d) return;
     if (d->ctx) cudaStreamSynchronize(d->ctx->stream);
     rcg_matrix_destroy(d->a);
-    for (void* p : {(void*)d->send_idx, (void*)d->sendbuf, (void*)d->xe, (void*)d->pe, (void*)d->dsum}) dev_free(p);
+    for (void* p : {(void*)d->send_idx, (void*)d->sendbuf, (void*)d->xe, (void*)d->pe, (void*)d->dsum, (void*)d->gbuf,
+                    (void*)d->ubuf, (void*)d->u2buf})
+        dev_free(p);
     delete d;
 }
 
@@ -751,14 +990,36 @@ int rcg_comm_create_loopback(int nparts, rcg_comm** out) {
         c->ev.resize(nparts);
         for (auto& e : c->ev) RCG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->dptrs = static_cast<double**>(dev_alloc_bytes(sizeof(double*) * nparts));
+        c->gptrs = static_cast<double**>(dev_alloc_bytes(sizeof(double*) * nparts));
         *out = c;
     });
 }
 
 void rcg_comm_destroy(rcg_comm* c) { delete c; }
 
-int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* b,
-                       double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
+int rcg_dbasis_create(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* w, int m, int kind,
+                      rcg_dbasis** out) {
+    return guard([&] {
+        require(comm && slabs && w && out, "rcg_dbasis_create: null argument");
+        *out = nullptr;
+        require(nslabs == comm->local_slabs(), "rcg_dbasis_create: slab count does not match the transport");
+        require(m >= 1 && m <= 128, "rcg_dbasis_create: m must be in [1, 128]");
+        require(kind == RCG_BASIS_DEFLATION || kind == RCG_BASIS_SC, "rcg_dbasis_create: unknown basis kind");
+        for (int s = 0; s < nslabs; ++s) require(slabs[s] && w[s], "rcg_dbasis_create: null slab / W");
+        *out = dbasis_create(comm, nslabs, slabs, w, m, kind);
+    });
+}
+
+void rcg_dbasis_destroy(rcg_dbasis* b) {
+    if (!b) return;
+    for (auto p : b->w) dev_free(p);
+    for (auto p : b->aw) dev_free(p);
+    for (auto p : b->l) dev_free(p);
+    delete b;
+}
+
+int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
+                   double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
     return guard([&] {
         require(comm && slabs && b && x && report, "dist_pcg_solve: null argument");
         require(nslabs == comm->local_slabs(), "dist_pcg_solve: slab count does not match the transport");
@@ -768,7 +1029,10 @@ int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, cons
             require(slabs[s]->nparts == comm->nparts(), "dist_pcg_solve: slab partition does not match the transport");
             if (nslabs > 1) require(slabs[s]->part == s, "dist_pcg_solve: loopback slabs must be given in part order");
         }
+        if (basis) require(static_cast<int>(basis->w.size()) == nslabs, "dist_pcg_solve: basis built for other slabs");
         DistSolve ds{comm, nslabs, slabs, cfg->max_iter, cfg->eps};
+        if (basis && basis->kind == RCG_BASIS_DEFLATION) ds.defl = basis;
+        if (basis && basis->kind == RCG_BASIS_SC) ds.sc = basis;
         ds.setup(b, x);
         ds.initial();
         const double wall = ds.run();
@@ -786,10 +1050,19 @@ int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, cons
             if (report->betas)
                 RCG_CK(cudaMemcpy(report->betas, c0->ws.bet, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
         }
-        if (h.done == kBroken)
-            throw Error(RCG_E_BREAKDOWN, h.status == kBrkRz ? "pcg: preconditioner not SPD ((r, z) <= 0)"
-                                                            : "pcg: matrix not SPD ((p, A p) <= 0)");
+        if (h.done == kBroken) {
+            const bool dfl = ds.defl != nullptr;
+            throw Error(RCG_E_BREAKDOWN, h.status == kBrkRz ? (dfl ? "deflated pcg: preconditioner not SPD ((r, z) <= 0)"
+                                                                   : "pcg: preconditioner not SPD ((r, z) <= 0)")
+                                                            : (dfl ? "deflated pcg: projected operator not SPD ((p, P^T A p) <= 0)"
+                                                                   : "pcg: matrix not SPD ((p, A p) <= 0)"));
+        }
     });
+}
+
+int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* b,
+                       double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
+    return rcg_dist_solve(comm, nslabs, slabs, nullptr, b, x, cfg, report);
 }
 
 }  // extern "C"

@@ -48,6 +48,15 @@ __global__ void __launch_bounds__(kStreamThreads) k_pupdate(const double* __rest
                                                             int32_t n, DevState* st, const double* __restrict__ W,
                                                             int64_t ldw, int k, const double* __restrict__ u);
 __global__ void k_zero_if(double* x, int32_t n, const DevState* st);
+__global__ void __launch_bounds__(kStreamThreads, 4) k_tallt(const double* __restrict__ B, int64_t ldb, int k,
+                                                          const double* __restrict__ y, int32_t n,
+                                                          double* partials, const double* __restrict__ L,
+                                                          double* __restrict__ out, int mode, DevState* st,
+                                                          int respect_done);
+__global__ void k_add_combination(double* __restrict__ x, const double* __restrict__ W, int64_t ldw, int k,
+                                  const double* __restrict__ u, int32_t n, const DevState* st, int only_ok);
+__global__ void k_sub_combination_ok(double* __restrict__ x, const double* __restrict__ W, int64_t ldw, int k,
+                                     const double* __restrict__ u, int32_t n, const DevState* st);
 #endif
 int stream_grid(const rcg_ctx* ctx, int64_t n);
 size_t spmv_smem(const rcg_matrix* a);

@@ -46,11 +46,16 @@ class LoopbackSystem:
         self.slabs = [api.DSlab(c, p, f) for c, p, f in zip(self.ctxs, self.plans, self.factors)]
         self.comm = api.Comm.loopback(nparts)
 
-    def solve(self, b: np.ndarray, x: np.ndarray, eps: float = 1e-8, max_iter: int = 1000) -> api.SolveReport:
+    def basis(self, w: np.ndarray, kind: str = "deflation") -> api.DBasis:
+        """Distributed basis from a global W given as (m, n) (one basis vector per row)."""
+        return api.DBasis(self.comm, self.slabs, [w[:, p.row_begin:p.row_end] for p in self.plans], kind)
+
+    def solve(self, b: np.ndarray, x: np.ndarray, eps: float = 1e-8, max_iter: int = 1000,
+              basis: Optional[api.DBasis] = None) -> api.SolveReport:
         """Global b, x (x updated in place) split along the slab bounds."""
         bs = [np.ascontiguousarray(b[p.row_begin:p.row_end]) for p in self.plans]
         xs = [np.ascontiguousarray(x[p.row_begin:p.row_end]) for p in self.plans]
-        rep = api.dist_pcg_solve(self.comm, self.slabs, bs, xs, eps, max_iter)
+        rep = api.dist_solve(self.comm, self.slabs, bs, xs, basis, eps, max_iter)
         for p, xl in zip(self.plans, xs):
             x[p.row_begin:p.row_end] = xl
         return rep
@@ -79,8 +84,13 @@ class NcclRank:
         dist.broadcast_object_list(obj, src=0)
         self.comm = api.Comm.nccl(obj[0], self.world, self.rank)
 
-    def solve(self, b_local, x_local, eps: float = 1e-8, max_iter: int = 1000) -> api.SolveReport:
-        return api.dist_pcg_solve(self.comm, [self.slab], [b_local], [x_local], eps, max_iter)
+    def basis(self, w_local: np.ndarray, kind: str = "deflation") -> api.DBasis:
+        """This rank's rows of W, (m, nloc) -- collective over the ranks."""
+        return api.DBasis(self.comm, [self.slab], [w_local], kind)
+
+    def solve(self, b_local, x_local, eps: float = 1e-8, max_iter: int = 1000,
+              basis: Optional[api.DBasis] = None) -> api.SolveReport:
+        return api.dist_solve(self.comm, [self.slab], [b_local], [x_local], basis, eps, max_iter)
 
 
 def scatter(v: np.ndarray, plans: Sequence[api.SlabPlan]):

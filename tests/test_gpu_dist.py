@@ -81,6 +81,40 @@ def test_loopback_zero_rhs_and_cap(oracle, problems):
     assert not rep.converged and rep.iterations == 7 and len(rep.history) == 7
 
 
+@pytest.mark.parametrize("method", ["deflation", "sc"])
+@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_loopback_deflated_and_sc_match_block_jacobi(oracle, problems, name, method, nparts):
+    """Row-partitioned W: distributed deflated PCG / SC-PCG against the oracle's single-process
+    solve with the same W and the block-Jacobi IC(0) of the same bounds."""
+    from paper_2203_08498_b200 import dist
+
+    sa, host = _scaled(oracle, problems, name)
+    f = oracle.ic0_factorize(sa, 0.0, nparts)
+    # W: error samples of an oracle solve (the sequence's construction, small m)
+    s_o = oracle.sampler_a(8, 5000, sa.n)
+    x1 = np.zeros(sa.n)
+    oracle.pcg_solve(sa, oracle.uniform_pm1(2, 0, sa.n), x1, kind=1, ic=f, max_iter=5000, sampler=s_o)
+    occ, _ = s_o.state()
+    w = np.stack([x1 - s_o.slot(j) for j in range(8) if occ[j]])
+    w /= np.linalg.norm(w, axis=1, keepdims=True)
+    b = oracle.uniform_pm1(17, 0, sa.n)
+    ob = oracle.basis(sa, w, 0 if method == "deflation" else 1)
+    xo = np.zeros(sa.n)
+    if method == "deflation":
+        ro = oracle.deflated_pcg_solve(sa, b, xo, ob, kind=1, ic=f, max_iter=5000)
+    else:
+        ro = oracle.pcg_solve(sa, b, xo, kind=2, ic=f, sc=ob, max_iter=5000)
+    system = dist.LoopbackSystem(host, nparts)
+    db = system.basis(w, method)
+    x = np.zeros(sa.n)
+    rep = system.solve(b, x, 1e-8, 5000, basis=db)
+    assert rep.converged and ro.converged
+    assert abs(rep.iterations - ro.iterations) <= 2, (rep.iterations, ro.iterations)
+    if rep.iterations == ro.iterations:
+        assert _rel(x, xo) <= 1e-6, _rel(x, xo)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
