@@ -90,6 +90,12 @@ int rcg_ic0_factorize(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const i
  * on the host from a's pattern, the numeric row merge + shift ladder by a level-ordered
  * sync-free kernel from a's device values; the factor is bitwise rcg_ic0_factorize's. */
 int rcg_ic0_factorize_device(rcg_ctx* ctx, const rcg_matrix* a, double shift, int num_blocks, rcg_ic** out);
+/* Tiled sweeps for a factor in the natural ordering of an nx x ny x nz grid (x fastest): a CTA
+ * owns a tile_x x tile_y block of (x, y) columns for all z and walks them in level steps; only
+ * dependencies across tiles travel through HBM.  Same operator (bitwise).  RCG_E_INVALID when
+ * the factor's pattern is not a supported stencil (the level-scheduled sweeps stay in use);
+ * tile_x = 0 switches back to them. */
+int rcg_ic_set_grid(rcg_ctx* ctx, rcg_ic* f, int32_t nx, int32_t ny, int32_t nz, int tile_x, int tile_y);
 /* upload an existing IcFactor (ic_preconditioner.hpp:18-37) so the operator is identical */
 int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_bounds,
                   const int32_t* l_row_start, const int32_t* l_col, const double* l_val,

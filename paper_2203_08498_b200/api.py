@@ -226,6 +226,10 @@ class IcFactor:
         check(lib.rcg_ic_export(self.h, *[_ptr(v) for v in out.values()]))
         return out
 
+    def set_grid(self, nx: int, ny: int, nz: int, tile_x: int = 16, tile_y: int = 8) -> None:
+        """Tiled sweeps for a natural-ordered nx x ny x nz grid (rcg_ic_set_grid); tile_x = 0 off."""
+        check(lib.rcg_ic_set_grid(self.ctx.h, self.h, int(nx), int(ny), int(nz), int(tile_x), int(tile_y)))
+
     def apply(self, r, z=None):
         """ic_apply (ic_preconditioner.hpp:47)."""
         r = _f64(r, self.n, "r")

@@ -206,6 +206,10 @@ int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos) {
 
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
+    if (grid_sweep_available(f)) {  // tiled sweep on a natural-ordered grid (icgrid.cu)
+        launch_grid_sweep(ctx, f, backward, a);
+        return;
+    }
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
     const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
@@ -494,7 +498,8 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
-                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d})
+                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->grid.tile_xy,
+                    (void*)f->grid.coef[0], (void*)f->grid.coef[1], (void*)f->grid.mask[0], (void*)f->grid.mask[1]})
         dev_free(p);
     delete f;
 }

@@ -182,6 +182,19 @@ struct rcg_matrix {
     int cap = 256;  // pipelined SpMV stage capacity (entries)
 };
 
+// tiled sweeps on a natural-ordered 3D grid (icgrid.cu)
+struct GridSched {
+    bool on = false;
+    int32_t nx = 0, ny = 0, nz = 0;
+    int tx = 0, ty = 0, wx = 1, wy = 1, wz = 1;
+    int ntiles = 0, max_ctas = 0;
+    int nslots[2] = {0, 0};                       // [0] forward (L), [1] backward (U)
+    int8_t sdx[2][16] = {}, sdy[2][16] = {}, sdz[2][16] = {};
+    double* coef[2] = {nullptr, nullptr};         // slot-major stencil coefficients
+    uint32_t* mask[2] = {nullptr, nullptr};       // per row: slots present
+    int32_t* tile_xy = nullptr;                   // ticket -> X | Y << 16
+};
+
 struct rcg_ic {
     int32_t n = 0;
     int64_t nnz_l = 0;
@@ -198,6 +211,7 @@ struct rcg_ic {
     int32_t *b_perm = nullptr, *b_prs = nullptr, *b_col = nullptr;
     double* b_val = nullptr;
     double* d = nullptr;
+    GridSched grid;
 };
 
 struct rcg_tall {

@@ -40,6 +40,8 @@ struct SweepArgs {
 int spmv_grid(const rcg_ctx* ctx, int32_t n);
 int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos);
 void ensure_host_image(const rcg_ic* f);  // icfactor.cu
+bool grid_sweep_available(const rcg_ic* f);  // icgrid.cu
+void launch_grid_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a);
 
 #ifdef __CUDACC__
 // solver.cu kernels reused by the multi-GPU slabs (dist.cu)
