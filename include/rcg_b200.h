@@ -38,6 +38,7 @@ typedef struct rcg_sampler rcg_sampler; /* device snapshot slots (SamplerState) 
 typedef struct rcg_dslab rcg_dslab;     /* one GPU's row slab of a multi-GPU solve */
 typedef struct rcg_comm rcg_comm;       /* slab transport: NCCL (one slab per process) or loopback */
 typedef struct rcg_dbasis rcg_dbasis;   /* row-partitioned W, AW + replicated chol(W^T A W) */
+typedef struct rcg_seq rcg_seq;         /* prepared sequence: scaled A, D^-1/2, IC(0) (run_sequence) */
 
 /* message of the last failing call on this thread; "" after success */
 const char* rcg_last_error(void);
@@ -323,6 +324,42 @@ void rcg_dbasis_destroy(rcg_dbasis* b);
  * iteration the m-vector W^T q (or W^T r) is allreduced before the replicated Cholesky solve. */
 int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
                    double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report);
+
+/* ------------------------------------------------------------------ the sequence (driver.cpp)
+ * run_sequence (driver.cpp:108-222) on the device: rcg_seq_prepare scales A and factors IC(0)
+ * once; rcg_seq_run runs one sequence of k_t right-hand sides (rhs: k_t vectors of length n back
+ * to back, host or device; x receives the k_t solutions of A x = b): scaled solve 1 with the
+ * error sampler, harvest + build_aux_matrix, SC preconditioner or deflation operator, solves
+ * 2..k_t from x0 = 0 (batched when cfg->batch), solutions and true relative residuals in the
+ * original scaling.  Errors use RCG_E_PARSE for invalid configs, as validate_config. */
+#define RCG_METHOD_CG 0         /* "cg" */
+#define RCG_METHOD_ICCG 1       /* "iccg" */
+#define RCG_METHOD_ES_SC_ICCG 2 /* "es-sc-iccg" */
+#define RCG_METHOD_ES_D_ICCG 3  /* "es-d-iccg" */
+typedef struct {
+    double eps;       /* RunConfig::eps */
+    int max_iter;     /* RunConfig::max_iter */
+    int sampling;     /* 'A' or 'B' (RunConfig::sampling) */
+    int m;            /* RunConfig::m (method A uses max(m, 2) slots) */
+    double theta;     /* RunConfig::theta (Ritz selection threshold) */
+    int keep_count;   /* > 0: keep that many Ritz vectors instead of theta (extension) */
+    int batch;        /* solves 2..k_t as batched multi-RHS kernel sequences */
+} rcg_seq_config;
+typedef struct {
+    int* iterations;      /* k_t (caller arrays; each may be NULL) */
+    int* converged;
+    double* wall_time;
+    double* true_relres;  /* ||b - A x|| / ||b|| with the unscaled A (driver.cpp:72-82) */
+    double* ritz_values;  /* ritz_cap doubles */
+    int ritz_cap;
+    int m_bar, m_tilde;
+    double theta_used;
+    double w_build_time, avg_iterations, avg_wall_time, setup_time;
+    int acceleration_inactive;
+} rcg_seq_report;
+int rcg_seq_prepare(rcg_ctx* ctx, const rcg_matrix* a_orig, int method, int blocks, rcg_seq** out);
+void rcg_seq_destroy(rcg_seq* s);
+int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq_config* cfg, rcg_seq_report* rep);
 
 #ifdef __cplusplus
 }

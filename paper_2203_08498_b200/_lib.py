@@ -26,6 +26,7 @@ RCG_PAYLOAD_X, RCG_PAYLOAD_R = 0, 1
 RCG_SAMPLER_A, RCG_SAMPLER_B = 0, 1
 RCG_BASIS_DEFLATION, RCG_BASIS_SC = 0, 1
 RCG_GEN_POISSON7, RCG_GEN_FV7_CONTRAST, RCG_GEN_Q1_27PT, RCG_GEN_KNN = 0, 1, 2, 3
+RCG_METHOD_CG, RCG_METHOD_ICCG, RCG_METHOD_ES_SC_ICCG, RCG_METHOD_ES_D_ICCG = 0, 1, 2, 3
 
 vp = C.c_void_p
 i32p = C.POINTER(C.c_int32)
@@ -89,6 +90,18 @@ class SlabPlanC(C.Structure):
         ("nnz", C.c_int64), ("row_start", i32p), ("col_idx", i32p), ("values", dp), ("halo_global", i32p),
         ("recv_count", i32p), ("send_count", i32p), ("send_idx", i32p), ("nparts", C.c_int), ("part", C.c_int),
     ]
+
+
+class SeqConfig(C.Structure):
+    _fields_ = [("eps", C.c_double), ("max_iter", C.c_int), ("sampling", C.c_int), ("m", C.c_int),
+                ("theta", C.c_double), ("keep_count", C.c_int), ("batch", C.c_int)]
+
+
+class SeqReport(C.Structure):
+    _fields_ = [("iterations", ip), ("converged", ip), ("wall_time", dp), ("true_relres", dp),
+                ("ritz_values", dp), ("ritz_cap", C.c_int), ("m_bar", C.c_int), ("m_tilde", C.c_int),
+                ("theta_used", C.c_double), ("w_build_time", C.c_double), ("avg_iterations", C.c_double),
+                ("avg_wall_time", C.c_double), ("setup_time", C.c_double), ("acceleration_inactive", C.c_int)]
 
 
 def _sig(name, restype, *args):
@@ -178,6 +191,9 @@ SIGNATURES = {
     "rcg_comm_destroy": (None, vp),
     "rcg_dist_pcg_solve": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                            C.POINTER(SolverConfig), C.POINTER(SolveReport)),
+    "rcg_seq_prepare": (C.c_int, vp, vp, C.c_int, C.c_int, C.POINTER(vp)),
+    "rcg_seq_destroy": (None, vp),
+    "rcg_seq_run": (C.c_int, vp, C.c_int, vp, vp, C.POINTER(SeqConfig), C.POINTER(SeqReport)),
     "rcg_dbasis_create": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_int, C.c_int, C.POINTER(vp)),
     "rcg_dbasis_destroy": (None, vp),
     "rcg_dist_solve": (C.c_int, vp, C.c_int, C.POINTER(vp), vp, C.POINTER(vp), C.POINTER(vp),

@@ -733,3 +733,45 @@ def dist_solve(comm: Comm, slabs, bs, xs, basis: Optional[DBasis] = None, eps: f
     check(lib.rcg_dist_solve(comm.h, ns, hs, basis.h if basis is not None else None, bp, xp, C.byref(cfg),
                              C.byref(rep)))
     return _finish(rep, bufs)
+
+
+# --------------------------------------------------------------------------- the sequence driver
+_METHODS = {"cg": L.RCG_METHOD_CG, "iccg": L.RCG_METHOD_ICCG, "es-sc-iccg": L.RCG_METHOD_ES_SC_ICCG,
+            "es-d-iccg": L.RCG_METHOD_ES_D_ICCG}
+
+
+class Sequence:
+    """run_sequence (driver.cpp:108-222) on the device: prepared once per matrix (scaling, IC(0)),
+    then `run(B, X, ...)` solves the k right-hand sides B (k, n) into X (k, n)."""
+
+    def __init__(self, ctx: Context, a_orig: CsrMatrix, method: str = "es-sc-iccg", blocks: int = 1):
+        if method not in _METHODS:
+            raise L.ParseError(f"config: unknown method '{method}'")
+        h = C.c_void_p()
+        check(lib.rcg_seq_prepare(ctx.h, a_orig.h, _METHODS[method], int(blocks), C.byref(h)))
+        self.h, self.ctx, self.n, self.method = h, ctx, a_orig.n, method
+
+    def run(self, B, X, eps: float = 1e-8, max_iter: int = 1000, sampling: str = "A", m: int = 16,
+            theta: float = 1e-3, keep_count: int = 0, batch: bool = True) -> dict:
+        k = len(B)
+        cfg = L.SeqConfig(float(eps), int(max_iter), ord(sampling), int(m), float(theta), int(keep_count),
+                          1 if batch else 0)
+        its = np.zeros(k, np.int32)
+        conv = np.zeros(k, np.int32)
+        wall = np.zeros(k)
+        trr = np.zeros(k)
+        ritz = np.zeros(max(1, 2 * m))
+        rep = L.SeqReport(its.ctypes.data_as(L.ip), conv.ctypes.data_as(L.ip), wall.ctypes.data_as(L.dp),
+                          trr.ctypes.data_as(L.dp), ritz.ctypes.data_as(L.dp), len(ritz))
+        check(lib.rcg_seq_run(self.h, k, _ptr(B), _ptr(X), C.byref(cfg), C.byref(rep)))
+        return dict(iterations=its.tolist(), converged=[bool(c) for c in conv], wall_time=wall.tolist(),
+                    true_relres=trr.tolist(), m_bar=rep.m_bar, m_tilde=rep.m_tilde,
+                    ritz_values=ritz[:min(rep.m_bar, len(ritz))].copy(), theta_used=rep.theta_used,
+                    w_build_time=rep.w_build_time, avg_iterations=rep.avg_iterations,
+                    avg_wall_time=rep.avg_wall_time, setup_time=rep.setup_time,
+                    acceleration_inactive=bool(rep.acceleration_inactive))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.rcg_seq_destroy(self.h)
+            self.h = None

@@ -1,0 +1,74 @@
+"""The device sequence driver (rcg_seq_prepare / rcg_seq_run, run_sequence driver.cpp:108-222)
+against the oracle's sequence (pinned to the reference): same m_bar / m_tilde, Ritz values,
+iterations +-2 per solve, solutions and true relative residuals in the original scaling."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from oracle import Matrix
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+@pytest.mark.parametrize("method", ["sc", "deflation"])
+@pytest.mark.parametrize("batch", [True, False])
+def test_device_sequence_matches_oracle(ctx, oracle, problems, name, method, batch):
+    from oracle.sequence import rhs_set, run_sequence as oracle_sequence
+    from paper_2203_08498_b200 import api
+
+    cfg = replace(problems.SMALL[name], method=method, n_rhs=5)
+    h = problems.generate(cfg)
+    ores = oracle_sequence(oracle, cfg, h)
+    a_o = Matrix.of(h)
+    _, dis = oracle.diagonal_scale(a_o)
+    b_orig, _ = rhs_set(oracle, cfg, h, a_o, dis)
+    B = np.stack(b_orig)
+    X = np.zeros_like(B)
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+    seq = api.Sequence(ctx, a, "es-sc-iccg" if method == "sc" else "es-d-iccg")
+    rep = seq.run(B, X, cfg.eps, cfg.max_iter, "A", cfg.sampler_m, keep_count=cfg.keep, batch=batch)
+    assert rep["m_bar"] == ores["m_bar"] and rep["m_tilde"] == ores["m_tilde"]
+    rv = np.asarray(ores["ritz_values"])[:rep["m_bar"]]
+    assert np.max(np.abs(rep["ritz_values"] - rv) / np.maximum(np.abs(rv), 1e-300)) <= 1e-6
+    for k in range(cfg.n_rhs):
+        assert rep["converged"][k]
+        assert abs(rep["iterations"][k] - ores["iterations"][k]) <= 2, (k, rep["iterations"], ores["iterations"])
+        assert rep["true_relres"][k] <= 10 * cfg.eps * 1e3 and abs(rep["true_relres"][k] - ores["true_relres"][k]) <= 1e-6
+        xo = dis * ores["solutions"][k]
+        assert np.linalg.norm(X[k] - xo) <= 1e-5 * np.linalg.norm(xo)
+
+
+def test_device_sequence_plain_methods(ctx, oracle, problems):
+    from oracle.sequence import rhs_set
+    from paper_2203_08498_b200 import api
+
+    cfg = replace(problems.SMALL["c1"], n_rhs=3)
+    h = problems.generate(cfg)
+    a_o = Matrix.of(h)
+    sa, dis = oracle.diagonal_scale(a_o)
+    b_orig, bs = rhs_set(oracle, cfg, h, a_o, dis)
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+    for method, kind in (("iccg", 1), ("cg", 0)):
+        X = np.zeros((3, h.n))
+        rep = api.Sequence(ctx, a, method).run(np.stack(b_orig), X, cfg.eps, cfg.max_iter)
+        assert rep["m_tilde"] == 0 and not rep["acceleration_inactive"]
+        f = oracle.ic0_factorize(sa) if kind == 1 else None
+        for k in range(3):
+            xo = np.zeros(h.n)
+            ro = oracle.pcg_solve(sa, bs[k], xo, kind=kind, ic=f, max_iter=cfg.max_iter)
+            assert abs(rep["iterations"][k] - ro.iterations) <= 2
+
+
+def test_device_sequence_config_errors(ctx, problems):
+    from paper_2203_08498_b200 import api
+    from paper_2203_08498_b200._lib import ParseError
+
+    h = problems.generate(problems.SMALL["c1"])
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+    with pytest.raises(ParseError):
+        api.Sequence(ctx, a, "gmres")
+    seq = api.Sequence(ctx, a, "iccg")
+    with pytest.raises(ParseError):
+        seq.run(np.zeros((2, h.n)), np.zeros((2, h.n)), eps=2.0)
