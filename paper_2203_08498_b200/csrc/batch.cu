@@ -158,76 +158,24 @@ __global__ void k_b_scatter(const double* __restrict__ in, int R, int64_t ldc, d
 // lane per row, RT interleaved vectors (each result bitwise the single-vector spmv)
 template <int RT, class Body>
 __device__ __forceinline__ void bspmv_rows(const SpmvArgs& a, const double* __restrict__ x, int cap, Body&& body) {
-    extern __shared__ __align__(16) unsigned char pipe_smem[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned char* base = pipe_smem + static_cast<size_t>(wid) * (16 + 2 * cap * 12);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base);
-    double* sv = reinterpret_cast<double*>(base + 16);
-    int32_t* sc = reinterpret_cast<int32_t*>(base + 16 + 2 * cap * 8);
-    if (lane == 0) {
-        mbar_init(&bar[0]);
-        mbar_init(&bar[1]);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    const int ntiles = (a.n + 31) / 32;
-    const int nw = gridDim.x * kPipeWarps;
-    unsigned phase[2] = {0u, 0u};
-    auto issue = [&](int t, int stg) -> bool {
-        const int32_t r0 = t * 32, rend = min(r0 + 32, a.n);
-        const int32_t e0a = __ldg(a.rs + r0) & ~3;
-        const int32_t e1a = (__ldg(a.rs + rend) + 3) & ~3;
-        const int cnt = e1a - e0a;
-        if (cnt > cap) return false;
-        if (lane == 0) {
-            fence_proxy_async();
-            mbar_expect_tx(&bar[stg], static_cast<unsigned>(cnt) * 12u);
-            if (cnt > 0) {
-                bulk_g2s(sv + stg * cap, a.va + e0a, static_cast<unsigned>(cnt) * 8u, &bar[stg]);
-                bulk_g2s(sc + stg * cap, a.ci + e0a, static_cast<unsigned>(cnt) * 4u, &bar[stg]);
-            }
-        }
-        return true;
-    };
-    int t = blockIdx.x * kPipeWarps + wid;
-    int stg = 0;
-    bool bulk_cur = t < ntiles ? issue(t, 0) : false;
-    for (; t < ntiles; t += nw) {
-        const int tn = t + nw;
-        const bool bulk_next = tn < ntiles ? issue(tn, stg ^ 1) : false;
-        const int32_t r0 = t * 32, row = r0 + lane, rend = min(r0 + 32, a.n);
-        const int32_t e1 = __ldg(a.rs + rend);
-        const int32_t my_b = row < a.n ? __ldg(a.rs + row) : e1;
-        const int32_t my_e = row < a.n ? __ldg(a.rs + row + 1) : e1;
-        double acc[RT];
+    csr_tiles(a.rs, a.ci, a.va, a.n, cap,
+              [&](int32_t r0, int32_t my_b, int32_t my_e, const double* vsrc, const int32_t* csrc, int32_t off) {
+                  const int32_t row = r0 + (threadIdx.x & 31);
+                  double acc[RT];
 #pragma unroll
-        for (int v = 0; v < RT; ++v) acc[v] = 0.0;
-        const double* vsrc = a.va;
-        const int32_t* csrc = a.ci;
-        int32_t off = 0;
-        if (bulk_cur) {
-            while (!mbar_try_wait(&bar[stg], phase[stg])) {
-            }
-            phase[stg] ^= 1u;
-            vsrc = sv + stg * cap;
-            csrc = sc + stg * cap;
-            off = __ldg(a.rs + r0) & ~3;
-        }
-        for (int32_t e = my_b; e < my_e; ++e) {
-            const double av = vsrc[e - off];
-            const double2* xv = reinterpret_cast<const double2*>(x + static_cast<int64_t>(csrc[e - off]) * RT);
+                  for (int v = 0; v < RT; ++v) acc[v] = 0.0;
+                  for (int32_t e = my_b; e < my_e; ++e) {
+                      const double av = vsrc[e - off];
+                      const double2* xv = reinterpret_cast<const double2*>(x + static_cast<int64_t>(csrc[e - off]) * RT);
 #pragma unroll
-            for (int v = 0; v < RT / 2; ++v) {
-                const double2 xx = __ldg(xv + v);
-                acc[2 * v] = fadd_mul(acc[2 * v], av, xx.x);
-                acc[2 * v + 1] = fadd_mul(acc[2 * v + 1], av, xx.y);
-            }
-        }
-        if (row < a.n) body(row, acc);
-        __syncwarp();
-        stg ^= 1;
-        bulk_cur = bulk_next;
-    }
+                      for (int v = 0; v < RT / 2; ++v) {
+                          const double2 xx = __ldg(xv + v);
+                          acc[2 * v] = fadd_mul(acc[2 * v], av, xx.x);
+                          acc[2 * v + 1] = fadd_mul(acc[2 * v + 1], av, xx.y);
+                      }
+                  }
+                  if (row < a.n) body(row, acc);
+              });
 }
 
 __device__ __forceinline__ void ldg4(const double* p, double* v) {
@@ -242,86 +190,38 @@ __device__ __forceinline__ void ldg4(const double* p, double* v) {
 template <int RT, class Body>
 __device__ __forceinline__ void bspmv_chunks(const SpmvArgs& a, const double* __restrict__ x, int cap, Body&& body) {
     constexpr int G = RT / 4;
-    extern __shared__ __align__(16) unsigned char pipe_smem[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned char* base = pipe_smem + static_cast<size_t>(wid) * (16 + 2 * cap * 12);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base);
-    double* sv = reinterpret_cast<double*>(base + 16);
-    int32_t* sc = reinterpret_cast<int32_t*>(base + 16 + 2 * cap * 8);
-    if (lane == 0) {
-        mbar_init(&bar[0]);
-        mbar_init(&bar[1]);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    const int ntiles = (a.n + 31) / 32;
-    const int nw = gridDim.x * kPipeWarps;
-    unsigned phase[2] = {0u, 0u};
-    auto issue = [&](int t, int stg) -> bool {
-        const int32_t r0 = t * 32, rend = min(r0 + 32, a.n);
-        const int32_t e0a = __ldg(a.rs + r0) & ~3;
-        const int32_t e1a = (__ldg(a.rs + rend) + 3) & ~3;
-        const int cnt = e1a - e0a;
-        if (cnt > cap) return false;
-        if (lane == 0) {
-            fence_proxy_async();
-            mbar_expect_tx(&bar[stg], static_cast<unsigned>(cnt) * 12u);
-            if (cnt > 0) {
-                bulk_g2s(sv + stg * cap, a.va + e0a, static_cast<unsigned>(cnt) * 8u, &bar[stg]);
-                bulk_g2s(sc + stg * cap, a.ci + e0a, static_cast<unsigned>(cnt) * 4u, &bar[stg]);
-            }
-        }
-        return true;
-    };
-    int t = blockIdx.x * kPipeWarps + wid;
-    int stg = 0;
-    bool bulk_cur = t < ntiles ? issue(t, 0) : false;
-    for (; t < ntiles; t += nw) {
-        const int tn = t + nw;
-        const bool bulk_next = tn < ntiles ? issue(tn, stg ^ 1) : false;
-        const int32_t r0 = t * 32;
-        const double* vsrc = a.va;
-        const int32_t* csrc = a.ci;
-        int32_t off = 0;
-        if (bulk_cur) {
-            while (!mbar_try_wait(&bar[stg], phase[stg])) {
-            }
-            phase[stg] ^= 1u;
-            vsrc = sv + stg * cap;
-            csrc = sc + stg * cap;
-            off = __ldg(a.rs + r0) & ~3;
-        }
+    const int lane = threadIdx.x & 31;
+    csr_tiles(a.rs, a.ci, a.va, a.n, cap,
+              [&](int32_t r0, int32_t my_b, int32_t my_e, const double* vsrc, const int32_t* csrc, int32_t off) {
 #pragma unroll
-        for (int pass = 0; pass < G; ++pass) {
-            const int item = pass * 32 + lane;
-            const int32_t row = r0 + item / G;
-            const int c = item % G;
-            if (row < a.n) {
-                const int32_t b = __ldg(a.rs + row), e = __ldg(a.rs + row + 1);
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                int32_t k = b;
-                for (; k + 1 < e; k += 2) {
-                    const double a0 = vsrc[k - off], a1 = vsrc[k + 1 - off];
-                    double x0[4], x1[4];
-                    ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
-                    ldg4(x + static_cast<int64_t>(csrc[k + 1 - off]) * RT + 4 * c, x1);
+                  for (int pass = 0; pass < G; ++pass) {
+                      const int item = pass * 32 + lane;
+                      const int32_t row = r0 + item / G;
+                      const int c = item % G;
+                      const int32_t b = __shfl_sync(0xffffffffu, my_b, item / G);
+                      const int32_t e = __shfl_sync(0xffffffffu, my_e, item / G);
+                      if (row < a.n) {
+                          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                          int32_t k = b;
+                          for (; k + 1 < e; k += 2) {
+                              const double a0 = vsrc[k - off], a1 = vsrc[k + 1 - off];
+                              double x0[4], x1[4];
+                              ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
+                              ldg4(x + static_cast<int64_t>(csrc[k + 1 - off]) * RT + 4 * c, x1);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(fadd_mul(acc[i], a0, x0[i]), a1, x1[i]);
-                }
-                if (k < e) {
-                    const double a0 = vsrc[k - off];
-                    double x0[4];
-                    ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
+                              for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(fadd_mul(acc[i], a0, x0[i]), a1, x1[i]);
+                          }
+                          if (k < e) {
+                              const double a0 = vsrc[k - off];
+                              double x0[4];
+                              ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(acc[i], a0, x0[i]);
-                }
-                body(row, c, acc);
-            }
-        }
-        __syncwarp();
-        stg ^= 1;
-        bulk_cur = bulk_next;
-    }
+                              for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(acc[i], a0, x0[i]);
+                          }
+                          body(row, c, acc);
+                      }
+                  }
+              });
 }
 
 // per-thread per-rhs accumulator update for chunk c (c is lane-dependent; unrolled select)
