@@ -164,15 +164,29 @@ __device__ __forceinline__ void bspmv_rows(const SpmvArgs& a, const double* __re
                   double acc[RT];
 #pragma unroll
                   for (int v = 0; v < RT; ++v) acc[v] = 0.0;
-                  for (int32_t e = my_b; e < my_e; ++e) {
-                      const double av = vsrc[e - off];
-                      const double2* xv = reinterpret_cast<const double2*>(x + static_cast<int64_t>(csrc[e - off]) * RT);
+                  // gathers issued eight entries at a time so their latencies overlap
+#pragma unroll 1
+                  for (int32_t e = my_b; e < my_e; e += 8) {
+                      const int m = min(8, my_e - e);
+                      double av[8];
+                      double2 xx[8][RT / 2];
 #pragma unroll
-                      for (int v = 0; v < RT / 2; ++v) {
-                          const double2 xx = __ldg(xv + v);
-                          acc[2 * v] = fadd_mul(acc[2 * v], av, xx.x);
-                          acc[2 * v + 1] = fadd_mul(acc[2 * v + 1], av, xx.y);
-                      }
+                      for (int k = 0; k < 8; ++k)
+                          if (k < m) {
+                              av[k] = vsrc[e - off + k];
+                              const double2* xv =
+                                  reinterpret_cast<const double2*>(x + static_cast<int64_t>(csrc[e - off + k]) * RT);
+#pragma unroll
+                              for (int v = 0; v < RT / 2; ++v) xx[k][v] = __ldg(xv + v);
+                          }
+#pragma unroll
+                      for (int k = 0; k < 8; ++k)
+                          if (k < m)
+#pragma unroll
+                              for (int v = 0; v < RT / 2; ++v) {
+                                  acc[2 * v] = fadd_mul(acc[2 * v], av[k], xx[k][v].x);
+                                  acc[2 * v + 1] = fadd_mul(acc[2 * v + 1], av[k], xx[k][v].y);
+                              }
                   }
                   if (row < a.n) body(row, acc);
               });
@@ -187,13 +201,24 @@ __device__ __forceinline__ void ldg4(const double* p, double* v) {
 // contiguous run) instead of one 16-byte piece per row.  Items of a 32-row tile are (row,
 // chunk) pairs, row-major; every value's sum runs over the row's entries in CSR order, so each
 // result is bitwise the single-vector spmv.  body(row, chunk, acc[4]).
+#ifndef RCG_BGATHER
+#define RCG_BGATHER 4
+#endif
+constexpr int kBGather = RCG_BGATHER;  // x chunks in flight per lane (RT = 4)
+#ifndef RCG_BSPMV_WIDE_BLOCKS
+#define RCG_BSPMV_WIDE_BLOCKS 3
+#endif
+// resident CTAs per SM of the batched SpMV kernels (register cap via __launch_bounds__, and the
+// grid): RT >= 8 measured faster with one more CTA per SM than the single-vector SpMV's two
+constexpr int bspmv_min_blocks(int rt) { return rt >= 8 ? RCG_BSPMV_WIDE_BLOCKS : 2; }
+
 template <int RT, class Body>
 __device__ __forceinline__ void bspmv_chunks(const SpmvArgs& a, const double* __restrict__ x, int cap, Body&& body) {
     constexpr int G = RT / 4;
     const int lane = threadIdx.x & 31;
     csr_tiles(a.rs, a.ci, a.va, a.n, cap,
               [&](int32_t r0, int32_t my_b, int32_t my_e, const double* vsrc, const int32_t* csrc, int32_t off) {
-#pragma unroll
+#pragma unroll 1
                   for (int pass = 0; pass < G; ++pass) {
                       const int item = pass * 32 + lane;
                       const int32_t row = r0 + item / G;
@@ -202,21 +227,43 @@ __device__ __forceinline__ void bspmv_chunks(const SpmvArgs& a, const double* __
                       const int32_t e = __shfl_sync(0xffffffffu, my_e, item / G);
                       if (row < a.n) {
                           double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                          int32_t k = b;
-                          for (; k + 1 < e; k += 2) {
-                              const double a0 = vsrc[k - off], a1 = vsrc[k + 1 - off];
-                              double x0[4], x1[4];
-                              ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
-                              ldg4(x + static_cast<int64_t>(csrc[k + 1 - off]) * RT + 4 * c, x1);
+                          if constexpr (RT <= 4) {
+                              // one chunk per row: gathers issued kBGather entries at a time
+#pragma unroll 1
+                              for (int32_t k = b; k < e; k += kBGather) {
+                                  const int m = min(kBGather, e - k);
+                                  double av[kBGather], xv[kBGather][4];
 #pragma unroll
-                              for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(fadd_mul(acc[i], a0, x0[i]), a1, x1[i]);
-                          }
-                          if (k < e) {
-                              const double a0 = vsrc[k - off];
-                              double x0[4];
-                              ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
+                                  for (int j = 0; j < kBGather; ++j)
+                                      if (j < m) {
+                                          av[j] = vsrc[k + j - off];
+                                          ldg4(x + static_cast<int64_t>(csrc[k + j - off]) * RT + 4 * c, xv[j]);
+                                      }
 #pragma unroll
-                              for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(acc[i], a0, x0[i]);
+                                  for (int j = 0; j < kBGather; ++j)
+                                      if (j < m)
+#pragma unroll
+                                          for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(acc[i], av[j], xv[j][i]);
+                              }
+                          } else {
+                              // wider rows: two gathers in flight keeps the register budget of three CTAs
+                              // per SM (more in flight per lane measured slower than more resident warps)
+                              int32_t k = b;
+                              for (; k + 1 < e; k += 2) {
+                                  const double a0 = vsrc[k - off], a1 = vsrc[k + 1 - off];
+                                  double x0[4], x1[4];
+                                  ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
+                                  ldg4(x + static_cast<int64_t>(csrc[k + 1 - off]) * RT + 4 * c, x1);
+#pragma unroll
+                                  for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(fadd_mul(acc[i], a0, x0[i]), a1, x1[i]);
+                              }
+                              if (k < e) {
+                                  const double a0 = vsrc[k - off];
+                                  double x0[4];
+                                  ldg4(x + static_cast<int64_t>(csrc[k - off]) * RT + 4 * c, x0);
+#pragma unroll
+                                  for (int i = 0; i < 4; ++i) acc[i] = fadd_mul(acc[i], a0, x0[i]);
+                              }
                           }
                           body(row, c, acc);
                       }
@@ -236,7 +283,7 @@ __device__ __forceinline__ void chunk_acc(double (&accs)[RT], int c, F&& f) {
 
 // r = b - A x for all RT; finaliser: bnorm, rho = rr, already-converged / zero-rhs flags
 template <int RT>
-__global__ void __launch_bounds__(kSpmvThreads) k_b_residual(SpmvArgs a, int cap, const double* __restrict__ b,
+__global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_residual(SpmvArgs a, int cap, const double* __restrict__ b,
                                                              const double* __restrict__ x, double* __restrict__ r,
                                                              BState* st, double* partials, int defer_check) {
     __shared__ double scratch[2 * RT * 32];
@@ -727,7 +774,7 @@ __global__ void __launch_bounds__(256) k_b_pupdate(const double* __restrict__ z,
 
 // q = A p (all RT), (p, q) per rhs -> alpha (unless the deflated path projects q first)
 template <int RT>
-__global__ void __launch_bounds__(kSpmvThreads) k_b_spmv_pq(SpmvArgs a, int cap, const double* __restrict__ p,
+__global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_pq(SpmvArgs a, int cap, const double* __restrict__ p,
                                                             double* __restrict__ q, BState* st, double* partials,
                                                             int project_later) {
     __shared__ double scratch[RT * 32];
@@ -1161,9 +1208,9 @@ struct BatchSolve {
         w = &batch_ws(slot, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
         sg = stream_grid(ctx, n);
         pg = spmv_grid(ctx, n);
-        if (RT >= 8) {  // wider rows: one more resident CTA per SM measured faster (RT 12: 272 -> 210 us)
+        if (bspmv_min_blocks(RT) > 2) {  // wider rows: one more resident CTA per SM (RT 12: 272 -> 210 us)
             const int blocks = ((n + 31) / 32 + kPipeWarps - 1) / kPipeWarps;
-            pg = std::max(1, std::min(blocks, ctx->num_sms * (ctx->spmv_bps + 1)));
+            pg = std::max(1, std::min(blocks, ctx->num_sms * (ctx->spmv_bps + bspmv_min_blocks(RT) - 2)));
         }
         eg = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((nrt + kElemThreads * 4 - 1) / (kElemThreads * 4), ctx->num_sms * 8)));
