@@ -87,6 +87,11 @@ class Context:
     def set_profiling(self, on: bool):
         check(lib.rcg_ctx_set_profiling(self.h, 1 if on else 0))
 
+    def set_sweep_kernel(self, mode: int):
+        """IC sweep kernel: 0 grid-wide sync-free, 1 one-cluster level-synchronous whenever it
+        fits, 2 by DAG shape (default).  Results are bitwise identical either way."""
+        check(lib.rcg_ctx_set_sweep_kernel(self.h, int(mode)))
+
     def record(self, slot: int):
         """CUDA event on the library stream (device-side timing)."""
         check(lib.rcg_ctx_event_record(self.h, slot))

@@ -370,6 +370,7 @@ int rcg_ctx_create(int device, rcg_ctx** out) {
         c->num_sms = prop.multiProcessorCount;
         if (const char* e = std::getenv("RCG_SWEEP_BPS")) c->sweep_bps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("RCG_SWEEP_BACKOFF_NS")) c->sweep_backoff_ns = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("RCG_SWEEP_CLUSTER")) c->sweep_cluster = std::atoi(e);
         if (const char* e = std::getenv("RCG_SPMV_BPS")) c->spmv_bps = std::max(1, std::atoi(e));
         RCG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         register_ctx(c, true);
@@ -410,10 +411,21 @@ void rcg_ctx_destroy(rcg_ctx* ctx) {
 }
 
 int rcg_ctx_synchronize(rcg_ctx* ctx) {
-    return guard([&] { RCG_CK(cudaStreamSynchronize(ctx->stream)); });
+    return guard([&] {
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+        static const bool prof = std::getenv("RCG_CL_PROF") != nullptr;  // dev: cluster sweep phases
+        if (prof) cluster_prof_dump("sync");
+    });
 }
 
 int64_t rcg_ctx_launch_count(const rcg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode) {
+    return guard([&] {
+        require(ctx != nullptr && mode >= 0 && mode <= 2, "rcg_ctx_set_sweep_kernel: mode must be 0, 1 or 2");
+        ctx->sweep_cluster = mode;
+    });
+}
 
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable) {
     return guard([&] {
@@ -462,6 +474,11 @@ int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units) {
 
 void rcg_ctx_reset_stats(rcg_ctx* ctx) {
     try {
+        static const bool prof = std::getenv("RCG_CL_PROF") != nullptr;
+        if (prof) {
+            cudaStreamSynchronize(ctx->stream);
+            cluster_prof_dump("reset");
+        }
         resolve_timers(ctx);
     } catch (...) {
     }

@@ -362,7 +362,8 @@ static int32_t levels_device(rcg_ctx* ctx, DevBag& bag, int32_t n, const int32_t
 // perm / prs / pcol / pidx of one sweep from the levels (descending: rows n-1..0 within a level)
 static void schedule_device(rcg_ctx* ctx, DevBag& bag, int32_t n, const int32_t* level, int32_t nlev,
                             const int32_t* rs, const int32_t* col, int64_t nnz, bool descending, int32_t*& perm,
-                            int32_t*& prs, int32_t*& pcol, int32_t*& pidx, int32_t& npos) {
+                            int32_t*& prs, int32_t*& pcol, int32_t*& pidx, int32_t& npos,
+                            std::vector<int32_t>& lptr) {
     const int g = grid_for(ctx, n);
     int32_t* rows = bag.get<int32_t>(n);
     int32_t* rows_s = bag.get<int32_t>(n);
@@ -391,6 +392,8 @@ static void schedule_device(rcg_ctx* ctx, DevBag& bag, int32_t n, const int32_t*
     }
     require(pp < (int64_t(1) << 31), "IC schedule: padded length exceeds int32");
     npos = static_cast<int32_t>(pp);
+    lptr.assign(ps.begin(), ps.end());
+    lptr.push_back(npos);
     int32_t* d_us = bag.get<int32_t>(nlev);
     int32_t* d_ps = bag.get<int32_t>(nlev);
     RCG_CK(cudaMemcpyAsync(d_us, us.data(), sizeof(int32_t) * nlev, cudaMemcpyHostToDevice, ctx->stream));
@@ -477,12 +480,12 @@ static void factorize_device(rcg_ctx* ctx, const rcg_matrix* A, double shift, in
     mark("forward levels");
     int32_t *fidx = nullptr, *bidx = nullptr;
     schedule_device(ctx, bag, n, level, f->fwd_levels, lrs, lcol, nnzl, false, f->f_perm, f->f_prs, f->f_col, fidx,
-                    f->f_npos);
+                    f->f_npos, f->h_lptr[0]);
     mark("forward schedule");
     f->bwd_levels = levels_device(ctx, bag, n, urs, lrs, lcol, level);
     mark("backward levels");
     schedule_device(ctx, bag, n, level, f->bwd_levels, urs, ucol, nnzl, true, f->b_perm, f->b_prs, f->b_col, bidx,
-                    f->b_npos);
+                    f->b_npos, f->h_lptr[1]);
     mark("backward schedule");
     // ---- numeric (device) with the reference shift ladder
     double* lval = bag.get<double>(nnzl);

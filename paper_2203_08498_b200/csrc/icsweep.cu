@@ -210,6 +210,7 @@ void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
         launch_grid_sweep(ctx, f, backward, a);
         return;
     }
+    if (launch_cluster_sweep(ctx, f, backward, a)) return;  // narrow levels: one cluster (icsweep_cl.cu)
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
     const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
@@ -280,7 +281,8 @@ static T* upload(rcg_ctx* ctx, const std::vector<T>& h) {
 int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vector<int32_t>& col,
                               const std::vector<double>& val, bool descending, std::vector<int32_t>& perm,
                               std::vector<int32_t>& prs, std::vector<int32_t>& pcol, std::vector<double>& pval,
-                              int32_t& npos, std::vector<int32_t>* pidx = nullptr) {
+                              int32_t& npos, std::vector<int32_t>* pidx = nullptr,
+                              std::vector<int32_t>* lptr = nullptr) {
     std::vector<int32_t> level(n, 0);
     int32_t nlev = 0;
     for (int32_t t = 0; t < n; ++t) {
@@ -298,6 +300,7 @@ int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vec
     const int64_t total = start[nlev];
     require(total < (1LL << 31), "IC schedule: padded length exceeds int32");
     npos = static_cast<int32_t>(total);
+    if (lptr) lptr->assign(start.begin(), start.end());
     perm.assign(total, -1);
     for (int32_t t = 0; t < n; ++t) {
         const int32_t i = descending ? n - 1 - t : t;
@@ -325,13 +328,15 @@ int32_t build_schedule(int32_t n, const std::vector<int32_t>& rs, const std::vec
 static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
     std::vector<int32_t> perm, prs, pcol;
     std::vector<double> pval;
-    f->fwd_levels = build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval, f->f_npos);
+    f->fwd_levels = build_schedule(f->n, f->h_lrs, f->h_lcol, f->h_lval, false, perm, prs, pcol, pval, f->f_npos,
+                                   nullptr, &f->h_lptr[0]);
     f->f_perm = upload(ctx, perm);
     f->f_prs = upload(ctx, prs);
     f->f_col = upload(ctx, pcol);
     f->f_val = upload(ctx, pval);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    f->bwd_levels = build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval, f->b_npos);
+    f->bwd_levels = build_schedule(f->n, f->h_urs, f->h_ucol, f->h_uval, true, perm, prs, pcol, pval, f->b_npos,
+                                   nullptr, &f->h_lptr[1]);
     f->b_perm = upload(ctx, perm);
     f->b_prs = upload(ctx, prs);
     f->b_col = upload(ctx, pcol);
@@ -497,6 +502,7 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
+    free_cluster_plans(f);
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
                     (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->grid.tile_xy,
                     (void*)f->grid.coef[0], (void*)f->grid.coef[1], (void*)f->grid.mask[0], (void*)f->grid.mask[1]})

@@ -140,6 +140,7 @@ struct Workspace {
 };
 
 struct BatchWs;  // batch.cu
+struct ClusterPlan;  // icsweep_cl.cu
 
 }  // namespace rcg
 
@@ -168,6 +169,7 @@ struct rcg_ctx {
     cudaEvent_t user_ev[16] = {};
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
+    int sweep_cluster = 2;      // IC sweep kernel: 0 grid, 1 cluster when it fits, 2 by shape
     int spmv_bps = 2;           // SpMV CTAs per SM (RCG_SPMV_BPS): leaves room for concurrent solves
     rcg::BatchWs* bws = nullptr;   // multi-RHS workspaces (batch.cu): a compacted phase
     rcg::BatchWs* bws2 = nullptr;  // reads one and writes the other
@@ -212,6 +214,10 @@ struct rcg_ic {
     double* b_val = nullptr;
     double* d = nullptr;
     GridSched grid;
+    // level starts of the padded schedules ([0] forward, [1] backward; nlev + 1 entries) and the
+    // lazily built cluster-sweep plans (icsweep_cl.cu)
+    std::vector<int32_t> h_lptr[2];
+    mutable rcg::ClusterPlan* cl[2] = {nullptr, nullptr};
 };
 
 struct rcg_tall {

@@ -1,0 +1,107 @@
+"""The one-cluster level-synchronous IC sweep (csrc/icsweep_cl.cu) against the grid-wide
+sync-free sweep (csrc/icsweep.cu) and the oracle: the sweep output, the (r, z) reduction and whole
+PCG / SC-PCG solves must be BITWISE identical whichever kernel runs (the kernel choice never
+changes an iterate), and both equal the reference ic_apply (src/ic_preconditioner.cpp:123-144)."""
+import numpy as np
+import pytest
+
+from oracle import Matrix
+
+pytestmark = pytest.mark.gpu
+
+GRID, CLUSTER, AUTO = 0, 1, 2
+
+
+@pytest.fixture
+def modes(ctx):
+    yield ctx
+    ctx.set_sweep_kernel(AUTO)
+
+
+def _scaled(ctx, h):
+    from paper_2203_08498_b200 import api
+
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+    return api.diagonal_scale(ctx, a)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "lap1d"])
+def test_cluster_sweep_bitwise(modes, oracle, problems, name):
+    from paper_2203_08498_b200 import api
+
+    ctx = modes
+    if name == "lap1d":  # a chain: n levels of one row (every level narrower than a warp)
+        n = 300
+        rs = np.concatenate([[0], np.cumsum([2 if i in (0, n - 1) else 3 for i in range(n)])]).astype(np.int32)
+        ci, va = [], []
+        for i in range(n):
+            for j in (i - 1, i, i + 1):
+                if 0 <= j < n:
+                    ci.append(j), va.append(2.0 if j == i else -1.0)
+        h = problems.HostCsr(n, rs, np.array(ci, np.int32), np.array(va))
+    else:
+        h = problems.generate(problems.SMALL[name])
+    sa, _ = _scaled(ctx, h)
+    f = api.IcFactor.factorize_device(ctx, sa)
+    a_o, _ = oracle.diagonal_scale(Matrix.of(h))
+    want = oracle.ic_apply(oracle.ic0_factorize(a_o), oracle.uniform_pm1(5, 0, h.n))
+    r = oracle.uniform_pm1(5, 0, h.n)
+    outs = {}
+    for mode in (GRID, CLUSTER):
+        ctx.set_sweep_kernel(mode)
+        outs[mode] = f.apply(r)
+    assert np.array_equal(outs[GRID], want)
+    assert np.array_equal(outs[CLUSTER], want)
+
+
+@pytest.mark.parametrize("method", ["ic", "sc"])
+def test_cluster_sweep_solves_bitwise(modes, problems, method):
+    """IC-PCG (rho from the backward sweep's fused reduction) and SC-PCG on C1: identical
+    iterates, histories and solutions under both kernels."""
+    from paper_2203_08498_b200 import api, sequence
+
+    ctx = modes
+    cfg = problems.CONFIGS["c1"]
+    h = problems.generate(cfg)
+    p = sequence.prepare(ctx, cfg, h, validate=False)
+    b = sequence.rhs(p, 0)[1]
+    res = {}
+    for mode in (GRID, CLUSTER):
+        ctx.set_sweep_kernel(mode)
+        if method == "ic":
+            x = np.zeros(h.n)
+            rep = api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x, cfg.eps, cfg.max_iter)
+        else:
+            s = api.SamplerState.method_a(ctx, cfg.sampler_m, cfg.max_iter, h.n)
+            x0 = np.zeros(h.n)
+            api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x0, cfg.eps, cfg.max_iter, observer=s)
+            _, _, _, w = api.build_aux_matrix(ctx, p.a, api.harvest_errors(ctx, x0, s), 1e-3, keep_count=cfg.keep)
+            basis = api.Basis(ctx, p.a, w, "sc")
+            x = np.zeros(h.n)
+            rep = api.pcg_solve(ctx, p.a, sequence.rhs(p, 1)[1], api.Sc(basis, p.ic), x, cfg.eps, cfg.max_iter)
+        res[mode] = (rep.iterations, np.array(rep.history), x.copy())
+    assert res[GRID][0] == res[CLUSTER][0]
+    assert np.array_equal(res[GRID][1], res[CLUSTER][1])
+    assert np.array_equal(res[GRID][2], res[CLUSTER][2])
+
+
+def test_cluster_sweep_c2_full(modes, problems):
+    """The bench matrix (C2, 382 levels): sweep output bitwise across kernels and an ICCG
+    window with identical histories."""
+    from paper_2203_08498_b200 import api, sequence
+
+    ctx = modes
+    cfg = problems.CONFIGS["c2"]
+    h = problems.generate(cfg)
+    p = sequence.prepare(ctx, cfg, h, validate=False)
+    r = problems.uniform_pm1(9, 0, h.n)
+    b = sequence.rhs(p, 0)[1]
+    outs = {}
+    for mode in (GRID, CLUSTER):
+        ctx.set_sweep_kernel(mode)
+        z = p.ic.apply(r)
+        x = np.zeros(h.n)
+        rep = api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x, cfg.eps, 40)
+        outs[mode] = (z, np.array(rep.history), x)
+    for k in range(3):
+        assert np.array_equal(outs[GRID][k], outs[CLUSTER][k])
