@@ -329,6 +329,23 @@ void rcg_dbasis_destroy(rcg_dbasis* b);
  * iteration the m-vector W^T q (or W^T r) is allreduced before the replicated Cholesky solve. */
 int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
                    double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report);
+/* solve 1 of the sequence over slabs: rcg_dist_pcg_solve with the error-sampling observer
+ * (pcg.cpp:88 + sampling.cpp:66-78): observers[s] = slab s's sampler (rcg_sampler_create with
+ * n = the slab's local rows, identical method / m / cap on every slab).  Every slab schedules the
+ * same iterations (the scalars are allreduced) and snapshots its own rows of x. */
+int rcg_dist_pcg_solve_sampled(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, rcg_sampler* const* observers,
+                               const double* const* b, double* const* x, const rcg_solver_config* cfg,
+                               rcg_solve_report* report);
+/* the recycling step over slabs -- harvest_errors + build_aux_matrix + ScPreconditioner /
+ * build_deflation_operator (recycling.cpp:17-96, deflation.cpp:45-76): errors x_final - slot per
+ * slab (exactly-zero columns skipped globally), MGS with allreduced dots (same drop rule), A Q by
+ * halo exchange, the allreduced Gram Q^T A Q eigensolved on every rank, Ritz values below theta
+ * (or the keep_count smallest, keep_count > 0), W = Q T_sel per slab -> *out (kind
+ * RCG_BASIS_DEFLATION or RCG_BASIS_SC; null when nothing is selected).  values receives the m_bar
+ * Ritz values (ascending; caller sizes it to the sampler's m). */
+int rcg_dist_recycle(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, rcg_sampler* const* samplers,
+                     const double* const* x_final, double theta, int keep_count, int kind, int* m_bar, double* values,
+                     double* theta_used, int* m_tilde, rcg_dbasis** out);
 
 /* ------------------------------------------------------------------ the sequence (driver.cpp)
  * run_sequence (driver.cpp:108-222) on the device: rcg_seq_prepare scales A and factors IC(0)

@@ -740,6 +740,48 @@ def dist_solve(comm: Comm, slabs, bs, xs, basis: Optional[DBasis] = None, eps: f
     return _finish(rep, bufs)
 
 
+def dist_pcg_solve_sampled(comm: Comm, slabs, samplers, bs, xs, eps: float = 1e-8,
+                           max_iter: int = 1000) -> SolveReport:
+    """Solve 1 of the sequence over row slabs (rcg_dist_pcg_solve_sampled): block-Jacobi PCG with
+    the error-sampling observer; samplers[s] = slab s's SamplerState (n = its local rows)."""
+    slabs = list(slabs)
+    ns = len(slabs)
+    bs = [_f64(b, s_.plan.nloc, "b") for b, s_ in zip(bs, slabs)]
+    hs = (C.c_void_p * ns)(*[s_.h.value for s_ in slabs])
+    sp = (C.c_void_p * ns)(*[o.h.value for o in samplers])
+    bp = (C.c_void_p * ns)(*[_ptr(b) for b in bs])
+    xp = (C.c_void_p * ns)(*[_ptr(x) for x in xs])
+    cfg = _cfg(eps, max_iter)
+    rep, bufs = _report(max(1, int(max_iter)))
+    check(lib.rcg_dist_pcg_solve_sampled(comm.h, ns, hs, sp, bp, xp, C.byref(cfg), C.byref(rep)))
+    return _finish(rep, bufs)
+
+
+def dist_recycle(comm: Comm, slabs, samplers, xs_final, theta: float = float("inf"), keep_count: int = 0,
+                 kind: str = "deflation"):
+    """The recycling step over row slabs (rcg_dist_recycle): harvest_errors + build_aux_matrix +
+    the distributed deflation / SC state.  Returns (m_bar, ritz_values, theta_used, m_tilde,
+    DBasis or None)."""
+    slabs = list(slabs)
+    ns = len(slabs)
+    hs = (C.c_void_p * ns)(*[s_.h.value for s_ in slabs])
+    sp = (C.c_void_p * ns)(*[o.h.value for o in samplers])
+    xs = [_f64(x, s_.plan.nloc, "x_final") for x, s_ in zip(xs_final, slabs)]
+    xp = (C.c_void_p * ns)(*[_ptr(x) for x in xs])
+    m_bar, m_tilde = C.c_int(), C.c_int()
+    th = C.c_double()
+    vals = np.zeros(max(1, max(o.m for o in samplers)))
+    h = C.c_void_p()
+    check(lib.rcg_dist_recycle(comm.h, ns, hs, sp, xp, float(theta), int(keep_count),
+                               L.RCG_BASIS_SC if kind == "sc" else L.RCG_BASIS_DEFLATION, C.byref(m_bar), _ptr(vals),
+                               C.byref(th), C.byref(m_tilde), C.byref(h)))
+    basis = None
+    if h.value:
+        basis = DBasis.__new__(DBasis)
+        basis.h, basis.kind, basis.slabs, basis.m, basis._cols = h, kind, slabs, m_tilde.value, None
+    return m_bar.value, vals[: m_bar.value].copy(), th.value, m_tilde.value, basis
+
+
 # --------------------------------------------------------------------------- the sequence driver
 _METHODS = {"cg": L.RCG_METHOD_CG, "iccg": L.RCG_METHOD_ICCG, "es-sc-iccg": L.RCG_METHOD_ES_SC_ICCG,
             "es-d-iccg": L.RCG_METHOD_ES_D_ICCG}

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <vector>
 
 #include "internal.cuh"
@@ -218,6 +219,61 @@ __global__ void __launch_bounds__(kStreamThreads) k_d_xr(double* __restrict__ x,
     block_sum<1>(acc, red);
     if (grid_reduce<1>(acc, partials, blockIdx.x, gridDim.x, &st->tick[kDistTick], tot, red) && threadIdx.x == 0)
         dsum[0] = tot[0];
+}
+
+// the error sampler after iteration st->iters (sampling.cpp:7-84): identical scalars on every
+// slab, so every slab schedules the same slots; converged iterations offer nothing (the observer
+// runs after the convergence test, pcg.cpp:81-88); an iteration that did not complete
+// (breakdown, or the solve already over) schedules nothing
+__global__ void k_d_sched(DevState* st, int* pending, int* occupied, int* stored_iter, const double* thresholds) {
+    if (st->smp_method < 0) return;
+    const int i = st->iters;
+    if (i == 0 || i == st->smp_pending_iter) {
+        st->smp_npending = 0;
+        return;
+    }
+    if (st->done == kConverged || st->done == kBroken) {
+        st->smp_npending = 0;
+        st->smp_pending_iter = i;
+        return;
+    }
+    smp_schedule(st, i, st->relres, pending, occupied, stored_iter, thresholds);
+}
+
+// copy this iteration's payload (x, or r) into the scheduled slots (local rows)
+__global__ void __launch_bounds__(kStreamThreads) k_d_sample(const double* __restrict__ x, const double* __restrict__ r,
+                                                             double* __restrict__ slots, int64_t ld,
+                                                             const int* __restrict__ pending, const DevState* st,
+                                                             int32_t n) {
+    const int np = st->smp_npending;
+    if (np == 0) return;
+    const double* src = st->smp_payload ? r : x;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double v = src[i];
+        for (int k = 0; k < np; ++k) slots[pending[k] * ld + i] = v;
+    }
+}
+
+// (u, v) over the local rows into *out (deterministic two-level reduction; no solver state)
+__global__ void __launch_bounds__(kStreamThreads) k_rr_dot(const double* __restrict__ u, const double* __restrict__ v,
+                                                           int32_t n, double* partials, unsigned int* tick,
+                                                           double* out) {
+    __shared__ double red[32];
+    __shared__ double tot[1];
+    double acc[1] = {0.0};
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        acc[0] = fadd_mul(acc[0], u[i], v[i]);
+    block_sum<1>(acc, red);
+    if (grid_reduce<1>(acc, partials, blockIdx.x, gridDim.x, tick, tot, red) && threadIdx.x == 0) *out = tot[0];
+}
+
+// w -= c q with c the allreduced (q, w) (the MGS update, dense.cpp:52-54); scale: w /= sqrt(c)
+__global__ void __launch_bounds__(kStreamThreads) k_rr_axpy(double* __restrict__ w, const double* __restrict__ q,
+                                                            const double* __restrict__ c, int32_t n, int scale) {
+    const double cv = *c;
+    const double nr = scale ? sqrt(cv) : 0.0;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        w[i] = scale ? __ddiv_rn(w[i], nr) : fsub_mul(w[i], cv, q[i]);
 }
 
 __global__ void k_d_pack(const double* __restrict__ v, const int32_t* __restrict__ idx, int32_t cnt,
@@ -526,6 +582,7 @@ struct DistSolve {
     const rcg_dbasis* defl = nullptr;  // deflated PCG (pcg.cpp:94-160)
     const rcg_dbasis* sc = nullptr;    // subspace correction around the block IC (subspace_correction.cpp)
     bool ic = false;
+    rcg_sampler* const* smp = nullptr;   // error sampler per slab (solve 1 of the sequence), or null
     std::vector<Staged> bst, xst;
     std::vector<double*> bdev;
 
@@ -553,7 +610,7 @@ struct DistSolve {
             const int64_t ntiles = ic ? sweep_tiles(d->ic) : (n + kSweepThreads - 1) / kSweepThreads;
             const int64_t ngroups = (ntiles + kGroup - 1) / kGroup;
             const int64_t red = std::max<int64_t>(ntiles, static_cast<int64_t>(kMaxRed) * ctx->num_sms * 8);
-            ensure_workspace(ctx, std::max(n, 1), std::max(m, 1), max_iter, red, ngroups, 1);
+            ensure_workspace(ctx, std::max(n, 1), std::max(m, 1), max_iter, red, ngroups, smp ? smp[s]->m : 1);
             ensure_g(d, std::max(m * m, 128));
             stage_in(ctx, b[s], n, bst[s]);
             bdev[s] = bst[s].dev;
@@ -566,6 +623,14 @@ struct DistSolve {
             h.max_iter = max_iter;
             h.eps = eps;
             h.smp_method = -1;
+            if (smp) {
+                require(smp[s]->n == n, "dist_pcg_solve: sampler rows do not match the slab");
+                h.smp_method = smp[s]->method;
+                h.smp_m = smp[s]->m;
+                h.smp_lmax = smp[s]->l_max;
+                h.smp_h = smp[s]->h;
+                h.smp_next = smp[s]->next_slot;
+            }
             std::memcpy(ctx->host_pinned, &h, sizeof(h));
             RCG_CK(cudaMemcpyAsync(ctx->ws.st, ctx->host_pinned, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
             if (ic) {
@@ -709,6 +774,19 @@ struct DistSolve {
         }
         comm->allreduce(sl, ns, 1);
         scalar(3);
+        if (smp) {  // the observer (sampling.cpp error_sampling_observer): schedule + snapshot
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                rcg_ctx* ctx = d->ctx;
+                rcg_sampler* sp = smp[s];
+                k_d_sched<<<1, 1, 0, ctx->stream>>>(ctx->ws.st, ctx->ws.smp_pending, sp->occupied, sp->stored_iter,
+                                                    sp->thresholds);
+                RCG_LAUNCHED(ctx);
+                k_d_sample<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                    d->xe, ctx->ws.r, sp->slots, sp->ld, ctx->ws.smp_pending, ctx->ws.st, d->nloc);
+                RCG_LAUNCHED(ctx);
+            }
+        }
         if (sc) {  // W^T r for the next apply (subspace_correction.cpp:50-51)
             std::vector<double*> rs(ns);
             for (int s = 0; s < ns; ++s) rs[s] = sl[s]->ctx->ws.r;
@@ -799,6 +877,13 @@ struct DistSolve {
         rcg_ctx* c0 = sl[0]->ctx;
         DevState h{};
         RCG_CK(cudaMemcpy(&h, c0->ws.st, sizeof(DevState), cudaMemcpyDeviceToHost));
+        if (smp)
+            for (int s = 0; s < ns; ++s) {  // the schedule state the sampler carries on (h, next slot)
+                DevState hs{};
+                RCG_CK(cudaMemcpy(&hs, sl[s]->ctx->ws.st, sizeof(DevState), cudaMemcpyDeviceToHost));
+                smp[s]->h = hs.smp_h;
+                smp[s]->next_slot = hs.smp_next;
+            }
         return h;
     }
 };
@@ -864,6 +949,195 @@ static rcg_dbasis* dbasis_create(rcg_comm* comm, int ns, rcg_dslab* const* sl, c
         throw;
     }
     return B;
+}
+
+// The sequence's recycling step over row slabs: harvest_errors (recycling.cpp:17-28)
+// per slab with the exactly-zero-column test made global, single-pass MGS (dense.cpp:45-61) with
+// every dot allreduced (the drop test sees the global norms), A Q by halo exchange + local SpMV,
+// the Gram Q^T A Q allreduced and eigensolved identically on every rank (cyclic Jacobi,
+// dense.cpp:63-144), count / theta selection (recycling.cpp:91-94), Ritz vectors W = Q T_sel per
+// slab, then the distributed deflation / SC state (dbasis_create).  Returns null when no Ritz
+// value is selected (empty W: the accelerated solves are plain block-Jacobi PCG, as the reference).
+static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rcg_sampler* const* smp,
+                                const double* const* xfin, double theta, int keep_count, int kind, int* m_bar,
+                                std::vector<double>& vals, double* theta_used, int* m_tilde) {
+    const int msl = smp[0]->m;
+    std::vector<int> occ(std::max(msl, 1), 0);
+    if (msl) RCG_CK(cudaMemcpy(occ.data(), smp[0]->occupied, sizeof(int) * msl, cudaMemcpyDeviceToHost));
+    std::vector<int> list;
+    for (int j = 0; j < msl; ++j)
+        if (occ[j]) list.push_back(j);
+    const int k0 = static_cast<int>(list.size());
+    struct Loc {
+        double *e = nullptr, *q = nullptr, *aq = nullptr, *w = nullptr, *c = nullptr;
+        int *nz = nullptr, *dl = nullptr;
+        Staged x;
+    };
+    std::vector<Loc> L(ns);
+    auto cleanup = [&] {
+        for (auto& l : L) {
+            for (double* p : {l.e, l.q, l.aq, l.w, l.c}) dev_free(p);
+            dev_free(l.nz);
+            dev_free(l.dl);
+        }
+    };
+    rcg_dbasis* out = nullptr;
+    try {
+        comm->begin(sl, ns);
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            const int32_t n = d->nloc;
+            require(smp[s]->n == n && smp[s]->m == msl, "dist_recycle: samplers do not match the slabs");
+            ensure_workspace(ctx, std::max(n, 1), kMaxRed, 1,
+                             std::max<int64_t>((n + kSweepThreads - 1) / kSweepThreads, int64_t(kMaxRed) * ctx->num_sms * 8),
+                             1, 1);
+            ensure_g(d, std::max({k0 * k0, k0, 128}));
+            stage_in(ctx, xfin[s], n, L[s].x);
+            const int64_t sz = std::max<int64_t>(int64_t(n) * std::max(k0, 1), 1);
+            L[s].e = dev_alloc(sz);
+            L[s].q = dev_alloc(sz);
+            L[s].aq = dev_alloc(sz);
+            L[s].c = dev_alloc(4);
+            L[s].nz = static_cast<int*>(dev_alloc_bytes(sizeof(int) * std::max(k0, 1)));
+            L[s].dl = static_cast<int*>(dev_alloc_bytes(sizeof(int) * std::max(k0, 1)));
+            RCG_CK(cudaMemsetAsync(L[s].nz, 0, sizeof(int) * std::max(k0, 1), ctx->stream));
+            if (k0) {
+                RCG_CK(cudaMemcpyAsync(L[s].dl, list.data(), sizeof(int) * k0, cudaMemcpyHostToDevice, ctx->stream));
+                if (n) {
+                    dim3 grid(stream_grid(ctx, n), std::min(k0, 64));
+                    k_harvest<<<grid, kStreamThreads, 0, ctx->stream>>>(L[s].x.dev, smp[s]->slots, smp[s]->ld, L[s].dl,
+                                                                        k0, 0, L[s].e, n, n, L[s].nz);
+                    RCG_LAUNCHED(ctx);
+                }
+            }
+        }
+        // exactly-zero columns are skipped globally (recycling.cpp:26): sum the per-slab flags
+        std::vector<int> cols;
+        if (k0) {
+            for (int s = 0; s < ns; ++s) {
+                std::vector<int> hz(k0);
+                RCG_CK(cudaMemcpyAsync(hz.data(), L[s].nz, sizeof(int) * k0, cudaMemcpyDeviceToHost, sl[s]->ctx->stream));
+                RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+                std::vector<double> hd(hz.begin(), hz.end());
+                RCG_CK(cudaMemcpy(sl[s]->gbuf, hd.data(), sizeof(double) * k0, cudaMemcpyHostToDevice));
+            }
+            comm->allreduce(sl, ns, k0, 1);
+            for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+            std::vector<double> g(k0);
+            RCG_CK(cudaMemcpy(g.data(), sl[0]->gbuf, sizeof(double) * k0, cudaMemcpyDeviceToHost));
+            for (int j = 0; j < k0; ++j)
+                if (g[j] > 0.0) cols.push_back(j);
+        }
+        // allreduced (u, v) of every slab's local rows -> dsum[0] on every slab; returns the total
+        auto gdot = [&](auto ucol, auto vcol, bool read) {
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                rcg_ctx* ctx = d->ctx;
+                k_rr_dot<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                    ucol(s), vcol(s), d->nloc, ctx->ws.partials, &ctx->ws.st->tick[kDistTick], d->dsum);
+                RCG_LAUNCHED(ctx);
+            }
+            comm->allreduce(sl, ns, 1, 0);
+            double h = 0.0;
+            if (read) {
+                for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+                RCG_CK(cudaMemcpy(&h, sl[0]->dsum, sizeof(double), cudaMemcpyDeviceToHost));
+            }
+            return h;
+        };
+        int kept = 0;
+        for (int src : cols) {
+            auto wcol = [&](int s) { return L[s].q + int64_t(kept) * sl[s]->nloc; };
+            for (int s = 0; s < ns; ++s)
+                if (sl[s]->nloc)
+                    RCG_CK(cudaMemcpyAsync(wcol(s), L[s].e + int64_t(src) * sl[s]->nloc, sizeof(double) * sl[s]->nloc,
+                                           cudaMemcpyDeviceToDevice, sl[s]->ctx->stream));
+            const double n0 = std::sqrt(gdot(wcol, wcol, true));
+            if (n0 == 0.0) continue;
+            for (int qi = 0; qi < kept; ++qi) {
+                auto qcol = [&](int s) { return L[s].q + int64_t(qi) * sl[s]->nloc; };
+                gdot(qcol, wcol, false);
+                for (int s = 0; s < ns; ++s) {
+                    rcg_ctx* ctx = sl[s]->ctx;
+                    k_rr_axpy<<<stream_grid(ctx, sl[s]->nloc), kStreamThreads, 0, ctx->stream>>>(
+                        wcol(s), qcol(s), sl[s]->dsum, sl[s]->nloc, 0);
+                    RCG_LAUNCHED(ctx);
+                }
+            }
+            const double n1 = std::sqrt(gdot(wcol, wcol, true));
+            if (n1 <= 1e-12 * n0) continue;   // numerically dependent, dropped (dense.cpp:56)
+            for (int s = 0; s < ns; ++s) {
+                rcg_ctx* ctx = sl[s]->ctx;
+                k_rr_axpy<<<stream_grid(ctx, sl[s]->nloc), kStreamThreads, 0, ctx->stream>>>(
+                    wcol(s), nullptr, sl[s]->dsum, sl[s]->nloc, 1);
+                RCG_LAUNCHED(ctx);
+            }
+            ++kept;
+        }
+        *m_bar = kept;
+        vals.clear();
+        if (kept == 0) {
+            cleanup();
+            if (theta_used) *theta_used = theta;
+            *m_tilde = 0;
+            return nullptr;
+        }
+        require(kept <= 128, "SmallSym: dimension " + std::to_string(kept) + " outside [0, 128]");
+        // A Q (rayleigh_ritz, recycling.cpp:48-53): halo exchange + local SpMV per column
+        for (int j = 0; j < kept; ++j) {
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                if (d->nloc)
+                    RCG_CK(cudaMemcpyAsync(d->pe, L[s].q + int64_t(j) * d->nloc, sizeof(double) * d->nloc,
+                                           cudaMemcpyDeviceToDevice, d->ctx->stream));
+            }
+            comm->halo(sl, ns, 1);
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                const int rc = rcg_spmv(d->ctx, d->a, d->pe, L[s].aq + int64_t(j) * d->nloc);
+                if (rc != RCG_OK) throw Error(rc, rcg_last_error());
+            }
+        }
+        // S = Q^T A Q, lower triangle allreduced then mirrored, eigensolved on every rank
+        std::vector<double> g;
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            gram_host(d->ctx, L[s].q, d->nloc, kept, L[s].aq, d->nloc, kept, d->nloc, true, g);
+            RCG_CK(cudaMemcpy(d->gbuf, g.data(), sizeof(double) * kept * kept, cudaMemcpyHostToDevice));
+        }
+        comm->allreduce(sl, ns, kept * kept, 1);
+        for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+        g.assign(static_cast<size_t>(kept) * kept, 0.0);
+        RCG_CK(cudaMemcpy(g.data(), sl[0]->gbuf, sizeof(double) * kept * kept, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < kept; ++i)
+            for (int j = 0; j < i; ++j) g[static_cast<size_t>(j) * kept + i] = g[static_cast<size_t>(i) * kept + j];
+        std::vector<double> T;
+        sym_eig_host(kept, g, vals, T);
+        double th = theta;
+        if (keep_count > 0)
+            th = kept > keep_count ? 0.5 * (vals[keep_count - 1] + vals[keep_count]) : std::numeric_limits<double>::infinity();
+        if (theta_used) *theta_used = th;
+        int sel = 0;
+        while (sel < kept && vals[sel] < th) ++sel;
+        *m_tilde = sel;
+        if (sel > 0) {
+            std::vector<const double*> wp(ns);
+            for (int s = 0; s < ns; ++s) {
+                rcg_dslab* d = sl[s];
+                L[s].w = dev_alloc(std::max<int64_t>(int64_t(d->nloc) * sel, 1));
+                combine_cols(d->ctx, L[s].q, d->nloc, kept, T.data(), sel, L[s].w, d->nloc, d->nloc);
+                wp[s] = L[s].w;
+            }
+            for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+            out = dbasis_create(comm, ns, sl, wp.data(), sel, kind);
+        }
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+    return out;
 }
 
 }  // namespace rcg
@@ -1018,8 +1292,9 @@ void rcg_dbasis_destroy(rcg_dbasis* b) {
     delete b;
 }
 
-int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
-                   double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
+static int dist_solve_impl(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis,
+                           rcg_sampler* const* observers, const double* const* b, double* const* x,
+                           const rcg_solver_config* cfg, rcg_solve_report* report) {
     return guard([&] {
         require(comm && slabs && b && x && report, "dist_pcg_solve: null argument");
         require(nslabs == comm->local_slabs(), "dist_pcg_solve: slab count does not match the transport");
@@ -1031,6 +1306,9 @@ int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rc
         }
         if (basis) require(static_cast<int>(basis->w.size()) == nslabs, "dist_pcg_solve: basis built for other slabs");
         DistSolve ds{comm, nslabs, slabs, cfg->max_iter, cfg->eps};
+        if (observers)
+            for (int s = 0; s < nslabs; ++s) require(observers[s] != nullptr, "dist_pcg_solve: null sampler");
+        ds.smp = observers;
         if (basis && basis->kind == RCG_BASIS_DEFLATION) ds.defl = basis;
         if (basis && basis->kind == RCG_BASIS_SC) ds.sc = basis;
         ds.setup(b, x);
@@ -1060,9 +1338,40 @@ int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rc
     });
 }
 
+int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
+                   double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
+    return dist_solve_impl(comm, nslabs, slabs, basis, nullptr, b, x, cfg, report);
+}
+
 int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* b,
                        double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
-    return rcg_dist_solve(comm, nslabs, slabs, nullptr, b, x, cfg, report);
+    return dist_solve_impl(comm, nslabs, slabs, nullptr, nullptr, b, x, cfg, report);
+}
+
+int rcg_dist_pcg_solve_sampled(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, rcg_sampler* const* observers,
+                               const double* const* b, double* const* x, const rcg_solver_config* cfg,
+                               rcg_solve_report* report) {
+    if (!observers) {
+        set_error("dist_pcg_solve_sampled: null samplers");
+        return RCG_E_INVALID;
+    }
+    return dist_solve_impl(comm, nslabs, slabs, nullptr, observers, b, x, cfg, report);
+}
+
+int rcg_dist_recycle(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, rcg_sampler* const* samplers,
+                     const double* const* x_final, double theta, int keep_count, int kind, int* m_bar, double* values,
+                     double* theta_used, int* m_tilde, rcg_dbasis** out) {
+    return guard([&] {
+        require(comm && slabs && samplers && x_final && m_bar && m_tilde && out, "dist_recycle: null argument");
+        require(nslabs == comm->local_slabs(), "dist_recycle: slab count does not match the transport");
+        require(kind == RCG_BASIS_DEFLATION || kind == RCG_BASIS_SC, "dist_recycle: unknown basis kind");
+        for (int s = 0; s < nslabs; ++s) require(slabs[s] && samplers[s] && x_final[s], "dist_recycle: null slab");
+        *out = nullptr;
+        std::vector<double> vals;
+        *out = dist_recycle(comm, nslabs, slabs, samplers, x_final, theta, keep_count, kind, m_bar, vals, theta_used,
+                            m_tilde);
+        if (values && !vals.empty()) std::memcpy(values, vals.data(), sizeof(double) * vals.size());
+    });
 }
 
 }  // extern "C"

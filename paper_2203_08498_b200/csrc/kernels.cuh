@@ -44,6 +44,42 @@ bool grid_sweep_available(const rcg_ic* f);  // icgrid.cu
 void launch_grid_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a);
 
 #ifdef __CUDACC__
+// The error sampler's schedule after iteration i (sampling.cpp:7-78): method A -- every h-th
+// iteration into slot (sum_l (-1)^l floor((i-1)/m^l)) mod m, h doubling at i == h m; method B --
+// every slot whose threshold the relative residual has crossed.  Appends the slots to fill to
+// `pending` (st->smp_npending).
+__device__ __forceinline__ void smp_schedule(DevState* st, int i, double relres, int* pending, int* occupied,
+                                             int* stored_iter, const double* thresholds) {
+    st->smp_npending = 0;
+    st->smp_pending_iter = i;
+    if (st->smp_method == 0) {
+        if (i % st->smp_h != 0) return;
+        long long acc = 0, pw = 1;
+        for (int l = 0; l <= st->smp_lmax; ++l) {
+            const long long term = (i - 1) / pw;
+            acc += (l % 2 == 0) ? term : -term;
+            pw *= st->smp_m;
+        }
+        const int s = static_cast<int>(acc % st->smp_m);
+        pending[st->smp_npending++] = s;
+        occupied[s] = 1;
+        stored_iter[s] = i;
+        if (i == st->smp_h * st->smp_m) st->smp_h *= 2;
+    } else if (st->smp_method == 1) {
+        while (st->smp_next <= st->smp_m) {
+            if (relres > thresholds[st->smp_next - 1]) break;
+            const int s = st->smp_next - 1;
+            pending[st->smp_npending++] = s;
+            occupied[s] = 1;
+            stored_iter[s] = i;
+            st->smp_next++;
+        }
+    }
+}
+__global__ void k_harvest(const double* __restrict__ x, const double* __restrict__ slots, int64_t lds,
+                          const int* __restrict__ list, int cnt, int raw, double* __restrict__ e, int64_t lde,
+                          int32_t n, int* __restrict__ nonzero);  // recycle.cu
+
 // solver.cu kernels reused by the multi-GPU slabs (dist.cu)
 __global__ void __launch_bounds__(kStreamThreads) k_pupdate(const double* __restrict__ z, double* __restrict__ p,
                                                             double* __restrict__ zs_reset, double* __restrict__ y_reset,

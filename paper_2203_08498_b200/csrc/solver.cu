@@ -193,32 +193,7 @@ struct XrArgs {
 };
 
 __device__ void sampler_schedule(XrArgs& a, int i, double relres) {
-    DevState* st = a.st;
-    st->smp_npending = 0;
-    st->smp_pending_iter = i;
-    if (st->smp_method == 0) {
-        if (i % st->smp_h != 0) return;
-        long long acc = 0, pw = 1;
-        for (int l = 0; l <= st->smp_lmax; ++l) {
-            const long long term = (i - 1) / pw;
-            acc += (l % 2 == 0) ? term : -term;
-            pw *= st->smp_m;
-        }
-        const int s = static_cast<int>(acc % st->smp_m);
-        a.pending[st->smp_npending++] = s;
-        a.occupied[s] = 1;
-        a.stored_iter[s] = i;
-        if (i == st->smp_h * st->smp_m) st->smp_h *= 2;
-    } else if (st->smp_method == 1) {
-        while (st->smp_next <= st->smp_m) {
-            if (relres > a.thresholds[st->smp_next - 1]) break;
-            const int s = st->smp_next - 1;
-            a.pending[st->smp_npending++] = s;
-            a.occupied[s] = 1;
-            a.stored_iter[s] = i;
-            st->smp_next++;
-        }
-    }
+    smp_schedule(a.st, i, relres, a.pending, a.occupied, a.stored_iter, a.thresholds);
 }
 
 __global__ void __launch_bounds__(kStreamThreads) k_xr(XrArgs a) {

@@ -50,6 +50,26 @@ class LoopbackSystem:
         """Distributed basis from a global W given as (m, n) (one basis vector per row)."""
         return api.DBasis(self.comm, self.slabs, [w[:, p.row_begin:p.row_end] for p in self.plans], kind)
 
+    def sequence(self, bs, eps: float = 1e-8, max_iter: int = 1000, sampler_m: int = 16, keep: int = 8,
+                 kind: str = "deflation") -> dict:
+        """run_sequence (driver.cpp:108-222) over the slabs on scaled right-hand sides bs (global
+        vectors): solve 1 with the method-A error sampler, the distributed recycling step (count
+        selection of `keep` Ritz vectors), then deflated / SC solves 2..k from x0 = 0."""
+        samplers = [api.SamplerState.method_a(c, sampler_m, max_iter, p.nloc) for c, p in zip(self.ctxs, self.plans)]
+        xs = [np.zeros(p.nloc) for p in self.plans]
+        r1 = api.dist_pcg_solve_sampled(self.comm, self.slabs, samplers, scatter(bs[0], self.plans), xs, eps, max_iter)
+        m_bar, vals, _, m_tilde, basis = api.dist_recycle(self.comm, self.slabs, samplers, xs, keep_count=keep, kind=kind)
+        out = {"iterations": [r1.iterations], "converged": [r1.converged], "solutions": [np.concatenate(xs)],
+               "m_bar": m_bar, "ritz_values": vals, "m_tilde": m_tilde, "histories": [r1.history]}
+        for b in bs[1:]:
+            x = np.zeros(self.n)
+            r = self.solve(b, x, eps, max_iter, basis)
+            out["iterations"].append(r.iterations)
+            out["converged"].append(r.converged)
+            out["solutions"].append(x)
+            out["histories"].append(r.history)
+        return out
+
     def solve(self, b: np.ndarray, x: np.ndarray, eps: float = 1e-8, max_iter: int = 1000,
               basis: Optional[api.DBasis] = None) -> api.SolveReport:
         """Global b, x (x updated in place) split along the slab bounds."""
@@ -91,6 +111,25 @@ class NcclRank:
     def solve(self, b_local, x_local, eps: float = 1e-8, max_iter: int = 1000,
               basis: Optional[api.DBasis] = None) -> api.SolveReport:
         return api.dist_solve(self.comm, [self.slab], [b_local], [x_local], basis, eps, max_iter)
+
+    def sequence(self, bs_local, eps: float = 1e-8, max_iter: int = 1000, sampler_m: int = 16, keep: int = 8,
+                 kind: str = "deflation") -> dict:
+        """run_sequence over the ranks (collective): bs_local = this rank's rows of the scaled
+        right-hand sides; solutions are this rank's rows."""
+        smp = api.SamplerState.method_a(self.ctx, sampler_m, max_iter, self.plan.nloc)
+        x1 = np.zeros(self.plan.nloc)
+        r1 = api.dist_pcg_solve_sampled(self.comm, [self.slab], [smp], [bs_local[0]], [x1], eps, max_iter)
+        m_bar, vals, _, m_tilde, basis = api.dist_recycle(self.comm, [self.slab], [smp], [x1], keep_count=keep,
+                                                           kind=kind)
+        out = {"iterations": [r1.iterations], "converged": [r1.converged], "solutions": [x1], "m_bar": m_bar,
+               "ritz_values": vals, "m_tilde": m_tilde}
+        for b in bs_local[1:]:
+            x = np.zeros(self.plan.nloc)
+            r = self.solve(b, x, eps, max_iter, basis)
+            out["iterations"].append(r.iterations)
+            out["converged"].append(r.converged)
+            out["solutions"].append(x)
+        return out
 
 
 def scatter(v: np.ndarray, plans: Sequence[api.SlabPlan]):

@@ -209,3 +209,109 @@ def test_gloo_two_ranks_match_block_jacobi_pcg(oracle, problems):
     ro = oracle.pcg_solve(sa, b, xo, kind=1, ic=f, eps=eps, max_iter=max_iter)
     assert abs(len(hists[0]) - ro.iterations) <= 1
     assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def _rank_recycle(rank, world, port, n, rs, ci, va, errors, out_q):
+    """dist.cu's dist_recycle in numpy on this rank's rows, over gloo (test executable spec):
+    global zero-column test, single-pass MGS with every dot allreduced (dense.cpp:45-61), A Q by
+    halo exchange + local SpMV, the allreduced Gram Q^T A Q eigensolved on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import Oracle
+    from paper_2203_08498_b200 import api
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    o = Oracle()
+    p = api.SlabPlan(n, rs, ci, va, world, rank)
+    soff = np.concatenate([[0], np.cumsum(p.send_count)])
+    roff = np.concatenate([[0], np.cumsum(p.recv_count)])
+    rows = np.repeat(np.arange(p.nloc), np.diff(p.row_start))
+
+    def allreduce(v):
+        t = torch.tensor(np.atleast_1d(v), dtype=torch.float64)
+        dist.all_reduce(t)
+        return t.numpy()
+
+    def halo(ext):
+        reqs, got = [], {}
+        for q in range(world):
+            if p.send_count[q]:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(ext[p.send_idx[soff[q]:soff[q + 1]]])), q))
+        for q in range(world):
+            if p.recv_count[q]:
+                got[q] = torch.empty(int(p.recv_count[q]), dtype=torch.float64)
+                reqs.append(dist.irecv(got[q], q))
+        for r in reqs:
+            r.wait()
+        for q, t in got.items():
+            ext[p.nloc + roff[q]:p.nloc + roff[q + 1]] = t.numpy()
+
+    e = errors[:, p.row_begin:p.row_end]
+    nz = allreduce((e != 0).any(axis=1).astype(np.float64))
+    qs = []
+    for j in np.nonzero(nz > 0)[0]:
+        w = e[j].copy()
+        n0 = np.sqrt(allreduce(w @ w)[0])
+        if n0 == 0.0:
+            continue
+        for qv in qs:
+            c = allreduce(qv @ w)[0]
+            w = w - c * qv
+        n1 = np.sqrt(allreduce(w @ w)[0])
+        if n1 <= 1e-12 * n0:
+            continue
+        qs.append(w / n1)
+    k = len(qs)
+    aq = []
+    for qv in qs:
+        ext = np.zeros(p.nloc + p.nhalo)
+        ext[:p.nloc] = qv
+        halo(ext)
+        y = np.zeros(p.nloc)
+        np.add.at(y, rows, p.values * ext[p.col_idx])
+        aq.append(y)
+    g = np.zeros((k, k))
+    for i in range(k):
+        for j in range(i + 1):
+            g[i, j] = qs[i] @ aq[j]
+    g = allreduce(g.ravel()).reshape(k, k)
+    s = np.tril(g) + np.tril(g, -1).T
+    vals, _ = o.sym_eig(s)
+    out_q.put((rank, k, np.asarray(vals)))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_recycling_matches_build_aux(oracle, problems):
+    """The distributed recycling step (rcg_dist_recycle's structure) on a block-Jacobi solve 1's
+    sampled errors, plus a duplicated and a zero column: same m_bar and Ritz values as the
+    oracle's build_aux_matrix on the assembled errors (recycling.cpp:81-96)."""
+    import torch.multiprocessing as mp
+
+    from oracle import Matrix
+
+    h = problems.generate(problems.SMALL["c1"])
+    sa, _ = oracle.diagonal_scale(Matrix.of(h))
+    world = 2
+    f = oracle.ic0_factorize(sa, 0.0, world)
+    smp = oracle.sampler_a(16, 500, h.n)
+    x = np.zeros(h.n)
+    oracle.pcg_solve(sa, oracle.uniform_pm1(5, 0, h.n), x, kind=1, ic=f, eps=1e-8, max_iter=500, sampler=smp)
+    errs = np.asarray(oracle.harvest_errors(x, smp))
+    errs = np.vstack([errs, errs[:1], np.zeros((1, h.n))])  # dependent + zero columns
+    m_bar_o, vals_o, _ = oracle.build_aux(sa, errs, float("inf"))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_recycle, args=(r, world, port, h.n, sa.rs, sa.ci, sa.va, errs, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for _, k, vals in res:
+        assert k == m_bar_o
+        assert np.allclose(vals, vals_o[:k], rtol=1e-9, atol=0)
+    assert np.array_equal(res[0][2], res[1][2])  # replicated eigensolve: identical on every rank

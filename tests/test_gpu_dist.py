@@ -148,3 +148,30 @@ def test_nccl_transport_world_one_equals_loopback(oracle, problems):
     assert r2.iterations == r1.iterations
     assert np.array_equal(r2.history, r1.history)
     assert np.array_equal(x2, x1)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_loopback_sequence_matches_block_jacobi_sequence(oracle, problems, name, nparts):
+    """run_sequence over row slabs (rcg_dist_pcg_solve_sampled + rcg_dist_recycle + rcg_dist_solve)
+    against the oracle's sequence with ic0_factorize(a, 0, G): solve 1 and the sampled iterations,
+    m_bar, Ritz values (<= 1e-6 at equal solve-1 counts) and every accelerated solve (+-2)."""
+    from oracle.sequence import run_sequence
+    from paper_2203_08498_b200 import dist
+
+    cfg = problems.SMALL[name]
+    h = problems.generate(cfg)
+    ref = run_sequence(oracle, cfg, h, blocks=nparts)
+    _, host = _scaled(oracle, problems, name)
+    system = dist.LoopbackSystem(host, nparts)
+    out = system.sequence(ref["scaled_rhs"], cfg.eps, cfg.max_iter, cfg.sampler_m, cfg.keep,
+                          "sc" if cfg.method == "sc" else "deflation")
+    assert all(out["converged"])
+    for k, (g, o) in enumerate(zip(out["iterations"], ref["iterations"])):
+        assert abs(g - o) <= 2, (k, out["iterations"], ref["iterations"])
+    if out["iterations"][0] == ref["iterations"][0]:
+        assert out["m_bar"] == ref["m_bar"]
+        assert out["m_tilde"] == ref["m_tilde"]
+        vo = np.asarray(ref["ritz_values"])[: out["m_bar"]]
+        assert np.allclose(out["ritz_values"], vo, rtol=1e-6, atol=0), (out["ritz_values"], vo)
+    assert out["iterations"][1] < out["iterations"][0] or out["m_tilde"] == 0
