@@ -202,7 +202,7 @@ SIGNATURES = {
     "rcg_dist_pcg_solve_sampled": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                    C.POINTER(SolverConfig), C.POINTER(SolveReport)),
     "rcg_dist_recycle": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.c_double, C.c_int, C.c_int,
-                         ip, dp, dp, ip, C.POINTER(vp)),
+                         ip, vp, dp, ip, C.POINTER(vp)),
 }
 
 for _name, (_res, *_args) in SIGNATURES.items():

@@ -135,6 +135,8 @@ def test_nccl_transport_world_one_equals_loopback(oracle, problems):
     lb = dist.LoopbackSystem(host, 1)
     x1 = np.zeros(sa.n)
     r1 = lb.solve(b, x1)
+    bs = [oracle.uniform_pm1(31 + k, 0, sa.n) for k in range(3)]
+    q1 = lb.sequence(bs, 1e-8, 2000, 16, 6, "sc")
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ["MASTER_PORT"] = str(_free_port())
     torch.cuda.set_device(0)
@@ -143,11 +145,16 @@ def test_nccl_transport_world_one_equals_loopback(oracle, problems):
         rank = dist.NcclRank(host)
         x2 = np.zeros(sa.n)
         r2 = rank.solve(b, x2)
+        q2 = rank.sequence(bs, 1e-8, 2000, 16, 6, "sc")
     finally:
         dist_.destroy_process_group()
     assert r2.iterations == r1.iterations
     assert np.array_equal(r2.history, r1.history)
     assert np.array_equal(x2, x1)
+    # the sequence (sampled solve 1, recycling, SC solves): bitwise across transports
+    assert q2["iterations"] == q1["iterations"] and q2["m_bar"] == q1["m_bar"]
+    assert np.array_equal(q2["ritz_values"], q1["ritz_values"])
+    assert all(np.array_equal(a, b_) for a, b_ in zip(q2["solutions"], q1["solutions"]))
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c4"])
