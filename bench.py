@@ -15,7 +15,8 @@ independent sample per host thread (the reference is serial; samples are indepen
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
 For N > 1 launch with torch.distributed.run; ranks run independent replicas of the workload
-(scaling "weak"; the row-slab partition is not in this build -- see DESIGN.md).
+(scaling "weak"); the row-slab partition (block-Jacobi IC(0), NCCL halo + allreduces) is measured
+on all N ranks as variants.row_slabs (one solve and one whole sequence).
 """
 from __future__ import annotations
 
@@ -182,7 +183,8 @@ def run_ours(args, rank, world, local_rank):
     ctx.record(3)
     e2e_ms = ctx.elapsed_ms(2, 3)
     # the multi-GPU row-slab path (all ranks take part): one distributed block-Jacobi ICCG solve
-    row_slabs = None if args.no_variants else measure_row_slabs(api, prep, host, pairs[0][1], cfg, rank, world, dev)
+    row_slabs = None if args.no_variants else measure_row_slabs(api, prep, host, pairs[0][1], cfg, rank, world, dev,
+                                                                   [b for _, b in pairs])
     # max over ranks
     t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
     it = torch.tensor([float(iters), float(e2e_iters)], dtype=torch.float64, device=dev)
@@ -294,7 +296,7 @@ def kernel_report(stats, n, nnz, nnz_l, m, steps, peak, peak_src):
     return kernels, roof
 
 
-def measure_row_slabs(api, prep, host, b_scaled, cfg, rank, world, dev):
+def measure_row_slabs(api, prep, host, b_scaled, cfg, rank, world, dev, seq_rhs):
     """the same matrix split into `world` row slabs (block-Jacobi IC(0) per GPU, NCCL
     halo exchange + three allreduces per iteration; loopback transport at N = 1), one ICCG solve
     of the step's first right-hand side.  Device time (events on each slab's stream), max over
@@ -304,6 +306,7 @@ def measure_row_slabs(api, prep, host, b_scaled, cfg, rank, world, dev):
     from paper_2203_08498_b200 import dist, problems as P
 
     scaled = P.HostCsr(host.n, host.row_start, host.col_idx, prep.a.values())
+    kind = "sc" if cfg.method == "sc" else "deflation"
     if world == 1:
         system = dist.LoopbackSystem(scaled, 1)
         solve = lambda x: system.solve(b_scaled, x, cfg.eps, cfg.max_iter)  # noqa: E731
@@ -315,15 +318,35 @@ def measure_row_slabs(api, prep, host, b_scaled, cfg, rank, world, dev):
         nloc = rk.plan.nloc
     solve(np.zeros(nloc))  # warm-up
     rep = solve(np.zeros(nloc))
-    t = torch.tensor([rep.wall_time * 1e3], dtype=torch.float64, device=dev)
+    # the whole sequence over the slabs: sampled solve 1, distributed recycling, accelerated solves
+    bs_all = list(seq_rhs)
+    if world == 1:
+        run_seq = lambda: system.sequence(bs_all, cfg.eps, cfg.max_iter, cfg.sampler_m, cfg.keep, kind)  # noqa: E731
+    else:
+        bl_all = [np.ascontiguousarray(v[rk.plan.row_begin:rk.plan.row_end]) for v in bs_all]
+        run_seq = lambda: rk.sequence(bl_all, cfg.eps, cfg.max_iter, cfg.sampler_m, cfg.keep, kind)  # noqa: E731
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    seq = run_seq()
+    torch.cuda.synchronize()
+    seq_s = time.perf_counter() - t0
+    t = torch.tensor([rep.wall_time * 1e3, seq_s * 1e3], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t.item())
+    ms, seq_ms = t.tolist()
+    its = int(sum(seq["iterations"]))
     return {"operator": f"block-Jacobi IC(0), {world} row slab(s) at floor(b n / {world}) (ic0_factorize(a, 0, {world}))",
             "transport": "nccl" if world > 1 else "loopback", "n": host.n, "iterations": rep.iterations,
             "converged": bool(rep.converged), "solve_ms": round(ms, 3),
             "ms_per_iteration": round(ms / max(rep.iterations, 1), 4),
-            "value": round(rep.iterations / (ms / 1e3), 2), "unit": "iters/s"}
+            "value": round(rep.iterations / (ms / 1e3), 2), "unit": "iters/s",
+            "sequence": {"what": f"rcg_dist_pcg_solve_sampled + rcg_dist_recycle ({kind}, m={cfg.keep}) + "
+                                 f"{len(bs_all) - 1} rcg_dist_solve, one pass, wall clock max over ranks",
+                         "iterations": [int(v) for v in seq["iterations"]], "m_bar": int(seq["m_bar"]),
+                         "m_tilde": int(seq["m_tilde"]), "ms": round(seq_ms, 2),
+                         "iters_per_s": round(its / (seq_ms / 1e3), 2)}}
 
 
 def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
