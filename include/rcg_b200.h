@@ -62,10 +62,11 @@ int rcg_ctx_event_elapsed(rcg_ctx* ctx, int slot_a, int slot_b, double* ms);
 int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launches);
 int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units);
 void rcg_ctx_reset_stats(rcg_ctx* ctx);
-/* IC sweep kernel selection (no effect on results: both kernels are bitwise identical):
- * 0 = grid-wide sync-free sweep, 1 = one-cluster level-synchronous sweep (icsweep_cl.cu)
- * whenever its plan fits, 2 = default (currently the grid sweep: the cluster sweep measured no
- * faster); RCG_SWEEP_CLUSTER overrides at context creation */
+/* IC sweep kernel selection (no effect on results: every variant is bitwise identical):
+ * 0 = grid-wide sync-free sweep (k_sweep), 1 = one-cluster level-synchronous sweep
+ * (icsweep_cl.cu) whenever its plan fits, 2 = default (k_sweep: the alternatives measured no
+ * faster), 3 = the load-pipelined grid sweep k_sweep_pf; RCG_SWEEP_CLUSTER overrides
+ * at context creation */
 int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode);
 
 /* ------------------------------------------------------------------ CSR (csr_matrix.hpp) */

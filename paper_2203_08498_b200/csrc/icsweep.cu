@@ -20,6 +20,7 @@
 // ordering's level count bounds it by dependency latency on C1-C3.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -164,11 +165,173 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
     }
 }
 
+// Pipelined variant (opt-in, rcg_ctx_set_sweep_kernel(ctx, 3)), written for wide levels
+// (hundreds of thousands of rows per level: C4, C5, the multicolour orderings), where each
+// warp's tile might be bound by its own chain of dependent loads (ticket -> perm / prs -> in / d
+// / entries -> parents).  Measured no faster there (C4 fwd 7.95 -> 9.56 ms, C2 multicolour
+// 66.7 -> 70.4 us, C4 multicolour 6.19 -> 5.82 ms), so it is not selected by default.  A three-stage software
+// pipeline keeps the next tiles' loads in flight while the current tile waits on its parents:
+// per iteration a warp takes the ticket of tile A, issues the perm / prs loads of tile B (ticket
+// from the previous iteration) and the in / d / entry loads of tile C (perm / prs from the
+// previous iteration), then processes the tile whose loads were issued one iteration earlier.
+// Deadlock-free like k_sweep: a warp holds at most three tiles, all above the one it processes,
+// so the smallest unfinished tile is always some warp's current tile.  Row arithmetic, publish
+// protocol and the (r, z) reduction are k_sweep's, so results are bitwise identical.
+template <bool BWD>
+__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_pf(SweepArgs a) {
+    if (a.st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int ntiles = (a.npos + kTile - 1) / kTile;
+    auto ticket = [&]() {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&a.tickets[0], 1);
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
+    // stage B: perm / prs in flight; stage C: in / d / first entry chunk in flight
+    int ta = ticket();
+    int tb = ntiles, tc = ntiles;
+    int32_t b_row = -1, b_beg = 0, b_end = 0;
+    int32_t c_row = -1, c_beg = 0, c_end = 0;
+    double c_in = 0.0, c_d = 1.0;
+    int32_t c_col[kDepChunk];
+    double c_val[kDepChunk];
+#pragma unroll
+    for (int j = 0; j < kDepChunk; ++j) {
+        c_col[j] = 0;
+        c_val[j] = 0.0;
+    }
+    while (tc < ntiles || tb < ntiles || ta < ntiles) {
+        // C' from B: the tile's inputs and first entry chunk
+        const int nc = tb;
+        int32_t n_row = -1, n_beg = 0, n_end = 0;
+        double n_in = 0.0, n_d = 1.0;
+        int32_t n_col[kDepChunk];
+        double n_val[kDepChunk];
+#pragma unroll
+        for (int j = 0; j < kDepChunk; ++j) {
+            n_col[j] = 0;
+            n_val[j] = 0.0;
+        }
+        if (nc < ntiles && b_row >= 0) {
+            n_row = b_row;
+            n_beg = b_beg;
+            n_end = b_end;
+            n_in = a.in[n_row];
+            if (BWD) n_d = __ldg(a.d + n_row);
+            const int cnt = min(kDepChunk, n_end - n_beg);
+#pragma unroll
+            for (int j = 0; j < kDepChunk; ++j)
+                if (j < cnt) {
+                    n_col[j] = __ldg(a.pcol + n_beg + j);
+                    n_val[j] = __ldg(a.pval + n_beg + j);
+                }
+        }
+        // B' from A: the tile's row map
+        const int nb = ta;
+        int32_t nb_row = -1, nb_beg = 0, nb_end = 0;
+        if (nb < ntiles) {
+            const int pos = nb * kTile + lane;
+            nb_row = pos < a.npos ? __ldg(a.perm + pos) : -1;
+            if (pos < a.npos) {
+                nb_beg = __ldg(a.prs + pos);
+                nb_end = __ldg(a.prs + pos + 1);
+            }
+        }
+        const int na = nb < ntiles ? ticket() : ntiles;
+        // process C (its loads were issued one iteration ago)
+        if (tc < ntiles) {
+            double contrib = 0.0;
+            if (c_row >= 0) {
+                double s = BWD ? __ddiv_rn(c_in, c_d) : c_in;
+                unsigned spins = 0;
+                for (int32_t e0 = c_beg;; e0 += kDepChunk) {
+                    const int cnt = min(kDepChunk, c_end - e0);
+                    const bool last = e0 + kDepChunk >= c_end;
+                    int32_t col[kDepChunk];
+                    double val[kDepChunk], dep[kDepChunk];
+#pragma unroll
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j < cnt) {
+                            col[j] = e0 == c_beg ? c_col[j] : __ldg(a.pcol + e0 + j);
+                            val[j] = e0 == c_beg ? c_val[j] : __ldg(a.pval + e0 + j);
+                        }
+#pragma unroll
+                    for (int j = 0; j < kDepChunk; ++j)
+                        if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
+                    while (true) {
+                        bool missing = false;
+#pragma unroll
+                        for (int j = 0; j < kDepChunk; ++j)
+                            if (j < cnt && is_sentinel(dep[j])) missing = true;
+                        if (!missing) {
+#pragma unroll
+                            for (int j = 0; j < kDepChunk; ++j)
+                                if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
+                            if (last) st_relaxed(a.out + c_row, publishable(s));
+                            break;
+                        }
+#pragma unroll
+                        for (int j = 0; j < kDepChunk; ++j)
+                            if (j < cnt && is_sentinel(dep[j])) dep[j] = ld_relaxed(a.out + col[j]);
+                        if (++spins == (1u << 24)) {  // bounded: a schedule fault is an error, never a hang
+                            atomicExch(&a.tickets[3], 1);
+#pragma unroll
+                            for (int j = 0; j < kDepChunk; ++j)
+                                if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
+                        }
+                    }
+                    if (last) break;
+                }
+                if (BWD && a.r) contrib = __dmul_rn(a.r[c_row], s);
+            }
+            if (BWD && a.r) {
+                double tot;
+                if (tile_reduce(contrib, tc, ntiles, a, &tot) && lane == 0) {
+                    DevState* st = a.st;   // src/pcg.cpp:65-71, as k_sweep
+                    const double rho = a.add_sc ? tot + st->scal[2] : tot;
+                    st->rho = rho;
+                    if (rho <= 0.0) {
+                        st->done = kBroken;
+                        st->status = kBrkRz;
+                    }
+                    st->beta = st->iter > 1 ? rho / st->rho_prev : 0.0;
+                }
+            }
+        }
+        // advance the pipeline
+        tc = nc;
+        c_row = n_row;
+        c_beg = n_beg;
+        c_end = n_end;
+        c_in = n_in;
+        c_d = n_d;
+#pragma unroll
+        for (int j = 0; j < kDepChunk; ++j) {
+            c_col[j] = n_col[j];
+            c_val[j] = n_val[j];
+        }
+        tb = nb;
+        b_row = nb_row;
+        b_beg = nb_beg;
+        b_end = nb_end;
+        ta = na;
+    }
+    if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x * (blockDim.x / 32)) - 1) {
+            a.tickets[0] = 0;
+            a.tickets[1] = 0;
+        }
+    }
+}
+
 void sweep_prepare_kernels() {
     static bool done = false;
     if (done) return;
     set_carveout(reinterpret_cast<const void*>(k_sweep<false>));
     set_carveout(reinterpret_cast<const void*>(k_sweep<true>));
+    set_carveout(reinterpret_cast<const void*>(k_sweep_pf<false>));
+    set_carveout(reinterpret_cast<const void*>(k_sweep_pf<true>));
     done = true;
 }
 
@@ -204,6 +367,13 @@ int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos) {
     return backward && entries_per_row > kDepChunk ? 1 : 2;
 }
 
+// The pipelined sweep (k_sweep_pf) only on request (ctx->sweep_cluster == 3): measured no faster
+// than k_sweep on the wide-level shapes it was written for.
+static bool sweep_pipelined(const rcg_ctx* ctx, const rcg_ic* f, bool backward, int64_t npos) {
+    (void)f, (void)backward, (void)npos;
+    return ctx->sweep_cluster == 3;
+}
+
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
     if (grid_sweep_available(f)) {  // tiled sweep on a natural-ordered grid (icgrid.cu)
@@ -212,14 +382,22 @@ void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     }
     if (launch_cluster_sweep(ctx, f, backward, a)) return;  // narrow levels: one cluster (icsweep_cl.cu)
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
-    const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
+    const bool pf = sweep_pipelined(ctx, f, backward, a.npos);
+    int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
+    if (pf) bps = std::min(bps, 4);   // k_sweep_pf: 128 registers, 4 resident CTAs per SM
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
     a.backoff_ns = ctx->sweep_backoff_ns;
     KTimer t(ctx, backward ? 2 : 1);
-    if (backward)
+    if (pf) {
+        if (backward)
+            k_sweep_pf<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
+        else
+            k_sweep_pf<false><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
+    } else if (backward) {
         k_sweep<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
-    else
+    } else {
         k_sweep<false><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
+    }
     RCG_LAUNCHED(ctx);
 }
 

@@ -157,7 +157,7 @@ def test_nccl_transport_world_one_equals_loopback(oracle, problems):
     assert all(np.array_equal(a, b_) for a, b_ in zip(q2["solutions"], q1["solutions"]))
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
 @pytest.mark.parametrize("nparts", [1, 2, 3])
 def test_loopback_sequence_matches_block_jacobi_sequence(oracle, problems, name, nparts):
     """run_sequence over row slabs (rcg_dist_pcg_solve_sampled + rcg_dist_recycle + rcg_dist_solve)

@@ -1,7 +1,8 @@
-"""The one-cluster level-synchronous IC sweep (csrc/icsweep_cl.cu) against the grid-wide
-sync-free sweep (csrc/icsweep.cu) and the oracle: the sweep output, the (r, z) reduction and whole
-PCG / SC-PCG solves must be BITWISE identical whichever kernel runs (the kernel choice never
-changes an iterate), and both equal the reference ic_apply (src/ic_preconditioner.cpp:123-144)."""
+"""The IC sweep variants -- grid-wide sync-free (k_sweep), pipelined wide-level (k_sweep_pf) and
+the one-cluster level-synchronous sweep (csrc/icsweep_cl.cu) -- against each other and the
+oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
+identical whichever kernel runs (the kernel choice never changes an iterate), and all equal the
+reference ic_apply (src/ic_preconditioner.cpp:123-144)."""
 import numpy as np
 import pytest
 
@@ -9,7 +10,8 @@ from oracle import Matrix
 
 pytestmark = pytest.mark.gpu
 
-GRID, CLUSTER, AUTO = 0, 1, 2
+GRID, CLUSTER, AUTO, PIPELINED = 0, 1, 2, 3
+MODES = (GRID, CLUSTER, PIPELINED)
 
 
 @pytest.fixture
@@ -25,7 +27,7 @@ def _scaled(ctx, h):
     return api.diagonal_scale(ctx, a)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c4", "lap1d"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "lap1d"])
 def test_cluster_sweep_bitwise(modes, oracle, problems, name):
     from paper_2203_08498_b200 import api
 
@@ -47,11 +49,11 @@ def test_cluster_sweep_bitwise(modes, oracle, problems, name):
     want = oracle.ic_apply(oracle.ic0_factorize(a_o), oracle.uniform_pm1(5, 0, h.n))
     r = oracle.uniform_pm1(5, 0, h.n)
     outs = {}
-    for mode in (GRID, CLUSTER):
+    for mode in MODES:
         ctx.set_sweep_kernel(mode)
         outs[mode] = f.apply(r)
-    assert np.array_equal(outs[GRID], want)
-    assert np.array_equal(outs[CLUSTER], want)
+    for mode in MODES:
+        assert np.array_equal(outs[mode], want), mode
 
 
 @pytest.mark.parametrize("method", ["ic", "sc"])
@@ -66,7 +68,7 @@ def test_cluster_sweep_solves_bitwise(modes, problems, method):
     p = sequence.prepare(ctx, cfg, h, validate=False)
     b = sequence.rhs(p, 0)[1]
     res = {}
-    for mode in (GRID, CLUSTER):
+    for mode in MODES:
         ctx.set_sweep_kernel(mode)
         if method == "ic":
             x = np.zeros(h.n)
@@ -80,9 +82,10 @@ def test_cluster_sweep_solves_bitwise(modes, problems, method):
             x = np.zeros(h.n)
             rep = api.pcg_solve(ctx, p.a, sequence.rhs(p, 1)[1], api.Sc(basis, p.ic), x, cfg.eps, cfg.max_iter)
         res[mode] = (rep.iterations, np.array(rep.history), x.copy())
-    assert res[GRID][0] == res[CLUSTER][0]
-    assert np.array_equal(res[GRID][1], res[CLUSTER][1])
-    assert np.array_equal(res[GRID][2], res[CLUSTER][2])
+    for mode in MODES:
+        assert res[GRID][0] == res[mode][0]
+        assert np.array_equal(res[GRID][1], res[mode][1])
+        assert np.array_equal(res[GRID][2], res[mode][2])
 
 
 def test_cluster_sweep_c2_full(modes, problems):
@@ -97,11 +100,34 @@ def test_cluster_sweep_c2_full(modes, problems):
     r = problems.uniform_pm1(9, 0, h.n)
     b = sequence.rhs(p, 0)[1]
     outs = {}
-    for mode in (GRID, CLUSTER):
+    for mode in MODES:
         ctx.set_sweep_kernel(mode)
         z = p.ic.apply(r)
         x = np.zeros(h.n)
         rep = api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x, cfg.eps, 40)
         outs[mode] = (z, np.array(rep.history), x)
+    for mode in MODES:
+        for k in range(3):
+            assert np.array_equal(outs[GRID][k], outs[mode][k])
+
+
+def test_pipelined_sweep_multicolour_c2(modes, problems):
+    """The wide-level pipelined sweep on the multicolour C2 operator (2 levels of ~1M rows, the
+    shape it is chosen for): bitwise the grid sweep, sweep output and an ICCG window."""
+    from paper_2203_08498_b200 import api, sequence
+
+    ctx = modes
+    cfg = problems.CONFIGS["c2"]
+    m, perm, _ = problems.multicolour(problems.generate(cfg))
+    p = sequence.prepare(ctx, cfg, m, validate=False, new_of_old=perm)
+    r = problems.uniform_pm1(9, 0, m.n)
+    b = sequence.rhs(p, 0)[1]
+    outs = {}
+    for mode in (GRID, PIPELINED):
+        ctx.set_sweep_kernel(mode)
+        z = p.ic.apply(r)
+        x = np.zeros(m.n)
+        rep = api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x, cfg.eps, 30)
+        outs[mode] = (z, np.array(rep.history), x)
     for k in range(3):
-        assert np.array_equal(outs[GRID][k], outs[CLUSTER][k])
+        assert np.array_equal(outs[GRID][k], outs[PIPELINED][k])
