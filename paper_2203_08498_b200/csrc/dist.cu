@@ -1208,7 +1208,8 @@ int rcg_dslab_create(rcg_ctx* ctx, const rcg_slab_plan* p, const rcg_ic* ic, rcg
 
 void rcg_dslab_destroy(rcg_dslab* d) {
     if (!d) return;
-    if (d->ctx) cudaStreamSynchronize(d->ctx->stream);
+    // the device, not the (borrowed) context: a caller may already have destroyed the context
+    cudaDeviceSynchronize();
     rcg_matrix_destroy(d->a);
     for (void* p : {(void*)d->send_idx, (void*)d->sendbuf, (void*)d->xe, (void*)d->pe, (void*)d->dsum, (void*)d->gbuf,
                     (void*)d->ubuf, (void*)d->u2buf})

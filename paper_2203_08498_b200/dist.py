@@ -58,6 +58,7 @@ class LoopbackSystem:
         samplers = [api.SamplerState.method_a(c, sampler_m, max_iter, p.nloc) for c, p in zip(self.ctxs, self.plans)]
         xs = [np.zeros(p.nloc) for p in self.plans]
         r1 = api.dist_pcg_solve_sampled(self.comm, self.slabs, samplers, scatter(bs[0], self.plans), xs, eps, max_iter)
+        self.last_samplers, self.last_x1 = samplers, [x.copy() for x in xs]   # kept for inspection (tests)
         m_bar, vals, _, m_tilde, basis = api.dist_recycle(self.comm, self.slabs, samplers, xs, keep_count=keep, kind=kind)
         out = {"iterations": [r1.iterations], "converged": [r1.converged], "solutions": [np.concatenate(xs)],
                "m_bar": m_bar, "ritz_values": vals, "m_tilde": m_tilde, "histories": [r1.history]}
@@ -69,6 +70,16 @@ class LoopbackSystem:
             out["solutions"].append(x)
             out["histories"].append(r.history)
         return out
+
+    def sampled_errors(self) -> np.ndarray:
+        """The last sequence's harvested errors x_final - slot (occupied slots in order), global
+        rows -- the shared input for checking the recycling step against the oracle."""
+        st = self.last_samplers[0].state()
+        occ = st[0] if isinstance(st, tuple) else st["occupied"]
+        cols = []
+        for j in np.nonzero(np.asarray(occ))[0]:
+            cols.append(np.concatenate([x - smp.slot(int(j)) for x, smp in zip(self.last_x1, self.last_samplers)]))
+        return np.array(cols).reshape(len(cols), self.n)
 
     def solve(self, b: np.ndarray, x: np.ndarray, eps: float = 1e-8, max_iter: int = 1000,
               basis: Optional[api.DBasis] = None) -> api.SolveReport:
