@@ -64,9 +64,9 @@ int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units);
 void rcg_ctx_reset_stats(rcg_ctx* ctx);
 /* IC sweep kernel selection (no effect on results: every variant is bitwise identical):
  * 0 = grid-wide sync-free sweep (k_sweep), 1 = one-cluster level-synchronous sweep
- * (icsweep_cl.cu) whenever its plan fits, 2 = default (k_sweep: the alternatives measured no
- * faster), 3 = the load-pipelined grid sweep k_sweep_pf; RCG_SWEEP_CLUSTER overrides
- * at context creation */
+ * (icsweep_cl.cu) whenever its plan fits, 2 = default (one launch per level -- icsweep_lv.cu --
+ * when the average level holds >= 600K rows, else k_sweep), 3 = the load-pipelined grid sweep
+ * k_sweep_pf, 4 = one launch per level always; RCG_SWEEP_CLUSTER overrides at context creation */
 int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode);
 
 /* ------------------------------------------------------------------ CSR (csr_matrix.hpp) */

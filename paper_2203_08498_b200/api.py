@@ -89,8 +89,8 @@ class Context:
 
     def set_sweep_kernel(self, mode: int):
         """IC sweep kernel: 0 grid-wide sync-free, 1 one-cluster level-synchronous whenever it
-        fits, 2 default (grid), 3 load-pipelined grid sweep.  Results are bitwise identical
-        either way."""
+        fits, 2 default (per-level launches for wide levels, else grid), 3 load-pipelined grid
+        sweep, 4 per-level launches always.  Results are bitwise identical either way."""
         check(lib.rcg_ctx_set_sweep_kernel(self.h, int(mode)))
 
     def record(self, slot: int):

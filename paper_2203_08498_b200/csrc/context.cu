@@ -422,7 +422,7 @@ int64_t rcg_ctx_launch_count(const rcg_ctx* ctx) { return ctx ? ctx->launches : 
 
 int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode) {
     return guard([&] {
-        require(ctx != nullptr && mode >= 0 && mode <= 3, "rcg_ctx_set_sweep_kernel: mode must be 0..3");
+        require(ctx != nullptr && mode >= 0 && mode <= 4, "rcg_ctx_set_sweep_kernel: mode must be 0..4");
         ctx->sweep_cluster = mode;
     });
 }

@@ -406,7 +406,8 @@ static void schedule_device(rcg_ctx* ctx, DevBag& bag, int32_t n, const int32_t*
     k_pos_len<<<grid_for(ctx, npos), 256, 0, ctx->stream>>>(perm, npos, rs, plen);
     prs = static_cast<int32_t*>(dev_alloc_bytes(sizeof(int32_t) * (static_cast<int64_t>(npos) + 1)));
     exclusive_sum(ctx, bag, plen, prs, static_cast<int64_t>(npos) + 1);
-    pcol = static_cast<int32_t*>(dev_alloc_bytes(sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    // + kCsrPad: the level sweep's tile engine widens bulk ranges to 16 bytes (k_level_sweep)
+    pcol = static_cast<int32_t*>(dev_alloc_bytes(sizeof(int32_t) * (std::max<int64_t>(nnz, 1) + kCsrPad)));
     pidx = bag.get<int32_t>(nnz);
     k_pos_fill<<<grid_for(ctx, npos), 256, 0, ctx->stream>>>(perm, npos, prs, rs, col, pcol, pidx);
 }
@@ -530,8 +531,8 @@ static void factorize_device(rcg_ctx* ctx, const rcg_matrix* A, double shift, in
         throw Error(RCG_E_BREAKDOWN, buf);
     }
     mark("numeric");
-    f->f_val = dev_alloc(std::max<int64_t>(nnzl, 1));
-    f->b_val = dev_alloc(std::max<int64_t>(nnzl, 1));
+    f->f_val = dev_alloc(std::max<int64_t>(nnzl, 1) + kCsrPad);
+    f->b_val = dev_alloc(std::max<int64_t>(nnzl, 1) + kCsrPad);
     if (nnzl > 0) {
         k_scatter<<<ge, kStreamThreads, 0, ctx->stream>>>(lval, l2u, uval, nnzl);
         k_gather<<<ge, kStreamThreads, 0, ctx->stream>>>(lval, fidx, f->f_val, nnzl);

@@ -380,7 +380,8 @@ void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
         launch_grid_sweep(ctx, f, backward, a);
         return;
     }
-    if (launch_cluster_sweep(ctx, f, backward, a)) return;  // narrow levels: one cluster (icsweep_cl.cu)
+    if (launch_level_sweep(ctx, f, backward, a)) return;    // wide levels: one launch per level (icsweep_lv.cu)
+    if (launch_cluster_sweep(ctx, f, backward, a)) return;  // opt-in: one cluster (icsweep_cl.cu)
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
     const bool pf = sweep_pipelined(ctx, f, backward, a.npos);
     int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
@@ -448,7 +449,8 @@ void ic_apply_dev(rcg_ctx* ctx, const rcg_ic* f, const double* r, double* z) {
 template <class T>
 static T* upload(rcg_ctx* ctx, const std::vector<T>& h) {
     void* p = nullptr;
-    RCG_CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(h.size(), 1)));
+    // + kCsrPad elements: the level sweep's tile engine widens bulk ranges to 16 bytes
+    RCG_CK(cudaMalloc(&p, sizeof(T) * (std::max<size_t>(h.size(), 1) + kCsrPad)));
     if (!h.empty()) RCG_CK(cudaMemcpyAsync(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
     return static_cast<T*>(p);
 }

@@ -105,6 +105,7 @@ void allow_smem(const void* kernel);
 int tile_capacity(int32_t n, const int32_t* rs);
 void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const double* x, double* r);
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
+bool launch_level_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);   // icsweep_lv.cu
 bool launch_cluster_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);  // icsweep_cl.cu
 void free_cluster_plans(rcg_ic* f);
 void cluster_prof_dump(const char* tag);  // dev: RCG_CL_PROF

@@ -1,5 +1,6 @@
-"""The IC sweep variants -- grid-wide sync-free (k_sweep), pipelined wide-level (k_sweep_pf) and
-the one-cluster level-synchronous sweep (csrc/icsweep_cl.cu) -- against each other and the
+"""The IC sweep variants -- grid-wide sync-free (k_sweep), load-pipelined (k_sweep_pf), one
+launch per level (csrc/icsweep_lv.cu) and the one-cluster level-synchronous sweep
+(csrc/icsweep_cl.cu) -- against each other and the
 oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
 identical whichever kernel runs (the kernel choice never changes an iterate), and all equal the
 reference ic_apply (src/ic_preconditioner.cpp:123-144)."""
@@ -10,8 +11,8 @@ from oracle import Matrix
 
 pytestmark = pytest.mark.gpu
 
-GRID, CLUSTER, AUTO, PIPELINED = 0, 1, 2, 3
-MODES = (GRID, CLUSTER, PIPELINED)
+GRID, CLUSTER, AUTO, PIPELINED, LEVEL = 0, 1, 2, 3, 4
+MODES = (GRID, CLUSTER, PIPELINED, LEVEL)
 
 
 @pytest.fixture
@@ -111,9 +112,9 @@ def test_cluster_sweep_c2_full(modes, problems):
             assert np.array_equal(outs[GRID][k], outs[mode][k])
 
 
-def test_pipelined_sweep_multicolour_c2(modes, problems):
-    """The wide-level pipelined sweep on the multicolour C2 operator (2 levels of ~1M rows, the
-    shape it is chosen for): bitwise the grid sweep, sweep output and an ICCG window."""
+def test_wide_level_sweeps_multicolour_c2(modes, problems):
+    """The wide-level variants on the multicolour C2 operator (2 levels of ~1M rows: the default
+    picks the per-level launches): bitwise the grid sweep, sweep output and an ICCG window."""
     from paper_2203_08498_b200 import api, sequence
 
     ctx = modes
@@ -123,11 +124,12 @@ def test_pipelined_sweep_multicolour_c2(modes, problems):
     r = problems.uniform_pm1(9, 0, m.n)
     b = sequence.rhs(p, 0)[1]
     outs = {}
-    for mode in (GRID, PIPELINED):
+    for mode in (GRID, PIPELINED, LEVEL, AUTO):
         ctx.set_sweep_kernel(mode)
         z = p.ic.apply(r)
         x = np.zeros(m.n)
         rep = api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x, cfg.eps, 30)
         outs[mode] = (z, np.array(rep.history), x)
-    for k in range(3):
-        assert np.array_equal(outs[GRID][k], outs[PIPELINED][k])
+    for mode in (PIPELINED, LEVEL, AUTO):
+        for k in range(3):
+            assert np.array_equal(outs[GRID][k], outs[mode][k]), mode
