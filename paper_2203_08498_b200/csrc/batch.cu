@@ -27,6 +27,7 @@ namespace rcg {
 
 constexpr int kRMax = 16;
 constexpr int kMaxRedB = 512;
+constexpr int kDepChunkHost = 8;  // the sweeps' dependency chunk (icsweep.cu kDepChunk)
 constexpr int kElemThreads = 192;  // a multiple of every RT (2, 4, 8, 12, 16): a thread keeps one rhs
 
 struct BState {
@@ -754,10 +755,17 @@ __global__ void __launch_bounds__(256) k_b_pupdate(const double* __restrict__ z,
             zi[2 * v + 1] = t.y;
         }
         if (W)
-            for (int j = 0; j < m; ++j) {
-                const double wj = __ldg(W + j * ldw + i);
+            for (int j0 = 0; j0 < m; j0 += 8) {  // eight column loads in flight, then the sums in order
+                const int mm = min(8, m - j0);
+                double wj[8];
 #pragma unroll
-                for (int v = 0; v < VW; ++v) zi[v] = fadd_mul(zi[v], us[j * RT + k0 + v], wj);
+                for (int t = 0; t < 8; ++t)
+                    if (t < mm) wj[t] = __ldg(W + (j0 + t) * ldw + i);
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (t < mm)
+#pragma unroll
+                        for (int v = 0; v < VW; ++v) zi[v] = fadd_mul(zi[v], us[(j0 + t) * RT + k0 + v], wj[t]);
             }
 #pragma unroll
         for (int v = 0; v < VW; ++v)
@@ -929,41 +937,81 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_b_tallt(const double* __res
     }
 }
 
-// y -= sum_j u[j][k] C_j (running rhs, lane per row) with (p, y) -> alpha (mode 0) or the
-// projected initial residual check (mode 1)
+// y -= sum_j u[j][k] C_j (running rhs) with (p, y) -> alpha (mode 0) or the projected initial
+// residual check (mode 1).  Chunked like k_b_pupdate: a thread carries VW consecutive values of
+// one row (coalesced 16-byte accesses, the block's chunk index fixed because kElemThreads is a
+// multiple of every G), u staged in shared memory (read as broadcasts: the m-loop is instruction-
+// bound at m = 32 otherwise); each value's update runs over j in order (subtract_combination).
 template <int RT>
-__global__ void __launch_bounds__(kStreamThreads) k_b_deflate(double* __restrict__ y, const double* __restrict__ Cm,
-                                                              int64_t ldc, int m, const double* __restrict__ u,
-                                                              const double* __restrict__ p, int32_t n, double* partials,
-                                                              BState* st, int mode) {
+__global__ void __launch_bounds__(kElemThreads) k_b_deflate(double* __restrict__ y, const double* __restrict__ Cm,
+                                                            int64_t ldc, int m, const double* __restrict__ u,
+                                                            const double* __restrict__ p, int32_t n, double* partials,
+                                                            BState* st, int mode) {
+    constexpr int VW = RT % 4 == 0 ? 4 : 2;
+    constexpr int G = RT / VW;
+    __shared__ double us[kMaxRedB];
     __shared__ double scratch[32 * RT];
     __shared__ double vals[RT];
     __shared__ double tot[RT];
     __shared__ int run[RT];
     if (st->nrun == 0 && mode == 0) return;
+    for (int t = threadIdx.x; t < m * RT; t += blockDim.x) us[t] = u[t];
     if (threadIdx.x < RT) run[threadIdx.x] = mode == 1 || st->done[threadIdx.x] == kRunning;
     __syncthreads();
-    double acc[RT];
+    const int c = threadIdx.x % G;  // fixed chunk: kElemThreads % G == 0, grid stride too
+    const int k0 = c * VW;
+    double acc[VW];
 #pragma unroll
-    for (int v = 0; v < RT; ++v) acc[v] = 0.0;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int64_t me = static_cast<int64_t>(i) * RT;
-        double yv[RT];
+    for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+    const int64_t items = static_cast<int64_t>(n) * G;
+    for (int64_t it = blockIdx.x * static_cast<int64_t>(kElemThreads) + threadIdx.x; it < items;
+         it += static_cast<int64_t>(gridDim.x) * kElemThreads) {
+        const int64_t i = it / G;
+        const int64_t e0 = it * VW;
+        double yv[VW];
 #pragma unroll
-        for (int v = 0; v < RT; ++v) yv[v] = y[me + v];
-        for (int j = 0; j < m; ++j) {
-            const double cj = __ldg(Cm + j * ldc + i);
+        for (int v = 0; v < VW / 2; ++v) {
+            const double2 t = reinterpret_cast<const double2*>(y + e0)[v];
+            yv[2 * v] = t.x;
+            yv[2 * v + 1] = t.y;
+        }
+        for (int j0 = 0; j0 < m; j0 += 8) {  // eight column loads in flight, then the updates in order
+            const int mm = min(8, m - j0);
+            double cj[8];
 #pragma unroll
-            for (int v = 0; v < RT; ++v) yv[v] = fsub_mul(yv[v], u[j * RT + v], cj);
+            for (int t = 0; t < 8; ++t)
+                if (t < mm) cj[t] = __ldg(Cm + (j0 + t) * ldc + i);
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (t < mm)
+#pragma unroll
+                    for (int v = 0; v < VW; ++v) yv[v] = fsub_mul(yv[v], us[(j0 + t) * RT + k0 + v], cj[t]);
+        }
+        double pv[VW];
+        if (mode == 0) {
+#pragma unroll
+            for (int v = 0; v < VW / 2; ++v) {
+                const double2 t = reinterpret_cast<const double2*>(p + e0)[v];
+                pv[2 * v] = t.x;
+                pv[2 * v + 1] = t.y;
+            }
         }
 #pragma unroll
-        for (int v = 0; v < RT; ++v)
-            if (run[v]) {
-                y[me + v] = yv[v];
-                acc[v] = mode == 0 ? fadd_mul(acc[v], p[me + v], yv[v]) : fadd_mul(acc[v], yv[v], yv[v]);
+        for (int v = 0; v < VW; ++v)
+            if (run[k0 + v]) {
+                y[e0 + v] = yv[v];
+                acc[v] = mode == 0 ? fadd_mul(acc[v], pv[v], yv[v]) : fadd_mul(acc[v], yv[v], yv[v]);
             }
     }
-    block_sum_dyn<RT>(acc, RT, scratch, vals);
+    double full[RT];  // this thread's chunk, zeros elsewhere (adding 0.0 is exact)
+#pragma unroll
+    for (int t = 0; t < RT; ++t) full[t] = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < G; ++cc)
+        if (cc == c)
+#pragma unroll
+            for (int v = 0; v < VW; ++v) full[cc * VW + v] = acc[v];
+    block_sum_dyn<RT>(full, RT, scratch, vals);
     if (grid_reduce_dyn(vals, RT, partials, &st->tick[3], tot) && threadIdx.x < RT) {
         const int k = threadIdx.x;
         if (mode == 0) {
@@ -1185,6 +1233,7 @@ struct BatchSolve {
     const rcg_basis* scb = nullptr;
     BatchWs* w = nullptr;
     int sg = 1, pg = 1;
+    int bcap = 256;  // batched SpMV stage capacity (entries per warp tile)
     int eg = 1;  // element-parallel grid (kElemThreads)
     int start_iter = 1;
     SlotMap map;  // slot k <-> original right-hand side map.col[k]
@@ -1208,6 +1257,19 @@ struct BatchSolve {
         w = &batch_ws(slot, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
         sg = stream_grid(ctx, n);
         pg = spmv_grid(ctx, n);
+        // The batched SpMV hides its RT-wide gathers with resident warps and L1: a matrix whose
+        // widest tile needs a big stage (C3's 27-point rows: ~900 entries -> 1 CTA per SM, no L1,
+        // 12 % of HBM) keeps a small stage (wider tiles read global memory through L1) instead.
+        // RCG_BSPMV_CAP overrides.
+        {
+            static const int env_cap = [] {
+                const char* e = std::getenv("RCG_BSPMV_CAP");
+                return e ? std::atoi(e) : 0;
+            }();
+            // measured (C3 / C5, RT 12): cap 896 12.1 / 3.5 ms, 384 7.5 / 2.0 ms, 128 4.1 / 1.46 ms --
+            // the L1 left to the gathers matters more than staging wide tiles
+            bcap = env_cap > 0 ? env_cap : (a->cap <= 256 ? a->cap : 128);
+        }
         if (bspmv_min_blocks(RT) > 2) {  // wider rows: one more resident CTA per SM (RT 12: 272 -> 210 us)
             const int blocks = ((n + 31) / 32 + kPipeWarps - 1) / kPipeWarps;
             pg = std::max(1, std::min(blocks, ctx->num_sms * (ctx->spmv_bps + bspmv_min_blocks(RT) - 2)));
@@ -1298,14 +1360,14 @@ struct BatchSolve {
             launch_fill_bits(ctx, w->zs, nrt, kSentinelBits);
         }
         const bool dfl = defl && defl->k > 0;
-        k_b_residual<RT><<<pg, kSpmvThreads, spmv_smem(a), ctx->stream>>>(sargs(), a->cap, w->b, w->x, w->r, w->st,
+        k_b_residual<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(sargs(), bcap, w->b, w->x, w->r, w->st,
                                                                           w->partials, dfl ? 1 : 0);
         RCG_LAUNCHED(ctx);
         if (dfl) {
             k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->r, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
-            k_b_deflate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr,
+            k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr,
                                                                     n, w->partials, w->st, 1);
             RCG_LAUNCHED(ctx);
         }
@@ -1344,7 +1406,7 @@ struct BatchSolve {
         const bool dfl = defl && defl->k > 0;
         {
             KTimer t(ctx, 5, RT);
-            k_b_spmv_pq<RT><<<pg, kSpmvThreads, spmv_smem(a), ctx->stream>>>(sargs(), a->cap, w->p, w->q, w->st,
+            k_b_spmv_pq<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(sargs(), bcap, w->p, w->q, w->st,
                                                                              w->partials, dfl ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
@@ -1353,7 +1415,7 @@ struct BatchSolve {
             k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 1);
             RCG_LAUNCHED(ctx);
-            k_b_deflate<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, n,
+            k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, n,
                                                                     w->partials, w->st, 0);
             RCG_LAUNCHED(ctx);
         }
@@ -1375,7 +1437,11 @@ struct BatchSolve {
         const rcg_ic* f = m->ic;
         // RCG_BSWEEP=0 selects the row-lane sweep (A/B only); default: chunk lanes
         static const int mode = std::getenv("RCG_BSWEEP") ? std::atoi(std::getenv("RCG_BSWEEP")) : 1;
-        const int bps0 = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, s.npos);
+        // residency: the single-sweep rule, except that the batched backward sweep keeps the
+        // forward's CTAs (C3 RT 12: bwd 14.3 -> 8.7 ms) and rows of more than one dependency chunk
+        // take 3 (C3 RT 12: fwd 5.4 -> 4.9, bwd 8.7 -> 7.8 ms)
+        int bps0 = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, false, s.npos);
+        if (ctx->sweep_bps <= 0 && f->n > 0 && static_cast<double>(f->nnz_l) / f->n > kDepChunkHost) bps0 = std::max(bps0, 3);
         s.backoff_ns = ctx->sweep_backoff_ns;
         KTimer t(ctx, backward ? 7 : 6, RT);
         if (mode != 0) {

@@ -1,5 +1,5 @@
-// icsweep_lv.cu -- IC(0) sweeps one LEVEL per launch, for factors whose levels are wide (C4's
-// 87K-row levels, C5, the multicolour orderings' 2-12 colours).
+// icsweep_lv.cu -- IC(0) sweeps one LEVEL per launch, for factors whose levels are very wide (the
+// multicolour orderings: 1M+ rows per colour on C2-C4).
 //
 // On very wide levels the sync-free sweep (icsweep.cu) is bound by each warp's chain of
 // dependent loads, not by the level chain (C4 multicolour: 2 levels of 67M rows at 19-22 % of
