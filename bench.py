@@ -172,6 +172,7 @@ def run_ours(args, rank, world, local_rank):
               "accelerated_ms": round(sum(w[k] for k in range(1, len(w), 16)) * 1e3, 2),
               "accelerated_iterations": last["iterations"][1:], "m_tilde": last["m_tilde"],
               "max_true_relres": max(last["true_relres"])}
+    cost = cost_model_report(n, n_nnz, cfg.keep, phases)
     # e2e through the public API with host buffers
     for _ in range(max(1, args.warmup // 2)):
         step_e2e()
@@ -228,6 +229,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof,
         "kernels": kernels,
         "phases_ms_untimed_step": phases,
+        "cost_model": cost,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -265,6 +267,29 @@ def algorithmic_bytes(c, n, nnz, nnz_l, m):
         2: (12 * nnz_l + 16 * n, 24 * n),   # U entries, perm+row starts, d | y in, z out, r
         4: (8 * m * n, 8 * n),              # W | the projected vector
     }.get(c % 5)
+
+
+def cost_model_report(n, nnz, m_tilde, phases):
+    """The paper's memory-traffic model (cost_model.cpp via paper_2203_08498_b200/cost_model.py)
+    at the measured HBM bandwidth against the step's measured per-iteration times, and
+    compare_measured's gamma (accelerated per-iteration time / ICCG per-iteration time; the
+    accelerated solves run batched, so per right-hand-side iteration)."""
+    from paper_2203_08498_b200 import cost_model as cm
+
+    bw = peaks()[0] * 1e9
+    p = cm.CostParams(float(n), float(nnz), float(m_tilde), bw)
+    it1, t1 = phases["solve1_iterations"], phases["solve1_ms"] * 1e-3
+    ita, ta = sum(phases["accelerated_iterations"]), phases["accelerated_ms"] * 1e-3
+    out = {"t_iccg_model_us": round(cm.t_iccg(p) * 1e6, 2), "t_sciccg_model_us": round(cm.t_sciccg(p) * 1e6, 2),
+           "gamma_predicted": round(cm.gamma_sciccg(m_tilde, nnz / max(n, 1)), 4)}
+    if it1 > 0 and t1 > 0:
+        out["iccg_measured_us"] = round(t1 / it1 * 1e6, 2)
+        out["iccg_model_fraction"] = round(cm.t_iccg(p) / (t1 / it1), 4)
+    if it1 > 0 and t1 > 0 and ita > 0:
+        c = cm.compare_measured(it1, t1, ita, ta, m_tilde, nnz / max(n, 1))
+        out.update(accelerated_us_per_rhs_iteration=round(ta / ita * 1e6, 2), gamma_measured=round(c.measured, 4),
+                   gamma_rel_error=round(c.rel_error, 4))
+    return out
 
 
 # inter-SM publish -> observe latency of one dependency hop (tools/pingpong.cu, B200: 0.36-0.54 us)
