@@ -260,6 +260,11 @@ typedef struct {
 } rcg_gen_params;
 int rcg_generate(const rcg_gen_params* p, int32_t* n, int64_t* nnz, int32_t** row_start,
                  int32_t** col_idx, double** values);
+/* the 7-point kinds (POISSON7, FV7_CONTRAST) assembled directly in HBM (no host arrays, no H2D):
+ * bitwise the host generator's CSR */
+int rcg_matrix_generate(rcg_ctx* ctx, const rcg_gen_params* p, rcg_matrix** out);
+/* the device matrix back to host arrays (row_start n + 1, col_idx / values nnz; any null skipped) */
+int rcg_matrix_export(rcg_ctx* ctx, const rcg_matrix* a, int32_t* row_start, int32_t* col_idx, double* values);
 /* UniformPm1 stream (rng.hpp:18-41): draws [skip, skip+n) of seed into out */
 void rcg_uniform_pm1(uint64_t seed, uint64_t skip, int64_t n, double* out);
 /* N(0,1) by Box-Muller over the same mt19937_64 stream (2 draws per pair) */

@@ -175,6 +175,8 @@ SIGNATURES = {
                              C.c_uint64, C.POINTER(SolveReport), C.POINTER(CondEstimate)),
     "rcg_lanczos_extremes": (C.c_int, C.c_int, vp, vp, dp, dp),
     "rcg_generate": (C.c_int, C.POINTER(GenParams), i32p, i64p, C.POINTER(i32p), C.POINTER(i32p), C.POINTER(dp)),
+    "rcg_matrix_generate": (C.c_int, vp, C.POINTER(GenParams), C.POINTER(vp)),
+    "rcg_matrix_export": (C.c_int, vp, vp, vp, vp, vp),
     "rcg_uniform_pm1": (None, C.c_uint64, C.c_uint64, C.c_int64, vp),
     "rcg_normal": (None, C.c_uint64, C.c_uint64, C.c_int64, vp),
     "rcg_host_free": (None, vp),

@@ -148,6 +148,14 @@ class CsrMatrix:
         check(lib.rcg_matrix_values(self.ctx.h, self.h, _ptr(out)))
         return out
 
+    def export(self):
+        """(row_start, col_idx, values) back on the host (rcg_matrix_export)."""
+        rs = np.empty(self.n + 1, np.int32)
+        ci = np.empty(self.nnz, np.int32)
+        va = np.empty(self.nnz)
+        check(lib.rcg_matrix_export(self.ctx.h, self.h, _ptr(rs), _ptr(ci), _ptr(va)))
+        return rs, ci, va
+
     def spmv(self, x, y=None):
         x = _f64(x, self.n, "x")
         if y is None:

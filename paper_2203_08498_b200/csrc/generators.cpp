@@ -62,13 +62,15 @@ Csr poisson7(int32_t N) {
 // Dirichlet neighbour contributes k_cell to the diagonal (unit coefficient gives C1 exactly).
 // `count` disjoint cubes of edge `size` cells (one-cell gap, off the boundary) at seeded
 // positions carry coefficient `contrast`.
-Csr fv7_contrast(int32_t N, int count, int size, double contrast, uint64_t seed) {
-    const int64_t n = static_cast<int64_t>(N) * N * N;
-    require(n < (1LL << 31), "generator: grid too large for int32 rows");
-    std::vector<float> kap(n, 1.0f);   // marker only; coefficient recomputed as double
-    std::vector<uint8_t> inc(n, 0);
+}  // namespace
+
+// inclusion origins of the FV contrast generator (shared with the device generator, gen_device.cu)
+void fv7_inclusion_origins(int32_t N, int count, int size, uint64_t seed, std::vector<int>& ox, std::vector<int>& oy,
+                           std::vector<int>& oz) {
     std::mt19937_64 g(seed);
-    std::vector<int> ox, oy, oz;
+    ox.clear();
+    oy.clear();
+    oz.clear();
     require(size >= 1 && size + 2 <= N, "generator: inclusion does not fit the grid");
     const int span = N - size - 1;  // origin in [1, span]
     int placed = 0;
@@ -86,6 +88,17 @@ Csr fv7_contrast(int32_t N, int count, int size, double contrast, uint64_t seed)
         ++placed;
     }
     require(placed == count, "generator: could not place the inclusions disjointly");
+}
+
+namespace {
+
+Csr fv7_contrast(int32_t N, int count, int size, double contrast, uint64_t seed) {
+    const int64_t n = static_cast<int64_t>(N) * N * N;
+    require(n < (1LL << 31), "generator: grid too large for int32 rows");
+    std::vector<float> kap(n, 1.0f);   // marker only; coefficient recomputed as double
+    std::vector<uint8_t> inc(n, 0);
+    std::vector<int> ox, oy, oz;
+    fv7_inclusion_origins(N, count, size, seed, ox, oy, oz);
     const int64_t sy = N, sz = static_cast<int64_t>(N) * N;
     for (int c = 0; c < count; ++c)
         for (int z = oz[c]; z < oz[c] + size; ++z)

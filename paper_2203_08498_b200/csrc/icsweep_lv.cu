@@ -13,7 +13,7 @@
 // Operator identity: each row is the reference loop (src/ic_preconditioner.cpp:130-143) --
 // forward s = r_i, s -= l_ik y_k in stored order; backward s = y_i / d_i, s -= u_ik z_k -- so the
 // output is bitwise k_sweep's; the (r, z) partials are formed per 32-position tile and reduced in
-// k_sweep's tile -> group -> total order (k_level_rho), so rho is bitwise too.
+// k_sweep's tile -> group -> total order (k_level_groups, k_level_total), so rho is bitwise too.
 // Roofline: the same algorithmic bytes as the sweep (12 nnz_L + 24..40 n per sweep), HBM-bound
 // per level; reported in the same kernel classes (1 forward, 2 backward).
 #include <algorithm>
@@ -80,23 +80,27 @@ __global__ void __launch_bounds__(kSpmvThreads) k_level_sweep(LevelArgs a) {
               });
 }
 
-// rho = (r, z) from the per-tile partials in k_sweep's tile_reduce order (groups of kGroup tiles
-// lane-strided then warp-summed, then the groups the same way) and the scalar update of
-// src/pcg.cpp:65-71 (+ the subspace-correction term)
-__global__ void __launch_bounds__(1024) k_level_rho(const double* __restrict__ partials, double* __restrict__ gpart,
-                                                    int ntiles, DevState* st, int add_sc) {
+// rho = (r, z) from the per-tile partials in k_sweep's tile_reduce order: k_level_groups sums each
+// group of kGroup tiles (lane-strided, then warp-summed; one warp per group), k_level_total the
+// groups the same way and runs the scalar update of src/pcg.cpp:65-71 (+ the SC term)
+__global__ void __launch_bounds__(256) k_level_groups(const double* __restrict__ partials, double* __restrict__ gpart,
+                                                      int ntiles, const DevState* st) {
     if (st->done) return;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int ngroups = (ntiles + kGroup - 1) / kGroup;
-    for (int g = w; g < ngroups; g += nw) {
-        const int gsize = min(kGroup, ntiles - g * kGroup);
-        double gs = 0.0;
-        for (int q = lane; q < gsize; q += 32) gs = __dadd_rn(gs, partials[g * kGroup + q]);
-        gs = warp_sum(gs);
-        if (lane == 0) gpart[g] = gs;
-    }
-    __syncthreads();
-    if (w != 0) return;
+    const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (g >= ngroups) return;
+    const int gsize = min(kGroup, ntiles - g * kGroup);
+    double gs = 0.0;
+    for (int q = lane; q < gsize; q += 32) gs = __dadd_rn(gs, partials[g * kGroup + q]);
+    gs = warp_sum(gs);
+    if (lane == 0) gpart[g] = gs;
+}
+
+__global__ void k_level_total(const double* __restrict__ gpart, int ntiles, DevState* st, int add_sc) {
+    if (st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int ngroups = (ntiles + kGroup - 1) / kGroup;
     double ts = 0.0;
     for (int q = lane; q < ngroups; q += 32) ts = __dadd_rn(ts, gpart[q]);
     ts = warp_sum(ts);
@@ -160,7 +164,11 @@ bool launch_level_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs&
         RCG_LAUNCHED(ctx);
     }
     if (backward && s.r) {
-        k_level_rho<<<1, 1024, 0, ctx->stream>>>(s.partials, s.gpart, (s.npos + 31) / 32, s.st, s.add_sc);
+        const int ntiles = (s.npos + 31) / 32;
+        const int ngroups = (ntiles + kGroup - 1) / kGroup;
+        k_level_groups<<<(ngroups + 7) / 8, 256, 0, ctx->stream>>>(s.partials, s.gpart, ntiles, s.st);
+        RCG_LAUNCHED(ctx);
+        k_level_total<<<1, 32, 0, ctx->stream>>>(s.gpart, ntiles, s.st, s.add_sc);
         RCG_LAUNCHED(ctx);
     }
     return true;

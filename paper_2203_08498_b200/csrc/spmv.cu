@@ -359,6 +359,19 @@ int rcg_matrix_values(rcg_ctx* ctx, const rcg_matrix* a, double* values_out) {
     });
 }
 
+int rcg_matrix_export(rcg_ctx* ctx, const rcg_matrix* a, int32_t* row_start, int32_t* col_idx, double* values) {
+    return guard([&] {
+        require(ctx && a, "rcg_matrix_export: null argument");
+        if (row_start)
+            RCG_CK(cudaMemcpyAsync(row_start, a->rs, sizeof(int32_t) * (a->n + 1), cudaMemcpyDefault, ctx->stream));
+        if (col_idx && a->nnz)
+            RCG_CK(cudaMemcpyAsync(col_idx, a->ci, sizeof(int32_t) * a->nnz, cudaMemcpyDefault, ctx->stream));
+        if (values && a->nnz)
+            RCG_CK(cudaMemcpyAsync(values, a->va, sizeof(double) * a->nnz, cudaMemcpyDefault, ctx->stream));
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int rcg_spmv(rcg_ctx* ctx, const rcg_matrix* a, const double* x, double* y) {
     return guard([&] {
         Staged xs, ys;

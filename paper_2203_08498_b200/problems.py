@@ -103,6 +103,18 @@ def generate(cfg: Config) -> HostCsr:
                    _adopt(va, nnz.value, C.c_double, np.float64))
 
 
+def generate_device(ctx, cfg: Config):
+    """The 7-point configs (C1, C2, C4) assembled directly in HBM (rcg_matrix_generate): an
+    api.CsrMatrix bitwise equal to generate(cfg), without host arrays or an H2D copy."""
+    from . import api
+
+    p = L.GenParams(cfg.kind, cfg.grid, cfg.inclusions, cfg.inclusion_size, cfg.contrast, cfg.sigma, cfg.knn_k,
+                    cfg.seed)
+    h = C.c_void_p()
+    check(lib.rcg_matrix_generate(ctx.h, C.byref(p), C.byref(h)))
+    return api.CsrMatrix(ctx, 0, None, None, None, _handle=h)
+
+
 def uniform_pm1(seed: int, skip: int, n: int) -> np.ndarray:
     out = np.empty(n)
     lib.rcg_uniform_pm1(C.c_uint64(seed), C.c_uint64(skip), n, out.ctypes.data)
