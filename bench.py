@@ -125,7 +125,8 @@ def run_ours(args, rank, world, local_rank):
     last = {}
 
     def run(B, X):
-        rep = seq.run(B, X, cfg.eps, cfg.max_iter, "A", cfg.sampler_m, keep_count=cfg.keep, batch=True)
+        rep = seq.run(B, X, cfg.eps, cfg.max_iter, "A", cfg.sampler_m, keep_count=cfg.keep, batch=True,
+                      condest=cfg.condest)  # C5: a Lanczos condition estimate on every solve
         last.update(rep)
         return sum(rep["iterations"])
 
@@ -172,6 +173,8 @@ def run_ours(args, rank, world, local_rank):
               "accelerated_ms": round(sum(w[k] for k in range(1, len(w), 16)) * 1e3, 2),
               "accelerated_iterations": last["iterations"][1:], "m_tilde": last["m_tilde"],
               "max_true_relres": max(last["true_relres"])}
+    if "kappa" in last:
+        phases["lanczos_kappa"] = [float(f"{v:.6g}") for v in last["kappa"]]
     cost = cost_model_report(n, n_nnz, cfg.keep, phases)
     # e2e through the public API with host buffers
     for _ in range(max(1, args.warmup // 2)):

@@ -384,6 +384,13 @@ typedef struct {
     double theta_used;
     double w_build_time, avg_iterations, avg_wall_time, setup_time;
     int acceleration_inactive;
+    /* k_t each (NULL to skip): the Lanczos estimate of every solve from its CG alpha / beta
+     * (the extremes of the tridiagonal T_k): lambda_min, lambda_max and kappa of
+     * the solve's preconditioned (solve 1: M^-1 A) or accelerated operator; NaN when a solve took
+     * no iteration */
+    double* lambda_min;
+    double* lambda_max;
+    double* kappa;
 } rcg_seq_report;
 int rcg_seq_prepare(rcg_ctx* ctx, const rcg_matrix* a_orig, int method, int blocks, rcg_seq** out);
 void rcg_seq_destroy(rcg_seq* s);

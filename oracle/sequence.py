@@ -68,6 +68,8 @@ def _record(o, out, rep, x, a_orig, b_orig, dis):
     out["iterations"].append(rep.iterations)
     out["converged"].append(rep.converged)
     out["histories"].append(rep.history)
+    out.setdefault("alphas", []).append(rep.alphas)
+    out.setdefault("betas", []).append(rep.betas)
     out["solutions"].append(x.copy())
     out["wall"].append(rep.wall_time)
     x_orig = dis * x

@@ -101,7 +101,8 @@ class SeqReport(C.Structure):
     _fields_ = [("iterations", ip), ("converged", ip), ("wall_time", dp), ("true_relres", dp),
                 ("ritz_values", dp), ("ritz_cap", C.c_int), ("m_bar", C.c_int), ("m_tilde", C.c_int),
                 ("theta_used", C.c_double), ("w_build_time", C.c_double), ("avg_iterations", C.c_double),
-                ("avg_wall_time", C.c_double), ("setup_time", C.c_double), ("acceleration_inactive", C.c_int)]
+                ("avg_wall_time", C.c_double), ("setup_time", C.c_double), ("acceleration_inactive", C.c_int),
+                ("lambda_min", dp), ("lambda_max", dp), ("kappa", dp)]
 
 
 def _sig(name, restype, *args):

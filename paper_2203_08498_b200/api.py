@@ -808,7 +808,7 @@ class Sequence:
         self.h, self.ctx, self.n, self.method = h, ctx, a_orig.n, method
 
     def run(self, B, X, eps: float = 1e-8, max_iter: int = 1000, sampling: str = "A", m: int = 16,
-            theta: float = 1e-3, keep_count: int = 0, batch: bool = True) -> dict:
+            theta: float = 1e-3, keep_count: int = 0, batch: bool = True, condest: bool = False) -> dict:
         k = len(B)
         cfg = L.SeqConfig(float(eps), int(max_iter), ord(sampling), int(m), float(theta), int(keep_count),
                           1 if batch else 0)
@@ -817,15 +817,19 @@ class Sequence:
         wall = np.zeros(k)
         trr = np.zeros(k)
         ritz = np.zeros(max(1, 2 * m))
+        lmin, lmax, kap = np.zeros(k), np.zeros(k), np.zeros(k)
         rep = L.SeqReport(its.ctypes.data_as(L.ip), conv.ctypes.data_as(L.ip), wall.ctypes.data_as(L.dp),
                           trr.ctypes.data_as(L.dp), ritz.ctypes.data_as(L.dp), len(ritz))
+        if condest:
+            rep.lambda_min, rep.lambda_max, rep.kappa = (v.ctypes.data_as(L.dp) for v in (lmin, lmax, kap))
         check(lib.rcg_seq_run(self.h, k, _ptr(B), _ptr(X), C.byref(cfg), C.byref(rep)))
         return dict(iterations=its.tolist(), converged=[bool(c) for c in conv], wall_time=wall.tolist(),
                     true_relres=trr.tolist(), m_bar=rep.m_bar, m_tilde=rep.m_tilde,
                     ritz_values=ritz[:min(rep.m_bar, len(ritz))].copy(), theta_used=rep.theta_used,
                     w_build_time=rep.w_build_time, avg_iterations=rep.avg_iterations,
                     avg_wall_time=rep.avg_wall_time, setup_time=rep.setup_time,
-                    acceleration_inactive=bool(rep.acceleration_inactive))
+                    acceleration_inactive=bool(rep.acceleration_inactive),
+                    **(dict(lambda_min=lmin.tolist(), lambda_max=lmax.tolist(), kappa=kap.tolist()) if condest else {}))
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -1074,6 +1074,8 @@ __global__ void __launch_bounds__(kElemThreads) k_b_xr(double* __restrict__ x, d
                 st->relres[k] = relres;
                 st->iters[k] = i;
                 hist[k * hist_ld + (i - 1)] = relres;
+                hist[(RT + k) * hist_ld + (i - 1)] = st->alpha[k];
+                hist[(2 * RT + k) * hist_ld + (i - 1)] = st->beta[k];
                 st->rho_prev[k] = st->rho[k];
                 if (relres <= st->eps) {
                     st->done[k] = kConverged;
@@ -1175,8 +1177,10 @@ __global__ void k_b_carry_state(const BState* __restrict__ a, BState* __restrict
         }
     }
     const int done_iters = a->iter - 1;
-    for (int k = 0; k < sel.cnt; ++k)
-        for (int i = t; i < done_iters; i += blockDim.x) hist_b[k * hist_ld + i] = hist_a[sel.slot[k] * hist_ld + i];
+    for (int blk = 0; blk < 3; ++blk)  // relres, alpha, beta blocks
+        for (int k = 0; k < sel.cnt; ++k)
+            for (int i = t; i < done_iters; i += blockDim.x)
+                hist_b[(blk * rt_out + k) * hist_ld + i] = hist_a[(blk * rt_in + sel.slot[k]) * hist_ld + i];
     for (int e = t; e < m * rt_out; e += blockDim.x) {
         const int j = e / rt_out, k = e % rt_out;
         u2b[e] = k < sel.cnt ? u2a[j * rt_in + sel.slot[k]] : 0.0;
@@ -1254,7 +1258,9 @@ struct BatchSolve {
         int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 3) / 4 : 1;  // >= RPW 4
         const int64_t groups = (ntiles + kGroup - 1) / kGroup;
         const int64_t part = std::max<int64_t>(ntiles * RT, static_cast<int64_t>(kMaxRedB) * ctx->num_sms * 8);
-        w = &batch_ws(slot, nrt, static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part, groups);
+        // history: relres, alpha, beta blocks of RT rows each (the CG coefficients feed the Lanczos estimate)
+        w = &batch_ws(slot, nrt, 3 * static_cast<int64_t>(RT) * (max_iter + 1), static_cast<int64_t>(mm) * RT, part,
+                      groups);
         sg = stream_grid(ctx, n);
         pg = spmv_grid(ctx, n);
         // The batched SpMV hides its RT-wide gathers with resident warps and L1: a matrix whose
@@ -1559,10 +1565,13 @@ struct BatchSolve {
                 r.iterations = (h.done[k] == kZeroRhs) ? 0 : h.iters[k];
                 r.converged = (h.done[k] == kConverged || h.done[k] == kZeroRhs) ? 1 : 0;
                 const int cnt = std::min(r.iterations, r.cap);
-                if (r.history && cnt > 0) {
-                    RCG_CK(cudaMemcpy(r.history, w->hist + static_cast<int64_t>(k) * (max_iter + 1), sizeof(double) * cnt,
-                                      cudaMemcpyDeviceToHost));
-                }
+                const int64_t hl = max_iter + 1;
+                if (r.history && cnt > 0)
+                    RCG_CK(cudaMemcpy(r.history, w->hist + k * hl, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+                if (r.alphas && cnt > 0)
+                    RCG_CK(cudaMemcpy(r.alphas, w->hist + (RT + k) * hl, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+                if (r.betas && cnt > 0)
+                    RCG_CK(cudaMemcpy(r.betas, w->hist + (2 * RT + k) * hl, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
                 if (h.done[k] == kBroken && (job.broken < 0 || out.col[q] < job.broken)) {
                     job.broken = out.col[q];
                     job.broken_status = h.status[k];

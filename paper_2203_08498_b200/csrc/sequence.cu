@@ -144,6 +144,15 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
             rcg_prec inner{s->ic ? RCG_PREC_IC : RCG_PREC_IDENTITY, s->ic, nullptr};
             std::vector<rcg_solve_report> reps(k_t);
             for (auto& r : reps) std::memset(&r, 0, sizeof(r));
+            // CG coefficients of every solve for the Lanczos estimate (condest on each solve, C5)
+            const bool lanczos = rep->lambda_min || rep->lambda_max || rep->kappa;
+            std::vector<double> coef(lanczos ? static_cast<size_t>(k_t) * 2 * cfg->max_iter : 0);
+            if (lanczos)
+                for (int k = 0; k < k_t; ++k) {
+                    reps[k].cap = cfg->max_iter;
+                    reps[k].alphas = coef.data() + static_cast<size_t>(2 * k) * cfg->max_iter;
+                    reps[k].betas = coef.data() + static_cast<size_t>(2 * k + 1) * cfg->max_iter;
+                }
             // solve 1 with the error-sampling observer (driver.cpp:147-160)
             if (recycled) {
                 if (cfg->sampling == 'A')
@@ -211,6 +220,14 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
                 if (rep->converged) rep->converged[k] = reps[k].converged;
                 if (rep->wall_time) rep->wall_time[k] = reps[k].wall_time;
                 if (rep->true_relres) rep->true_relres[k] = h[0] == 0.0 ? 0.0 : std::sqrt(h[1]) / std::sqrt(h[0]);
+                if (lanczos) {
+                    double lo = NAN, hi = NAN;
+                    const int it = std::min(reps[k].iterations, cfg->max_iter);
+                    if (it >= 1) lanczos_extremes_host(it, reps[k].alphas, reps[k].betas, &lo, &hi);
+                    if (rep->lambda_min) rep->lambda_min[k] = lo;
+                    if (rep->lambda_max) rep->lambda_max[k] = hi;
+                    if (rep->kappa) rep->kappa[k] = hi / lo;
+                }
                 if (k > 0) {
                     acc_it += reps[k].iterations;
                     acc_wall += reps[k].wall_time;

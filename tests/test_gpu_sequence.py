@@ -72,3 +72,30 @@ def test_device_sequence_config_errors(ctx, problems):
     seq = api.Sequence(ctx, a, "iccg")
     with pytest.raises(ParseError):
         seq.run(np.zeros((2, h.n)), np.zeros((2, h.n)), eps=2.0)
+
+
+@pytest.mark.parametrize("name", ["c5", "c1"])
+@pytest.mark.parametrize("batch", [True, False])
+def test_sequence_lanczos_condest_each_solve(ctx, oracle, problems, name, batch):
+    """C5's protocol: a Lanczos condition-number estimate on every solve of the sequence, from
+    the solve's own CG alpha / beta (batched solves record them per right-hand
+    side) -- within the north star's 1 % of the oracle's estimate from its alpha / beta."""
+    from oracle.sequence import rhs_set, run_sequence as oracle_sequence
+    from paper_2203_08498_b200 import api
+
+    cfg = replace(problems.SMALL[name], n_rhs=4)
+    h = problems.generate(cfg)
+    ores = oracle_sequence(oracle, cfg, h)
+    a_o = Matrix.of(h)
+    _, dis = oracle.diagonal_scale(a_o)
+    b_orig, _ = rhs_set(oracle, cfg, h, a_o, dis)
+    X = np.zeros((cfg.n_rhs, h.n))
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+    seq = api.Sequence(ctx, a, "es-sc-iccg" if cfg.method == "sc" else "es-d-iccg")
+    rep = seq.run(np.stack(b_orig), X, cfg.eps, cfg.max_iter, "A", cfg.sampler_m, keep_count=cfg.keep, batch=batch,
+                  condest=True)
+    for k in range(cfg.n_rhs):
+        lo, hi = oracle.lanczos_extremes(ores["alphas"][k], ores["betas"][k])
+        assert abs(rep["kappa"][k] / (hi / lo) - 1.0) <= 0.01, (k, rep["kappa"][k], hi / lo)
+        assert rep["lambda_min"][k] > 0 and rep["lambda_max"][k] >= rep["lambda_min"][k]
+    assert rep["kappa"][1] < rep["kappa"][0]  # the accelerated operator is better conditioned
