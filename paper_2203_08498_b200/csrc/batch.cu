@@ -836,11 +836,11 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
 // (mode 1) and f.u (mode 2).  Host grid: X x P (BatchSolve::tgrid).
 template <int RT>
 __device__ __host__ constexpr int tallt_jc() {
-    return RT <= 4 ? 8 : (RT <= 8 ? 4 : 2);
+    return RT <= 8 ? 4 : 2;   // RT 4 with 8 columns spilled (R 4 slower than R 8)
 }
 
 template <int RT>
-__global__ void __launch_bounds__(kElemThreads, 6) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
+__global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
                                                             const double* __restrict__ y, int32_t n,
                                                             double* partials, const double* __restrict__ L,
                                                             double* __restrict__ u, int mode, BState* st,
@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_b_tallt(const double* __res
     constexpr int JC = tallt_jc<RT>();
     constexpr int VW = RT % 4 == 0 ? 4 : 2;  // values per thread: G = RT/VW threads per row
     constexpr int G = RT / VW;
-    __shared__ double scratch[32 * JC * RT];
+    __shared__ double scratch[RT >= 12 ? 32 * JC * RT : kElemThreads * JC * (RT % 4 == 0 ? 4 : 2)];
     __shared__ double bvals[JC * RT];
     __shared__ double tot[kMaxRedB];
     __shared__ double fk[6][128];
@@ -887,19 +887,35 @@ __global__ void __launch_bounds__(kElemThreads, 6) k_b_tallt(const double* __res
                     for (int v = 0; v < VW; ++v) acc[jc][v] = fadd_mul(acc[jc][v], wj, yv[v]);
                 }
         }
-        double full[JC * RT];  // this thread's chunk, zeros elsewhere (adding 0.0 is exact)
+        if constexpr (RT >= 12) {
+            double full[JC * RT];  // this thread's chunk, zeros elsewhere (adding 0.0 is exact)
 #pragma unroll
-        for (int t = 0; t < JC * RT; ++t) full[t] = 0.0;
+            for (int t = 0; t < JC * RT; ++t) full[t] = 0.0;
 #pragma unroll
-        for (int cc = 0; cc < G; ++cc)
-            if (cc == c)
+            for (int cc = 0; cc < G; ++cc)
+                if (cc == c)
 #pragma unroll
-                for (int jc = 0; jc < JC; ++jc)
+                    for (int jc = 0; jc < JC; ++jc)
 #pragma unroll
-                    for (int v = 0; v < VW; ++v) full[jc * RT + cc * VW + v] = acc[jc][v];
-        block_sum_dyn<JC * RT>(full, mc * RT, scratch, bvals);
-        for (int t = threadIdx.x; t < mc * RT; t += blockDim.x)
-            partials[static_cast<int64_t>(j0 * RT + t) * X + x] = bvals[t];
+                        for (int v = 0; v < VW; ++v) full[jc * RT + cc * VW + v] = acc[jc][v];
+            block_sum_dyn<JC * RT>(full, mc * RT, scratch, bvals);
+            for (int t = threadIdx.x; t < mc * RT; t += blockDim.x)
+                partials[static_cast<int64_t>(j0 * RT + t) * X + x] = bvals[t];
+        } else {
+            // block sum per output (jc, k): the threads of chunk c = k / VW in thread order (fixed),
+            // through shared memory (a per-thread JC x RT array spills at RT <= 8, JC = 4)
+#pragma unroll
+            for (int jc = 0; jc < JC; ++jc)
+#pragma unroll
+                for (int v = 0; v < VW; ++v) scratch[threadIdx.x * (JC * VW) + jc * VW + v] = acc[jc][v];
+            __syncthreads();
+            for (int o = threadIdx.x; o < mc * RT; o += blockDim.x) {
+                const int jc = o / RT, k = o % RT, cc = k / VW, v = k % VW;
+                double sv = 0.0;
+                for (int t = cc; t < kElemThreads; t += G) sv = __dadd_rn(sv, scratch[t * (JC * VW) + jc * VW + v]);
+                partials[static_cast<int64_t>(j0 * RT + o) * X + x] = sv;
+            }
+        }
     }
     __threadfence();
     __syncthreads();
@@ -1330,7 +1346,7 @@ struct BatchSolve {
     // k_b_tallt grid: X row ranges x P sibling column passes, about 4 CTAs per SM
     int tgrid(int mcols) const {
         const int P = std::max(1, (mcols + tallt_jc<RT>() - 1) / tallt_jc<RT>());
-        const int X = std::max(1, std::min((n + 255) / 256, ctx->num_sms * 6 / P));  // one wave
+        const int X = std::max(1, std::min((n + 255) / 256, ctx->num_sms * (RT <= 8 ? 4 : 6) / P));  // one wave
         return X * P;
     }  // (kElemThreads threads per CTA)
 
