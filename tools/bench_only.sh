@@ -1,0 +1,3 @@
+# dev: the default bench line (+ reference arm)
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
