@@ -372,6 +372,8 @@ typedef struct {
     double theta;     /* RunConfig::theta (Ritz selection threshold) */
     int keep_count;   /* > 0: keep that many Ritz vectors instead of theta (extension) */
     int batch;        /* solves 2..k_t as batched multi-RHS kernel sequences */
+    int memory;       /* 0: auto -- memory-lean recycling (errors / MGS in the sampler slots, streamed
+                       * Gram) and unbatched solves when HBM is short (C4 on one GPU); 1: lean always */
 } rcg_seq_config;
 typedef struct {
     int* iterations;      /* k_t (caller arrays; each may be NULL) */

@@ -94,7 +94,7 @@ class SlabPlanC(C.Structure):
 
 class SeqConfig(C.Structure):
     _fields_ = [("eps", C.c_double), ("max_iter", C.c_int), ("sampling", C.c_int), ("m", C.c_int),
-                ("theta", C.c_double), ("keep_count", C.c_int), ("batch", C.c_int)]
+                ("theta", C.c_double), ("keep_count", C.c_int), ("batch", C.c_int), ("memory", C.c_int)]
 
 
 class SeqReport(C.Structure):

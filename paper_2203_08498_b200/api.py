@@ -808,10 +808,12 @@ class Sequence:
         self.h, self.ctx, self.n, self.method = h, ctx, a_orig.n, method
 
     def run(self, B, X, eps: float = 1e-8, max_iter: int = 1000, sampling: str = "A", m: int = 16,
-            theta: float = 1e-3, keep_count: int = 0, batch: bool = True, condest: bool = False) -> dict:
+            theta: float = 1e-3, keep_count: int = 0, batch: bool = True, condest: bool = False,
+            lean: bool = False) -> dict:
+        """lean: the memory-lean recycling step always (default: only when HBM is short)."""
         k = len(B)
         cfg = L.SeqConfig(float(eps), int(max_iter), ord(sampling), int(m), float(theta), int(keep_count),
-                          1 if batch else 0)
+                          1 if batch else 0, 1 if lean else 0)
         its = np.zeros(k, np.int32)
         conv = np.zeros(k, np.int32)
         wall = np.zeros(k)

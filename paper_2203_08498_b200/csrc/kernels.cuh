@@ -108,6 +108,12 @@ void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args)
 bool launch_level_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);   // icsweep_lv.cu
 bool launch_cluster_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);  // icsweep_cl.cu
 void free_cluster_plans(rcg_ic* f);
+// memory-lean recycling step (recycle.cu): errors, MGS and the streamed Rayleigh-Ritz Gram in the
+// sampler's slots; W is a new n x m~ block
+void lean_build_aux(rcg_ctx* ctx, const rcg_matrix* a, const double* x_dev, rcg_sampler* s, double theta,
+                    int keep_count, int* m_bar, std::vector<double>& vals, double* theta_used, rcg_tall** w_out);
+// rcg_basis_create, optionally adopting w's column block (recycle.cu)
+void basis_build(rcg_ctx* ctx, const rcg_matrix* a, rcg_tall* w, int who, bool adopt, rcg_basis** out);
 void cluster_prof_dump(const char* tag);  // dev: RCG_CL_PROF
 SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward);
 void check_sweep_watchdog(rcg_ctx* ctx);

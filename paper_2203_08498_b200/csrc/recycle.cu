@@ -259,23 +259,26 @@ static double dev_dot(rcg_ctx* ctx, const double* a, const double* b, int32_t n,
     return h;
 }
 
-// single-pass MGS (src/dense.cpp:45-61)
-static rcg_tall* mgs(rcg_ctx* ctx, const rcg_tall* v, double drop_tol) {
-    ensure_red(ctx, v->n);
-    rcg_tall* e = tall_alloc(v->n, v->k);
-    const int32_t n = v->n;
+// single-pass MGS (src/dense.cpp:45-61) of the vk columns at v (leading dimension vld) into e
+// (leading dimension eld); returns the number kept.  e may be v itself (in place: the kept column
+// `kept` <= src is a column already consumed).
+static int mgs_core(rcg_ctx* ctx, const double* v, int64_t vld, int vk, int32_t n, double* e, int64_t eld,
+                    double drop_tol) {
+    ensure_red(ctx, n);
     const int g = stream_grid(ctx, n);
-    double* c = dev_alloc(v->k + 2);
+    double* c = dev_alloc(vk + 2);
     int kept = 0;
     try {
-        for (int src = 0; src < v->k; ++src) {
-            double* w = e->d + kept * e->ld;
-            k_copy_col<<<g, kStreamThreads, 0, ctx->stream>>>(v->d + src * v->ld, w, n);
-            RCG_LAUNCHED(ctx);
-            const double n0 = std::sqrt(dev_dot(ctx, w, w, n, c + v->k));
+        for (int src = 0; src < vk; ++src) {
+            double* w = e + kept * eld;
+            if (w != v + src * vld) {
+                k_copy_col<<<g, kStreamThreads, 0, ctx->stream>>>(v + src * vld, w, n);
+                RCG_LAUNCHED(ctx);
+            }
+            const double n0 = std::sqrt(dev_dot(ctx, w, w, n, c + vk));
             if (n0 == 0.0) continue;
             for (int q = 0; q <= kept; ++q) {
-                k_mgs_pass<<<g, kStreamThreads, 0, ctx->stream>>>(w, e->d, e->ld, q, kept, c, n, ctx->ws.partials,
+                k_mgs_pass<<<g, kStreamThreads, 0, ctx->stream>>>(w, e, eld, q, kept, c, n, ctx->ws.partials,
                                                                   &ctx->ws.st->tick[7]);
                 RCG_LAUNCHED(ctx);
             }
@@ -291,11 +294,20 @@ static rcg_tall* mgs(rcg_ctx* ctx, const rcg_tall* v, double drop_tol) {
         RCG_CK(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
         dev_free(c);
-        rcg_tall_destroy(e);
         throw;
     }
     dev_free(c);
-    e->k = kept;
+    return kept;
+}
+
+static rcg_tall* mgs(rcg_ctx* ctx, const rcg_tall* v, double drop_tol) {
+    rcg_tall* e = tall_alloc(v->n, v->k);
+    try {
+        e->k = mgs_core(ctx, v->d, v->ld, v->k, v->n, e->d, e->ld, drop_tol);
+    } catch (...) {
+        rcg_tall_destroy(e);
+        throw;
+    }
     return e;
 }
 
@@ -387,6 +399,147 @@ void condest_ritz(rcg_ctx* ctx, const rcg_matrix* a, const double* x_dev, rcg_sa
     }
     rcg_tall_destroy(errs);
     rcg_tall_destroy(e);
+}
+
+
+// ------------------------------------------------------------------ memory-lean recycling
+// For problems whose error block does not fit next to the sampler slots (C4 on one GPU: 64 slots
+// of 1.07 GB, and the standard path's E, its MGS copy and A E would add 3 x 69 GB): the errors
+// are formed in place in the slots (x - slot, recycling.cpp:17-28; exactly-zero columns skipped
+// and the rest compacted in slot order), orthonormalised in place (same MGS and drop rule), and
+// the Rayleigh-Ritz Gram is streamed one column at a time (S[:, j] = Q^T (A q_j), lower triangle
+// mirrored as rayleigh_ritz does) -- one extra n-vector instead of an n x k block.  The Ritz
+// values agree with the standard path to rounding (different dot grouping).  The sampler's slots
+// hold the orthonormal basis afterwards: the sampler is spent.
+__global__ void k_harvest_inplace(const double* __restrict__ x, double* __restrict__ slots, int64_t lds,
+                                  const int* __restrict__ list, int cnt, int32_t n, int* __restrict__ nonzero) {
+    for (int j = blockIdx.y; j < cnt; j += gridDim.y) {
+        double* s = slots + list[j] * lds;
+        int nz = 0;
+        for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            const double v = __dsub_rn(x[i], s[i]);
+            s[i] = v;
+            nz |= (v != 0.0);
+        }
+        if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(nonzero + j, 1);
+    }
+}
+
+void lean_build_aux(rcg_ctx* ctx, const rcg_matrix* a, const double* x_dev, rcg_sampler* s, double theta,
+                    int keep_count, int* m_bar, std::vector<double>& vals, double* theta_used, rcg_tall** w_out) {
+    *w_out = nullptr;
+    const int32_t n = s->n;
+    std::vector<int> occ(s->m);
+    RCG_CK(cudaMemcpy(occ.data(), s->occupied, sizeof(int) * s->m, cudaMemcpyDeviceToHost));
+    std::vector<int> list;
+    for (int j = 0; j < s->m; ++j)
+        if (occ[j]) list.push_back(j);
+    const int k0 = static_cast<int>(list.size());
+    int kk = 0;
+    if (k0 > 0 && n > 0) {
+        int* dl = static_cast<int*>(dev_alloc_bytes(sizeof(int) * k0));
+        int* nz = static_cast<int*>(dev_alloc_bytes(sizeof(int) * k0));
+        RCG_CK(cudaMemcpyAsync(dl, list.data(), sizeof(int) * k0, cudaMemcpyHostToDevice, ctx->stream));
+        RCG_CK(cudaMemsetAsync(nz, 0, sizeof(int) * k0, ctx->stream));
+        dim3 grid(stream_grid(ctx, n), std::min(k0, 64));
+        k_harvest_inplace<<<grid, kStreamThreads, 0, ctx->stream>>>(x_dev, s->slots, s->ld, dl, k0, n, nz);
+        RCG_LAUNCHED(ctx);
+        std::vector<int> hz(k0);
+        RCG_CK(cudaMemcpyAsync(hz.data(), nz, sizeof(int) * k0, cudaMemcpyDeviceToHost, ctx->stream));
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+        dev_free(dl);
+        dev_free(nz);
+        for (int j = 0; j < k0; ++j) {  // compact in slot order (targets are consumed columns)
+            if (!hz[j]) continue;
+            if (list[j] != kk)
+                RCG_CK(cudaMemcpyAsync(s->slots + kk * s->ld, s->slots + list[j] * s->ld, sizeof(double) * n,
+                                       cudaMemcpyDeviceToDevice, ctx->stream));
+            ++kk;
+        }
+    }
+    const int kept = kk ? mgs_core(ctx, s->slots, s->ld, kk, n, s->slots, s->ld, 1e-12) : 0;
+    *m_bar = kept;
+    vals.clear();
+    std::vector<double> T;
+    if (kept > 0) {
+        require(kept <= 128, "SmallSym: dimension " + std::to_string(kept) + " outside [0, 128]");
+        std::vector<double> S(static_cast<size_t>(kept) * kept, 0.0), f;
+        double* y = dev_alloc(std::max<int64_t>(s->ld, 1));
+        try {
+            for (int j = 0; j < kept; ++j) {
+                const int rc = rcg_spmv(ctx, a, s->slots + j * s->ld, y);
+                if (rc != RCG_OK) throw Error(rc, rcg_last_error());
+                tall_dot_host(ctx, s->slots, s->ld, kept, y, n, f);
+                for (int i = j; i < kept; ++i) S[static_cast<size_t>(i) * kept + j] = f[i];
+            }
+        } catch (...) {
+            dev_free(y);
+            throw;
+        }
+        dev_free(y);
+        for (int i = 0; i < kept; ++i)
+            for (int j = 0; j < i; ++j) S[static_cast<size_t>(j) * kept + i] = S[static_cast<size_t>(i) * kept + j];
+        sym_eig_host(kept, S, vals, T);
+    }
+    double th = theta;
+    if (keep_count > 0)
+        th = kept > keep_count ? 0.5 * (vals[keep_count - 1] + vals[keep_count]) : std::numeric_limits<double>::infinity();
+    if (theta_used) *theta_used = th;
+    int sel = 0;
+    while (sel < kept && vals[sel] < th) ++sel;
+    rcg_tall* out = tall_alloc(n, sel);
+    try {
+        combine_cols(ctx, s->slots, s->ld, kept, T.data(), sel, out->d, out->ld, n);
+    } catch (...) {
+        rcg_tall_destroy(out);
+        throw;
+    }
+    *w_out = out;
+}
+
+// rcg_basis_create; adopt = take over w's column block instead of copying it (w->d becomes null:
+// the memory-lean sequence on C4, where a 34 GB copy of W does not fit next to W and A W)
+void basis_build(rcg_ctx* ctx, const rcg_matrix* a, rcg_tall* w, int who, bool adopt, rcg_basis** out) {
+    {
+        *out = nullptr;
+        const char* whom = who == RCG_BASIS_SC ? "ScPreconditioner" : "build_deflation_operator";
+        if (w->k > 0 && w->n != a->n) throw Error(RCG_E_INVALID, std::string(whom) + ": W row count does not match A");
+        require(w->k <= 128, "SmallSym: dimension " + std::to_string(w->k) + " outside [0, 128]");
+        auto* b = new rcg_basis();
+        try {
+            b->n = a->n;
+            b->k = w->k;
+            b->ld = w->ld;
+            b->who = who;
+            if (b->k > 0) {
+                if (adopt) {
+                    b->w = w->d;
+                    w->d = nullptr;
+                } else {
+                    b->w = dev_alloc(b->ld * b->k);
+                    RCG_CK(cudaMemcpyAsync(b->w, w->d, sizeof(double) * b->ld * b->k, cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
+                }
+                b->aw = dev_alloc(b->ld * b->k);
+                launch_spmm(ctx, a, b->w, b->ld, b->aw, b->ld, b->k);
+                std::vector<double> s;
+                gram_host(ctx, b->w, b->ld, b->k, b->aw, b->ld, b->k, b->n, true, s);
+                const int k = b->k;
+                for (int i = 0; i < k; ++i)
+                    for (int j = 0; j < i; ++j) s[static_cast<size_t>(j) * k + i] = s[static_cast<size_t>(i) * k + j];
+                int bad = -1;
+                if (!chol_factor_host(k, s, b->h_l, &bad))
+                    throw Error(RCG_E_BREAKDOWN, std::string(whom) + ": W^T A W not SPD");
+                b->l = dev_alloc(static_cast<int64_t>(k) * k);
+                RCG_CK(cudaMemcpyAsync(b->l, b->h_l.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, ctx->stream));
+                RCG_CK(cudaStreamSynchronize(ctx->stream));
+            }
+        } catch (...) {
+            rcg_basis_destroy(b);
+            throw;
+        }
+        *out = b;
+    }
 }
 
 }  // namespace rcg
@@ -619,40 +772,7 @@ int rcg_build_aux_matrix(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* erro
 
 // ------------------------------------------------------------------ basis (deflation / SC)
 int rcg_basis_create(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* w, int who, rcg_basis** out) {
-    return guard([&] {
-        *out = nullptr;
-        const char* whom = who == RCG_BASIS_SC ? "ScPreconditioner" : "build_deflation_operator";
-        if (w->k > 0 && w->n != a->n) throw Error(RCG_E_INVALID, std::string(whom) + ": W row count does not match A");
-        require(w->k <= 128, "SmallSym: dimension " + std::to_string(w->k) + " outside [0, 128]");
-        auto* b = new rcg_basis();
-        try {
-            b->n = a->n;
-            b->k = w->k;
-            b->ld = w->ld;
-            b->who = who;
-            if (b->k > 0) {
-                b->w = dev_alloc(b->ld * b->k);
-                b->aw = dev_alloc(b->ld * b->k);
-                RCG_CK(cudaMemcpyAsync(b->w, w->d, sizeof(double) * b->ld * b->k, cudaMemcpyDeviceToDevice, ctx->stream));
-                launch_spmm(ctx, a, b->w, b->ld, b->aw, b->ld, b->k);
-                std::vector<double> s;
-                gram_host(ctx, b->w, b->ld, b->k, b->aw, b->ld, b->k, b->n, true, s);
-                const int k = b->k;
-                for (int i = 0; i < k; ++i)
-                    for (int j = 0; j < i; ++j) s[static_cast<size_t>(j) * k + i] = s[static_cast<size_t>(i) * k + j];
-                int bad = -1;
-                if (!chol_factor_host(k, s, b->h_l, &bad))
-                    throw Error(RCG_E_BREAKDOWN, std::string(whom) + ": W^T A W not SPD");
-                b->l = dev_alloc(static_cast<int64_t>(k) * k);
-                RCG_CK(cudaMemcpyAsync(b->l, b->h_l.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, ctx->stream));
-                RCG_CK(cudaStreamSynchronize(ctx->stream));
-            }
-        } catch (...) {
-            rcg_basis_destroy(b);
-            throw;
-        }
-        *out = b;
-    });
+    return guard([&] { basis_build(ctx, a, const_cast<rcg_tall*>(w), who, false, out); });
 }
 
 void rcg_basis_destroy(rcg_basis* b) {

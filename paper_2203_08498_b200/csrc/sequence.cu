@@ -167,16 +167,33 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
             rep->w_build_time = 0.0;
             if (recycled) {
                 const auto t0 = std::chrono::steady_clock::now();
-                ck(rcg_harvest_errors(ctx, xs, smp, &errors));
-                std::vector<double> vals(std::max(errors->k, 1));
-                ck(rcg_build_aux_matrix(ctx, s->a, errors, cfg->theta, cfg->keep_count, &rep->m_bar, vals.data(),
-                                        &rep->theta_used, &w));
+                // the standard recycling step keeps the slots, the error block, its MGS copy and A E
+                // (3 x m x n doubles beyond the slots); short of HBM, the lean step works in the slots
+                bool lean = cfg->memory == 1;
+                if (!lean) {
+                    size_t fr = 0, tot = 0;
+                    RCG_CK(cudaMemGetInfo(&fr, &tot));
+                    const double need = (3.0 * smp->m + std::max(cfg->keep_count, 1)) * 8.0 * static_cast<double>(smp->ld);
+                    lean = static_cast<double>(fr) < 1.1 * need;
+                }
+                std::vector<double> vals;
+                if (lean) {
+                    lean_build_aux(ctx, s->a, xs, smp, cfg->theta, cfg->keep_count, &rep->m_bar, vals, &rep->theta_used,
+                                   &w);
+                    rcg_sampler_destroy(smp);  // spent: its slots held the errors and the basis
+                    smp = nullptr;
+                } else {
+                    ck(rcg_harvest_errors(ctx, xs, smp, &errors));
+                    vals.assign(std::max(errors->k, 1), 0.0);
+                    ck(rcg_build_aux_matrix(ctx, s->a, errors, cfg->theta, cfg->keep_count, &rep->m_bar, vals.data(),
+                                            &rep->theta_used, &w));
+                }
                 rep->m_tilde = w->k;
                 if (rep->ritz_values)
                     std::memcpy(rep->ritz_values, vals.data(), sizeof(double) * std::min(rep->m_bar, rep->ritz_cap));
-                if (rep->m_tilde > 0)
-                    ck(rcg_basis_create(ctx, s->a, w, s->method == RCG_METHOD_ES_SC_ICCG ? RCG_BASIS_SC : RCG_BASIS_DEFLATION,
-                                        &basis));
+                if (rep->m_tilde > 0)  // lean: the basis takes W's block over instead of copying it
+                    basis_build(ctx, s->a, w, s->method == RCG_METHOD_ES_SC_ICCG ? RCG_BASIS_SC : RCG_BASIS_DEFLATION,
+                                lean, &basis);
                 RCG_CK(cudaStreamSynchronize(ctx->stream));
                 rep->w_build_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             }
@@ -186,11 +203,20 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
             const bool use_sc = basis && s->method == RCG_METHOD_ES_SC_ICCG;
             const rcg_basis* defl = basis && s->method == RCG_METHOD_ES_D_ICCG ? basis : nullptr;
             const rcg_prec* m2 = use_sc ? &sc : &inner;
+            // batched solves keep ~10 interleaved vectors of RT right-hand sides: unbatched when HBM
+            // is short (auto memory mode)
+            bool batch = cfg->batch != 0;
+            if (batch && cfg->memory == 0 && k_t > 1) {
+                size_t fr = 0, tot = 0;
+                RCG_CK(cudaMemGetInfo(&fr, &tot));
+                const int rt = (std::min(16, k_t - 1) + 3) / 4 * 4;
+                batch = static_cast<double>(fr) > 1.1 * 10.0 * 8.0 * rt * static_cast<double>(n);
+            }
             for (int k = 1; k < k_t;) {
-                const int cnt = cfg->batch ? std::min(16, k_t - k) : 1;
+                const int cnt = batch ? std::min(16, k_t - k) : 1;
                 double* B = bs + static_cast<int64_t>(k) * n;
                 double* X = xs + static_cast<int64_t>(k) * n;
-                if (cnt > 1 || cfg->batch) {
+                if (cnt > 1 || batch) {
                     if (defl)
                         ck(rcg_deflated_pcg_solve_batch(ctx, s->a, B, m2, defl, X, &scfg, cnt, &reps[k]));
                     else

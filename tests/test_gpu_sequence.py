@@ -99,3 +99,28 @@ def test_sequence_lanczos_condest_each_solve(ctx, oracle, problems, name, batch)
         assert abs(rep["kappa"][k] / (hi / lo) - 1.0) <= 0.01, (k, rep["kappa"][k], hi / lo)
         assert rep["lambda_min"][k] > 0 and rep["lambda_max"][k] >= rep["lambda_min"][k]
     assert rep["kappa"][1] < rep["kappa"][0]  # the accelerated operator is better conditioned
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_lean_sequence_matches_oracle(ctx, oracle, problems, name):
+    """The memory-lean recycling step (errors / MGS in the sampler slots, streamed Gram, the basis
+    adopting W -- what C4 needs on one GPU), forced on small configs: same m_bar / m_tilde, Ritz
+    values <= 1e-6, iterations +-2 as the oracle's sequence."""
+    from oracle.sequence import rhs_set, run_sequence as oracle_sequence
+    from paper_2203_08498_b200 import api
+
+    cfg = replace(problems.SMALL[name], n_rhs=4)
+    h = problems.generate(cfg)
+    ores = oracle_sequence(oracle, cfg, h)
+    a_o = Matrix.of(h)
+    _, dis = oracle.diagonal_scale(a_o)
+    b_orig, _ = rhs_set(oracle, cfg, h, a_o, dis)
+    X = np.zeros((cfg.n_rhs, h.n))
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+    seq = api.Sequence(ctx, a, "es-sc-iccg" if cfg.method == "sc" else "es-d-iccg")
+    rep = seq.run(np.stack(b_orig), X, cfg.eps, cfg.max_iter, "A", cfg.sampler_m, keep_count=cfg.keep, lean=True)
+    assert rep["m_bar"] == ores["m_bar"] and rep["m_tilde"] == ores["m_tilde"]
+    rv = np.asarray(ores["ritz_values"])[:rep["m_bar"]]
+    assert np.max(np.abs(rep["ritz_values"] - rv) / np.maximum(np.abs(rv), 1e-300)) <= 1e-6
+    for k in range(cfg.n_rhs):
+        assert rep["converged"][k] and abs(rep["iterations"][k] - ores["iterations"][k]) <= 2
