@@ -28,6 +28,10 @@ namespace rcg {
 constexpr int kRMax = 16;
 constexpr int kMaxRedB = 512;
 constexpr int kDepChunkHost = 8;  // the sweeps' dependency chunk (icsweep.cu kDepChunk)
+#ifndef RCG_TALLT_UNROLL
+#define RCG_TALLT_UNROLL 8  // measured: 2 175 us, 4 150 us, 8 146 us (C2, RT 12)
+#endif
+constexpr int kTalltUnroll = RCG_TALLT_UNROLL;  // rows in flight per thread in k_b_tallt
 constexpr int kElemThreads = 192;  // a multiple of every RT (2, 4, 8, 12, 16): a thread keeps one rhs
 
 struct BState {
@@ -834,6 +838,9 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
 // for the siblings; W once).  Per output: thread partials, a fixed-order block sum, then the
 // last CTA sums the row ranges in order.  Finaliser per rhs: u[:,k] = (W^T A W)^-1 f[:,k]
 // (mode 1) and f.u (mode 2).  Host grid: X x P (BatchSolve::tgrid).
+#ifndef RCG_TALLT_UNROLL
+#define RCG_TALLT_UNROLL 8  // measured: 2 175 us, 4 150 us, 8 146 us (C2, RT 12)
+#endif
 template <int RT>
 __device__ __host__ constexpr int tallt_jc() {
     return RT <= 8 ? 4 : 2;   // RT 4 with 8 columns spilled (R 4 slower than R 8)
@@ -869,7 +876,7 @@ __global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const
 #pragma unroll
             for (int v = 0; v < VW; ++v) acc[jc][v] = 0.0;
         const int64_t it1 = static_cast<int64_t>(i1) * G;
-#pragma unroll 4
+#pragma unroll kTalltUnroll
         for (int64_t it = static_cast<int64_t>(i0) * G + threadIdx.x; it < it1; it += kElemThreads) {
             const int64_t i = it / G;
             double yv[VW];
