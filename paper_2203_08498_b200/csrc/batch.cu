@@ -838,9 +838,6 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
 // for the siblings; W once).  Per output: thread partials, a fixed-order block sum, then the
 // last CTA sums the row ranges in order.  Finaliser per rhs: u[:,k] = (W^T A W)^-1 f[:,k]
 // (mode 1) and f.u (mode 2).  Host grid: X x P (BatchSolve::tgrid).
-#ifndef RCG_TALLT_UNROLL
-#define RCG_TALLT_UNROLL 8  // measured: 2 175 us, 4 150 us, 8 146 us (C2, RT 12)
-#endif
 template <int RT>
 __device__ __host__ constexpr int tallt_jc() {
     return RT <= 8 ? 4 : 2;   // RT 4 with 8 columns spilled (R 4 slower than R 8)
