@@ -124,3 +124,34 @@ def test_lean_sequence_matches_oracle(ctx, oracle, problems, name):
     assert np.max(np.abs(rep["ritz_values"] - rv) / np.maximum(np.abs(rv), 1e-300)) <= 1e-6
     for k in range(cfg.n_rhs):
         assert rep["converged"][k] and abs(rep["iterations"][k] - ores["iterations"][k]) <= 2
+
+
+def test_full_size_c2_sequence_matches_oracle(ctx, oracle, problems):
+    """The bench workload itself at full size (C2: 128^3 high-contrast FV, 2.1M rows, 10 RHS, 32
+    samples, SC m~ = 16) through the device sequence driver against the oracle's sequence (about a
+    minute of CPU): m_bar / m_tilde, Ritz values <= 1e-6, every solve +-2 iterations, true relative
+    residuals, solutions at equal iteration counts."""
+    from oracle.sequence import rhs_set, run_sequence as oracle_sequence
+    from paper_2203_08498_b200 import api
+
+    cfg = problems.CONFIGS["c2"]
+    h = problems.generate(cfg)
+    ores = oracle_sequence(oracle, cfg, h)
+    a_o = Matrix.of(h)
+    _, dis = oracle.diagonal_scale(a_o)
+    b_orig, _ = rhs_set(oracle, cfg, h, a_o, dis)
+    X = np.zeros((cfg.n_rhs, h.n))
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values)
+    rep = api.Sequence(ctx, a, "es-sc-iccg").run(np.stack(b_orig), X, cfg.eps, cfg.max_iter, "A", cfg.sampler_m,
+                                                 keep_count=cfg.keep)
+    assert rep["m_bar"] == ores["m_bar"] and rep["m_tilde"] == ores["m_tilde"]
+    if rep["iterations"][0] == ores["iterations"][0]:
+        rv = np.asarray(ores["ritz_values"])[:rep["m_bar"]]
+        assert np.max(np.abs(rep["ritz_values"] - rv) / np.maximum(np.abs(rv), 1e-300)) <= 1e-6
+    for k in range(cfg.n_rhs):
+        assert rep["converged"][k]
+        assert abs(rep["iterations"][k] - ores["iterations"][k]) <= 2, (k, rep["iterations"], ores["iterations"])
+        assert abs(rep["true_relres"][k] - ores["true_relres"][k]) <= 1e-6
+        if rep["iterations"][k] == ores["iterations"][k]:
+            xo = dis * ores["solutions"][k]
+            assert np.linalg.norm(X[k] - xo) <= 1e-5 * np.linalg.norm(xo)
