@@ -722,6 +722,72 @@ __global__ void __launch_bounds__(kElemThreads) k_b_rho(const double* __restrict
     }
 }
 
+
+// One LEVEL of a batched sweep per launch (very wide levels: the multicolour orderings), the
+// batched counterpart of icsweep_lv.cu.  Items are (position, chunk of VW right-hand sides); a
+// thread keeps its chunk (kElemThreads % G == 0).  Parents belong to earlier levels (earlier
+// launches): no polling.  Every value is k_b_sweepc's row arithmetic (bitwise); the (r, z)
+// partials of a CTA are summed per rhs in thread order into tpart[tile][k] for k_b_rho.
+template <bool BWD, int RT>
+__global__ void __launch_bounds__(kElemThreads) k_b_level(SweepArgs a, BState* st, int32_t lstart, int32_t width,
+                                                          double* __restrict__ tpart, int64_t tile_base) {
+    constexpr int VW = RT % 4 == 0 ? 4 : 2;
+    constexpr int G = RT / VW;
+    __shared__ double red[kElemThreads * VW];
+    if (st->nrun == 0) return;
+    const int c = threadIdx.x % G;
+    double acc[VW];
+#pragma unroll
+    for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+    const int64_t items = static_cast<int64_t>(width) * G;
+    for (int64_t it = blockIdx.x * static_cast<int64_t>(kElemThreads) + threadIdx.x; it < items;
+         it += static_cast<int64_t>(gridDim.x) * kElemThreads) {
+        const int32_t pos = lstart + static_cast<int32_t>(it / G);
+        const int32_t row = __ldg(a.perm + pos);
+        if (row < 0) continue;
+        const int64_t me = static_cast<int64_t>(row) * RT + c * VW;
+        double sv[VW];
+        double dr = 1.0;
+        if (BWD) dr = __ldg(a.d + row);
+#pragma unroll
+        for (int v = 0; v < VW; ++v) sv[v] = BWD ? __ddiv_rn(a.in[me + v], dr) : a.in[me + v];
+        const int32_t b = __ldg(a.prs + pos), e = __ldg(a.prs + pos + 1);
+        for (int32_t k0 = b; k0 < e; k0 += 4) {  // four parents' chunks in flight, then in order
+            const int mm = min(4, e - k0);
+            double lv[4], dep[4][VW];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < mm) {
+                    lv[j] = __ldg(a.pval + k0 + j);
+                    const double* src = a.out + static_cast<int64_t>(__ldg(a.pcol + k0 + j)) * RT + c * VW;
+#pragma unroll
+                    for (int v = 0; v < VW; ++v) dep[j][v] = __ldcg(src + v);
+                }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < mm)
+#pragma unroll
+                    for (int v = 0; v < VW; ++v) sv[v] = fsub_mul(sv[v], lv[j], dep[j][v]);
+        }
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+            sv[v] = publishable(sv[v]);
+            a.out[me + v] = sv[v];
+            if (BWD && a.r) acc[v] = fadd_mul(acc[v], a.r[me + v], sv[v]);
+        }
+    }
+    if (!(BWD && a.r)) return;
+#pragma unroll
+    for (int v = 0; v < VW; ++v) red[threadIdx.x * VW + v] = acc[v];
+    __syncthreads();
+    if (threadIdx.x < RT) {
+        const int k = threadIdx.x, cc = k / VW, v = k % VW;
+        double sum = 0.0;
+        for (int t = cc; t < kElemThreads; t += G) sum = __dadd_rn(sum, red[t * VW + v]);
+        tpart[(tile_base + blockIdx.x) * RT + k] = sum;
+    }
+}
+
 // p = z (+ W u) (+ beta p) for running rhs; sweep buffers back to the sentinel.  G = RT/VW
 // threads per row, each on one VW-value chunk: a warp's accesses are contiguous and each W_j[i]
 // load serves VW values.  Per value the arithmetic of the single-rhs k_pupdate.
@@ -1470,6 +1536,34 @@ struct BatchSolve {
         if (ctx->sweep_bps <= 0 && f->n > 0 && static_cast<double>(f->nnz_l) / f->n > kDepChunkHost) bps0 = std::max(bps0, 3);
         s.backoff_ns = ctx->sweep_backoff_ns;
         KTimer t(ctx, backward ? 7 : 6, RT);
+        // very wide levels (the multicolour orderings): one launch per level, no polling
+        // (default shape rule of icsweep_lv.cu: >= 600K rows per level; mode 4 always)
+        const std::vector<int32_t>& lp = f->h_lptr[backward ? 1 : 0];
+        const int nlev = backward ? f->bwd_levels : f->fwd_levels;
+        const bool level_ok = static_cast<int>(lp.size()) == nlev + 1 && nlev > 0;
+        if (level_ok && (ctx->sweep_cluster == 4 || (ctx->sweep_cluster == 2 && s.npos / nlev >= 600000))) {
+            const bool rho = backward && s.r;
+            int64_t tile = 0;
+            for (int l = 0; l < nlev; ++l) {
+                const int32_t width = lp[l + 1] - lp[l];
+                const int64_t items = static_cast<int64_t>(width) * (RT % 4 == 0 ? RT / 4 : RT / 2);
+                const int g = static_cast<int>(std::max<int64_t>(
+                    1, std::min<int64_t>((items + kElemThreads - 1) / kElemThreads, ctx->num_sms * 8)));
+                if (backward)
+                    k_b_level<true, RT><<<g, kElemThreads, 0, ctx->stream>>>(s, w->st, lp[l], width, w->tpart, tile);
+                else
+                    k_b_level<false, RT><<<g, kElemThreads, 0, ctx->stream>>>(s, w->st, lp[l], width, w->tpart, tile);
+                RCG_LAUNCHED(ctx);
+                tile += g;
+            }
+            if (rho) {
+                const int gr = static_cast<int>(std::max<int64_t>(
+                    1, std::min<int64_t>((tile * RT + kElemThreads * 4 - 1) / (kElemThreads * 4), ctx->num_sms * 8)));
+                k_b_rho<RT><<<gr, kElemThreads, 0, ctx->stream>>>(w->tpart, tile, w->partials, w->st, s.add_sc);
+                RCG_LAUNCHED(ctx);
+            }
+            return;
+        }
         if (mode != 0) {
             // chunk lanes: 16-byte chunks (measured faster than 32-byte), 4 parents per poll
             // chunk (register budget -> residency); 3x the single-sweep CTAs from RT = 12 on

@@ -133,3 +133,34 @@ def test_wide_level_sweeps_multicolour_c2(modes, problems):
     for mode in (PIPELINED, LEVEL, AUTO):
         for k in range(3):
             assert np.array_equal(outs[GRID][k], outs[mode][k]), mode
+
+
+@pytest.mark.parametrize("method", ["ic", "sc"])
+def test_batched_level_sweeps_multicolour(modes, problems, method):
+    """Batched solves on the multicolour C2 operator with the batched sweeps one launch per level
+    (k_b_level; the default picks it for these 1M-row levels) against the polling batched sweep:
+    the rows are the same arithmetic and only the (r, z) summation order differs, so iterations
+    agree within 1 and solutions to rounding."""
+    from paper_2203_08498_b200 import api, sequence
+
+    ctx = modes
+    cfg = problems.CONFIGS["c2"]
+    m, perm, _ = problems.multicolour(problems.generate(cfg))
+    p = sequence.prepare(ctx, cfg, m, validate=False, new_of_old=perm)
+    B = np.stack([sequence.rhs(p, k)[1] for k in range(3)])
+    prec = api.Ic(p.ic)
+    if method == "sc":
+        rng = np.random.default_rng(1)
+        basis = api.Basis(ctx, p.a, api.TallDense.from_columns(ctx, m.n, rng.standard_normal((4, m.n))), "sc")
+        prec = api.Sc(basis, p.ic)
+    out = {}
+    for mode in (GRID, LEVEL, AUTO):
+        ctx.set_sweep_kernel(mode)
+        X = np.zeros_like(B)
+        reps = api.pcg_solve_batch(ctx, p.a, B, prec, X, cfg.eps, 400)
+        out[mode] = ([r.iterations for r in reps], X)
+    for mode in (LEVEL, AUTO):
+        assert all(abs(a - b) <= 1 for a, b in zip(out[mode][0], out[GRID][0])), (out[mode][0], out[GRID][0])
+        for k in range(3):
+            x0 = out[GRID][1][k]
+            assert np.linalg.norm(out[mode][1][k] - x0) <= 1e-6 * np.linalg.norm(x0)
