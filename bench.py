@@ -325,7 +325,8 @@ def kernel_report(stats, n, nnz, nnz_l, m, steps, peak, peak_src, levels=None):
     e = kernels[CLASS_NAMES[best]]
     t = traffic.get(CLASS_NAMES[best])
     roof = {"bound": "hbm", "kernel": CLASS_NAMES[best], "achieved": e["achieved_gbs"], "peak": peak, "unit": "GB/s",
-            "frac": round(e["achieved_gbs"] / peak, 4), "traffic": t["dram_bytes"] if isinstance(t, dict) else t,
+            "frac": round(e["achieved_gbs"] / peak, 4), "frac_of_spec_8tbs": round(e["achieved_gbs"] / 8000.0, 4),
+            "traffic": t["dram_bytes"] if isinstance(t, dict) else t,
             "peak_source": peak_src}
     if isinstance(t, dict):  # the ncu capture's launch carried rhs_per_launch right-hand sides
         roof["traffic_rhs_per_launch"] = t["rhs_per_launch"]
