@@ -1569,7 +1569,8 @@ struct BatchSolve {
             // chunk (register budget -> residency); 3x the single-sweep CTAs from RT = 12 on
             constexpr int rpw = 32 / (RT / 2);
             // (re-measured end of round 1, C2 fwd / bwd: RT 12 x1 992/1298, x2 632/788, x3 578/657,
-            // x4 620/681 us; RT 4 x2 497/535, x3 506/559 us)
+            // x4 620/681 us; RT 4 x2 497/535, x3 506/559 us.  32-byte chunks (VW 4, half the
+            // polling lanes) again slower: RT 12 700/828, RT 8 660/739, RT 16 668/744 us)
             const int cmul = RT >= 12 ? 3 : 2;
             const int ntiles = (s.npos + rpw * 4 - 1) / (rpw * 4);  // CTAs of 4 warp tiles
             const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps0 * cmul));
