@@ -969,14 +969,28 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
         if (occ[j]) list.push_back(j);
     const int k0 = static_cast<int>(list.size());
     struct Loc {
-        double *e = nullptr, *q = nullptr, *aq = nullptr, *w = nullptr, *c = nullptr;
+        double *e = nullptr, *q = nullptr, *aq = nullptr, *w = nullptr, *c = nullptr, *y = nullptr;
         int *nz = nullptr, *dl = nullptr;
         Staged x;
+        double *eb = nullptr, *qb = nullptr;  // error / basis blocks (own buffers, or the slots when lean)
+        int64_t eld = 0, qld = 0;
     };
     std::vector<Loc> L(ns);
+    // Memory-lean mode (RCG_DIST_LEAN=1, or automatically when the error block, its MGS copy and
+    // A Q do not fit next to the slots -- C4 at G = 1-2): the errors and the MGS basis live in the
+    // sampler slots and the Gram is streamed (one n-vector), as lean_build_aux on one GPU; the
+    // slots are released once W is formed (the samplers are spent).
+    bool lean = std::getenv("RCG_DIST_LEAN") && std::atoi(std::getenv("RCG_DIST_LEAN")) == 1;
+    if (!lean) {
+        size_t fr = 0, tot = 0;
+        RCG_CK(cudaMemGetInfo(&fr, &tot));
+        double need = 0.0;
+        for (int s = 0; s < ns; ++s) need += 3.0 * k0 * 8.0 * static_cast<double>(sl[s]->nloc);
+        lean = static_cast<double>(fr) < 1.1 * need;  // (loopback slabs share one GPU)
+    }
     auto cleanup = [&] {
         for (auto& l : L) {
-            for (double* p : {l.e, l.q, l.aq, l.w, l.c}) dev_free(p);
+            for (double* p : {l.e, l.q, l.aq, l.w, l.c, l.y}) dev_free(p);
             dev_free(l.nz);
             dev_free(l.dl);
         }
@@ -995,9 +1009,18 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
             ensure_g(d, std::max({k0 * k0, k0, 128}));
             stage_in(ctx, xfin[s], n, L[s].x);
             const int64_t sz = std::max<int64_t>(int64_t(n) * std::max(k0, 1), 1);
-            L[s].e = dev_alloc(sz);
-            L[s].q = dev_alloc(sz);
-            L[s].aq = dev_alloc(sz);
+            if (lean) {
+                L[s].eb = L[s].qb = smp[s]->slots;
+                L[s].eld = L[s].qld = smp[s]->ld;
+                L[s].y = dev_alloc(std::max<int64_t>(n, 1));
+            } else {
+                L[s].e = dev_alloc(sz);
+                L[s].q = dev_alloc(sz);
+                L[s].aq = dev_alloc(sz);
+                L[s].eb = L[s].e;
+                L[s].qb = L[s].q;
+                L[s].eld = L[s].qld = n;
+            }
             L[s].c = dev_alloc(4);
             L[s].nz = static_cast<int*>(dev_alloc_bytes(sizeof(int) * std::max(k0, 1)));
             L[s].dl = static_cast<int*>(dev_alloc_bytes(sizeof(int) * std::max(k0, 1)));
@@ -1006,8 +1029,12 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
                 RCG_CK(cudaMemcpyAsync(L[s].dl, list.data(), sizeof(int) * k0, cudaMemcpyHostToDevice, ctx->stream));
                 if (n) {
                     dim3 grid(stream_grid(ctx, n), std::min(k0, 64));
-                    k_harvest<<<grid, kStreamThreads, 0, ctx->stream>>>(L[s].x.dev, smp[s]->slots, smp[s]->ld, L[s].dl,
-                                                                        k0, 0, L[s].e, n, n, L[s].nz);
+                    if (lean)  // column j of the errors stays in slot list[j]
+                        k_harvest_inplace<<<grid, kStreamThreads, 0, ctx->stream>>>(L[s].x.dev, smp[s]->slots, smp[s]->ld,
+                                                                                    L[s].dl, k0, n, L[s].nz);
+                    else
+                        k_harvest<<<grid, kStreamThreads, 0, ctx->stream>>>(L[s].x.dev, smp[s]->slots, smp[s]->ld,
+                                                                            L[s].dl, k0, 0, L[s].e, n, n, L[s].nz);
                     RCG_LAUNCHED(ctx);
                 }
             }
@@ -1047,16 +1074,19 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
             return h;
         };
         int kept = 0;
+        // error column src: column src of the own block, or slot list[src] in place (lean: the
+        // basis column `kept` <= src <= list[src] is never a later source)
+        auto ecol = [&](int s, int src) { return L[s].eb + int64_t(lean ? list[src] : src) * L[s].eld; };
         for (int src : cols) {
-            auto wcol = [&](int s) { return L[s].q + int64_t(kept) * sl[s]->nloc; };
+            auto wcol = [&](int s) { return L[s].qb + int64_t(kept) * L[s].qld; };
             for (int s = 0; s < ns; ++s)
-                if (sl[s]->nloc)
-                    RCG_CK(cudaMemcpyAsync(wcol(s), L[s].e + int64_t(src) * sl[s]->nloc, sizeof(double) * sl[s]->nloc,
-                                           cudaMemcpyDeviceToDevice, sl[s]->ctx->stream));
+                if (sl[s]->nloc && wcol(s) != ecol(s, src))
+                    RCG_CK(cudaMemcpyAsync(wcol(s), ecol(s, src), sizeof(double) * sl[s]->nloc, cudaMemcpyDeviceToDevice,
+                                           sl[s]->ctx->stream));
             const double n0 = std::sqrt(gdot(wcol, wcol, true));
             if (n0 == 0.0) continue;
             for (int qi = 0; qi < kept; ++qi) {
-                auto qcol = [&](int s) { return L[s].q + int64_t(qi) * sl[s]->nloc; };
+                auto qcol = [&](int s) { return L[s].qb + int64_t(qi) * L[s].qld; };
                 gdot(qcol, wcol, false);
                 for (int s = 0; s < ns; ++s) {
                     rcg_ctx* ctx = sl[s]->ctx;
@@ -1084,26 +1114,37 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
             return nullptr;
         }
         require(kept <= 128, "SmallSym: dimension " + std::to_string(kept) + " outside [0, 128]");
-        // A Q (rayleigh_ritz, recycling.cpp:48-53): halo exchange + local SpMV per column
+        // A Q (rayleigh_ritz, recycling.cpp:48-53): halo exchange + local SpMV per column; lean:
+        // each column's local Q^T (A q_j) right away (streamed Gram), no A Q block
+        std::vector<std::vector<double>> sloc(ns, std::vector<double>(static_cast<size_t>(kept) * kept, 0.0));
         for (int j = 0; j < kept; ++j) {
             for (int s = 0; s < ns; ++s) {
                 rcg_dslab* d = sl[s];
                 if (d->nloc)
-                    RCG_CK(cudaMemcpyAsync(d->pe, L[s].q + int64_t(j) * d->nloc, sizeof(double) * d->nloc,
+                    RCG_CK(cudaMemcpyAsync(d->pe, L[s].qb + int64_t(j) * L[s].qld, sizeof(double) * d->nloc,
                                            cudaMemcpyDeviceToDevice, d->ctx->stream));
             }
             comm->halo(sl, ns, 1);
             for (int s = 0; s < ns; ++s) {
                 rcg_dslab* d = sl[s];
-                const int rc = rcg_spmv(d->ctx, d->a, d->pe, L[s].aq + int64_t(j) * d->nloc);
+                double* yj = lean ? L[s].y : L[s].aq + int64_t(j) * d->nloc;
+                const int rc = rcg_spmv(d->ctx, d->a, d->pe, yj);
                 if (rc != RCG_OK) throw Error(rc, rcg_last_error());
+                if (lean) {
+                    std::vector<double> f;
+                    gram_host(d->ctx, L[s].qb, L[s].qld, kept, yj, d->nloc, 1, d->nloc, false, f);
+                    for (int i = j; i < kept; ++i) sloc[s][static_cast<size_t>(i) * kept + j] = f[i];
+                }
             }
         }
         // S = Q^T A Q, lower triangle allreduced then mirrored, eigensolved on every rank
         std::vector<double> g;
         for (int s = 0; s < ns; ++s) {
             rcg_dslab* d = sl[s];
-            gram_host(d->ctx, L[s].q, d->nloc, kept, L[s].aq, d->nloc, kept, d->nloc, true, g);
+            if (lean)
+                g = sloc[s];
+            else
+                gram_host(d->ctx, L[s].q, d->nloc, kept, L[s].aq, d->nloc, kept, d->nloc, true, g);
             RCG_CK(cudaMemcpy(d->gbuf, g.data(), sizeof(double) * kept * kept, cudaMemcpyHostToDevice));
         }
         comm->allreduce(sl, ns, kept * kept, 1);
@@ -1126,10 +1167,15 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
             for (int s = 0; s < ns; ++s) {
                 rcg_dslab* d = sl[s];
                 L[s].w = dev_alloc(std::max<int64_t>(int64_t(d->nloc) * sel, 1));
-                combine_cols(d->ctx, L[s].q, d->nloc, kept, T.data(), sel, L[s].w, d->nloc, d->nloc);
+                combine_cols(d->ctx, L[s].qb, L[s].qld, kept, T.data(), sel, L[s].w, d->nloc, d->nloc);
                 wp[s] = L[s].w;
             }
             for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
+            if (lean)  // the samplers are spent: their slots make room for W's copy and A W
+                for (int s = 0; s < ns; ++s) {
+                    dev_free(smp[s]->slots);
+                    smp[s]->slots = nullptr;
+                }
             out = dbasis_create(comm, ns, sl, wp.data(), sel, kind);
         }
     } catch (...) {

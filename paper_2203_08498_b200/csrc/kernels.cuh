@@ -76,6 +76,8 @@ __device__ __forceinline__ void smp_schedule(DevState* st, int i, double relres,
         }
     }
 }
+__global__ void k_harvest_inplace(const double* __restrict__ x, double* __restrict__ slots, int64_t lds,
+                                  const int* __restrict__ list, int cnt, int32_t n, int* __restrict__ nonzero);  // recycle.cu
 __global__ void k_harvest(const double* __restrict__ x, const double* __restrict__ slots, int64_t lds,
                           const int* __restrict__ list, int cnt, int raw, double* __restrict__ e, int64_t lde,
                           int32_t n, int* __restrict__ nonzero);  // recycle.cu

@@ -692,6 +692,7 @@ int rcg_sampler_state(const rcg_sampler* s, int* occupied, int* stored_iter) {
 int rcg_sampler_slot(rcg_ctx* ctx, const rcg_sampler* s, int slot, double* out) {
     return guard([&] {
         require(slot >= 0 && slot < s->m, "sampler: slot out of range");
+        require(s->slots != nullptr || s->n == 0, "sampler: spent by a memory-lean recycling step");
         if (s->n == 0) return;
         RCG_CK(cudaMemcpyAsync(out, s->slots + slot * s->ld, sizeof(double) * s->n, cudaMemcpyDefault, ctx->stream));
         RCG_CK(cudaStreamSynchronize(ctx->stream));

@@ -21,28 +21,33 @@ def bounds(n: int, nparts: int) -> np.ndarray:
     return (np.arange(nparts + 1, dtype=np.int64) * n) // nparts
 
 
-def block_factor(ctx: api.Context, plan: api.SlabPlan, shift: float = 0.0) -> api.IcFactor:
+def block_factor(ctx: api.Context, plan: api.SlabPlan, shift: float = 0.0, device: bool = False) -> api.IcFactor:
+    """The slab's diagonal-block IC(0): host restatement, or (device=True) the device
+    factorisation -- bitwise the same factor (tests/test_gpu_icfactor.py), much faster on C4."""
     rs, ci, va = plan.diagonal_block()
+    if device:
+        return api.IcFactor.factorize_device(ctx, api.CsrMatrix(ctx, plan.nloc, rs, ci, va, validate=False), shift, 1)
     return api.IcFactor.factorize(ctx, plan.nloc, rs, ci, va, shift, 1)
 
 
-def agree_factors(ctxs, plans, allreduce_max: Callable[[float], float]):
+def agree_factors(ctxs, plans, allreduce_max: Callable[[float], float], device: bool = False):
     """Block factors of the local slabs with the reference's global shift ladder: each block runs
     the ladder, the ranks take the largest shift (allreduce_max), and blocks that stopped lower
     are refactorised at it."""
-    fs = [block_factor(c, p) for c, p in zip(ctxs, plans)]
+    fs = [block_factor(c, p, 0.0, device) for c, p in zip(ctxs, plans)]
     s = allreduce_max(max(f.shift_used for f in fs))
-    return [f if f.shift_used == s else block_factor(c, p, s) for f, c, p in zip(fs, ctxs, plans)]
+    return [f if f.shift_used == s else block_factor(c, p, s, device) for f, c, p in zip(fs, ctxs, plans)]
 
 
 class LoopbackSystem:
     """All G slabs of a matrix in this process on one GPU (one context / stream per slab)."""
 
-    def __init__(self, host, nparts: int, preconditioner: str = "ic", device: int = 0):
+    def __init__(self, host, nparts: int, preconditioner: str = "ic", device: int = 0, device_factor: bool = False):
         self.n, self.nparts = host.n, nparts
         self.ctxs = [api.Context(device) for _ in range(nparts)]
         self.plans = [api.SlabPlan(host.n, host.row_start, host.col_idx, host.values, nparts, b) for b in range(nparts)]
-        self.factors = agree_factors(self.ctxs, self.plans, lambda v: v) if preconditioner == "ic" else [None] * nparts
+        self.factors = (agree_factors(self.ctxs, self.plans, lambda v: v, device_factor) if preconditioner == "ic"
+                        else [None] * nparts)
         self.slabs = [api.DSlab(c, p, f) for c, p, f in zip(self.ctxs, self.plans, self.factors)]
         self.comm = api.Comm.loopback(nparts)
 

@@ -186,3 +186,30 @@ def test_loopback_sequence_matches_block_jacobi_sequence(oracle, problems, name,
     if out["iterations"][0] == ref["iterations"][0]:
         assert out["m_bar"] == ref["m_bar"]
     assert out["iterations"][1] < out["iterations"][0] or out["m_tilde"] == 0
+
+
+@pytest.mark.parametrize("name", ["c1", "c4"])
+@pytest.mark.parametrize("nparts", [1, 2])
+def test_loopback_lean_sequence(oracle, problems, name, nparts, monkeypatch):
+    """The memory-lean distributed recycling step (RCG_DIST_LEAN=1: errors / MGS in the sampler
+    slots, streamed Gram, slots released before the basis -- what C4 needs at G = 1-2) and the
+    device block factor: the block-Jacobi sequence of the oracle, +-2 iterations per solve, m_bar,
+    Ritz values <= 1e-6 at equal solve-1 counts."""
+    from oracle.sequence import run_sequence
+    from paper_2203_08498_b200 import dist
+
+    monkeypatch.setenv("RCG_DIST_LEAN", "1")
+    cfg = problems.SMALL[name]
+    h = problems.generate(cfg)
+    ref = run_sequence(oracle, cfg, h, blocks=nparts)
+    _, host = _scaled(oracle, problems, name)
+    system = dist.LoopbackSystem(host, nparts, device_factor=True)
+    out = system.sequence(ref["scaled_rhs"], cfg.eps, cfg.max_iter, cfg.sampler_m, cfg.keep,
+                          "sc" if cfg.method == "sc" else "deflation")
+    assert all(out["converged"])
+    for k, (g, o) in enumerate(zip(out["iterations"], ref["iterations"])):
+        assert abs(g - o) <= 2, (k, out["iterations"], ref["iterations"])
+    if out["iterations"][0] == ref["iterations"][0]:
+        assert out["m_bar"] == ref["m_bar"] and out["m_tilde"] == ref["m_tilde"]
+        vo = np.asarray(ref["ritz_values"])[: out["m_bar"]]
+        assert np.allclose(out["ritz_values"], vo, rtol=1e-6, atol=0)
