@@ -1,0 +1,53 @@
+"""Full BASELINE.json sizes against the oracle (minutes of CPU; the scaled-down configs are in the
+other files): the core kernels BITWISE on C3 (16.8M rows, 449M entries), C4 (134M rows, 938M
+entries) and C5 (4M-point kNN) -- diagonal scaling, SpMV and the IC(0) sweeps with the device
+factor against the oracle's factor -- and the C5 ICCG solve within the north-star bars."""
+import numpy as np
+import pytest
+
+from oracle import Matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _scaled_pair(ctx, oracle, problems, name):
+    from paper_2203_08498_b200 import api
+
+    h = problems.generate(problems.CONFIGS[name])
+    a_o, dis_o = oracle.diagonal_scale(Matrix.of(h))
+    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values, validate=False)
+    sa, dis = api.diagonal_scale(ctx, a)
+    del a
+    assert np.array_equal(dis, dis_o)
+    assert np.array_equal(sa.values(), a_o.va)
+    return h, a_o, sa
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_full_size_kernels_bitwise(ctx, oracle, problems, name):
+    from paper_2203_08498_b200 import api
+
+    h, a_o, sa = _scaled_pair(ctx, oracle, problems, name)
+    x = oracle.uniform_pm1(17, 0, h.n)
+    assert np.array_equal(sa.spmv(x), oracle.spmv(a_o, x)), "spmv"
+    f = api.IcFactor.factorize_device(ctx, sa)
+    f_o = oracle.ic0_factorize(a_o)
+    assert np.array_equal(f.apply(x), oracle.ic_apply(f_o, x)), "ic_apply"
+
+
+def test_full_size_c5_iccg_solve(ctx, oracle, problems):
+    """C5 (4M-point kNN Laplacian): IC(0)-PCG on the scaled matrix, iterations +-2 and the
+    solution at equal counts against the oracle."""
+    from paper_2203_08498_b200 import api
+
+    cfg = problems.CONFIGS["c5"]
+    h, a_o, sa = _scaled_pair(ctx, oracle, problems, "c5")
+    b = oracle.spmv(a_o, problems.normal(cfg.rhs_seed, 0, h.n))
+    f = api.IcFactor.factorize_device(ctx, sa)
+    f_o = oracle.ic0_factorize(a_o)
+    xg, xo = np.zeros(h.n), np.zeros(h.n)
+    rg = api.pcg_solve(ctx, sa, b, api.Ic(f), xg, cfg.eps, cfg.max_iter)
+    ro = oracle.pcg_solve(a_o, b, xo, kind=1, ic=f_o, eps=cfg.eps, max_iter=cfg.max_iter)
+    assert rg.converged and ro.converged and abs(rg.iterations - ro.iterations) <= 2
+    if rg.iterations == ro.iterations:
+        assert np.linalg.norm(xg - xo) <= 1e-8 * np.linalg.norm(xo)
