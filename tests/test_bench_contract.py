@@ -1,0 +1,36 @@
+"""bench.py's contract pieces that run without a GPU: the reference arm (the reference library on
+the host cores, one JSON line with impl / cpu_baseline / e2e) and the cost-model report."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    from oracle import REF_SO
+
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--steps", "1", "--warmup", "1", "--ref-threads", "2"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "iters/s"
+    assert line["cpu_baseline"]["cores"] == 2 and line["cpu_baseline"]["kind"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["higher_is_better"] is True and line["config"]["workload"].startswith("c1")
+
+
+def test_cost_model_report_fields():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    rep = bench.cost_model_report(2097152, 14581760, 16, {"solve1_iterations": 168, "solve1_ms": 190.4,
+                                                          "accelerated_iterations": [68, 157], "accelerated_ms": 80.0})
+    assert rep["gamma_predicted"] > 1.0 and 0 < rep["iccg_model_fraction"] < 1.0
+    assert rep["gamma_measured"] == pytest.approx((80.0 / 225) / (190.4 / 168), rel=1e-3)
