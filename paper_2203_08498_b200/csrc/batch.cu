@@ -1537,7 +1537,9 @@ struct BatchSolve {
         s.backoff_ns = ctx->sweep_backoff_ns;
         KTimer t(ctx, backward ? 7 : 6, RT);
         // very wide levels (the multicolour orderings): one launch per level, no polling
-        // (default shape rule of icsweep_lv.cu: >= 600K rows per level; mode 4 always)
+        // (default shape rule of icsweep_lv.cu: >= 600K rows per level; mode 4 always).  Forced on
+        // natural orderings at RT 8 it wins only on C4 (fwd 27.3 -> 20.8, bwd 37.7 -> 33.4 ms) and
+        // loses on C5 (707 -> 842 us) and C3 (4.1 -> 17.3 ms)
         const std::vector<int32_t>& lp = f->h_lptr[backward ? 1 : 0];
         const int nlev = backward ? f->bwd_levels : f->fwd_levels;
         const bool level_ok = static_cast<int>(lp.size()) == nlev + 1 && nlev > 0;
