@@ -203,17 +203,24 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
             const bool use_sc = basis && s->method == RCG_METHOD_ES_SC_ICCG;
             const rcg_basis* defl = basis && s->method == RCG_METHOD_ES_D_ICCG ? basis : nullptr;
             const rcg_prec* m2 = use_sc ? &sc : &inner;
-            // batched solves keep ~10 interleaved vectors of RT right-hand sides: unbatched when HBM
-            // is short (auto memory mode)
+            // batched solves keep ~10 interleaved vectors of RT right-hand sides: when HBM is short
+            // (auto memory mode), the widest batch whose workspace fits (C4 on one GPU: a few
+            // right-hand sides per kernel sequence instead of one), else unbatched
             bool batch = cfg->batch != 0;
+            int max_cnt = 16;
             if (batch && cfg->memory == 0 && k_t > 1) {
                 size_t fr = 0, tot = 0;
                 RCG_CK(cudaMemGetInfo(&fr, &tot));
-                const int rt = (std::min(16, k_t - 1) + 3) / 4 * 4;
-                batch = static_cast<double>(fr) > 1.1 * 10.0 * 8.0 * rt * static_cast<double>(n);
+                max_cnt = 0;
+                for (int rt : {16, 12, 8, 4, 2})
+                    if (static_cast<double>(fr) > 1.1 * 10.0 * 8.0 * rt * static_cast<double>(n)) {
+                        max_cnt = rt;
+                        break;
+                    }
+                batch = max_cnt > 0;
             }
             for (int k = 1; k < k_t;) {
-                const int cnt = batch ? std::min(16, k_t - k) : 1;
+                const int cnt = batch ? std::min(max_cnt, k_t - k) : 1;
                 double* B = bs + static_cast<int64_t>(k) * n;
                 double* X = xs + static_cast<int64_t>(k) * n;
                 if (cnt > 1 || batch) {
