@@ -117,9 +117,24 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
         const int64_t total = static_cast<int64_t>(k_t) * n;
         const bool recycled = s->method == RCG_METHOD_ES_SC_ICCG || s->method == RCG_METHOD_ES_D_ICCG;
         rcg_solver_config scfg{cfg->eps, cfg->max_iter, 0};
-        // scaled right-hand sides (scaling.cpp:8-12) and zero initial guesses
+        // scaled right-hand sides (scaling.cpp:8-12) and zero initial guesses.  Host right-hand
+        // sides: solve 1's comes in first on the library stream, the others on a side stream
+        // behind solve 1 (joined before the accelerated solves), so the H2D copy is hidden
         Staged bst;
-        stage_in(ctx, rhs, total, bst);
+        const bool host_rhs = !is_device_ptr(rhs) && k_t > 1;
+        cudaStream_t side = nullptr;
+        cudaEvent_t rhs_in = nullptr;
+        if (host_rhs) {
+            bst.dev = dev_alloc(std::max<int64_t>(total, 1));
+            bst.owned = true;
+            RCG_CK(cudaMemcpyAsync(bst.dev, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+            RCG_CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            RCG_CK(cudaEventCreateWithFlags(&rhs_in, cudaEventDisableTiming));
+            RCG_CK(cudaMemcpyAsync(bst.dev + n, rhs + n, sizeof(double) * (total - n), cudaMemcpyHostToDevice, side));
+            RCG_CK(cudaEventRecord(rhs_in, side));
+        } else {
+            stage_in(ctx, rhs, total, bst);
+        }
         double* bs = dev_alloc(std::max<int64_t>(total, 1));
         double* xs = dev_alloc(std::max<int64_t>(total, 1));
         double* ax = dev_alloc(std::max(n, 1));
@@ -129,6 +144,15 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
         rcg_tall *errors = nullptr, *w = nullptr;
         rcg_basis* basis = nullptr;
         auto cleanup = [&] {
+            if (side) {
+                cudaStreamSynchronize(side);
+                cudaStreamDestroy(side);
+                side = nullptr;
+            }
+            if (rhs_in) {
+                cudaEventDestroy(rhs_in);
+                rhs_in = nullptr;
+            }
             rcg_basis_destroy(basis);
             rcg_tall_destroy(w);
             rcg_tall_destroy(errors);
@@ -139,7 +163,7 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
             RCG_CK(cudaMemsetAsync(xs, 0, sizeof(double) * total, ctx->stream));
             RCG_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), ctx->stream));
             const int g = stream_grid(ctx, total);
-            k_scale_rows<<<g, kStreamThreads, 0, ctx->stream>>>(s->dis, bst.dev, bs, n, total);
+            k_scale_rows<<<g, kStreamThreads, 0, ctx->stream>>>(s->dis, bst.dev, bs, n, host_rhs ? n : total);
             RCG_LAUNCHED(ctx);
             rcg_prec inner{s->ic ? RCG_PREC_IC : RCG_PREC_IDENTITY, s->ic, nullptr};
             std::vector<rcg_solve_report> reps(k_t);
@@ -218,6 +242,11 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
                         break;
                     }
                 batch = max_cnt > 0;
+            }
+            if (host_rhs) {  // the other right-hand sides are in: scale them
+                RCG_CK(cudaStreamWaitEvent(ctx->stream, rhs_in, 0));
+                k_scale_rows<<<g, kStreamThreads, 0, ctx->stream>>>(s->dis, bst.dev + n, bs + n, n, total - n);
+                RCG_LAUNCHED(ctx);
             }
             for (int k = 1; k < k_t;) {
                 const int cnt = batch ? std::min(max_cnt, k_t - k) : 1;
