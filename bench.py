@@ -62,7 +62,7 @@ class Clocks:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", os.environ.get("RCG_CLOCKS_MS", "200")], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -143,9 +143,12 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     ctx.synchronize()
     ctxs = _all_contexts(prep)
+    # CUDA-event class timers inside the timed region only on the sweep classes (the level-chain
+    # bound kernels, the roofline's candidates): timing every launch (~3,000 per step) costs ~3 %
+    # of the step; the other classes are timed over the same number of separate steps after it
     for c_ in ctxs:
         c_.synchronize()
-        c_.set_profiling(PROFILE_TIMED)
+        c_.set_profiling(PROFILE_TIMED, classes=TIMED_CLASSES)
         c_.reset_stats()
     launches0 = sum(c_.launches for c_ in ctxs)
     iters = 0
@@ -156,13 +159,16 @@ def run_ours(args, rank, world, local_rank):
         ctx.record(1)
         ms = ctx.elapsed_ms(0, 1)
     launches = sum(c_.launches for c_ in ctxs) - launches0
-    if not PROFILE_TIMED:  # kernel statistics from separate profiled steps
-        for c_ in ctxs:
-            c_.set_profiling(True)
-        for _ in range(args.steps):
-            step_device()
-        ctxs = _all_contexts(prep)
-    stats = kernel_stats(ctxs)
+    stats_timed = kernel_stats(ctxs)
+    ctxs = _all_contexts(prep)
+    for c_ in ctxs:
+        c_.set_profiling(True)
+        c_.reset_stats()
+    for _ in range(args.steps):
+        step_device()
+    ctxs = _all_contexts(prep)
+    stats_rest = kernel_stats(ctxs)
+    stats = {c: (stats_timed[c] if PROFILE_TIMED and c in TIMED_CLASSES else stats_rest[c]) for c in stats_rest}
     for c_ in ctxs:
         c_.set_profiling(False)
     # phase breakdown of one extra (untimed) step, from the driver's report
@@ -234,6 +240,8 @@ def run_ours(args, rank, world, local_rank):
         "phases_ms_untimed_step": phases,
         "cost_model": cost,
         "gpu_launches": int(launches),
+        "kernel_timing": {"timed_region_classes": [CLASS_NAMES[c] for c in TIMED_CLASSES] if PROFILE_TIMED else [],
+                          "other_classes": "CUDA events over the same number of separate steps after the timed region"},
         "clocks": clk.summary(),
     }
     if not args.no_variants:
@@ -444,6 +452,7 @@ def measure_multicolour(api, problems, sequence, ctx, cfg, host, args, peak):
 # concurrent single solves on their own streams
 _conc = os.environ.get("RCG_CONCURRENCY", "batch")
 PROFILE_TIMED = os.environ.get("RCG_BENCH_PROFILE_TIMED", "1") == "1"
+TIMED_CLASSES = (1, 2, 6, 7)  # single / batched forward and backward sweeps
 CONCURRENCY = _conc if _conc == "batch" else int(_conc)
 
 

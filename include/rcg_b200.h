@@ -56,6 +56,9 @@ int64_t rcg_ctx_launch_count(const rcg_ctx* ctx);
  * launches each carry RT right-hand sides -- rcg_ctx_kernel_units returns the sum of RT over a
  * class's launches).  Used by bench.py for the roofline. */
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable);
+/* which kernel classes are timed while profiling (bit c = class c; default all): timing a subset
+ * keeps the event overhead out of a timed region */
+int rcg_ctx_set_profiling_mask(rcg_ctx* ctx, unsigned mask);
 /* CUDA events on the context stream (slots 0..15) for device-side timing by callers */
 int rcg_ctx_event_record(rcg_ctx* ctx, int slot);
 int rcg_ctx_event_elapsed(rcg_ctx* ctx, int slot_a, int slot_b, double* ms);

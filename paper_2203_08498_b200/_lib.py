@@ -121,6 +121,7 @@ SIGNATURES = {
     "rcg_ctx_synchronize": (C.c_int, vp),
     "rcg_ctx_launch_count": (C.c_int64, vp),
     "rcg_ctx_set_profiling": (C.c_int, vp, C.c_int),
+    "rcg_ctx_set_profiling_mask": (C.c_int, vp, C.c_uint),
     "rcg_ctx_set_sweep_kernel": (C.c_int, vp, C.c_int),
     "rcg_ctx_event_record": (C.c_int, vp, C.c_int),
     "rcg_ctx_event_elapsed": (C.c_int, vp, C.c_int, C.c_int, dp),

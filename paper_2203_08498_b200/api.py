@@ -84,7 +84,10 @@ class Context:
     def launches(self) -> int:
         return int(lib.rcg_ctx_launch_count(self.h))
 
-    def set_profiling(self, on: bool):
+    def set_profiling(self, on: bool, classes=None):
+        """Kernel-class timers on / off; classes: the class ids to time (default all)."""
+        mask = 0x3FF if classes is None else sum(1 << int(c) for c in classes)
+        check(lib.rcg_ctx_set_profiling_mask(self.h, mask))
         check(lib.rcg_ctx_set_profiling(self.h, 1 if on else 0))
 
     def set_sweep_kernel(self, mode: int):

@@ -318,13 +318,16 @@ static cudaEvent_t pooled_event(rcg_ctx* ctx) {
 }
 
 KTimer::KTimer(rcg_ctx* c, int k, int u) : ctx(c), cls(k), units(u) {
-    if (!ctx->profiling) return;
+    if (!ctx->profiling || !((ctx->profile_mask >> k) & 1u)) {
+        cls = -1;
+        return;
+    }
     start = pooled_event(ctx);
     RCG_CK(cudaEventRecord(start, ctx->stream));
 }
 
 KTimer::~KTimer() {
-    if (!ctx->profiling) return;
+    if (!ctx->profiling || cls < 0) return;
     cudaEvent_t stop = pooled_event(ctx);
     cudaEventRecord(stop, ctx->stream);
     ctx->ev_pending.push_back({cls, units, start, stop});
@@ -425,6 +428,10 @@ int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode) {
         require(ctx != nullptr && mode >= 0 && mode <= 4, "rcg_ctx_set_sweep_kernel: mode must be 0..4");
         ctx->sweep_cluster = mode;
     });
+}
+
+int rcg_ctx_set_profiling_mask(rcg_ctx* ctx, unsigned mask) {
+    return guard([&] { ctx->profile_mask = mask; });
 }
 
 int rcg_ctx_set_profiling(rcg_ctx* ctx, int enable) {

@@ -155,6 +155,7 @@ struct rcg_ctx {
     rcg::Workspace ws;
     double* host_pinned = nullptr;   // small pinned scratch for scalar readbacks
     bool profiling = false;
+    unsigned profile_mask = 0x3FFu;  // kernel classes timed while profiling (bit per class)
     double stat_ms[kStatClasses] = {};
     int64_t stat_n[kStatClasses] = {};
     int64_t stat_units[kStatClasses] = {};  // right-hand sides carried (batched: RT per launch)
