@@ -28,7 +28,35 @@ def _scaled(ctx, h):
     return api.diagonal_scale(ctx, a)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "lap1d"])
+def _dense_csr(problems, dense):
+    n = dense.shape[0]
+    rs, ci, va = [0], [], []
+    for i in range(n):
+        for j in range(n):
+            if dense[i, j] != 0.0 or i == j:
+                ci.append(j), va.append(dense[i, j])
+        rs.append(len(ci))
+    return problems.HostCsr(n, np.array(rs, np.int32), np.array(ci, np.int32), np.array(va))
+
+
+def _edge(problems, name):
+    """The edge matrices of test_gpu_edges.py: 1 x 1, diagonal (one level), arrow (ragged rows:
+    row 0 couples to every row, so level 1 holds n - 1 rows of 2-3 entries)."""
+    if name == "one":
+        return _dense_csr(problems, np.array([[4.0]]))
+    if name == "diag":
+        return _dense_csr(problems, np.diag(np.arange(1.0, 70.0)))
+    n = 300
+    rng = np.random.default_rng(3)
+    a = np.zeros((n, n))
+    a[0, 1:] = a[1:, 0] = -rng.uniform(0.1, 1.0, n - 1) / n
+    for i in range(1, n - 1):
+        a[i, i + 1] = a[i + 1, i] = -0.3
+    a[np.arange(n), np.arange(n)] = 2.0
+    return _dense_csr(problems, a)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "lap1d", "one", "diag", "arrow"])
 def test_cluster_sweep_bitwise(modes, oracle, problems, name):
     from paper_2203_08498_b200 import api
 
@@ -42,6 +70,8 @@ def test_cluster_sweep_bitwise(modes, oracle, problems, name):
                 if 0 <= j < n:
                     ci.append(j), va.append(2.0 if j == i else -1.0)
         h = problems.HostCsr(n, rs, np.array(ci, np.int32), np.array(va))
+    elif name in ("one", "diag", "arrow"):
+        h = _edge(problems, name)
     else:
         h = problems.generate(problems.SMALL[name])
     sa, _ = _scaled(ctx, h)
