@@ -188,6 +188,41 @@ def test_loopback_sequence_matches_block_jacobi_sequence(oracle, problems, name,
     assert out["iterations"][1] < out["iterations"][0] or out["m_tilde"] == 0
 
 
+@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_loopback_sampled_method_b(oracle, problems, name, nparts):
+    """Solve 1 over row slabs with the method-B sampler (snapshots at the relative-residual
+    crossings eps^(j/(m+1)), sampling.cpp) against the oracle's block-Jacobi PCG with the same
+    sampler: iterations +-2; at equal counts the same occupied slots at the same iterations, and
+    every slot (x at that iteration, slab rows concatenated) within the solution tolerance."""
+    from paper_2203_08498_b200 import api, dist
+
+    sa, host = _scaled(oracle, problems, name)
+    b = oracle.uniform_pm1(5, 0, sa.n)
+    system = dist.LoopbackSystem(host, nparts)
+    samplers = [api.SamplerState.method_b(c, 6, 1e-8, p.nloc) for c, p in zip(system.ctxs, system.plans)]
+    xs = [np.zeros(p.nloc) for p in system.plans]
+    rep = api.dist_pcg_solve_sampled(system.comm, system.slabs, samplers, dist.scatter(b, system.plans), xs,
+                                     1e-8, 5000)
+    f = oracle.ic0_factorize(sa, 0.0, nparts)
+    so = oracle.sampler_b(6, 1e-8, sa.n)
+    xo = np.zeros(sa.n)
+    ro = oracle.pcg_solve(sa, b, xo, kind=1, ic=f, sampler=so, max_iter=5000)
+    _, _, tol = _oracle_block_jacobi(oracle, sa, b, nparts)
+    assert rep.converged and ro.converged
+    assert abs(rep.iterations - ro.iterations) <= 2, (rep.iterations, ro.iterations)
+    states = [s.state() for s in samplers]
+    for occ, it in states[1:]:   # every slab schedules the same iterations
+        assert np.array_equal(occ, states[0][0]) and np.array_equal(it, states[0][1])
+    if rep.iterations == ro.iterations:
+        oo, io = so.state()
+        assert np.array_equal(states[0][0], oo) and np.array_equal(states[0][1], io)
+        for j in np.nonzero(oo)[0]:
+            slot = np.concatenate([s.slot(int(j)) for s in samplers])
+            assert _rel(slot, so.slot(int(j))) <= tol, (j, _rel(slot, so.slot(int(j))), tol)
+        assert _rel(np.concatenate(xs), xo) <= tol
+
+
 @pytest.mark.parametrize("name", ["c1", "c4"])
 @pytest.mark.parametrize("nparts", [1, 2])
 def test_loopback_lean_sequence(oracle, problems, name, nparts, monkeypatch):
