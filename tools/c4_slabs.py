@@ -3,7 +3,8 @@
 distributed sampled solve 1, memory-lean distributed recycling (automatic at this size), deflated
 solves over the slabs.  40 samples (BASELINE.json leaves C4's count open).  Prints one JSON line.
 
-usage: python tools/c4_slabs.py [G]
+usage: python tools/c4_slabs.py [G] [config]   (config: c4 by default; c5 runs the 4M-point kNN
+Laplacian through the same path, with its irregular halo, 48 samples as BASELINE.json states)
 """
 import json
 import os
@@ -19,7 +20,10 @@ from paper_2203_08498_b200 import api, dist, problems  # noqa: E402
 
 def main():
     G = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-    cfg = replace(problems.CONFIGS["c4"], sampler_m=40)
+    name = sys.argv[2] if len(sys.argv) > 2 else "c4"
+    cfg = problems.CONFIGS[name]
+    if name == "c4":
+        cfg = replace(cfg, sampler_m=40)
     ctx = api.Context(0)
     t0 = time.perf_counter()
     h = problems.generate(cfg)
@@ -34,7 +38,8 @@ def main():
     system = dist.LoopbackSystem(scaled, G, device_factor=True)
     t_slabs = time.perf_counter() - t0
     t0 = time.perf_counter()
-    out = system.sequence(bs, cfg.eps, cfg.max_iter, cfg.sampler_m, cfg.keep, "deflation")
+    out = system.sequence(bs, cfg.eps, cfg.max_iter, cfg.sampler_m, cfg.keep,
+                          "sc" if cfg.method == "sc" else "deflation")
     secs = time.perf_counter() - t0
     its = int(sum(out["iterations"]))
     print(json.dumps({"config": cfg.name, "slabs": G, "n": scaled.n, "samples": cfg.sampler_m,
