@@ -1,0 +1,80 @@
+"""The C++ drop-in (paper_2203_08498_b200/bridge): one program written against the reference's
+public API (bridge_driver.cpp) linked against the unmodified reference library and against the
+reference library with src/pcg.cpp replaced by recycg_b200_bridge.cpp over librcg_b200.
+
+CPU: the reference-linked program runs the sequence, and the bridge-linked one fails loudly
+without a GPU (std::runtime_error from RCG_E_CUDA -- no CPU fallback).  GPU (-m gpu): both runs
+agree -- iterations +-2 per solve, the sampler's occupied slots and stored iterations, m_bar and
+Ritz values (<= 1e-6), solutions <= 1e-8 at equal counts.  The binaries are built by build() where
+the reference headers exist (this container) and travel to the GPU box prebuilt."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "paper_2203_08498_b200", "bridge", "_build")
+REF_BIN = os.path.join(BIN, "bridge_driver_ref")
+GPU_BIN = os.path.join(BIN, "bridge_driver_b200")
+
+needs_bins = pytest.mark.skipif(not (os.path.exists(REF_BIN) and os.path.exists(GPU_BIN)),
+                                reason="bridge binaries not built (build() needs the reference headers)")
+
+
+def _run(binary, out, grid):
+    os.makedirs(out, exist_ok=True)
+    return subprocess.run([binary, str(out), str(grid)], capture_output=True, text=True, timeout=600)
+
+
+def _load(out):
+    rep = json.load(open(os.path.join(out, "report.json")))
+    xs = {(s["kind"], s["k"]): np.fromfile(os.path.join(out, f"{s['kind']}{s['k']}.bin")) for s in rep["solves"]}
+    return rep, xs
+
+
+@needs_bins
+def test_reference_linked_driver_runs(tmp_path):
+    p = _run(REF_BIN, tmp_path / "ref", 16)
+    assert p.returncode == 0, p.stderr
+    rep, xs = _load(tmp_path / "ref")
+    assert rep["n"] == 16 ** 3 and all(s["converged"] for s in rep["solves"])
+    assert rep["m_tilde"] <= rep["m_bar"] <= 16
+    assert all(x.shape == (rep["n"],) for x in xs.values())
+
+
+@needs_bins
+def test_bridge_fails_loudly_without_gpu(tmp_path):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    p = _run(GPU_BIN, tmp_path / "gpu", 8)
+    assert p.returncode == 1
+    assert "no CPU fallback" in p.stderr
+
+
+@pytest.mark.gpu
+@needs_bins
+@pytest.mark.parametrize("grid", [16, 32, 48])
+def test_bridge_matches_reference(tmp_path, grid):
+    pr = _run(REF_BIN, tmp_path / "ref", grid)
+    pg = _run(GPU_BIN, tmp_path / "gpu", grid)
+    assert pr.returncode == 0, pr.stderr
+    assert pg.returncode == 0, pg.stderr
+    ref, xr = _load(tmp_path / "ref")
+    gpu, xg = _load(tmp_path / "gpu")
+    for sr, sg in zip(ref["solves"], gpu["solves"]):
+        assert (sr["kind"], sr["k"]) == (sg["kind"], sg["k"])
+        assert sg["converged"] and abs(sg["iterations"] - sr["iterations"]) <= 2, (sr, sg)
+        assert sg["history_len"] == sg["iterations"]
+        if sg["iterations"] == sr["iterations"]:
+            key = (sr["kind"], sr["k"])
+            rel = np.linalg.norm(xg[key] - xr[key]) / np.linalg.norm(xr[key])
+            assert rel <= 1e-8, (key, rel)
+    if gpu["solves"][0]["iterations"] == ref["solves"][0]["iterations"]:
+        # the device sampler replayed into the host SamplerState: the same schedule
+        assert gpu["occupied"] == ref["occupied"] and gpu["stored_iterations"] == ref["stored_iterations"]
+        assert gpu["m_bar"] == ref["m_bar"] and gpu["m_tilde"] == ref["m_tilde"]
+        assert np.allclose(gpu["ritz"], ref["ritz"], rtol=1e-6, atol=0)
