@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "recycg/condest.hpp"
 #include "recycg/csr_matrix.hpp"
 #include "recycg/deflation.hpp"
 #include "recycg/ic_preconditioner.hpp"
@@ -119,7 +120,15 @@ int main(int argc, char** argv) {
         }
         Vector xc(static_cast<std::size_t>(a.n()), 0.0);
         record("cg", 1, pcg_solve(a, scaling.scale_rhs(rhs(a0, 1)), id, xc, cfg), xc);
-        js += "], \"occupied\": " + occ + "], \"stored_iterations\": " + its + "], \"m_bar\": " +
+        // pcg_with_condest (condest.cpp:28-143) with IC(0), 20 samples, seed 42
+        Vector xe(static_cast<std::size_t>(a.n()), 0.0);
+        const CondestResult ce = pcg_with_condest(a, scaling.scale_rhs(rhs(a0, 2)), ic, xe, cfg, 20, 42);
+        record("condest", 2, ce.solve, xe);
+        char cbuf[160];
+        std::snprintf(cbuf, sizeof cbuf,
+                      "\"condest\": {\"lambda_max\": %.17g, \"lambda_min\": %.17g, \"kappa\": %.17g, \"power_iterations\": %d}, ",
+                      ce.estimate.lambda_max, ce.estimate.lambda_min, ce.estimate.kappa, ce.estimate.power_iterations);
+        js += std::string("], ") + cbuf + "\"occupied\": " + occ + "], \"stored_iterations\": " + its + "], \"m_bar\": " +
               std::to_string(aux.m_bar) + ", \"m_tilde\": " + std::to_string(defl.k()) + ", \"ritz\": [";
         for (int j = 0; j < aux.spectrum.k(); ++j) {
             char buf[40];

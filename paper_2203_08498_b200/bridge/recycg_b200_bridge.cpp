@@ -1,9 +1,10 @@
 // recycg_b200_bridge.cpp -- definitions of the reference's hot-path declarations
-// (proj/include/recycg/pcg.hpp:39-52: pcg_solve, deflated_pcg_solve) over librcg_b200.  Linked
-// INSTEAD of src/pcg.cpp into a build of the reference library; the rest of the reference is
-// unchanged.  The solves run on the GPU (device-resident PCG loop, IC(0) sweeps on the
-// reference's ordering, deflation projections); there is no CPU path here -- without a GPU every
-// call throws std::runtime_error (RCG_E_CUDA).
+// (proj/include/recycg/pcg.hpp:39-52: pcg_solve, deflated_pcg_solve; condest.hpp:46-48:
+// pcg_with_condest) over librcg_b200.  Linked INSTEAD of src/pcg.cpp and src/condest.cpp into a
+// build of the reference library; the rest of the reference is unchanged.  The solves run on the
+// GPU (device-resident PCG loop, IC(0) sweeps on the reference's ordering, deflation
+// projections); there is no CPU path here -- without a GPU every call throws std::runtime_error
+// (RCG_E_CUDA).
 //
 // Conventions kept from the reference:
 //  * argument checks and messages of pcg.cpp:17-26 / :98-99 (std::invalid_argument);
@@ -27,6 +28,7 @@
 #include <vector>
 
 #include "rcg_b200.h"
+#include "recycg/condest.hpp"
 #include "recycg/deflation.hpp"
 #include "recycg/ic_preconditioner.hpp"
 #include "recycg/pcg.hpp"
@@ -229,6 +231,39 @@ SolveReport deflated_pcg_solve(const CsrMatrix& a, const Vector& b, const Precon
     rep.wall_time = r.wall_time;
     if (cfg.record_history) rep.history.assign(hist.begin(), hist.begin() + r.iterations);
     return rep;
+}
+
+// condest.cpp:28-143: the PCG iterate of pcg_solve plus the fused power iteration (lambda_max)
+// and the method-A sampled Ritz values (lambda_min), all inside the device loop
+CondestResult pcg_with_condest(const CsrMatrix& a, const Vector& b, const Preconditioner& m, Vector& x,
+                               const SolverConfig& cfg, int m_samples, std::uint64_t v0_seed) {
+    if (!(cfg.eps > 0.0 && cfg.eps < 1.0)) throw std::invalid_argument("SolverConfig: eps must be in (0, 1)");
+    if (cfg.max_iter < 1) throw std::invalid_argument("SolverConfig: max_iter must be >= 1");
+    const std::size_t n = static_cast<std::size_t>(a.n());
+    if (b.size() != n || x.size() != n)
+        throw std::invalid_argument("pcg_with_condest: vector size does not match matrix");
+    const rcg_prec p = prec_of(m);
+    std::vector<double> hist(static_cast<std::size_t>(cfg.record_history ? cfg.max_iter : 0));
+    std::vector<double> ritz(static_cast<std::size_t>(m_samples > 0 ? m_samples : 1));
+    rcg_solver_config c{cfg.eps, cfg.max_iter, cfg.record_history ? 1 : 0};
+    rcg_solve_report r{0, 0, 0.0, static_cast<int>(hist.size()), hist.empty() ? nullptr : hist.data(), nullptr,
+                       nullptr};
+    rcg_cond_estimate e{};
+    e.ritz_values = ritz.data();
+    rethrow(rcg_pcg_with_condest(ctx(), device(a), b.data(), &p, x.data(), &c, m_samples, v0_seed, &r, &e));
+    CondestResult out;
+    out.solve.iterations = r.iterations;
+    out.solve.converged = r.converged != 0;
+    out.solve.wall_time = r.wall_time;
+    if (cfg.record_history) out.solve.history.assign(hist.begin(), hist.begin() + r.iterations);
+    out.estimate.lambda_max = e.lambda_max;
+    out.estimate.lambda_min = e.lambda_min;
+    out.estimate.kappa = e.kappa;
+    out.estimate.power_iterations = e.power_iterations;
+    out.estimate.power_unsettled = e.power_unsettled != 0;
+    out.estimate.lambda_min_available = e.lambda_min_available != 0;
+    out.estimate.ritz_values.assign(ritz.begin(), ritz.begin() + e.nritz);
+    return out;
 }
 
 }  // namespace recycg

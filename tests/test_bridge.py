@@ -1,12 +1,14 @@
 """The C++ drop-in (paper_2203_08498_b200/bridge): one program written against the reference's
 public API (bridge_driver.cpp) linked against the unmodified reference library and against the
-reference library with src/pcg.cpp replaced by recycg_b200_bridge.cpp over librcg_b200.
+reference library with src/pcg.cpp and src/condest.cpp replaced by recycg_b200_bridge.cpp over
+librcg_b200.
 
 CPU: the reference-linked program runs the sequence, and the bridge-linked one fails loudly
 without a GPU (std::runtime_error from RCG_E_CUDA -- no CPU fallback).  GPU (-m gpu): both runs
 agree -- iterations +-2 per solve, the sampler's occupied slots and stored iterations, m_bar and
-Ritz values (<= 1e-6), solutions <= 1e-8 at equal counts.  The binaries are built by build() where
-the reference headers exist (this container) and travel to the GPU box prebuilt."""
+Ritz values (<= 1e-6), solutions <= 1e-8 at equal counts, the condition estimate within 1 %.  The
+binaries are built by build() where the reference headers exist (this container) and travel to
+the GPU box prebuilt."""
 import json
 import os
 import subprocess
@@ -73,6 +75,10 @@ def test_bridge_matches_reference(tmp_path, grid):
             key = (sr["kind"], sr["k"])
             rel = np.linalg.norm(xg[key] - xr[key]) / np.linalg.norm(xr[key])
             assert rel <= 1e-8, (key, rel)
+    # pcg_with_condest: kappa within 1 % (north star), lambda_max from the same power iteration
+    cr, cg = ref["condest"], gpu["condest"]
+    assert abs(cg["kappa"] - cr["kappa"]) <= 0.01 * cr["kappa"], (cr, cg)
+    assert abs(cg["lambda_max"] - cr["lambda_max"]) <= 1e-6 * cr["lambda_max"], (cr, cg)
     if gpu["solves"][0]["iterations"] == ref["solves"][0]["iterations"]:
         # the device sampler replayed into the host SamplerState: the same schedule
         assert gpu["occupied"] == ref["occupied"] and gpu["stored_iterations"] == ref["stored_iterations"]
