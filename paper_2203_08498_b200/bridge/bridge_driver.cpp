@@ -7,6 +7,8 @@
 // recycg_b200_bridge.cpp (GPU).  tests/test_gpu_bridge.py compares the two runs.
 //
 // usage: bridge_driver OUT_DIR [grid]   (writes OUT_DIR/report.json and OUT_DIR/x<k>.bin)
+//        bridge_driver --errors          (the error contract: one "case: exception: message" line
+//                                         per misuse / breakdown case, pcg.cpp:17-26 and :55-75)
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -73,7 +75,42 @@ void dump(const std::string& path, const Vector& x) {
 
 }  // namespace
 
+// every failure the reference reports through exceptions, one line each
+int error_cases() {
+    const CsrMatrix a = poisson7(4);
+    const IdentityPreconditioner id;
+    const IcPreconditioner ic(ic0_factorize(a));
+    auto run = [](const char* name, auto&& f) {
+        try {
+            f();
+            std::printf("%s: no exception\n", name);
+        } catch (const BreakdownError& e) {
+            std::printf("%s: BreakdownError: %s\n", name, e.what());
+        } catch (const std::invalid_argument& e) {
+            std::printf("%s: invalid_argument: %s\n", name, e.what());
+        } catch (const std::exception& e) {
+            std::printf("%s: other: %s\n", name, e.what());
+        }
+    };
+    const std::size_t n = static_cast<std::size_t>(a.n());
+    SolverConfig cfg;
+    run("eps_zero", [&] { Vector x(n, 0.0); cfg.eps = 0.0; pcg_solve(a, Vector(n, 1.0), ic, x, cfg); });
+    cfg.eps = 1e-8;
+    run("max_iter_zero", [&] { Vector x(n, 0.0); SolverConfig c = cfg; c.max_iter = 0; pcg_solve(a, Vector(n, 1.0), id, x, c); });
+    run("size_b", [&] { Vector x(n, 0.0); pcg_solve(a, Vector(n - 1, 1.0), id, x, cfg); });
+    run("size_x", [&] { Vector x(n + 1, 0.0); deflated_pcg_solve(a, Vector(n, 1.0), id, DeflationOperator{}, x, cfg); });
+    run("condest_size", [&] { Vector x(n + 1, 0.0); pcg_with_condest(a, Vector(n, 1.0), id, x, cfg, 8, 42); });
+    // A = [[1, 2], [2, 1]] (eigenvalues 3, -1), b = (1, -1): (p, A p) = -2 at the first iteration
+    const CsrMatrix indef(2, {0, 2, 4}, {0, 1, 0, 1}, {1.0, 2.0, 2.0, 1.0});
+    run("pap_breakdown", [&] { Vector x(2, 0.0); pcg_solve(indef, Vector{1.0, -1.0}, id, x, cfg); });
+    run("deflated_pap_breakdown", [&] { Vector x(2, 0.0); deflated_pcg_solve(indef, Vector{1.0, -1.0}, id, DeflationOperator{}, x, cfg); });
+    run("zero_rhs", [&] { Vector x(n, 0.0); const SolveReport r = pcg_solve(a, Vector(n, 0.0), ic, x, cfg);
+                          std::printf("zero_rhs: iterations %d converged %d\n", r.iterations, r.converged ? 1 : 0); });
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc >= 2 && std::string(argv[1]) == "--errors") return error_cases();
     if (argc < 2) {
         std::fprintf(stderr, "usage: %s OUT_DIR [grid]\n", argv[0]);
         return 2;

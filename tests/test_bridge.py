@@ -84,3 +84,15 @@ def test_bridge_matches_reference(tmp_path, grid):
         assert gpu["occupied"] == ref["occupied"] and gpu["stored_iterations"] == ref["stored_iterations"]
         assert gpu["m_bar"] == ref["m_bar"] and gpu["m_tilde"] == ref["m_tilde"]
         assert np.allclose(gpu["ritz"], ref["ritz"], rtol=1e-6, atol=0)
+
+
+@pytest.mark.gpu
+@needs_bins
+def test_bridge_error_contract():
+    """Misuse and breakdown through the bridge raise the reference's exception types with the
+    reference's messages (pcg.cpp:17-26, :66-75, :123-134; condest.cpp:31-37), and a zero
+    right-hand side converges at 0 iterations (pcg.cpp:43-48): line-for-line the reference run."""
+    pr = subprocess.run([REF_BIN, "--errors"], capture_output=True, text=True, timeout=120)
+    pg = subprocess.run([GPU_BIN, "--errors"], capture_output=True, text=True, timeout=120)
+    assert pr.returncode == 0 and pg.returncode == 0, (pr.stderr, pg.stderr)
+    assert pg.stdout.splitlines() == pr.stdout.splitlines()
