@@ -134,7 +134,8 @@ int main(int argc, char** argv) {
             js += std::string(k || std::string(kind) != "iccg_sampled" ? ", " : "") + "{\"kind\": \"" + kind +
                   "\", \"k\": " + std::to_string(k) + ", \"iterations\": " + std::to_string(r.iterations) +
                   ", \"converged\": " + (r.converged ? "true" : "false") +
-                  ", \"history_len\": " + std::to_string(r.history.size()) + "}";
+                  ", \"history_len\": " + std::to_string(r.history.size()) +
+                  ", \"wall_time\": " + std::to_string(r.wall_time) + "}";
             dump(out + "/" + kind + std::to_string(k) + ".bin", x);
         };
 
