@@ -13,7 +13,7 @@ from . import Matrix, Oracle
 
 
 def rhs_set(o: Oracle, cfg, host, a_orig: Matrix, dis, new_of_old=None):
-    from paper_2203_08498_b200.problems import solution_stream
+    from .inputs import solution_stream
 
     xs = [solution_stream(cfg, host.n, k) for k in range(cfg.n_rhs)]
     if new_of_old is not None:  # multicolour variant: the solver sees P A P^T and P x

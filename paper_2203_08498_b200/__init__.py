@@ -6,8 +6,20 @@ kernels for SpMV, level-scheduled IC(0) sweeps, fused PCG vector ops, deflation 
 correction projections, the Rayleigh-Ritz step and the condition estimators.  ``api`` mirrors
 the reference solver API over that C-ABI; ``problems`` generates the BASELINE.json inputs;
 ``sequence`` runs the paper's sequence protocol.
-"""
-from . import api, problems  # noqa: F401
-from ._lib import LIB_PATH  # noqa: F401
 
-__version__ = "0.1.0"
+Submodules load lazily, so ``paper_2203_08498_b200.configs`` (plain data) can be read without
+mapping the library; every module that calls it (``api``, ``problems``, ...) raises at import
+when librcg_b200.so is missing -- there is no fallback.
+"""
+import importlib
+
+__version__ = "0.2.0"
+_LAZY = ("api", "problems", "sequence", "dist", "cost_model", "configs", "_lib")
+
+
+def __getattr__(name):
+    if name in _LAZY:
+        return importlib.import_module(f".{name}", __name__)
+    if name == "LIB_PATH":
+        return importlib.import_module("._lib", __name__).LIB_PATH
+    raise AttributeError(name)

@@ -14,7 +14,7 @@
 #include <thread>
 #include <vector>
 
-#include "internal.cuh"
+#include "host_error.h"
 
 namespace rcg {
 namespace {

@@ -17,15 +17,11 @@
 #include <vector>
 
 #include "rcg_b200.h"
+#include "host_error.h"
 
 namespace rcg {
 
-// ------------------------------------------------------------------ errors
-struct Error : std::runtime_error {
-    int code;
-    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
+// ------------------------------------------------------------------ errors (host_error.h)
 [[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
 #define RCG_CK(call)                                                              \
     do {                                                                          \
@@ -38,31 +34,6 @@ struct Error : std::runtime_error {
         if (e__ != cudaSuccess) ::rcg::throw_cuda(e__, "launch", __FILE__, __LINE__); \
         (ctx)->launches++;                                                         \
     } while (0)
-
-void set_error(const std::string& msg);
-void clear_error();
-
-template <class F>
-int guard(F&& f) {
-    try {
-        clear_error();
-        f();
-        return RCG_OK;
-    } catch (const Error& e) {
-        set_error(e.what());
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        set_error("host out of memory");
-        return RCG_E_CUDA;
-    } catch (const std::exception& e) {
-        set_error(e.what());
-        return RCG_E_CUDA;
-    }
-}
-
-inline void require(bool ok, const std::string& msg, int code = RCG_E_INVALID) {
-    if (!ok) throw Error(code, msg);
-}
 
 // ------------------------------------------------------------------ constants
 constexpr int kStreamThreads = 256;   // streaming / reduction kernels

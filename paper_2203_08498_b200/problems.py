@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import weakref
-from dataclasses import dataclass, replace
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -17,55 +17,7 @@ from . import _lib as L
 from ._lib import check, lib
 
 
-@dataclass(frozen=True)
-class Config:
-    name: str
-    kind: int
-    grid: int                 # N per axis, or the number of points (kNN)
-    n_rhs: int
-    rhs: str                  # 'uniform' | 'normal' | 'drift'
-    sampler_m: int
-    keep: int                 # m~ Ritz vectors kept (count-based selection)
-    method: str               # 'deflation' | 'sc'
-    condest: bool = False
-    inclusions: int = 0
-    inclusion_size: int = 0
-    contrast: float = 1.0
-    sigma: float = 0.0
-    knn_k: int = 10
-    seed: int = 20220317
-    rhs_seed: int = 1
-    eps: float = 1e-8
-    max_iter: int = 5000
-    blocks: int = 1
-    note: str = ""
-
-
-CONFIGS = {
-    "c1": Config("c1_poisson7_32", L.RCG_GEN_POISSON7, 32, 4, "uniform", 16, 8, "deflation",
-                 note="32^3 7-pt Poisson, IC(0)-CG, 4 RHS, 16 samples, deflation m=8 (CPU-runnable case)"),
-    "c2": Config("c2_fv7_contrast_128", L.RCG_GEN_FV7_CONTRAST, 128, 10, "normal", 32, 16, "sc",
-                 inclusions=8, inclusion_size=8, contrast=1e6,
-                 note="128^3 high-contrast 7-pt FV, 8 inclusions 8^3 at 1e6, 10 RHS, 32 samples, SC m=16"),
-    "c3": Config("c3_q1_27pt_256", L.RCG_GEN_Q1_27PT, 256, 20, "drift", 64, 32, "deflation", sigma=2.0,
-                 note="256^3 Q1 27-pt, log-normal exp(N(0,4)), 20 RHS drifting, 64 samples, deflation m=32"),
-    "c4": Config("c4_fv7_contrast_512", L.RCG_GEN_FV7_CONTRAST, 512, 8, "normal", 64, 32, "deflation",
-                 inclusions=64, inclusion_size=16, contrast=1e6,
-                 note="512^3 high-contrast 7-pt, 64 inclusions 16^3, 8 RHS, deflation m=32"),
-    "c5": Config("c5_knn_laplacian_4M", L.RCG_GEN_KNN, 4_000_000, 16, "normal", 48, 24, "deflation", condest=True,
-                 knn_k=10, note="4M-point kNN (k=10) graph Laplacian, 16 solves, condest each solve, deflation m=24"),
-}
-
-# scaled-down variants with the same structure, for parity tests the oracle finishes in seconds
-SMALL = {
-    "c1": CONFIGS["c1"],
-    "c2": replace(CONFIGS["c2"], name="c2_small_24", grid=24, n_rhs=4, inclusions=2, inclusion_size=4, sampler_m=16,
-                  keep=6),
-    "c3": replace(CONFIGS["c3"], name="c3_small_12", grid=12, n_rhs=4, sampler_m=16, keep=6),
-    "c4": replace(CONFIGS["c4"], name="c4_small_28", grid=28, n_rhs=3, inclusions=4, inclusion_size=4, sampler_m=16,
-                  keep=6),
-    "c5": replace(CONFIGS["c5"], name="c5_small_8k", grid=8000, n_rhs=3, sampler_m=16, keep=6),
-}
+from .configs import CONFIGS, SMALL, Config  # noqa: F401,E402  (re-exported)
 
 
 @dataclass
