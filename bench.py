@@ -176,7 +176,7 @@ def run_ours(args, rank, world, local_rank):
     w = last["wall_time"]
     phases = {"solve1_ms": round(w[0] * 1e3, 2), "solve1_iterations": last["iterations"][0],
               "rr_basis_ms": round(last["w_build_time"] * 1e3, 2),
-              "accelerated_ms": round(sum(w[k] for k in range(1, len(w), 16)) * 1e3, 2),
+              "accelerated_ms": round(sum(w[1:]) * 1e3, 2),
               "accelerated_iterations": last["iterations"][1:], "m_tilde": last["m_tilde"],
               "max_true_relres": max(last["true_relres"])}
     if "kappa" in last:

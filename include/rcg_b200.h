@@ -128,6 +128,9 @@ int rcg_tall_k(const rcg_tall* t);
 int32_t rcg_tall_n(const rcg_tall* t);
 /* column-major n x k, leading dimension n */
 int rcg_tall_download(rcg_ctx* ctx, const rcg_tall* t, double* cols_out);
+/* a TallDense held as k separate columns (host or device pointers, each of length n) -- the
+ * reference's std::vector<Vector> layout (dense.hpp:11-22), no host-side packing needed */
+int rcg_tall_create_cols(rcg_ctx* ctx, int32_t n, int k, const double* const* cols, rcg_tall** out);
 /* mgs_orthonormalize(v, drop_tol) -- dense.hpp:50 */
 int rcg_mgs_orthonormalize(rcg_ctx* ctx, const rcg_tall* v, double drop_tol, rcg_tall** out);
 
@@ -148,6 +151,11 @@ int rcg_sampler_slot(rcg_ctx* ctx, const rcg_sampler* s, int slot, double* out);
 /* ------------------------------------------------------------------ recycling (recycling.hpp) */
 /* harvest_errors(x_final, s) -- recycling.hpp:19 */
 int rcg_harvest_errors(rcg_ctx* ctx, const double* x_final, const rcg_sampler* s, rcg_tall** out);
+/* harvest_errors(x_final, s) -- recycling.hpp:19 -- for snapshots the caller holds: slots = the
+ * k occupied slots of a host SamplerState in slot order (sampling.hpp:39-44); exactly-zero
+ * differences are skipped (recycling.cpp:26) */
+int rcg_harvest_columns(rcg_ctx* ctx, const double* x_final, int32_t n, int k, const double* const* slots,
+                        rcg_tall** out);
 /* harvest_stored(s) -- recycling.hpp:23 */
 int rcg_harvest_stored(rcg_ctx* ctx, const rcg_sampler* s, rcg_tall** out);
 /* rayleigh_ritz(a, e) -- recycling.hpp:38: values (k, host) and optional Ritz vectors */
@@ -166,6 +174,15 @@ int rcg_build_aux_matrix(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* erro
 int rcg_basis_create(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* w, int who, rcg_basis** out);
 void rcg_basis_destroy(rcg_basis* b);
 int rcg_basis_k(const rcg_basis* b);
+/* a basis from the fields of an existing DeflationOperator / ScPreconditioner exactly as they are
+ * (W and AW as k host or device columns of length n, chol(W^T A W) row-major k x k): the operator
+ * that object applies, nothing recomputed */
+int rcg_basis_create_from(rcg_ctx* ctx, int32_t n, int k, const double* const* w_cols, const double* const* aw_cols,
+                          const double* chol_l, int who, rcg_basis** out);
+/* the host fields of DeflationOperator / ScPreconditioner (deflation.hpp:18-20,
+ * subspace_correction.hpp:31-36): AW column-major with leading dimension n (n * k doubles) and
+ * chol(W^T A W) row-major k x k (SmallChol::l); either may be NULL */
+int rcg_basis_export(rcg_ctx* ctx, const rcg_basis* b, double* aw_cols, double* chol_l);
 /* DeflationOperator::project_pt / project_p / direct_component -- deflation.hpp:24-32 */
 int rcg_project_pt(rcg_ctx* ctx, const rcg_basis* b, const double* y, double* out);
 int rcg_project_p(rcg_ctx* ctx, const rcg_basis* b, const double* x, double* out);
@@ -181,7 +198,8 @@ typedef struct {
 typedef struct {
     int iterations;
     int converged;
-    double wall_time;   /* seconds around the iteration loop (device events) */
+    double wall_time;   /* seconds around the iteration loop (device events); a batched solve
+                         * reports the batch's time divided by its right-hand sides */
     int cap;            /* capacity of the optional host arrays below */
     double* history;    /* relres per iteration (SolveReport::history) */
     double* alphas;     /* CG alpha_i per iteration (Lanczos input), optional */
@@ -196,6 +214,11 @@ typedef struct {
     const rcg_ic* ic;
     const rcg_basis* sc;
 } rcg_prec;
+
+/* Preconditioner::apply(r, z) -- preconditioner.hpp:13 -- on the device: IcPreconditioner
+ * (ic_apply, bitwise) or ScPreconditioner::apply (subspace_correction.cpp:47-57: inner, then
+ * z += W chol(W^T r)); an identity preconditioner needs no call (z = r) */
+int rcg_prec_apply(rcg_ctx* ctx, const rcg_prec* m, const double* r, double* z);
 
 #define RCG_PAYLOAD_X 0 /* error_sampling_observer    -- sampling.hpp:67 */
 #define RCG_PAYLOAD_R 1 /* residual_sampling_observer -- sampling.hpp:70 */

@@ -145,6 +145,7 @@ SIGNATURES = {
     "rcg_ic_export": (C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp),
     "rcg_ic_apply": (C.c_int, vp, vp, vp, vp),
     "rcg_tall_create": (C.c_int, vp, C.c_int32, C.c_int, vp, C.POINTER(vp)),
+    "rcg_tall_create_cols": (C.c_int, vp, C.c_int32, C.c_int, C.POINTER(vp), C.POINTER(vp)),
     "rcg_tall_destroy": (None, vp),
     "rcg_tall_k": (C.c_int, vp),
     "rcg_tall_n": (C.c_int32, vp),
@@ -156,15 +157,19 @@ SIGNATURES = {
     "rcg_sampler_state": (C.c_int, vp, vp, vp),
     "rcg_sampler_slot": (C.c_int, vp, vp, C.c_int, vp),
     "rcg_harvest_errors": (C.c_int, vp, vp, vp, C.POINTER(vp)),
+    "rcg_harvest_columns": (C.c_int, vp, vp, C.c_int32, C.c_int, C.POINTER(vp), C.POINTER(vp)),
     "rcg_harvest_stored": (C.c_int, vp, vp, C.POINTER(vp)),
     "rcg_rayleigh_ritz": (C.c_int, vp, vp, vp, vp, C.POINTER(vp)),
     "rcg_build_aux_matrix": (C.c_int, vp, vp, vp, C.c_double, C.c_int, ip, vp, dp, C.POINTER(vp)),
     "rcg_basis_create": (C.c_int, vp, vp, vp, C.c_int, C.POINTER(vp)),
     "rcg_basis_destroy": (None, vp),
     "rcg_basis_k": (C.c_int, vp),
+    "rcg_basis_create_from": (C.c_int, vp, C.c_int32, C.c_int, C.POINTER(vp), C.POINTER(vp), vp, C.c_int, C.POINTER(vp)),
+    "rcg_basis_export": (C.c_int, vp, vp, vp, vp),
     "rcg_project_pt": (C.c_int, vp, vp, vp, vp),
     "rcg_project_p": (C.c_int, vp, vp, vp, vp),
     "rcg_direct_component": (C.c_int, vp, vp, vp, vp),
+    "rcg_prec_apply": (C.c_int, vp, C.POINTER(Prec), vp, vp),
     "rcg_pcg_solve": (C.c_int, vp, vp, vp, C.POINTER(Prec), vp, C.POINTER(SolverConfig), vp, C.c_int,
                       C.POINTER(SolveReport)),
     "rcg_deflated_pcg_solve": (C.c_int, vp, vp, vp, C.POINTER(Prec), vp, vp, C.POINTER(SolverConfig),

@@ -57,6 +57,27 @@ def _f64(a, n=None, name="vector"):
     return a
 
 
+def _out(a, shape, name="x"):
+    """An output (or in/out) buffer the library writes: contiguous float64 of exactly `shape`
+    (numpy host or CUDA torch).  The reference throws invalid_argument on a size mismatch
+    (pcg.cpp:20-26); a short or float32 buffer here would be an out-of-bounds write."""
+    if isinstance(a, np.ndarray):
+        ok_t, ok_c = a.dtype == np.float64, a.flags["C_CONTIGUOUS"]
+    elif hasattr(a, "data_ptr"):
+        import torch
+
+        ok_t, ok_c = a.dtype == torch.float64, a.is_contiguous()
+    else:
+        raise InvalidArgument(f"{name}: unsupported buffer type {type(a)!r}")
+    if not ok_t:
+        raise InvalidArgument(f"{name} must be float64")
+    if not ok_c:
+        raise InvalidArgument(f"{name} must be contiguous")
+    if tuple(a.shape) != tuple(shape):
+        raise InvalidArgument(f"{name}: size does not match matrix (shape {tuple(a.shape)}, expected {tuple(shape)})")
+    return a
+
+
 class Context:
     """One GPU and one CUDA stream (rcg_ctx)."""
 
@@ -163,6 +184,7 @@ class CsrMatrix:
         x = _f64(x, self.n, "x")
         if y is None:
             y = np.empty(self.n) if isinstance(x, np.ndarray) else x.new_empty(self.n)
+        _out(y, (self.n,), "y")
         check(lib.rcg_spmv(self.ctx.h, self.h, _ptr(x), _ptr(y)))
         return y
 
@@ -482,6 +504,7 @@ def pcg_solve(ctx: Context, a: CsrMatrix, b, m, x, eps: float = 1e-8, max_iter: 
     """pcg_solve (pcg.hpp:39-41); x is updated in place.  observer: a SamplerState fed the
     iterate (payload 'x', error_sampling_observer) or the residual ('r')."""
     b = _f64(b, a.n, "b")
+    _out(x, (a.n,), "x")
     cfg = _cfg(eps, max_iter)
     rep, bufs = _report(max(1, int(max_iter)))
     p = _prec(m)
@@ -495,6 +518,7 @@ def deflated_pcg_solve(ctx: Context, a: CsrMatrix, b, m, defl: Optional[Basis], 
                        max_iter: int = 1000) -> SolveReport:
     """deflated_pcg_solve (pcg.hpp:50-52); defl None is the empty W."""
     b = _f64(b, a.n, "b")
+    _out(x, (a.n,), "x")
     cfg = _cfg(eps, max_iter)
     rep, bufs = _report(max(1, int(max_iter)))
     p = _prec(m)
@@ -515,6 +539,7 @@ def _batch(fn, ctx, a, B, m, X, eps, max_iter, defl=None):
         Bm = torch.stack(list(B)).contiguous() if isinstance(B, list) else B.contiguous()
     if Bm.shape[-1] != a.n:
         raise InvalidArgument("batch solve: right-hand side length does not match matrix")
+    _out(X, (R, a.n), "X")
     cfg = _cfg(eps, max_iter)
     reps = (L.SolveReport * R)()
     bufs = []
@@ -547,6 +572,7 @@ def pcg_with_condest(ctx: Context, a: CsrMatrix, b, m, x, eps: float = 1e-8, max
                      m_samples: int = 20, v0_seed: int = 42):
     """pcg_with_condest (condest.hpp:46-48) plus the Lanczos estimate; returns (report, estimate)."""
     b = _f64(b, a.n, "b")
+    _out(x, (a.n,), "x")
     cfg = _cfg(eps, max_iter)
     rep, bufs = _report(max(1, int(max_iter)))
     est = L.CondEstimate()
@@ -704,7 +730,7 @@ def dist_pcg_solve(comm: Comm, slabs, bs, xs, eps: float = 1e-8, max_iter: int =
     bs = [_f64(b, s.plan.nloc, "b") for b, s in zip(bs, slabs)]
     hs = (C.c_void_p * ns)(*[s.h.value for s in slabs])
     bp = (C.c_void_p * ns)(*[_ptr(b) for b in bs])
-    xp = (C.c_void_p * ns)(*[_ptr(x) for x in xs])
+    xp = (C.c_void_p * ns)(*[_ptr(_out(x, (s_.plan.nloc,), "x")) for x, s_ in zip(xs, slabs)])
     cfg = _cfg(eps, max_iter)
     rep, bufs = _report(max(1, int(max_iter)))
     check(lib.rcg_dist_pcg_solve(comm.h, ns, hs, bp, xp, C.byref(cfg), C.byref(rep)))
@@ -744,7 +770,7 @@ def dist_solve(comm: Comm, slabs, bs, xs, basis: Optional[DBasis] = None, eps: f
     bs = [_f64(b, s_.plan.nloc, "b") for b, s_ in zip(bs, slabs)]
     hs = (C.c_void_p * ns)(*[s_.h.value for s_ in slabs])
     bp = (C.c_void_p * ns)(*[_ptr(b) for b in bs])
-    xp = (C.c_void_p * ns)(*[_ptr(x) for x in xs])
+    xp = (C.c_void_p * ns)(*[_ptr(_out(x, (s_.plan.nloc,), "x")) for x, s_ in zip(xs, slabs)])
     cfg = _cfg(eps, max_iter)
     rep, bufs = _report(max(1, int(max_iter)))
     check(lib.rcg_dist_solve(comm.h, ns, hs, basis.h if basis is not None else None, bp, xp, C.byref(cfg),
@@ -762,7 +788,7 @@ def dist_pcg_solve_sampled(comm: Comm, slabs, samplers, bs, xs, eps: float = 1e-
     hs = (C.c_void_p * ns)(*[s_.h.value for s_ in slabs])
     sp = (C.c_void_p * ns)(*[o.h.value for o in samplers])
     bp = (C.c_void_p * ns)(*[_ptr(b) for b in bs])
-    xp = (C.c_void_p * ns)(*[_ptr(x) for x in xs])
+    xp = (C.c_void_p * ns)(*[_ptr(_out(x, (s_.plan.nloc,), "x")) for x, s_ in zip(xs, slabs)])
     cfg = _cfg(eps, max_iter)
     rep, bufs = _report(max(1, int(max_iter)))
     check(lib.rcg_dist_pcg_solve_sampled(comm.h, ns, hs, sp, bp, xp, C.byref(cfg), C.byref(rep)))
@@ -815,6 +841,8 @@ class Sequence:
             lean: bool = False) -> dict:
         """lean: the memory-lean recycling step always (default: only when HBM is short)."""
         k = len(B)
+        _out(B, (k, self.n), "B")  # read-only here, but passed raw: same contract
+        _out(X, (k, self.n), "X")
         cfg = L.SeqConfig(float(eps), int(max_iter), ord(sampling), int(m), float(theta), int(keep_count),
                           1 if batch else 0, 1 if lean else 0)
         its = np.zeros(k, np.int32)

@@ -1,18 +1,31 @@
 // bridge_driver.cpp -- a program written against the reference's public C++ API only
-// (proj/include/recycg): the run_sequence shape of driver.cpp:108-222 on a 7-point Poisson
-// matrix -- diagonal scaling, IC(0), solve 1 with the error sampler, the recycling step
-// (harvest_errors + build_aux_matrix), build_deflation_operator, deflated solves 2..k, plus a
-// plain CG solve.  The SAME source is linked twice (Makefile): against the whole reference
-// library (CPU) and against the reference library with src/pcg.cpp replaced by
-// recycg_b200_bridge.cpp (GPU).  tests/test_gpu_bridge.py compares the two runs.
+// (proj/include/recycg; no bridge header): the run_sequence shape of driver.cpp:108-222.  The
+// SAME source is linked twice (Makefile): against the whole reference library (CPU) and against
+// the reference library with its hot-path modules replaced by the bridge (GPU).
+// tests/test_bridge.py compares the two runs.
 //
-// usage: bridge_driver OUT_DIR [grid]   (writes OUT_DIR/report.json and OUT_DIR/x<k>.bin)
-//        bridge_driver --errors          (the error contract: one "case: exception: message" line
-//                                         per misuse / breakdown case, pcg.cpp:17-26 and :55-75)
+// usage: bridge_driver OUT_DIR [grid]
+//            7-point Poisson: scaling, IC(0), solve 1 with the reference's own
+//            error_sampling_observer, harvest_errors + build_aux_matrix, build_deflation_operator,
+//            deflated solves, CG, pcg_with_condest, plus single calls of spmv_dual, ic_apply,
+//            project_pt / project_p / direct_component, mgs_orthonormalize, rayleigh_ritz,
+//            harvest_stored and ScPreconditioner::apply (their outputs are compared)
+//        bridge_driver OUT_DIR --csr FILE --method sc|deflation --rhs K --samples M --keep KEEP
+//            the sequence on a matrix read from FILE (int32 n, int64 nnz, row_start, col_idx,
+//            values): solve 1 with the sampler, build_aux_matrix (theta = +inf, the KEEP smallest
+//            Ritz vectors), then ScPreconditioner(IC(0), W) or build_deflation_operator(W) and
+//            solves 2..K -- the C2 bench protocol through the reference API
+//        bridge_driver --errors
+//            the error contract: one "case: exception: message" line per misuse / breakdown case
+//            (pcg.cpp:17-26 and :55-75)
+// Writes OUT_DIR/report.json and OUT_DIR/<kind><k>.bin (solutions).
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
+#include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -25,7 +38,7 @@
 #include "recycg/recycling.hpp"
 #include "recycg/sampling.hpp"
 #include "recycg/scaling.hpp"
-#include "recycg_b200.hpp"
+#include "recycg/subspace_correction.hpp"
 
 using namespace recycg;
 
@@ -109,76 +122,202 @@ int error_cases() {
     return 0;
 }
 
+namespace {
+
+std::string jnum(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    return buf;
+}
+
+std::string jlist(const std::vector<double>& v) {
+    std::string s = "[";
+    for (std::size_t j = 0; j < v.size(); ++j) s += (j ? ", " : "") + jnum(v[j]);
+    return s + "]";
+}
+
+struct Recorder {
+    std::string out, js;
+    bool first = true;
+    void solve(const char* kind, int k, const SolveReport& r, const Vector& x) {
+        js += std::string(first ? "" : ", ") + "{\"kind\": \"" + kind + "\", \"k\": " + std::to_string(k) +
+              ", \"iterations\": " + std::to_string(r.iterations) + ", \"converged\": " +
+              (r.converged ? "true" : "false") + ", \"history_len\": " + std::to_string(r.history.size()) +
+              ", \"wall_time\": " + jnum(r.wall_time) + "}";
+        first = false;
+        dump(out + "/" + kind + std::to_string(k) + ".bin", x);
+    }
+};
+
+CsrMatrix read_csr(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open " + path);
+    std::int32_t n = 0;
+    std::int64_t nnz = 0;
+    bool ok = std::fread(&n, sizeof n, 1, f) == 1 && std::fread(&nnz, sizeof nnz, 1, f) == 1;
+    std::vector<index_t> rs(ok ? static_cast<std::size_t>(n) + 1 : 0), ci(ok ? static_cast<std::size_t>(nnz) : 0);
+    std::vector<double> va(ci.size());
+    ok = ok && std::fread(rs.data(), sizeof(index_t), rs.size(), f) == rs.size() &&
+         std::fread(ci.data(), sizeof(index_t), ci.size(), f) == ci.size() &&
+         std::fread(va.data(), sizeof(double), va.size(), f) == va.size();
+    std::fclose(f);
+    if (!ok) throw std::runtime_error("short read " + path);
+    return CsrMatrix(n, std::move(rs), std::move(ci), std::move(va));
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// run_sequence (driver.cpp:108-222) through the public API: the C2 bench protocol when FILE is
+// the C2 matrix (10 RHS, 32 samples, SC with the 16 smallest Ritz vectors)
+int sequence_mode(const std::string& out, const std::string& csr, const std::string& method, int n_rhs, int m,
+                  int keep) {
+    using clock = std::chrono::steady_clock;
+    const auto t_all = clock::now();
+    const CsrMatrix a0 = read_csr(csr);
+    auto t0 = clock::now();
+    auto [a, scaling] = diagonal_scale(a0);
+    auto inner = std::make_shared<IcPreconditioner>(ic0_factorize(a));
+    const double t_setup = seconds_since(t0);
+    SolverConfig cfg;
+    cfg.eps = 1e-8;
+    cfg.max_iter = 5000;
+    cfg.record_history = true;
+    Recorder rec{out, "{\"n\": " + std::to_string(a.n()) + ", \"solves\": ["};
+    t0 = clock::now();
+    SamplerState s = SamplerState::method_a(std::max(m, 2), cfg.max_iter);  // driver.cpp:142
+    Vector x(static_cast<std::size_t>(a.n()), 0.0);
+    rec.solve("iccg_sampled", 0, pcg_solve(a, scaling.scale_rhs(rhs(a0, 0)), *inner, x, cfg, error_sampling_observer(s)), x);
+    const double t_solve1 = seconds_since(t0);
+    t0 = clock::now();
+    const AuxBasis aux = build_aux_matrix(a, harvest_errors(x, s), std::numeric_limits<double>::infinity());
+    TallDense w(a.n());
+    for (int j = 0; j < std::min<int>(keep, aux.w.k()); ++j) w.cols.push_back(aux.w.cols[static_cast<std::size_t>(j)]);
+    std::unique_ptr<ScPreconditioner> sc;
+    DeflationOperator defl;
+    if (method == "sc")
+        sc = std::make_unique<ScPreconditioner>(inner, a, w);
+    else
+        defl = build_deflation_operator(a, w);
+    const double t_basis = seconds_since(t0);
+    t0 = clock::now();
+    for (int k = 1; k < n_rhs; ++k) {
+        Vector xk(static_cast<std::size_t>(a.n()), 0.0);
+        const Vector bk = scaling.scale_rhs(rhs(a0, k));
+        if (sc)
+            rec.solve("accelerated", k, pcg_solve(a, bk, *sc, xk, cfg), xk);
+        else
+            rec.solve("accelerated", k, deflated_pcg_solve(a, bk, *inner, defl, xk, cfg), xk);
+    }
+    const double t_acc = seconds_since(t0);
+    rec.js += "], \"m_bar\": " + std::to_string(aux.m_bar) + ", \"m_tilde\": " + std::to_string(w.k()) +
+              ", \"ritz\": " + jlist(aux.spectrum.values) + ", \"seconds\": {\"setup\": " + jnum(t_setup) +
+              ", \"solve1\": " + jnum(t_solve1) + ", \"recycle_and_basis\": " + jnum(t_basis) +
+              ", \"accelerated\": " + jnum(t_acc) + ", \"total\": " + jnum(seconds_since(t_all)) + "}}\n";
+    FILE* f = std::fopen((out + "/report.json").c_str(), "w");
+    if (!f) throw std::runtime_error("cannot write report.json");
+    std::fputs(rec.js.c_str(), f);
+    std::fclose(f);
+    std::fputs(rec.js.c_str(), stdout);
+    return 0;
+}
+
+}  // namespace
+
 int main(int argc, char** argv) {
     if (argc >= 2 && std::string(argv[1]) == "--errors") return error_cases();
     if (argc < 2) {
-        std::fprintf(stderr, "usage: %s OUT_DIR [grid]\n", argv[0]);
+        std::fprintf(stderr, "usage: %s OUT_DIR [grid] | OUT_DIR --csr FILE --method sc|deflation --rhs K "
+                             "--samples M --keep KEEP\n", argv[0]);
         return 2;
     }
     const std::string out = argv[1];
-    const int grid = argc > 2 ? std::atoi(argv[2]) : 32;
-    const int m = 16, cap = 5000, n_rhs = 4;
-    const double theta = 0.05;
     try {
+        if (argc > 2 && std::string(argv[2]) == "--csr") {
+            std::string csr, method = "sc";
+            int n_rhs = 10, m = 32, keep = 16;
+            for (int i = 2; i + 1 < argc; i += 2) {
+                const std::string k = argv[i], v = argv[i + 1];
+                if (k == "--csr") csr = v;
+                else if (k == "--method") method = v;
+                else if (k == "--rhs") n_rhs = std::atoi(v.c_str());
+                else if (k == "--samples") m = std::atoi(v.c_str());
+                else if (k == "--keep") keep = std::atoi(v.c_str());
+            }
+            return sequence_mode(out, csr, method, n_rhs, m, keep);
+        }
+        const int grid = argc > 2 ? std::atoi(argv[2]) : 32;
+        const int m = 16, cap = 5000, n_rhs = 4;
+        const double theta = 0.05;
         const CsrMatrix a0 = poisson7(grid);
         auto [a, scaling] = diagonal_scale(a0);
-        const IcPreconditioner ic(ic0_factorize(a));
+        auto ic = std::make_shared<IcPreconditioner>(ic0_factorize(a));
         const IdentityPreconditioner id;
         SolverConfig cfg;
         cfg.eps = 1e-8;
         cfg.max_iter = cap;
         cfg.record_history = true;
+        Recorder rec{out, "{\"n\": " + std::to_string(a.n()) + ", \"solves\": ["};
 
-        std::string js = "{\"n\": " + std::to_string(a.n()) + ", \"solves\": [";
-        auto record = [&](const char* kind, int k, const SolveReport& r, const Vector& x) {
-            js += std::string(k || std::string(kind) != "iccg_sampled" ? ", " : "") + "{\"kind\": \"" + kind +
-                  "\", \"k\": " + std::to_string(k) + ", \"iterations\": " + std::to_string(r.iterations) +
-                  ", \"converged\": " + (r.converged ? "true" : "false") +
-                  ", \"history_len\": " + std::to_string(r.history.size()) +
-                  ", \"wall_time\": " + std::to_string(r.wall_time) + "}";
-            dump(out + "/" + kind + std::to_string(k) + ".bin", x);
-        };
-
-        // solve 1 with the error sampler (driver.cpp:150-160)
+        // solve 1 with the reference's own error sampler (driver.cpp:150-160)
         SamplerState s = SamplerState::method_a(m, cap);
         Vector x(static_cast<std::size_t>(a.n()), 0.0);
         const Vector b0 = scaling.scale_rhs(rhs(a0, 0));
-        record("iccg_sampled", 0, pcg_solve(a, b0, ic, x, cfg, b200::error_sampling_observer_a(s, cap)), x);
-        std::string occ = "[", its = "[";
+        rec.solve("iccg_sampled", 0, pcg_solve(a, b0, *ic, x, cfg, error_sampling_observer(s)), x);
+        std::vector<double> occ, its;
         for (int j = 0; j < m; ++j) {
-            occ += std::string(j ? ", " : "") + (s.occupied(j) ? "1" : "0");
-            its += std::string(j ? ", " : "") + std::to_string(s.occupied(j) ? s.stored_iteration(j) : 0);
+            occ.push_back(s.occupied(j) ? 1 : 0);
+            its.push_back(s.occupied(j) ? s.stored_iteration(j) : 0);
         }
-        // the recycling step on the host (recycling.cpp:81-96) and the deflation operator
-        const AuxBasis aux = build_aux_matrix(a, harvest_errors(x, s), theta);
+        // the recycling step (recycling.cpp:81-96) and the deflation operator
+        const TallDense errors = harvest_errors(x, s);
+        const AuxBasis aux = build_aux_matrix(a, errors, theta);
         const DeflationOperator defl = build_deflation_operator(a, aux.w);
         for (int k = 1; k < n_rhs; ++k) {
             Vector xk(static_cast<std::size_t>(a.n()), 0.0);
-            record("deflated", k, deflated_pcg_solve(a, scaling.scale_rhs(rhs(a0, k)), ic, defl, xk, cfg), xk);
+            rec.solve("deflated", k, deflated_pcg_solve(a, scaling.scale_rhs(rhs(a0, k)), *ic, defl, xk, cfg), xk);
         }
         Vector xc(static_cast<std::size_t>(a.n()), 0.0);
-        record("cg", 1, pcg_solve(a, scaling.scale_rhs(rhs(a0, 1)), id, xc, cfg), xc);
+        rec.solve("cg", 1, pcg_solve(a, scaling.scale_rhs(rhs(a0, 1)), id, xc, cfg), xc);
+        // subspace correction around IC(0) with the same W (subspace_correction.cpp:27-57)
+        const ScPreconditioner sc(ic, a, aux.w);
+        Vector xs(static_cast<std::size_t>(a.n()), 0.0);
+        rec.solve("sc", 1, pcg_solve(a, scaling.scale_rhs(rhs(a0, 1)), sc, xs, cfg), xs);
         // pcg_with_condest (condest.cpp:28-143) with IC(0), 20 samples, seed 42
         Vector xe(static_cast<std::size_t>(a.n()), 0.0);
-        const CondestResult ce = pcg_with_condest(a, scaling.scale_rhs(rhs(a0, 2)), ic, xe, cfg, 20, 42);
-        record("condest", 2, ce.solve, xe);
-        char cbuf[160];
-        std::snprintf(cbuf, sizeof cbuf,
-                      "\"condest\": {\"lambda_max\": %.17g, \"lambda_min\": %.17g, \"kappa\": %.17g, \"power_iterations\": %d}, ",
-                      ce.estimate.lambda_max, ce.estimate.lambda_min, ce.estimate.kappa, ce.estimate.power_iterations);
-        js += std::string("], ") + cbuf + "\"occupied\": " + occ + "], \"stored_iterations\": " + its + "], \"m_bar\": " +
-              std::to_string(aux.m_bar) + ", \"m_tilde\": " + std::to_string(defl.k()) + ", \"ritz\": [";
-        for (int j = 0; j < aux.spectrum.k(); ++j) {
-            char buf[40];
-            std::snprintf(buf, sizeof buf, "%s%.17g", j ? ", " : "", aux.spectrum.values[static_cast<std::size_t>(j)]);
-            js += buf;
-        }
-        js += "]}\n";
+        const CondestResult ce = pcg_with_condest(a, scaling.scale_rhs(rhs(a0, 2)), *ic, xe, cfg, 20, 42);
+        rec.solve("condest", 2, ce.solve, xe);
+        // single calls of the other hot-path functions on fixed inputs
+        const Vector v = rhs(a0, 7), u = rhs(a0, 8);
+        Vector y1, y2, z, zs;
+        spmv_dual(a, v, u, y1, y2);
+        ic_apply(ic->factor(), v, z);
+        sc.apply(v, zs);
+        dump(out + "/op_spmv_dual1.bin", y1);
+        dump(out + "/op_spmv_dual2.bin", y2);
+        dump(out + "/op_ic_apply.bin", z);
+        dump(out + "/op_sc_apply.bin", zs);
+        dump(out + "/op_project_pt.bin", defl.project_pt(v));
+        dump(out + "/op_project_p.bin", defl.project_p(v));
+        dump(out + "/op_direct_component.bin", defl.direct_component(v));
+        const TallDense q = mgs_orthonormalize(errors);
+        const RitzSpectrum rr = rayleigh_ritz(a, q);
+        for (int j = 0; j < std::min<int>(2, q.k()); ++j) dump(out + "/op_mgs" + std::to_string(j) + ".bin", q.cols[j]);
+        const TallDense st = harvest_stored(s);
+        rec.js += "], \"condest\": {\"lambda_max\": " + jnum(ce.estimate.lambda_max) + ", \"lambda_min\": " +
+                  jnum(ce.estimate.lambda_min) + ", \"kappa\": " + jnum(ce.estimate.kappa) +
+                  ", \"power_iterations\": " + std::to_string(ce.estimate.power_iterations) + "}, \"occupied\": " +
+                  jlist(occ) + ", \"stored_iterations\": " + jlist(its) + ", \"m_bar\": " + std::to_string(aux.m_bar) +
+                  ", \"m_tilde\": " + std::to_string(defl.k()) + ", \"ritz\": " + jlist(aux.spectrum.values) +
+                  ", \"mgs_k\": " + std::to_string(q.k()) + ", \"rr_values\": " + jlist(rr.values) +
+                  ", \"harvest_stored_k\": " + std::to_string(st.k()) + ", \"errors_k\": " + std::to_string(errors.k()) +
+                  ", \"sc_chol_k\": " + std::to_string(sc.subspace_dim()) + "}\n";
         FILE* f = std::fopen((out + "/report.json").c_str(), "w");
         if (!f) throw std::runtime_error("cannot write report.json");
-        std::fputs(js.c_str(), f);
+        std::fputs(rec.js.c_str(), f);
         std::fclose(f);
-        std::fputs(js.c_str(), stdout);
+        std::fputs(rec.js.c_str(), stdout);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "bridge_driver: %s\n", e.what());
         return 1;

@@ -1,33 +1,29 @@
-// recycg_b200_bridge.cpp -- definitions of the reference's hot-path declarations
-// (proj/include/recycg/pcg.hpp:39-52: pcg_solve, deflated_pcg_solve; condest.hpp:46-48:
-// pcg_with_condest) over librcg_b200.  Linked INSTEAD of src/pcg.cpp and src/condest.cpp into a
-// build of the reference library; the rest of the reference is unchanged.  The solves run on the
-// GPU (device-resident PCG loop, IC(0) sweeps on the reference's ordering, deflation
-// projections); there is no CPU path here -- without a GPU every call throws std::runtime_error
-// (RCG_E_CUDA).
+// recycg_b200_bridge.cpp -- the reference's solver entry points over librcg_b200: pcg_solve and
+// deflated_pcg_solve (proj/include/recycg/pcg.hpp:39-52, replacing src/pcg.cpp) and
+// pcg_with_condest (condest.hpp:46-48, replacing src/condest.cpp).  Linked into a build of the
+// reference library together with recycg_b200_ops.cpp (the other hot-path modules) and
+// bridge_core.cpp; the rest of the reference is unchanged.  The solves run on the GPU
+// (device-resident PCG loop, IC(0) sweeps on the reference's ordering, deflation projections,
+// subspace correction); there is no CPU path -- without a GPU every call throws
+// std::runtime_error (RCG_E_CUDA).
 //
 // Conventions kept from the reference:
 //  * argument checks and messages of pcg.cpp:17-26 / :98-99 (std::invalid_argument);
-//  * status -> exception: RCG_E_INVALID -> std::invalid_argument, RCG_E_BREAKDOWN ->
-//    BreakdownError (the reference's "(r, z) <= 0" / "(p, A p) <= 0" messages), RCG_E_PARSE ->
-//    ParseError, RCG_E_CUDA -> std::runtime_error;
-//  * preconditioners dispatched by dynamic type {IdentityPreconditioner, IcPreconditioner};
-//    ScPreconditioner keeps its inner preconditioner private (subspace_correction.hpp:34), so it
-//    cannot be mirrored on the device from outside and throws std::invalid_argument here;
-//  * the observer: recycg::b200::SamplingObserver (recycg_b200.hpp) is run on the device and
-//    replayed into the host SamplerState; any other non-empty observer throws
-//    std::invalid_argument (the device loop does not call back per iteration);
-//  * device images of CsrMatrix / IcFactor / DeflationOperator are cached by object identity
-//    (the reference types are immutable after construction).
+//  * status -> exception mapping (bridge_core.hpp);
+//  * preconditioners dispatched by dynamic type {IdentityPreconditioner, IcPreconditioner,
+//    ScPreconditioner over an identity or IC(0) inner};
+//  * the observer: the error / residual sampling observers of sampling.hpp:67-70 (the reference's
+//    own factory functions, defined by recycg_b200_ops.cpp as a named functor) run on the device
+//    inside the solve and are replayed into the host SamplerState; any other non-empty observer
+//    throws std::invalid_argument (the device loop does not call back per iteration).
 #include <cstring>
 #include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
-#include <tuple>
 #include <vector>
 
-#include "rcg_b200.h"
+#include "bridge_core.hpp"
 #include "recycg/condest.hpp"
 #include "recycg/deflation.hpp"
 #include "recycg/ic_preconditioner.hpp"
@@ -39,92 +35,7 @@
 namespace recycg {
 namespace {
 
-void rethrow(int st) {
-    if (st == RCG_OK) return;
-    const std::string m = rcg_last_error();
-    if (st == RCG_E_INVALID) throw std::invalid_argument(m);
-    if (st == RCG_E_BREAKDOWN) throw BreakdownError(m);
-    if (st == RCG_E_PARSE) throw ParseError(m);
-    throw std::runtime_error("librcg_b200: " + m);
-}
-
-rcg_ctx* ctx() {
-    static rcg_ctx* c = [] {
-        rcg_ctx* p = nullptr;
-        rethrow(rcg_ctx_create(0, &p));
-        return p;
-    }();
-    return c;
-}
-
-// identity key: object address + its payload address + size (a destroyed object's address reused
-// by another object of different contents would have to reuse the payload buffer as well)
-using Key = std::tuple<const void*, const void*, std::size_t>;
-struct Images {
-    std::map<Key, rcg_matrix*> mats;
-    std::map<Key, rcg_ic*> ics;
-    std::map<Key, rcg_basis*> bases;
-};
-Images& images() {
-    static Images im;
-    return im;
-}
-
-rcg_matrix* device(const CsrMatrix& a) {
-    const Key k{&a, a.values().data(), a.values().size()};
-    auto& m = images().mats;
-    auto it = m.find(k);
-    if (it != m.end()) return it->second;
-    rcg_matrix* d = nullptr;
-    // validate = 0: a CsrMatrix is validated by its constructor (csr_matrix.cpp:36-87)
-    rethrow(rcg_matrix_create(ctx(), a.n(), a.row_start().data(), a.col_idx().data(), a.values().data(), 0, &d));
-    m.emplace(k, d);
-    return d;
-}
-
-rcg_ic* device(const IcFactor& f) {
-    const Key k{&f, f.l_val.data(), f.l_val.size()};
-    auto& m = images().ics;
-    auto it = m.find(k);
-    if (it != m.end()) return it->second;
-    rcg_ic* d = nullptr;
-    rethrow(rcg_ic_create(ctx(), f.n, f.num_blocks(), f.block_bounds.data(), f.l_row_start.data(), f.l_col.data(),
-                          f.l_val.data(), f.d.data(), f.u_row_start.data(), f.u_col.data(), f.u_val.data(),
-                          f.shift_used, &d));
-    m.emplace(k, d);
-    return d;
-}
-
-// DeflationOperator (deflation.hpp:17-33): W uploaded column-major; AW and chol(W^T A W) are
-// rebuilt on the device from W (build_deflation_operator, deflation.cpp:45-76)
-rcg_basis* device(const CsrMatrix& a, const DeflationOperator& defl) {
-    if (defl.empty()) return nullptr;
-    const Key k{&defl, defl.w.cols[0].data(), static_cast<std::size_t>(defl.k())};
-    auto& m = images().bases;
-    auto it = m.find(k);
-    if (it != m.end()) return it->second;
-    const std::size_t n = static_cast<std::size_t>(defl.w.n);
-    std::vector<double> cols(n * static_cast<std::size_t>(defl.k()));
-    for (int j = 0; j < defl.k(); ++j) std::memcpy(cols.data() + j * n, defl.w.cols[j].data(), n * sizeof(double));
-    rcg_tall* w = nullptr;
-    rethrow(rcg_tall_create(ctx(), defl.w.n, defl.k(), cols.data(), &w));
-    rcg_basis* b = nullptr;
-    const int st = rcg_basis_create(ctx(), device(a), w, RCG_BASIS_DEFLATION, &b);
-    rcg_tall_destroy(w);
-    rethrow(st);
-    m.emplace(k, b);
-    return b;
-}
-
-rcg_prec prec_of(const Preconditioner& m) {
-    if (dynamic_cast<const IdentityPreconditioner*>(&m)) return {RCG_PREC_IDENTITY, nullptr, nullptr};
-    if (auto* ic = dynamic_cast<const IcPreconditioner*>(&m)) return {RCG_PREC_IC, device(ic->factor()), nullptr};
-    if (dynamic_cast<const ScPreconditioner*>(&m))
-        throw std::invalid_argument(
-            "pcg_solve: ScPreconditioner's inner preconditioner is private (subspace_correction.hpp:34); "
-            "expose it to run subspace correction on the GPU");
-    throw std::invalid_argument("pcg_solve: preconditioner type has no GPU implementation");
-}
+using namespace b200::detail;
 
 // pcg.cpp:17-26
 void check_inputs(const CsrMatrix& a, const Vector& b, const Vector& x, const SolverConfig& cfg) {
@@ -168,20 +79,13 @@ void replay(SamplerState& s, const rcg_sampler* d, int offered, const std::vecto
     }
     for (int j = 0; j < m; ++j)
         if (static_cast<bool>(occ[j]) != s.occupied(j) || (occ[j] && it[j] != s.stored_iteration(j)))
-            throw std::runtime_error("pcg_solve: device sampler and host SamplerState schedules disagree");
+            throw std::runtime_error(
+                "pcg_solve: device sampler and host SamplerState schedules disagree (a method-A state made "
+                "with an iteration cap below the solve's iteration count, or a method-B state made with "
+                "another eps than the solve's)");
 }
 
 }  // namespace
-
-namespace b200 {
-void release_device_images() {
-    auto& im = images();
-    for (auto& kv : im.bases) rcg_basis_destroy(kv.second);
-    for (auto& kv : im.ics) rcg_ic_destroy(kv.second);
-    for (auto& kv : im.mats) rcg_matrix_destroy(kv.second);
-    im = Images{};
-}
-}  // namespace b200
 
 SolveReport pcg_solve(const CsrMatrix& a, const Vector& b, const Preconditioner& m, Vector& x,
                       const SolverConfig& cfg, const IterationObserver& observer) {
@@ -189,21 +93,28 @@ SolveReport pcg_solve(const CsrMatrix& a, const Vector& b, const Preconditioner&
     const b200::SamplingObserver* so = observer ? observer.target<b200::SamplingObserver>() : nullptr;
     if (observer && !so)
         throw std::invalid_argument(
-            "pcg_solve: this observer cannot run inside the device loop; use recycg::b200::"
-            "error_sampling_observer_a/_b or residual_sampling_observer_a (recycg_b200.hpp)");
-    const rcg_prec p = prec_of(m);
+            "pcg_solve: this observer cannot run inside the device loop; use error_sampling_observer / "
+            "residual_sampling_observer (sampling.hpp:67-70)");
+    const PrecRef p = prec_of(m);
+    const MatrixRef ad = device(a);
     Sampler smp;
     if (so) {
         if (so->s->stored_count() != 0)
             throw std::invalid_argument("pcg_solve: the sampler must be fresh (no stored snapshots)");
+        // the device schedule equals the host state's whenever the host's method-A cap is at
+        // least the solve's iteration count (m^l_max > cap >= T: the extra alternating-sum terms
+        // vanish) -- the driver makes it with cap = max_iter (driver.cpp:142); method B uses the
+        // solve's eps (driver.cpp:143).  replay() verifies the outcome.
         const bool meth_b = so->s->method() == SamplingMethod::B;
-        rethrow(rcg_sampler_create(ctx(), meth_b ? RCG_SAMPLER_B : RCG_SAMPLER_A, so->s->m(),
-                                   meth_b ? 1 : so->iteration_cap, meth_b ? so->eps : 0.5, a.n(), &smp.h));
+        const int cap = so->iteration_cap > 0 ? so->iteration_cap : cfg.max_iter;
+        const double eps = so->eps > 0.0 ? so->eps : cfg.eps;
+        rethrow(rcg_sampler_create(ctx(), meth_b ? RCG_SAMPLER_B : RCG_SAMPLER_A, so->s->m(), meth_b ? 1 : cap,
+                                   meth_b ? eps : 0.5, a.n(), &smp.h));
     }
     std::vector<double> hist(static_cast<std::size_t>(cfg.max_iter));
     rcg_solver_config c{cfg.eps, cfg.max_iter, 1};
     rcg_solve_report r{0, 0, 0.0, cfg.max_iter, hist.data(), nullptr, nullptr};
-    rethrow(rcg_pcg_solve(ctx(), device(a), b.data(), &p, x.data(), &c, smp.h,
+    rethrow(rcg_pcg_solve(ctx(), ad.get(), b.data(), &p.p, x.data(), &c, smp.h,
                           so && so->residual ? RCG_PAYLOAD_R : RCG_PAYLOAD_X, &r));
     SolveReport rep;
     rep.iterations = r.iterations;
@@ -219,12 +130,14 @@ SolveReport deflated_pcg_solve(const CsrMatrix& a, const Vector& b, const Precon
     check_inputs(a, b, x, cfg);
     if (!defl.empty() && defl.w.n != a.n())
         throw std::invalid_argument("deflated_pcg_solve: W row count does not match A");
-    const rcg_prec p = prec_of(m);
+    const PrecRef p = prec_of(m);
+    const MatrixRef ad = device(a);
+    const BasisRef bd = device_basis(defl.w, defl.aw, defl.waw_chol, RCG_BASIS_DEFLATION);
     std::vector<double> hist(static_cast<std::size_t>(cfg.record_history ? cfg.max_iter : 0));
     rcg_solver_config c{cfg.eps, cfg.max_iter, cfg.record_history ? 1 : 0};
     rcg_solve_report r{0, 0, 0.0, static_cast<int>(hist.size()), hist.empty() ? nullptr : hist.data(), nullptr,
                        nullptr};
-    rethrow(rcg_deflated_pcg_solve(ctx(), device(a), b.data(), &p, device(a, defl), x.data(), &c, &r));
+    rethrow(rcg_deflated_pcg_solve(ctx(), ad.get(), b.data(), &p.p, bd.get(), x.data(), &c, &r));
     SolveReport rep;
     rep.iterations = r.iterations;
     rep.converged = r.converged != 0;
@@ -242,7 +155,8 @@ CondestResult pcg_with_condest(const CsrMatrix& a, const Vector& b, const Precon
     const std::size_t n = static_cast<std::size_t>(a.n());
     if (b.size() != n || x.size() != n)
         throw std::invalid_argument("pcg_with_condest: vector size does not match matrix");
-    const rcg_prec p = prec_of(m);
+    const PrecRef p = prec_of(m);
+    const MatrixRef ad = device(a);
     std::vector<double> hist(static_cast<std::size_t>(cfg.record_history ? cfg.max_iter : 0));
     std::vector<double> ritz(static_cast<std::size_t>(m_samples > 0 ? m_samples : 1));
     rcg_solver_config c{cfg.eps, cfg.max_iter, cfg.record_history ? 1 : 0};
@@ -250,7 +164,7 @@ CondestResult pcg_with_condest(const CsrMatrix& a, const Vector& b, const Precon
                        nullptr};
     rcg_cond_estimate e{};
     e.ritz_values = ritz.data();
-    rethrow(rcg_pcg_with_condest(ctx(), device(a), b.data(), &p, x.data(), &c, m_samples, v0_seed, &r, &e));
+    rethrow(rcg_pcg_with_condest(ctx(), ad.get(), b.data(), &p.p, x.data(), &c, m_samples, v0_seed, &r, &e));
     CondestResult out;
     out.solve.iterations = r.iterations;
     out.solve.converged = r.converged != 0;

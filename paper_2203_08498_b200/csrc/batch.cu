@@ -1756,7 +1756,9 @@ static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const
         stage_out_end(ctx, X, static_cast<int64_t>(n) * nrhs, xo);
         RCG_CK(cudaStreamSynchronize(ctx->stream));
         check_sweep_watchdog(ctx);
-        for (int k = 0; k < nrhs; ++k) reps[k].wall_time = job.wall;
+        // per right-hand side: the batch's loop time shared out, so sums over solves (the
+        // sequence driver's avg_wall_time, driver.cpp:197-205) keep their per-solve meaning
+        for (int k = 0; k < nrhs; ++k) reps[k].wall_time = job.wall / nrhs;
         if (job.broken >= 0) {
             const bool dfl = defl && defl->k > 0;
             throw Error(RCG_E_BREAKDOWN, std::string(dfl ? "deflated pcg" : "pcg") + ": breakdown in right-hand side " +

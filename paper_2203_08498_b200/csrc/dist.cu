@@ -504,6 +504,7 @@ struct LoopComm : rcg_comm {
     cudaStream_t cs = nullptr;
     cudaEvent_t ev_join = nullptr;
     std::vector<cudaEvent_t> ev;
+    std::vector<cudaEvent_t> ev_read;  // receiver b finished copying out of the senders' buffers
     double** dptrs = nullptr;  // device arrays of the slabs' dsum / gbuf pointers
     double** gptrs = nullptr;
     std::vector<double*> hd, hg;
@@ -513,6 +514,7 @@ struct LoopComm : rcg_comm {
         if (dptrs) dev_free(dptrs);
         if (gptrs) dev_free(gptrs);
         for (auto e : ev) cudaEventDestroy(e);
+        for (auto e : ev_read) cudaEventDestroy(e);
         if (ev_join) cudaEventDestroy(ev_join);
         if (cs) cudaStreamDestroy(cs);
     }
@@ -557,7 +559,14 @@ struct LoopComm : rcg_comm {
                 RCG_CK(cudaMemcpyAsync(ext + d->nloc + d->recv_off[q], s[q]->sendbuf + s[q]->send_off[b],
                                        sizeof(double) * d->recv_count[q], cudaMemcpyDeviceToDevice, d->ctx->stream));
             }
+            RCG_CK(cudaEventRecord(ev_read[b], d->ctx->stream));
         }
+        // write-after-read: slab q may pack its next halo into sendbuf only after every receiver
+        // has copied this one out (back-to-back halo loops -- basis build, A Q -- have no
+        // allreduce in between to join the streams)
+        for (int q = 0; q < ns; ++q)
+            for (int b = 0; b < ns; ++b)
+                if (b != q && s[b]->recv_count[q]) RCG_CK(cudaStreamWaitEvent(s[q]->ctx->stream, ev_read[b], 0));
     }
 };
 
@@ -1310,6 +1319,8 @@ int rcg_comm_create_loopback(int nparts, rcg_comm** out) {
         RCG_CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         c->ev.resize(nparts);
         for (auto& e : c->ev) RCG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_read.resize(nparts);
+        for (auto& e : c->ev_read) RCG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->dptrs = static_cast<double**>(dev_alloc_bytes(sizeof(double*) * nparts));
         c->gptrs = static_cast<double**>(dev_alloc_bytes(sizeof(double*) * nparts));
         *out = c;

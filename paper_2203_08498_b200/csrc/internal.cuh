@@ -35,6 +35,11 @@ namespace rcg {
         (ctx)->launches++;                                                         \
     } while (0)
 
+// a C-ABI status from a nested entry point, rethrown with its message
+inline void ck(int rc) {
+    if (rc != RCG_OK) throw Error(rc, rcg_last_error());
+}
+
 // ------------------------------------------------------------------ constants
 constexpr int kStreamThreads = 256;   // streaming / reduction kernels
 constexpr int kSweepThreads = 128;    // rows per sweep tile

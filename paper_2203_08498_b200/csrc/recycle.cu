@@ -569,6 +569,79 @@ void rcg_tall_destroy(rcg_tall* t) {
     delete t;
 }
 
+// a TallDense held as separate host (or device) columns -- the reference's std::vector<Vector>
+int rcg_tall_create_cols(rcg_ctx* ctx, int32_t n, int k, const double* const* cols, rcg_tall** out) {
+    return guard([&] {
+        *out = nullptr;
+        require(n >= 0 && k >= 0, "TallDense: bad dimensions");
+        require(k == 0 || cols, "TallDense: null column array");
+        rcg_tall* t = tall_alloc(n, k);
+        try {
+            for (int j = 0; j < k && n > 0; ++j) {
+                require(cols[j] != nullptr, "TallDense: null column");
+                RCG_CK(cudaMemcpyAsync(t->d + j * t->ld, cols[j], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
+            }
+            RCG_CK(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            rcg_tall_destroy(t);
+            throw;
+        }
+        *out = t;
+    });
+}
+
+// harvest_errors (recycling.cpp:17-28) for snapshots held by the caller (a host SamplerState's
+// occupied slots, in slot order): E[:,j] = x_final - slot_j, exactly-zero columns skipped
+int rcg_harvest_columns(rcg_ctx* ctx, const double* x_final, int32_t n, int k, const double* const* slots,
+                        rcg_tall** out) {
+    return guard([&] {
+        *out = nullptr;
+        rcg_tall* t = nullptr;
+        ck(rcg_tall_create_cols(ctx, n, k, slots, &t));
+        if (k == 0 || n == 0) {
+            t->k = 0;
+            *out = t;
+            return;
+        }
+        int* dl = nullptr;
+        int* nz = nullptr;
+        try {
+            Staged xs;
+            stage_in(ctx, x_final, n, xs);
+            std::vector<int> list(k);
+            for (int j = 0; j < k; ++j) list[j] = j;
+            dl = static_cast<int*>(dev_alloc_bytes(sizeof(int) * k));
+            nz = static_cast<int*>(dev_alloc_bytes(sizeof(int) * k));
+            RCG_CK(cudaMemcpyAsync(dl, list.data(), sizeof(int) * k, cudaMemcpyHostToDevice, ctx->stream));
+            RCG_CK(cudaMemsetAsync(nz, 0, sizeof(int) * k, ctx->stream));
+            dim3 grid(stream_grid(ctx, n), std::min(k, 64));
+            k_harvest_inplace<<<grid, kStreamThreads, 0, ctx->stream>>>(xs.dev, t->d, t->ld, dl, k, n, nz);
+            RCG_LAUNCHED(ctx);
+            std::vector<int> hz(k);
+            RCG_CK(cudaMemcpyAsync(hz.data(), nz, sizeof(int) * k, cudaMemcpyDeviceToHost, ctx->stream));
+            RCG_CK(cudaStreamSynchronize(ctx->stream));
+            int kept = 0;
+            for (int j = 0; j < k; ++j) {
+                if (!hz[j]) continue;  // exactly zero column: skipped (recycling.cpp:26)
+                if (j != kept)
+                    RCG_CK(cudaMemcpyAsync(t->d + kept * t->ld, t->d + j * t->ld, sizeof(double) * n,
+                                           cudaMemcpyDeviceToDevice, ctx->stream));
+                ++kept;
+            }
+            t->k = kept;
+            RCG_CK(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            dev_free(dl);
+            dev_free(nz);
+            rcg_tall_destroy(t);
+            throw;
+        }
+        dev_free(dl);
+        dev_free(nz);
+        *out = t;
+    });
+}
+
 int rcg_tall_k(const rcg_tall* t) { return t ? t->k : 0; }
 int32_t rcg_tall_n(const rcg_tall* t) { return t ? t->n : 0; }
 
@@ -785,6 +858,96 @@ void rcg_basis_destroy(rcg_basis* b) {
 }
 
 int rcg_basis_k(const rcg_basis* b) { return b ? b->k : 0; }
+
+// a basis from the fields of an existing host DeflationOperator / ScPreconditioner (W, AW and
+// chol(W^T A W) as they are -- the operator that object applies), no recomputation
+int rcg_basis_create_from(rcg_ctx* ctx, int32_t n, int k, const double* const* w_cols, const double* const* aw_cols,
+                          const double* chol_l, int who, rcg_basis** out) {
+    return guard([&] {
+        *out = nullptr;
+        require(n >= 0 && k >= 0 && k <= 128, "SmallSym: dimension " + std::to_string(k) + " outside [0, 128]");
+        require(k == 0 || (w_cols && aw_cols && chol_l), "basis: null W / AW / Cholesky factor");
+        auto* b = new rcg_basis();
+        try {
+            b->n = n;
+            b->k = k;
+            b->ld = ld_of(n);
+            b->who = who;
+            if (k > 0) {
+                b->w = dev_alloc(b->ld * k);
+                b->aw = dev_alloc(b->ld * k);
+                for (int j = 0; j < k && n > 0; ++j) {
+                    require(w_cols[j] && aw_cols[j], "basis: null column");
+                    RCG_CK(cudaMemcpyAsync(b->w + j * b->ld, w_cols[j], sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
+                    RCG_CK(cudaMemcpyAsync(b->aw + j * b->ld, aw_cols[j], sizeof(double) * n, cudaMemcpyDefault,
+                                           ctx->stream));
+                }
+                b->h_l.assign(chol_l, chol_l + static_cast<size_t>(k) * k);
+                b->l = dev_alloc(static_cast<int64_t>(k) * k);
+                RCG_CK(cudaMemcpyAsync(b->l, b->h_l.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, ctx->stream));
+                RCG_CK(cudaStreamSynchronize(ctx->stream));
+            }
+        } catch (...) {
+            rcg_basis_destroy(b);
+            throw;
+        }
+        *out = b;
+    });
+}
+
+// the basis back on the host: AW column-major (ld n) and chol(W^T A W) row-major k x k
+int rcg_basis_export(rcg_ctx* ctx, const rcg_basis* b, double* aw_cols, double* chol_l) {
+    return guard([&] {
+        require(b != nullptr, "basis: null handle");
+        if (aw_cols && b->k > 0 && b->n > 0) {
+            RCG_CK(cudaMemcpy2DAsync(aw_cols, sizeof(double) * b->n, b->aw, sizeof(double) * b->ld, sizeof(double) * b->n,
+                                     b->k, cudaMemcpyDefault, ctx->stream));
+            RCG_CK(cudaStreamSynchronize(ctx->stream));
+        }
+        if (chol_l && b->k > 0) std::memcpy(chol_l, b->h_l.data(), sizeof(double) * b->k * b->k);
+    });
+}
+
+// Preconditioner::apply on the device: identity copies, IC(0) is ic_apply, subspace correction is
+// ScPreconditioner::apply (subspace_correction.cpp:47-57): z = inner(r), then z += W u with
+// u = chol(W^T r), columns added in order (z_i += u_j w_ij, rounded product then sum)
+int rcg_prec_apply(rcg_ctx* ctx, const rcg_prec* m, const double* r, double* z) {
+    return guard([&] {
+        require(m != nullptr, "preconditioner: null");
+        int32_t n = -1;
+        if (m->ic) n = m->ic->n;
+        if (m->sc) n = m->sc->n;
+        require(m->kind == RCG_PREC_IDENTITY || m->kind == RCG_PREC_IC || m->kind == RCG_PREC_SC,
+                "preconditioner: unknown kind");
+        require(m->kind != RCG_PREC_IC || m->ic, "preconditioner: IC without a factor");
+        require(m->kind != RCG_PREC_SC || m->sc, "preconditioner: SC without a basis");
+        require(n >= 0, "preconditioner: an identity preconditioner has no length here (z = r needs no call)");
+        Staged rs, zs;
+        stage_in(ctx, r, n, rs);
+        stage_out_begin(ctx, z, n, zs);
+        if (m->ic)
+            ic_apply_dev(ctx, m->ic, rs.dev, zs.dev);
+        else if (zs.dev != rs.dev && n > 0)
+            RCG_CK(cudaMemcpyAsync(zs.dev, rs.dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (m->kind == RCG_PREC_SC && m->sc->k > 0) {
+            const rcg_basis* b = m->sc;
+            std::vector<double> f, u(b->k);
+            tall_dot_host(ctx, b->w, b->ld, b->k, rs.dev, b->n, f);
+            chol_solve_host(b->k, b->h_l, f.data(), u.data());
+            for (double& v : u) v = -v;  // z - (-u_j) w_j == z + u_j w_j exactly
+            double* ud = dev_alloc(b->k);
+            RCG_CK(cudaMemcpyAsync(ud, u.data(), sizeof(double) * b->k, cudaMemcpyHostToDevice, ctx->stream));
+            k_apply_combination<<<stream_grid(ctx, n), kStreamThreads, 0, ctx->stream>>>(zs.dev, b->w, b->ld, b->k, ud,
+                                                                                        n, zs.dev, 0);
+            RCG_LAUNCHED(ctx);
+            RCG_CK(cudaStreamSynchronize(ctx->stream));
+            dev_free(ud);
+        }
+        stage_out_end(ctx, z, n, zs);
+        RCG_CK(cudaStreamSynchronize(ctx->stream));
+        check_sweep_watchdog(ctx);
+    });
+}
 
 static int projection(rcg_ctx* ctx, const rcg_basis* b, const double* y, double* out, int which) {
     return guard([&] {

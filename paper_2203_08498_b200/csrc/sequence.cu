@@ -58,10 +58,6 @@ __global__ void __launch_bounds__(kStreamThreads) k_true_relres(const double* __
     }
 }
 
-static void ck(int rc) {
-    if (rc != RCG_OK) throw Error(rc, rcg_last_error());
-}
-
 }  // namespace rcg
 
 using namespace rcg;

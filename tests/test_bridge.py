@@ -1,7 +1,8 @@
 """The C++ drop-in (paper_2203_08498_b200/bridge): one program written against the reference's
-public API (bridge_driver.cpp) linked against the unmodified reference library and against the
-reference library with src/pcg.cpp and src/condest.cpp replaced by recycg_b200_bridge.cpp over
-librcg_b200.
+public API only (bridge_driver.cpp) linked against the unmodified reference library and against
+the reference library with its hot-path modules (pcg, condest, ic_preconditioner, sampling,
+recycling, deflation, subspace_correction; spmv / spmv_dual / mgs_orthonormalize) replaced by the
+bridge over librcg_b200.
 
 CPU: the reference-linked program runs the sequence, and the bridge-linked one fails loudly
 without a GPU (std::runtime_error from RCG_E_CUDA -- no CPU fallback).  GPU (-m gpu): both runs
@@ -75,6 +76,18 @@ def test_bridge_matches_reference(tmp_path, grid):
             key = (sr["kind"], sr["k"])
             rel = np.linalg.norm(xg[key] - xr[key]) / np.linalg.norm(xr[key])
             assert rel <= 1e-8, (key, rel)
+    # the single calls: SpMV and the IC sweeps bitwise, projections / SC apply at rounding level
+    def op(d, name):
+        return np.fromfile(os.path.join(d, f"op_{name}.bin"))
+
+    for name in ("spmv_dual1", "spmv_dual2", "ic_apply"):
+        assert np.array_equal(op(tmp_path / "gpu", name), op(tmp_path / "ref", name)), name
+    for name in ("sc_apply", "project_pt", "project_p", "direct_component", "mgs0", "mgs1"):
+        a, b = op(tmp_path / "gpu", name), op(tmp_path / "ref", name)
+        assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b), name
+    assert gpu["mgs_k"] == ref["mgs_k"] and gpu["harvest_stored_k"] == ref["harvest_stored_k"]
+    assert gpu["errors_k"] == ref["errors_k"] and gpu["sc_chol_k"] == ref["sc_chol_k"]
+    assert np.allclose(gpu["rr_values"], ref["rr_values"], rtol=1e-8, atol=0)
     # pcg_with_condest: kappa within 1 % (north star), lambda_max from the same power iteration
     cr, cg = ref["condest"], gpu["condest"]
     assert abs(cg["kappa"] - cr["kappa"]) <= 0.01 * cr["kappa"], (cr, cg)
@@ -96,3 +109,59 @@ def test_bridge_error_contract():
     pg = subprocess.run([GPU_BIN, "--errors"], capture_output=True, text=True, timeout=120)
     assert pr.returncode == 0 and pg.returncode == 0, (pr.stderr, pg.stderr)
     assert pg.stdout.splitlines() == pr.stdout.splitlines()
+
+
+def _write_csr(path, h):
+    with open(path, "wb") as f:
+        np.array([h.n], np.int32).tofile(f)
+        np.array([h.nnz], np.int64).tofile(f)
+        h.row_start.astype(np.int32).tofile(f)
+        h.col_idx.astype(np.int32).tofile(f)
+        h.values.astype(np.float64).tofile(f)
+
+
+def run_sequence_both(tmp_path, cfg_name="c2", method="sc", n_rhs=10, samples=32, keep=16, small=False):
+    """Both builds of bridge_driver in sequence mode on a BASELINE config matrix."""
+    from oracle import inputs
+
+    cfg = (inputs.SMALL if small else inputs.CONFIGS)[cfg_name]
+    csr = tmp_path / "a.csr"
+    _write_csr(csr, inputs.generate(cfg))
+    out = {}
+    for tag, binary in (("ref", REF_BIN), ("gpu", GPU_BIN)):
+        d = tmp_path / tag
+        os.makedirs(d, exist_ok=True)
+        p = subprocess.run([binary, str(d), "--csr", str(csr), "--method", method, "--rhs", str(n_rhs), "--samples",
+                            str(samples), "--keep", str(keep)], capture_output=True, text=True, timeout=1800)
+        assert p.returncode == 0, p.stderr
+        out[tag] = _load(d)
+    return out
+
+
+def _check_sequence(out):
+    (ref, xr), (gpu, xg) = out["ref"], out["gpu"]
+    assert gpu["m_bar"] == ref["m_bar"] and gpu["m_tilde"] == ref["m_tilde"]
+    for sr, sg in zip(ref["solves"], gpu["solves"]):
+        assert sg["converged"] and abs(sg["iterations"] - sr["iterations"]) <= 2, (sr, sg)
+    if gpu["solves"][0]["iterations"] == ref["solves"][0]["iterations"]:
+        rv = np.asarray(ref["ritz"])
+        assert np.max(np.abs(np.asarray(gpu["ritz"]) - rv) / np.abs(rv)) <= 1e-6
+
+
+@pytest.mark.gpu
+@needs_bins
+@pytest.mark.parametrize("method", ["sc", "deflation"])
+def test_bridge_sequence_small(tmp_path, method):
+    """The sequence protocol through recycg:: on the scaled-down C2 (both accelerations)."""
+    _check_sequence(run_sequence_both(tmp_path, "c2", method, n_rhs=4, samples=16, keep=6, small=True))
+
+
+@pytest.mark.gpu
+@needs_bins
+def test_bridge_c2_sequence(tmp_path):
+    """The bench protocol (C2: 128^3 high-contrast FV, 10 RHS, 32 samples, SC with the 16 smallest
+    Ritz vectors) end to end through the reference's own C++ API, every hot-path call on the GPU,
+    against the reference-linked build of the same program (about 2 minutes of CPU)."""
+    out = run_sequence_both(tmp_path)
+    _check_sequence(out)
+    assert out["gpu"][0]["seconds"]["total"] < out["ref"][0]["seconds"]["total"]

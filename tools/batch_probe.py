@@ -28,7 +28,7 @@ def main():
         stats = {c % 5: ctx.kernel_stats(c) for c in (range(5) if R == 1 else range(5, 10))}
         ctx.set_profiling(False)
         its = max(r.iterations for r in reps)
-        print(json.dumps({"R": R, "iters": its, "ms_per_iter": round(reps[0].wall_time / its * 1e3, 3),
+        print(json.dumps({"R": R, "iters": its, "ms_per_iter": round(sum(r.wall_time for r in reps) / its * 1e3, 3),
                           "us": {c: round(t / max(n, 1) * 1e3, 1) for c, (t, n) in stats.items()}}), flush=True)
 
 

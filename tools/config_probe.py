@@ -84,8 +84,8 @@ def probe(ctx, name, h, batch, pk, levels_note=""):
             gbs = bytes_of(c, n, nnz, nnz_l, rt) / (us * 1e-6) / 1e9
             bt[key] = {"us": round(us, 1), "rhs_per_launch": round(rt, 2), "gbs": round(gbs, 1),
                        "frac": round(gbs / pk, 4)}
-        out["batched"] = {"R": batch, "ms_per_iter": round(reps_b[0].wall_time / its * 1e3, 4),
-                          "ms_per_rhs_iter": round(reps_b[0].wall_time / its / batch * 1e3, 4), **bt}
+        out["batched"] = {"R": batch, "ms_per_iter": round(reps_b[0].wall_time * batch / its * 1e3, 4),
+                          "ms_per_rhs_iter": round(reps_b[0].wall_time / its * 1e3, 4), **bt}
     ctx.set_profiling(False)
     del p
     return out
