@@ -95,6 +95,18 @@ def solution_stream(cfg: Config, n: int, k: int) -> np.ndarray:
     raise ValueError(cfg.rhs)
 
 
+def solution_streams(cfg: Config, n: int, count: int):
+    """x_0 .. x_{count-1} in order with O(count) draws for the drifting stream (same values as
+    solution_stream)."""
+    x = None
+    for k in range(count):
+        if cfg.rhs == "drift":
+            x = normal(cfg.rhs_seed, 0, n) if k == 0 else x + 0.1 * normal(cfg.rhs_seed, k * n, n)
+            yield x
+        else:
+            yield solution_stream(cfg, n, k)
+
+
 def multicolour(a: HostCsr):
     """(P A P^T, new_of_old, ncolors) for the multicolour variant (greedy colouring)."""
     new_of_old = np.empty(a.n, np.int32)

@@ -40,6 +40,21 @@ def prepare(ctx: api.Context, cfg: Config, host: HostCsr, validate: bool = True,
     return Prepared(ctx, cfg, host, a_orig, a, dis, ic, time.perf_counter() - t0, new_of_old)
 
 
+def rhs_all(p: Prepared) -> list:
+    """[(b_orig, b_scaled)] for every solve of the sequence (one pass over the solution stream)."""
+    from .problems import solution_streams
+
+    out = []
+    for x in solution_streams(p.cfg, p.host.n, p.cfg.n_rhs):
+        if p.new_of_old is not None:
+            xp = np.empty_like(x)
+            xp[p.new_of_old] = x
+            x = xp
+        b = p.a_orig.spmv(x)
+        out.append((b, p.dis * b))
+    return out
+
+
 def rhs(p: Prepared, k: int) -> tuple[np.ndarray, np.ndarray]:
     """(b_orig, b_scaled) of solve k (0-based): b = A x_k, scaled by D^-1/2 (scaling.cpp:8-12)."""
     x = solution_stream(p.cfg, p.host.n, k)

@@ -117,3 +117,22 @@ def spectral_fixture(n, smalls, seed, oracle_obj):
     rs = np.arange(0, n * n + 1, n, dtype=np.int32)
     ci = np.tile(np.arange(n, dtype=np.int32), n)
     return n, rs, ci, full.reshape(-1).copy(), np.array(lam), q
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    """Record the achieved difference and the bar of a parity check (gpurun_out/parity/*.jsonl;
+    the round's copy is committed as profiles/parity_r2.json), so a green test also shows how far
+    from its bar it passed."""
+    import json
+
+    d = os.path.join(ROOT, "gpurun_out", "parity")
+    os.makedirs(d, exist_ok=True)
+    path = os.path.join(d, f"parity_{os.getpid()}.jsonl")
+
+    def log(test: str, **kw):
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": test, **{k: (float(v) if isinstance(v, (np.floating, float)) else v)
+                                                 for k, v in kw.items()}}, default=str) + "\n")
+
+    return log

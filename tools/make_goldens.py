@@ -62,8 +62,13 @@ def main() -> None:
     ap.add_argument("config")
     ap.add_argument("--workers", type=int, default=os.cpu_count() or 8)
     ap.add_argument("--solves", type=int, default=None, help="only the first k solves (debug)")
+    ap.add_argument("--floor", action="store_true",
+                    help="add solve 1's rounding floor to an existing golden: the oracle's own relative "
+                         "change when every dot product is summed backwards / pairwise (DESIGN.md section 4)")
     args = ap.parse_args()
     cfg = {**CONFIGS, **VARIANTS}[args.config]
+    if args.floor:
+        return add_floor(cfg)
     o = Oracle()
     t_all = time.perf_counter()
     wall = {}
@@ -174,6 +179,59 @@ def main() -> None:
         json.dump(out, f, indent=1)
     np.savez_compressed(stem + "_x.npz", rows=idx, x=xs_sample)
     log("wrote", stem + ".json", "iterations", out["iterations"], f"total {wall['total_s']:.0f}s")
+
+
+def add_floor(cfg) -> None:
+    """Solve 1 three ways (sequential dots, reversed, pairwise; run concurrently): the spread of
+    the solution and of the iteration count is the problem's own sensitivity to reduction order,
+    the parity floor for the GPU's (parallel, fixed-order) reductions."""
+    path = os.path.join(GOLDEN, cfg.name + ".json")
+    gold = json.load(open(path))
+    o = Oracle()
+    h = inputs.generate(cfg)
+    n = h.n
+    a_orig = Matrix.of(h)
+    a, dis = o.diagonal_scale(a_orig)
+    ic = o.ic0_factorize(a)
+    x0 = next(inputs.solution_streams(cfg, n, 1))
+    b = dis * o.spmv(a_orig, x0)
+    idx = sample_rows(n)
+    res = {}
+
+    def solve(order):
+        x = np.zeros(n)
+        # the dot order is a process-wide switch: one oracle library instance per order
+        oo = Oracle() if order == 0 else _oracle_with_order(order)
+        rep = oo.pcg_solve(a, b, x, kind=1, ic=ic, eps=cfg.eps, max_iter=cfg.max_iter)
+        res[order] = (rep.iterations, x)
+        log("floor solve, dot order", order, rep.iterations, "its")
+
+    with ThreadPoolExecutor(max_workers=3) as pool:
+        list(pool.map(solve, (0, 1, 2)))
+    base_it, base_x = res[0]
+    nb = np.linalg.norm(base_x)
+    floor = max(float(np.linalg.norm(res[k][1] - base_x) / nb) for k in (1, 2))
+    gold["solve1_floor"] = {"rel_solution": floor, "iterations": [res[k][0] for k in (0, 1, 2)],
+                            "note": "oracle solve 1 with dot products summed sequentially / backwards / pairwise"}
+    assert base_it == gold["iterations"][0], (base_it, gold["iterations"][0])
+    with open(path, "w") as f:
+        json.dump(gold, f, indent=1)
+    log("floor", floor, "iterations", gold["solve1_floor"]["iterations"], "sample rows", idx.size)
+
+
+def _oracle_with_order(order):
+    """A separate copy of liboracle.so (its own global dot-order switch) summing in `order`."""
+    import shutil
+    import tempfile
+
+    from oracle import ORACLE_SO
+
+    d = tempfile.mkdtemp(prefix="orc_order")
+    p = os.path.join(d, f"liboracle_{order}.so")
+    shutil.copy(ORACLE_SO, p)
+    oo = Oracle(p)
+    oo.lib.orc_set_dot_order(order)
+    return oo
 
 
 if __name__ == "__main__":
