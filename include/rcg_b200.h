@@ -66,10 +66,9 @@ int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launc
 int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units);
 void rcg_ctx_reset_stats(rcg_ctx* ctx);
 /* IC sweep kernel selection (no effect on results: every variant is bitwise identical):
- * 0 = grid-wide sync-free sweep (k_sweep), 1 = one-cluster level-synchronous sweep
- * (icsweep_cl.cu) whenever its plan fits, 2 = default (one launch per level -- icsweep_lv.cu --
- * when the average level holds >= 600K rows, else k_sweep), 3 = the load-pipelined grid sweep
- * k_sweep_pf, 4 = one launch per level always; RCG_SWEEP_CLUSTER overrides at context creation */
+ * 0 = grid-wide sync-free sweep (k_sweep), 2 = default (one launch per level -- icsweep_lv.cu --
+ * when the average level holds >= 600K rows, else k_sweep), 4 = one launch per level always;
+ * RCG_SWEEP_CLUSTER overrides at context creation */
 int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode);
 
 /* ------------------------------------------------------------------ CSR (csr_matrix.hpp) */
@@ -92,20 +91,14 @@ int rcg_diagonal_scale(rcg_ctx* ctx, const rcg_matrix* a, rcg_matrix** scaled, d
 
 /* ------------------------------------------------------------------ IC(0) (ic_preconditioner.hpp) */
 /* ic0_factorize(a, shift, num_blocks) -- ic_preconditioner.hpp:44: zero-fill L D L^T with the
- * reference shift ladder, computed on the host (one-time setup) from host CSR arrays, then
- * uploaded with its level schedules. */
+ * reference shift ladder from CSR arrays (host or device): rcg_ic0_factorize_device over a
+ * temporary device copy of the matrix. */
 int rcg_ic0_factorize(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const int32_t* col_idx,
                       const double* values, double shift, int num_blocks, rcg_ic** out);
-/* ic0_factorize on the device: pattern work (L / U patterns, level schedules)
- * on the host from a's pattern, the numeric row merge + shift ladder by a level-ordered
- * sync-free kernel from a's device values; the factor is bitwise rcg_ic0_factorize's. */
+/* ic0_factorize on the device (ic_preconditioner.cpp:12-121): pattern work (L / U
+ * patterns, Kahn levels, level schedules) by device kernels, the numeric row merge + shift ladder
+ * by a level-ordered sync-free kernel; the factor is bitwise the reference's. */
 int rcg_ic0_factorize_device(rcg_ctx* ctx, const rcg_matrix* a, double shift, int num_blocks, rcg_ic** out);
-/* Tiled sweeps for a factor in the natural ordering of an nx x ny x nz grid (x fastest): a CTA
- * owns a tile_x x tile_y block of (x, y) columns for all z and walks them in level steps; only
- * dependencies across tiles travel through HBM.  Same operator (bitwise).  RCG_E_INVALID when
- * the factor's pattern is not a supported stencil (the level-scheduled sweeps stay in use);
- * tile_x = 0 switches back to them. */
-int rcg_ic_set_grid(rcg_ctx* ctx, rcg_ic* f, int32_t nx, int32_t ny, int32_t nz, int tile_x, int tile_y);
 /* upload an existing IcFactor (ic_preconditioner.hpp:18-37) so the operator is identical */
 int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_bounds,
                   const int32_t* l_row_start, const int32_t* l_col, const double* l_val,
@@ -286,8 +279,11 @@ typedef struct {
 } rcg_gen_params;
 int rcg_generate(const rcg_gen_params* p, int32_t* n, int64_t* nnz, int32_t** row_start,
                  int32_t** col_idx, double** values);
-/* the 7-point kinds (POISSON7, FV7_CONTRAST) assembled directly in HBM (no host arrays, no H2D):
- * bitwise the host generator's CSR */
+/* every kind assembled directly in HBM, bitwise the host generator's CSR (
+ * replaces the host assembly that feeds parse_matrix_market-style ingest, matrix_market.cpp:30-117):
+ * POISSON7 / FV7_CONTRAST with no host arrays; Q1_27PT from the host's seeded element
+ * coefficients ((N+1)^3 doubles); KNN from the host's seeded points (exact kNN search, symmetric
+ * union and weights on the device; k <= 32) */
 int rcg_matrix_generate(rcg_ctx* ctx, const rcg_gen_params* p, rcg_matrix** out);
 /* the device matrix back to host arrays (row_start n + 1, col_idx / values nnz; any null skipped) */
 int rcg_matrix_export(rcg_ctx* ctx, const rcg_matrix* a, int32_t* row_start, int32_t* col_idx, double* values);

@@ -138,7 +138,6 @@ SIGNATURES = {
     "rcg_diagonal_scale": (C.c_int, vp, vp, C.POINTER(vp), vp),
     "rcg_ic0_factorize": (C.c_int, vp, C.c_int32, vp, vp, vp, C.c_double, C.c_int, C.POINTER(vp)),
     "rcg_ic0_factorize_device": (C.c_int, vp, vp, C.c_double, C.c_int, C.POINTER(vp)),
-    "rcg_ic_set_grid": (C.c_int, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int, C.c_int),
     "rcg_ic_create": (C.c_int, vp, C.c_int32, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, C.c_double, C.POINTER(vp)),
     "rcg_ic_destroy": (None, vp),
     "rcg_ic_info": (C.c_int, vp, i64p, dp, i32p, i32p),

@@ -112,9 +112,8 @@ class Context:
         check(lib.rcg_ctx_set_profiling(self.h, 1 if on else 0))
 
     def set_sweep_kernel(self, mode: int):
-        """IC sweep kernel: 0 grid-wide sync-free, 1 one-cluster level-synchronous whenever it
-        fits, 2 default (per-level launches for wide levels, else grid), 3 load-pipelined grid
-        sweep, 4 per-level launches always.  Results are bitwise identical either way."""
+        """IC sweep kernel: 0 grid-wide sync-free, 2 default (per-level launches for wide levels,
+        else grid-wide), 4 per-level launches always.  Results are bitwise identical either way."""
         check(lib.rcg_ctx_set_sweep_kernel(self.h, int(mode)))
 
     def record(self, slot: int):
@@ -264,10 +263,6 @@ class IcFactor:
                    u_row_start=np.empty(n + 1, np.int32), u_col=np.empty(nnz, np.int32), u_val=np.empty(nnz))
         check(lib.rcg_ic_export(self.h, *[_ptr(v) for v in out.values()]))
         return out
-
-    def set_grid(self, nx: int, ny: int, nz: int, tile_x: int = 16, tile_y: int = 8) -> None:
-        """Tiled sweeps for a natural-ordered nx x ny x nz grid (rcg_ic_set_grid); tile_x = 0 off."""
-        check(lib.rcg_ic_set_grid(self.ctx.h, self.h, int(nx), int(ny), int(nz), int(tile_x), int(tile_y)))
 
     def apply(self, r, z=None):
         """ic_apply (ic_preconditioner.hpp:47)."""

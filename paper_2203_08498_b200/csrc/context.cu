@@ -373,7 +373,10 @@ int rcg_ctx_create(int device, rcg_ctx** out) {
         c->num_sms = prop.multiProcessorCount;
         if (const char* e = std::getenv("RCG_SWEEP_BPS")) c->sweep_bps = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("RCG_SWEEP_BACKOFF_NS")) c->sweep_backoff_ns = std::max(0, std::atoi(e));
-        if (const char* e = std::getenv("RCG_SWEEP_CLUSTER")) c->sweep_cluster = std::atoi(e);
+        if (const char* e = std::getenv("RCG_SWEEP_CLUSTER")) {
+            const int m = std::atoi(e);
+            if (m == 0 || m == 2 || m == 4) c->sweep_cluster = m;
+        }
         if (const char* e = std::getenv("RCG_SPMV_BPS")) c->spmv_bps = std::max(1, std::atoi(e));
         RCG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         register_ctx(c, true);
@@ -416,8 +419,6 @@ void rcg_ctx_destroy(rcg_ctx* ctx) {
 int rcg_ctx_synchronize(rcg_ctx* ctx) {
     return guard([&] {
         RCG_CK(cudaStreamSynchronize(ctx->stream));
-        static const bool prof = std::getenv("RCG_CL_PROF") != nullptr;  // dev: cluster sweep phases
-        if (prof) cluster_prof_dump("sync");
     });
 }
 
@@ -425,7 +426,8 @@ int64_t rcg_ctx_launch_count(const rcg_ctx* ctx) { return ctx ? ctx->launches : 
 
 int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode) {
     return guard([&] {
-        require(ctx != nullptr && mode >= 0 && mode <= 4, "rcg_ctx_set_sweep_kernel: mode must be 0..4");
+        require(ctx != nullptr && (mode == 0 || mode == 2 || mode == 4),
+                "rcg_ctx_set_sweep_kernel: mode must be 0 (grid-wide), 2 (by shape) or 4 (per level)");
         ctx->sweep_cluster = mode;
     });
 }
@@ -481,11 +483,6 @@ int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units) {
 
 void rcg_ctx_reset_stats(rcg_ctx* ctx) {
     try {
-        static const bool prof = std::getenv("RCG_CL_PROF") != nullptr;
-        if (prof) {
-            cudaStreamSynchronize(ctx->stream);
-            cluster_prof_dump("reset");
-        }
         resolve_timers(ctx);
     } catch (...) {
     }

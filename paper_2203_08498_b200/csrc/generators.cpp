@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "gen_math.h"
 #include "host_error.h"
 
 namespace rcg {
@@ -90,6 +91,32 @@ void fv7_inclusion_origins(int32_t N, int count, int size, uint64_t seed, std::v
     require(placed == count, "generator: could not place the inclusions disjointly");
 }
 
+// C3's element coefficients exp(sigma N(0,1)), (N+1)^3 of them, element (ex, ey, ez) at
+// ex + M (ey + M ez): one seeded mt19937_64 stream through Box-Muller (shared with gen_device.cu,
+// which assembles the 27-point rows from them in HBM)
+void q1_element_coefficients(int32_t N, double sigma, uint64_t seed, std::vector<double>& ke) {
+    const int64_t M = static_cast<int64_t>(N) + 1;
+    ke.assign(static_cast<size_t>(M * M * M), 0.0);
+    std::mt19937_64 g(seed);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t e = 0; e < M * M * M; e += 2) {
+        const double a = u01(g), b = u01(g);
+        const double r = std::sqrt(-2.0 * std::log(1.0 - a));
+        ke[e] = std::exp(sigma * r * std::cos(two_pi * b));
+        if (e + 1 < M * M * M) ke[e + 1] = std::exp(sigma * r * std::sin(two_pi * b));
+    }
+}
+
+// C5's points: 3 npts uniform [0, 1) draws, point i = (P[3i], P[3i+1], P[3i+2]); and the edge
+// count G of the bucket grid the exact kNN search uses (shared with gen_device.cu)
+void knn_points(int32_t npts, uint64_t seed, std::vector<double>& P) {
+    P.assign(3 * static_cast<size_t>(npts), 0.0);
+    std::mt19937_64 g(seed);
+    for (auto& v : P) v = u01(g);
+}
+
+int knn_grid_size(int32_t npts) { return std::max(1, static_cast<int>(std::cbrt(static_cast<double>(npts) / 2.0))); }
+
 namespace {
 
 Csr fv7_contrast(int32_t N, int count, int size, double contrast, uint64_t seed) {
@@ -156,17 +183,8 @@ Csr q1_27pt(int32_t N, double sigma, uint64_t seed) {
     const int64_t n = static_cast<int64_t>(N) * N * N;
     require(n < (1LL << 31), "generator: grid too large for int32 rows");
     const int64_t M = N + 1;  // elements per axis
-    std::vector<double> ke(M * M * M);
-    {
-        std::mt19937_64 g(seed);
-        const double two_pi = 6.283185307179586476925286766559;
-        for (int64_t e = 0; e < M * M * M; e += 2) {
-            const double a = u01(g), b = u01(g);
-            const double r = std::sqrt(-2.0 * std::log(1.0 - a));
-            ke[e] = std::exp(sigma * r * std::cos(two_pi * b));
-            if (e + 1 < M * M * M) ke[e + 1] = std::exp(sigma * r * std::sin(two_pi * b));
-        }
-    }
+    std::vector<double> ke;
+    q1_element_coefficients(N, sigma, seed, ke);
     auto E = [&](int64_t ex, int64_t ey, int64_t ez) { return ke[ex + M * (ey + M * ez)]; };
     Csr a;
     a.n = static_cast<int32_t>(n);
@@ -228,18 +246,29 @@ Csr q1_27pt(int32_t N, double sigma, uint64_t seed) {
     return a;
 }
 
+// sum of f(0..n-1): sequential within gm::kSumChunk-term chunks, then over the chunk sums
+template <class F>
+double chunked_sum(size_t n, F f) {
+    double total = 0.0;
+    for (size_t c0 = 0; c0 < n; c0 += gm::kSumChunk) {
+        double s = 0.0;
+        for (size_t t = c0; t < std::min(n, c0 + gm::kSumChunk); ++t) s += f(t);
+        total += s;
+    }
+    return total;
+}
+
 // ---- C5: symmetric kNN graph Laplacian over uniform points in the unit cube.
 // Edge (i,j) if j is among the k nearest of i or vice versa; w = exp(-d^2/h^2) with h the mean
 // distance over all directed kNN pairs; L = D - W + 1e-6 * mean(degree) I.  Rows keep generation
-// order.  Exact kNN by a uniform bucket grid and expanding shells (multi-threaded).
+// order.  Exact kNN by a uniform bucket grid and expanding shells (multi-threaded).  exp and the
+// two global means use gen_math.h (portable exp, fixed chunk order), so the device generator
+// (gen_device.cu) produces the same bits.
 Csr knn_laplacian(int32_t npts, int k, uint64_t seed) {
     require(npts > k && k >= 1, "generator: kNN needs more points than neighbours");
-    std::vector<double> P(3 * static_cast<size_t>(npts));
-    {
-        std::mt19937_64 g(seed);
-        for (auto& v : P) v = u01(g);
-    }
-    const int G = std::max(1, static_cast<int>(std::cbrt(static_cast<double>(npts) / 2.0)));
+    std::vector<double> P;
+    knn_points(npts, seed, P);
+    const int G = knn_grid_size(npts);
     const double cell = 1.0 / G;
     auto cidx = [&](double v) { return std::min(G - 1, static_cast<int>(v * G)); };
     std::vector<int32_t> cstart(static_cast<size_t>(G) * G * G + 1, 0), order(npts);
@@ -308,9 +337,8 @@ Csr knn_laplacian(int32_t npts, int k, uint64_t seed) {
             });
         for (auto& th : pool) th.join();
     }
-    double hsum = 0.0;
-    for (size_t t = 0; t < nd2.size(); ++t) hsum += std::sqrt(nd2[t]);
-    const double h = hsum / static_cast<double>(nd2.size());
+    // h = mean kNN distance, summed in gm's fixed chunk order (the device generator's order)
+    const double h = chunked_sum(nd2.size(), [&](size_t t) { return std::sqrt(nd2[t]); }) / static_cast<double>(nd2.size());
     // symmetric union: directed edges plus reversed, sorted and deduplicated per row
     std::vector<int64_t> deg(npts + 1, 0);
     for (int32_t i = 0; i < npts; ++i)
@@ -349,13 +377,11 @@ Csr knn_laplacian(int32_t npts, int k, uint64_t seed) {
         const double dx = P[3 * j] - P[3 * i], dy = P[3 * j + 1] - P[3 * i + 1], dz = P[3 * j + 2] - P[3 * i + 2];
         // symmetric in (i, j): the squared distance is formed from |differences|
         const double d2 = dx * dx + dy * dy + dz * dz;
-        return std::exp(-d2 / (h * h));
+        return gm::exp(-d2 / (h * h));
     };
     for (int32_t i = 0; i < npts; ++i)
         for (int64_t p = deg[i]; p < deg[i] + rowlen[i]; ++p) degree[i] += wt(i, adj[p]);
-    double mdeg = 0.0;
-    for (double d : degree) mdeg += d;
-    mdeg /= npts;
+    const double mdeg = chunked_sum(degree.size(), [&](size_t t) { return degree[t]; }) / npts;
     int64_t p = 0;
     for (int32_t i = 0; i < npts; ++i) {
         a.rs[i] = static_cast<int32_t>(p);

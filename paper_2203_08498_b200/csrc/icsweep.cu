@@ -165,173 +165,11 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
     }
 }
 
-// Pipelined variant (opt-in, rcg_ctx_set_sweep_kernel(ctx, 3)), written for wide levels
-// (hundreds of thousands of rows per level: C4, C5, the multicolour orderings), where each
-// warp's tile might be bound by its own chain of dependent loads (ticket -> perm / prs -> in / d
-// / entries -> parents).  Measured no faster there (C4 fwd 7.95 -> 9.56 ms, C2 multicolour
-// 66.7 -> 70.4 us, C4 multicolour 6.19 -> 5.82 ms), so it is not selected by default.  A three-stage software
-// pipeline keeps the next tiles' loads in flight while the current tile waits on its parents:
-// per iteration a warp takes the ticket of tile A, issues the perm / prs loads of tile B (ticket
-// from the previous iteration) and the in / d / entry loads of tile C (perm / prs from the
-// previous iteration), then processes the tile whose loads were issued one iteration earlier.
-// Deadlock-free like k_sweep: a warp holds at most three tiles, all above the one it processes,
-// so the smallest unfinished tile is always some warp's current tile.  Row arithmetic, publish
-// protocol and the (r, z) reduction are k_sweep's, so results are bitwise identical.
-template <bool BWD>
-__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep_pf(SweepArgs a) {
-    if (a.st->done) return;
-    const int lane = threadIdx.x & 31;
-    const int ntiles = (a.npos + kTile - 1) / kTile;
-    auto ticket = [&]() {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(&a.tickets[0], 1);
-        return __shfl_sync(0xffffffffu, t, 0);
-    };
-    // stage B: perm / prs in flight; stage C: in / d / first entry chunk in flight
-    int ta = ticket();
-    int tb = ntiles, tc = ntiles;
-    int32_t b_row = -1, b_beg = 0, b_end = 0;
-    int32_t c_row = -1, c_beg = 0, c_end = 0;
-    double c_in = 0.0, c_d = 1.0;
-    int32_t c_col[kDepChunk];
-    double c_val[kDepChunk];
-#pragma unroll
-    for (int j = 0; j < kDepChunk; ++j) {
-        c_col[j] = 0;
-        c_val[j] = 0.0;
-    }
-    while (tc < ntiles || tb < ntiles || ta < ntiles) {
-        // C' from B: the tile's inputs and first entry chunk
-        const int nc = tb;
-        int32_t n_row = -1, n_beg = 0, n_end = 0;
-        double n_in = 0.0, n_d = 1.0;
-        int32_t n_col[kDepChunk];
-        double n_val[kDepChunk];
-#pragma unroll
-        for (int j = 0; j < kDepChunk; ++j) {
-            n_col[j] = 0;
-            n_val[j] = 0.0;
-        }
-        if (nc < ntiles && b_row >= 0) {
-            n_row = b_row;
-            n_beg = b_beg;
-            n_end = b_end;
-            n_in = a.in[n_row];
-            if (BWD) n_d = __ldg(a.d + n_row);
-            const int cnt = min(kDepChunk, n_end - n_beg);
-#pragma unroll
-            for (int j = 0; j < kDepChunk; ++j)
-                if (j < cnt) {
-                    n_col[j] = __ldg(a.pcol + n_beg + j);
-                    n_val[j] = __ldg(a.pval + n_beg + j);
-                }
-        }
-        // B' from A: the tile's row map
-        const int nb = ta;
-        int32_t nb_row = -1, nb_beg = 0, nb_end = 0;
-        if (nb < ntiles) {
-            const int pos = nb * kTile + lane;
-            nb_row = pos < a.npos ? __ldg(a.perm + pos) : -1;
-            if (pos < a.npos) {
-                nb_beg = __ldg(a.prs + pos);
-                nb_end = __ldg(a.prs + pos + 1);
-            }
-        }
-        const int na = nb < ntiles ? ticket() : ntiles;
-        // process C (its loads were issued one iteration ago)
-        if (tc < ntiles) {
-            double contrib = 0.0;
-            if (c_row >= 0) {
-                double s = BWD ? __ddiv_rn(c_in, c_d) : c_in;
-                unsigned spins = 0;
-                for (int32_t e0 = c_beg;; e0 += kDepChunk) {
-                    const int cnt = min(kDepChunk, c_end - e0);
-                    const bool last = e0 + kDepChunk >= c_end;
-                    int32_t col[kDepChunk];
-                    double val[kDepChunk], dep[kDepChunk];
-#pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
-                        if (j < cnt) {
-                            col[j] = e0 == c_beg ? c_col[j] : __ldg(a.pcol + e0 + j);
-                            val[j] = e0 == c_beg ? c_val[j] : __ldg(a.pval + e0 + j);
-                        }
-#pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
-                        if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
-                    while (true) {
-                        bool missing = false;
-#pragma unroll
-                        for (int j = 0; j < kDepChunk; ++j)
-                            if (j < cnt && is_sentinel(dep[j])) missing = true;
-                        if (!missing) {
-#pragma unroll
-                            for (int j = 0; j < kDepChunk; ++j)
-                                if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
-                            if (last) st_relaxed(a.out + c_row, publishable(s));
-                            break;
-                        }
-#pragma unroll
-                        for (int j = 0; j < kDepChunk; ++j)
-                            if (j < cnt && is_sentinel(dep[j])) dep[j] = ld_relaxed(a.out + col[j]);
-                        if (++spins == (1u << 24)) {  // bounded: a schedule fault is an error, never a hang
-                            atomicExch(&a.tickets[3], 1);
-#pragma unroll
-                            for (int j = 0; j < kDepChunk; ++j)
-                                if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
-                        }
-                    }
-                    if (last) break;
-                }
-                if (BWD && a.r) contrib = __dmul_rn(a.r[c_row], s);
-            }
-            if (BWD && a.r) {
-                double tot;
-                if (tile_reduce(contrib, tc, ntiles, a, &tot) && lane == 0) {
-                    DevState* st = a.st;   // src/pcg.cpp:65-71, as k_sweep
-                    const double rho = a.add_sc ? tot + st->scal[2] : tot;
-                    st->rho = rho;
-                    if (rho <= 0.0) {
-                        st->done = kBroken;
-                        st->status = kBrkRz;
-                    }
-                    st->beta = st->iter > 1 ? rho / st->rho_prev : 0.0;
-                }
-            }
-        }
-        // advance the pipeline
-        tc = nc;
-        c_row = n_row;
-        c_beg = n_beg;
-        c_end = n_end;
-        c_in = n_in;
-        c_d = n_d;
-#pragma unroll
-        for (int j = 0; j < kDepChunk; ++j) {
-            c_col[j] = n_col[j];
-            c_val[j] = n_val[j];
-        }
-        tb = nb;
-        b_row = nb_row;
-        b_beg = nb_beg;
-        b_end = nb_end;
-        ta = na;
-    }
-    if (lane == 0) {
-        __threadfence();
-        if (atomicAdd(&a.tickets[1], 1) == static_cast<int>(gridDim.x * (blockDim.x / 32)) - 1) {
-            a.tickets[0] = 0;
-            a.tickets[1] = 0;
-        }
-    }
-}
-
 void sweep_prepare_kernels() {
     static bool done = false;
     if (done) return;
     set_carveout(reinterpret_cast<const void*>(k_sweep<false>));
     set_carveout(reinterpret_cast<const void*>(k_sweep<true>));
-    set_carveout(reinterpret_cast<const void*>(k_sweep_pf<false>));
-    set_carveout(reinterpret_cast<const void*>(k_sweep_pf<true>));
     done = true;
 }
 
@@ -367,38 +205,18 @@ int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos) {
     return backward && entries_per_row > kDepChunk ? 1 : 2;
 }
 
-// The pipelined sweep (k_sweep_pf) only on request (ctx->sweep_cluster == 3): measured no faster
-// than k_sweep on the wide-level shapes it was written for.
-static bool sweep_pipelined(const rcg_ctx* ctx, const rcg_ic* f, bool backward, int64_t npos) {
-    (void)f, (void)backward, (void)npos;
-    return ctx->sweep_cluster == 3;
-}
-
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
-    if (grid_sweep_available(f)) {  // tiled sweep on a natural-ordered grid (icgrid.cu)
-        launch_grid_sweep(ctx, f, backward, a);
-        return;
-    }
-    if (launch_level_sweep(ctx, f, backward, a)) return;    // wide levels: one launch per level (icsweep_lv.cu)
-    if (launch_cluster_sweep(ctx, f, backward, a)) return;  // opt-in: one cluster (icsweep_cl.cu)
+    if (launch_level_sweep(ctx, f, backward, a)) return;  // wide levels: one launch per level (icsweep_lv.cu)
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
-    const bool pf = sweep_pipelined(ctx, f, backward, a.npos);
-    int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
-    if (pf) bps = std::min(bps, 4);   // k_sweep_pf: 128 registers, 4 resident CTAs per SM
+    const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
     a.backoff_ns = ctx->sweep_backoff_ns;
     KTimer t(ctx, backward ? 2 : 1);
-    if (pf) {
-        if (backward)
-            k_sweep_pf<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
-        else
-            k_sweep_pf<false><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
-    } else if (backward) {
+    if (backward)
         k_sweep<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
-    } else {
+    else
         k_sweep<false><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
-    }
     RCG_LAUNCHED(ctx);
 }
 
@@ -525,119 +343,27 @@ static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
     RCG_CK(cudaStreamSynchronize(ctx->stream));
 }
 
-// ------------------------------------------------------------------ host IC(0) (setup only)
-// Restates src/ic_preconditioner.cpp:12-121: zero-fill L D L^T of A + shift diag(A), sorted
-// row merge for the shared pattern, block-Jacobi drop of columns before the block start, shift
-// ladder 0 -> 0.01 -> x2 (20 retries), then the row-wise transpose for the backward sweep.
-// It runs once per matrix on the host; the per-iteration operator is the device sweep above.
-static bool factor_attempt(int32_t n, const int32_t* rs, const int32_t* ci, const double* va, double shift,
-                           rcg_ic* f) {
-    f->h_lrs.assign(static_cast<size_t>(n) + 1, 0);
-    f->h_lcol.clear();
-    f->h_lval.clear();
-    f->h_d.assign(n, 0.0);
-    f->shift = shift;
-    std::vector<int32_t>& lc = f->h_lcol;
-    std::vector<double>& lv = f->h_lval;
-    std::vector<double>& d = f->h_d;
-    size_t blk = 0;
-    for (int32_t i = 0; i < n; ++i) {
-        while (i >= f->h_bounds[blk + 1]) ++blk;
-        const int32_t lo = f->h_bounds[blk];
-        const int32_t first = static_cast<int32_t>(lc.size());
-        f->h_lrs[i] = first;
-        double diag = 0.0;
-        for (int32_t k = rs[i]; k < rs[i + 1]; ++k) {
-            const int32_t j = ci[k];
-            if (j >= i) {
-                if (j == i) diag = va[k];
-                break;
-            }
-            if (j < lo) continue;
-            double acc = va[k];
-            int32_t pa = first, pb = f->h_lrs[j];
-            const int32_t ea = static_cast<int32_t>(lc.size()), eb = f->h_lrs[j + 1];
-            while (pa < ea && pb < eb) {
-                if (lc[pa] == lc[pb]) {
-                    acc -= lv[pa] * d[lc[pa]] * lv[pb];
-                    ++pa;
-                    ++pb;
-                } else if (lc[pa] < lc[pb]) {
-                    ++pa;
-                } else {
-                    ++pb;
-                }
-            }
-            lc.push_back(j);
-            lv.push_back(acc / d[j]);
-        }
-        double piv = diag * (1.0 + shift);
-        for (size_t p = first; p < lc.size(); ++p) piv -= lv[p] * lv[p] * d[lc[p]];
-        if (piv <= 0.0) return false;
-        d[i] = piv;
-        f->h_lrs[i + 1] = static_cast<int32_t>(lc.size());
-    }
-    return true;
-}
-
-static void transpose_factor(rcg_ic* f) {
-    const int32_t n = f->n;
-    f->h_urs.assign(static_cast<size_t>(n) + 1, 0);
-    f->h_ucol.assign(f->h_lcol.size(), 0);
-    f->h_uval.assign(f->h_lval.size(), 0.0);
-    for (int32_t c : f->h_lcol) f->h_urs[c + 1]++;
-    std::partial_sum(f->h_urs.begin(), f->h_urs.end(), f->h_urs.begin());
-    std::vector<int32_t> fillpos(f->h_urs.begin(), f->h_urs.end() - 1);
-    for (int32_t i = 0; i < n; ++i)
-        for (int32_t k = f->h_lrs[i]; k < f->h_lrs[i + 1]; ++k) {
-            const int32_t dst = fillpos[f->h_lcol[k]]++;
-            f->h_ucol[dst] = i;
-            f->h_uval[dst] = f->h_lval[k];
-        }
-}
-
 }  // namespace rcg
 
 using namespace rcg;
 
 extern "C" {
 
+// ic0_factorize from host CSR arrays: the device factorisation (icfactor.cu) over a temporary
+// device copy of the matrix -- the same factor bit for bit (tests/test_gpu_icfactor.py)
 int rcg_ic0_factorize(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const int32_t* col_idx,
                       const double* values, double shift, int num_blocks, rcg_ic** out) {
     return guard([&] {
+        require(ctx && out, "rcg_ic0_factorize: null argument");
         *out = nullptr;
         if (num_blocks < 1 || num_blocks > std::max<int32_t>(n, 1))
             throw Error(RCG_E_INVALID, "ic0_factorize: num_blocks must be in [1, n]");
         if (shift < 0.0) throw Error(RCG_E_INVALID, "ic0_factorize: shift must be >= 0");
-        require(!is_device_ptr(row_start), "rcg_ic0_factorize: CSR arrays must be host memory");
-        auto* f = new rcg_ic();
-        try {
-            f->n = n;
-            f->h_bounds.resize(static_cast<size_t>(num_blocks) + 1);
-            for (int b = 0; b <= num_blocks; ++b)
-                f->h_bounds[b] = static_cast<int32_t>((static_cast<int64_t>(b) * n) / num_blocks);
-            double s = shift;
-            bool ok = false;
-            const int retries = 20;
-            for (int attempt = 0; attempt <= retries && !ok; ++attempt) {
-                ok = factor_attempt(n, row_start, col_idx, values, s, f);
-                if (!ok) s = (s == 0.0) ? 0.01 : 2.0 * s;
-            }
-            if (!ok) {
-                char buf[160];
-                std::snprintf(buf, sizeof buf,
-                              "IC breakdown: no positive-pivot factorization after %d shift retries (last shift %f)",
-                              retries, s);
-                throw Error(RCG_E_BREAKDOWN, buf);
-            }
-            f->nnz_l = static_cast<int64_t>(f->h_lval.size());
-            transpose_factor(f);
-            finish_ic(ctx, f);
-        } catch (...) {
-            rcg_ic_destroy(f);
-            throw;
-        }
-        *out = f;
+        rcg_matrix* a = nullptr;
+        ck(rcg_matrix_create(ctx, n, row_start, col_idx, values, 0, &a));
+        const int rc = rcg_ic0_factorize_device(ctx, a, shift, num_blocks, out);
+        rcg_matrix_destroy(a);
+        ck(rc);
     });
 }
 
@@ -682,10 +408,8 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
-    free_cluster_plans(f);
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
-                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->grid.tile_xy,
-                    (void*)f->grid.coef[0], (void*)f->grid.coef[1], (void*)f->grid.mask[0], (void*)f->grid.mask[1]})
+                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d})
         dev_free(p);
     delete f;
 }

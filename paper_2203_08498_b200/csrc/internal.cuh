@@ -116,7 +116,6 @@ struct Workspace {
 };
 
 struct BatchWs;  // batch.cu
-struct ClusterPlan;  // icsweep_cl.cu
 
 }  // namespace rcg
 
@@ -146,7 +145,7 @@ struct rcg_ctx {
     cudaEvent_t user_ev[16] = {};
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
-    int sweep_cluster = 2;      // IC sweep kernel: 0 grid, 1 cluster when it fits, 2 by shape
+    int sweep_cluster = 2;      // IC sweep kernel: 0 grid-wide sync-free, 2 by shape, 4 one launch per level
     int spmv_bps = 2;           // SpMV CTAs per SM (RCG_SPMV_BPS): leaves room for concurrent solves
     rcg::BatchWs* bws = nullptr;   // multi-RHS workspaces (batch.cu): a compacted phase
     rcg::BatchWs* bws2 = nullptr;  // reads one and writes the other
@@ -159,19 +158,6 @@ struct rcg_matrix {
     int32_t* ci = nullptr;
     double* va = nullptr;
     int cap = 256;  // pipelined SpMV stage capacity (entries)
-};
-
-// tiled sweeps on a natural-ordered 3D grid (icgrid.cu)
-struct GridSched {
-    bool on = false;
-    int32_t nx = 0, ny = 0, nz = 0;
-    int tx = 0, ty = 0, wx = 1, wy = 1, wz = 1;
-    int ntiles = 0, max_ctas = 0;
-    int nslots[2] = {0, 0};                       // [0] forward (L), [1] backward (U)
-    int8_t sdx[2][16] = {}, sdy[2][16] = {}, sdz[2][16] = {};
-    double* coef[2] = {nullptr, nullptr};         // slot-major stencil coefficients
-    uint32_t* mask[2] = {nullptr, nullptr};       // per row: slots present
-    int32_t* tile_xy = nullptr;                   // ticket -> X | Y << 16
 };
 
 struct rcg_ic {
@@ -190,11 +176,8 @@ struct rcg_ic {
     int32_t *b_perm = nullptr, *b_prs = nullptr, *b_col = nullptr;
     double* b_val = nullptr;
     double* d = nullptr;
-    GridSched grid;
-    // level starts of the padded schedules ([0] forward, [1] backward; nlev + 1 entries) and the
-    // lazily built cluster-sweep plans (icsweep_cl.cu)
+    // level starts of the padded schedules ([0] forward, [1] backward; nlev + 1 entries)
     std::vector<int32_t> h_lptr[2];
-    mutable rcg::ClusterPlan* cl[2] = {nullptr, nullptr};
 };
 
 struct rcg_tall {

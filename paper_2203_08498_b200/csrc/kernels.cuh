@@ -40,8 +40,6 @@ struct SweepArgs {
 int spmv_grid(const rcg_ctx* ctx, int32_t n);
 int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos);
 void ensure_host_image(const rcg_ic* f);  // icfactor.cu
-bool grid_sweep_available(const rcg_ic* f);  // icgrid.cu
-void launch_grid_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a);
 
 #ifdef __CUDACC__
 // The error sampler's schedule after iteration i (sampling.cpp:7-78): method A -- every h-th
@@ -108,15 +106,12 @@ int tile_capacity(int32_t n, const int32_t* rs);
 void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const double* x, double* r);
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
 bool launch_level_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);   // icsweep_lv.cu
-bool launch_cluster_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);  // icsweep_cl.cu
-void free_cluster_plans(rcg_ic* f);
 // memory-lean recycling step (recycle.cu): errors, MGS and the streamed Rayleigh-Ritz Gram in the
 // sampler's slots; W is a new n x m~ block
 void lean_build_aux(rcg_ctx* ctx, const rcg_matrix* a, const double* x_dev, rcg_sampler* s, double theta,
                     int keep_count, int* m_bar, std::vector<double>& vals, double* theta_used, rcg_tall** w_out);
 // rcg_basis_create, optionally adopting w's column block (recycle.cu)
 void basis_build(rcg_ctx* ctx, const rcg_matrix* a, rcg_tall* w, int who, bool adopt, rcg_basis** out);
-void cluster_prof_dump(const char* tag);  // dev: RCG_CL_PROF
 SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward);
 void check_sweep_watchdog(rcg_ctx* ctx);
 int64_t sweep_tiles(const rcg_ic* f);

@@ -56,8 +56,9 @@ def generate(cfg: Config) -> HostCsr:
 
 
 def generate_device(ctx, cfg: Config):
-    """The 7-point configs (C1, C2, C4) assembled directly in HBM (rcg_matrix_generate): an
-    api.CsrMatrix bitwise equal to generate(cfg), without host arrays or an H2D copy."""
+    """Any config assembled directly in HBM (rcg_matrix_generate): an api.CsrMatrix bitwise equal
+    to generate(cfg), without host CSR arrays or their H2D copy (C3 uploads its element
+    coefficients, C5 its points)."""
     from . import api
 
     p = L.GenParams(cfg.kind, cfg.grid, cfg.inclusions, cfg.inclusion_size, cfg.contrast, cfg.sigma, cfg.knn_k,

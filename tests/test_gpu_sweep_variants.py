@@ -1,7 +1,5 @@
-"""The IC sweep variants -- grid-wide sync-free (k_sweep), load-pipelined (k_sweep_pf), one
-launch per level (csrc/icsweep_lv.cu) and the one-cluster level-synchronous sweep
-(csrc/icsweep_cl.cu) -- against each other and the
-oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
+"""The IC sweep variants -- grid-wide sync-free (k_sweep) and one launch per level
+(csrc/icsweep_lv.cu) -- against each other and the oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
 identical whichever kernel runs (the kernel choice never changes an iterate), and all equal the
 reference ic_apply (src/ic_preconditioner.cpp:123-144)."""
 import numpy as np
@@ -11,8 +9,8 @@ from oracle import Matrix
 
 pytestmark = pytest.mark.gpu
 
-GRID, CLUSTER, AUTO, PIPELINED, LEVEL = 0, 1, 2, 3, 4
-MODES = (GRID, CLUSTER, PIPELINED, LEVEL)
+GRID, AUTO, LEVEL = 0, 2, 4
+MODES = (GRID, AUTO, LEVEL)
 
 
 @pytest.fixture
@@ -57,7 +55,7 @@ def _edge(problems, name):
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "lap1d", "one", "diag", "arrow"])
-def test_cluster_sweep_bitwise(modes, oracle, problems, name):
+def test_sweep_variants_bitwise(modes, oracle, problems, name):
     from paper_2203_08498_b200 import api
 
     ctx = modes
@@ -88,7 +86,7 @@ def test_cluster_sweep_bitwise(modes, oracle, problems, name):
 
 
 @pytest.mark.parametrize("method", ["ic", "sc"])
-def test_cluster_sweep_solves_bitwise(modes, problems, method):
+def test_sweep_variant_solves_bitwise(modes, problems, method):
     """IC-PCG (rho from the backward sweep's fused reduction) and SC-PCG on C1: identical
     iterates, histories and solutions under both kernels."""
     from paper_2203_08498_b200 import api, sequence
@@ -119,7 +117,7 @@ def test_cluster_sweep_solves_bitwise(modes, problems, method):
         assert np.array_equal(res[GRID][2], res[mode][2])
 
 
-def test_cluster_sweep_c2_full(modes, problems):
+def test_sweep_variants_c2_full(modes, problems):
     """The bench matrix (C2, 382 levels): sweep output bitwise across kernels and an ICCG
     window with identical histories."""
     from paper_2203_08498_b200 import api, sequence
@@ -154,13 +152,13 @@ def test_wide_level_sweeps_multicolour_c2(modes, problems):
     r = problems.uniform_pm1(9, 0, m.n)
     b = sequence.rhs(p, 0)[1]
     outs = {}
-    for mode in (GRID, PIPELINED, LEVEL, AUTO):
+    for mode in (GRID, LEVEL, AUTO):
         ctx.set_sweep_kernel(mode)
         z = p.ic.apply(r)
         x = np.zeros(m.n)
         rep = api.pcg_solve(ctx, p.a, b, api.Ic(p.ic), x, cfg.eps, 30)
         outs[mode] = (z, np.array(rep.history), x)
-    for mode in (PIPELINED, LEVEL, AUTO):
+    for mode in (LEVEL, AUTO):
         for k in range(3):
             assert np.array_equal(outs[GRID][k], outs[mode][k]), mode
 

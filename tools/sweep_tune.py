@@ -27,10 +27,6 @@ def main():
     a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values, validate=False)
     sa, dis = api.diagonal_scale(ctx, a)
     f = api.IcFactor.factorize_device(ctx, sa)
-    tile = os.environ.get("RCG_GRID_TILE")  # e.g. 16x8: tiled sweeps on the natural 3D grid
-    if tile and cfg.kind != 3:
-        tx, ty = (int(v) for v in tile.split("x"))
-        f.set_grid(cfg.grid, cfg.grid, cfg.grid, tx, ty)
     r = torch.from_numpy(problems.uniform_pm1(1, 0, h.n)).cuda()
     z = torch.empty_like(r)
     for _ in range(3):
