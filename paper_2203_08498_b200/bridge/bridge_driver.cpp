@@ -171,8 +171,27 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 
 // run_sequence (driver.cpp:108-222) through the public API: the C2 bench protocol when FILE is
 // the C2 matrix (10 RHS, 32 samples, SC with the 16 smallest Ritz vectors)
+// W (k columns of n doubles) to / from a file: the shared-input protocol runs the accelerated
+// solves of both builds on the same basis
+void write_w(const std::string& path, const TallDense& w) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write " + path);
+    for (const Vector& c : w.cols) std::fwrite(c.data(), sizeof(double), c.size(), f);
+    std::fclose(f);
+}
+
+TallDense read_w(const std::string& path, index_t n) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open " + path);
+    TallDense w(n);
+    Vector c(static_cast<std::size_t>(n));
+    while (std::fread(c.data(), sizeof(double), c.size(), f) == c.size()) w.cols.push_back(c);
+    std::fclose(f);
+    return w;
+}
+
 int sequence_mode(const std::string& out, const std::string& csr, const std::string& method, int n_rhs, int m,
-                  int keep) {
+                  int keep, const std::string& w_in) {
     using clock = std::chrono::steady_clock;
     const auto t_all = clock::now();
     const CsrMatrix a0 = read_csr(csr);
@@ -194,6 +213,8 @@ int sequence_mode(const std::string& out, const std::string& csr, const std::str
     const AuxBasis aux = build_aux_matrix(a, harvest_errors(x, s), std::numeric_limits<double>::infinity());
     TallDense w(a.n());
     for (int j = 0; j < std::min<int>(keep, aux.w.k()); ++j) w.cols.push_back(aux.w.cols[static_cast<std::size_t>(j)]);
+    write_w(out + "/w.bin", w);
+    if (!w_in.empty()) w = read_w(w_in, a.n());  // shared-input protocol: the other build's basis
     std::unique_ptr<ScPreconditioner> sc;
     DeflationOperator defl;
     if (method == "sc")
@@ -229,13 +250,13 @@ int main(int argc, char** argv) {
     if (argc >= 2 && std::string(argv[1]) == "--errors") return error_cases();
     if (argc < 2) {
         std::fprintf(stderr, "usage: %s OUT_DIR [grid] | OUT_DIR --csr FILE --method sc|deflation --rhs K "
-                             "--samples M --keep KEEP\n", argv[0]);
+                             "--samples M --keep KEEP [--w W.bin]\n", argv[0]);
         return 2;
     }
     const std::string out = argv[1];
     try {
         if (argc > 2 && std::string(argv[2]) == "--csr") {
-            std::string csr, method = "sc";
+            std::string csr, method = "sc", w_in;
             int n_rhs = 10, m = 32, keep = 16;
             for (int i = 2; i + 1 < argc; i += 2) {
                 const std::string k = argv[i], v = argv[i + 1];
@@ -244,8 +265,9 @@ int main(int argc, char** argv) {
                 else if (k == "--rhs") n_rhs = std::atoi(v.c_str());
                 else if (k == "--samples") m = std::atoi(v.c_str());
                 else if (k == "--keep") keep = std::atoi(v.c_str());
+                else if (k == "--w") w_in = v;
             }
-            return sequence_mode(out, csr, method, n_rhs, m, keep);
+            return sequence_mode(out, csr, method, n_rhs, m, keep, w_in);
         }
         const int grid = argc > 2 ? std::atoi(argv[2]) : 32;
         const int m = 16, cap = 5000, n_rhs = 4;

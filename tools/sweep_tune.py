@@ -20,14 +20,15 @@ def main():
     mc = name.endswith("mc")
     name = name[:-2] if mc else name
     cfg = problems.CONFIGS.get(name) or problems.SMALL[name.replace("s_", "")]
-    h = problems.generate(cfg)
-    if mc:  # multicolour variant: sweeps have ncolors levels
-        h = problems.multicolour(h)[0]
     ctx = api.Context(0)
-    a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values, validate=False)
+    if mc:  # multicolour variant: sweeps have ncolors levels
+        h = problems.multicolour(problems.generate(cfg))[0]
+        a = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, h.values, validate=False)
+    else:
+        a = problems.generate_device(ctx, cfg)
     sa, dis = api.diagonal_scale(ctx, a)
     f = api.IcFactor.factorize_device(ctx, sa)
-    r = torch.from_numpy(problems.uniform_pm1(1, 0, h.n)).cuda()
+    r = torch.from_numpy(problems.uniform_pm1(1, 0, sa.n)).cuda()
     z = torch.empty_like(r)
     for _ in range(3):
         f.apply(r, z)
@@ -43,7 +44,7 @@ def main():
     for _ in range(reps):
         sa.spmv(r, z)
     sp = ctx.kernel_stats(0)
-    print(json.dumps({"config": cfg.name, "n": h.n, "fwd_levels": f.fwd_levels, "bwd_levels": f.bwd_levels,
+    print(json.dumps({"config": cfg.name, "n": sa.n, "pencil": f.pencil, "mode": os.environ.get("RCG_SWEEP_CLUSTER", "2"), "fwd_levels": f.fwd_levels, "bwd_levels": f.bwd_levels,
                       "bps": os.environ.get("RCG_SWEEP_BPS", "4"),
                       "backoff": os.environ.get("RCG_SWEEP_BACKOFF_NS", "32"),
                       "fwd_us": round(fw[0] / fw[1] * 1e3, 1), "bwd_us": round(bw[0] / bw[1] * 1e3, 1),
