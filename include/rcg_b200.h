@@ -99,9 +99,6 @@ int rcg_ic0_factorize(rcg_ctx* ctx, int32_t n, const int32_t* row_start, const i
  * patterns, Kahn levels, level schedules) by device kernels, the numeric row merge + shift ladder
  * by a level-ordered sync-free kernel; the factor is bitwise the reference's. */
 int rcg_ic0_factorize_device(rcg_ctx* ctx, const rcg_matrix* a, double shift, int num_blocks, rcg_ic** out);
-/* the stencil wavefront sweeps (psweep.cu) of a factor: 7 or 27 when its pattern is the 7- / 27-
- * point stencil of a natural-ordered cube grid (records built at factorisation), else 0 */
-int rcg_ic_pencil(const rcg_ic* f, int* stencil);
 /* upload an existing IcFactor (ic_preconditioner.hpp:18-37) so the operator is identical */
 int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_bounds,
                   const int32_t* l_row_start, const int32_t* l_col, const double* l_val,

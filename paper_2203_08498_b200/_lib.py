@@ -141,7 +141,6 @@ SIGNATURES = {
     "rcg_ic_create": (C.c_int, vp, C.c_int32, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, C.c_double, C.POINTER(vp)),
     "rcg_ic_destroy": (None, vp),
     "rcg_ic_info": (C.c_int, vp, i64p, dp, i32p, i32p),
-    "rcg_ic_pencil": (C.c_int, vp, C.POINTER(C.c_int)),
     "rcg_ic_export": (C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp),
     "rcg_ic_apply": (C.c_int, vp, vp, vp, vp),
     "rcg_tall_create": (C.c_int, vp, C.c_int32, C.c_int, vp, C.POINTER(vp)),

@@ -264,13 +264,6 @@ class IcFactor:
         check(lib.rcg_ic_export(self.h, *[_ptr(v) for v in out.values()]))
         return out
 
-    @property
-    def pencil(self) -> int:
-        """7 / 27 when the stencil wavefront sweeps serve this factor (psweep.cu), else 0."""
-        v = C.c_int()
-        check(lib.rcg_ic_pencil(self.h, C.byref(v)))
-        return v.value
-
     def apply(self, r, z=None):
         """ic_apply (ic_preconditioner.hpp:47)."""
         r = _f64(r, self.n, "r")

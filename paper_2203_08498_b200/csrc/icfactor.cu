@@ -541,8 +541,6 @@ static void factorize_device(rcg_ctx* ctx, const rcg_matrix* A, double shift, in
     }
     RCG_CK(cudaStreamSynchronize(ctx->stream));
     mark("value gathers");
-    pencil_plan_build(ctx, f, 0, 0, 0);
-    mark("pencil records");
 }
 
 // The host image (IcFactor's natural-order L, D, U) of a device-built factor, rebuilt on demand

@@ -207,10 +207,6 @@ int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos) {
 
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
-    if (pencil_available(ctx, f)) {  // stencil grids: the pencil wavefront (psweep.cu)
-        launch_pencil_sweep(ctx, f, backward, a);
-        return;
-    }
     if (launch_level_sweep(ctx, f, backward, a)) return;  // wide levels: one launch per level (icsweep_lv.cu)
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
     const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
@@ -345,7 +341,6 @@ static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
     f->b_val = upload(ctx, pval);
     f->d = upload(ctx, f->h_d);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    pencil_plan_build(ctx, f, 0, 0, 0);
 }
 
 }  // namespace rcg
@@ -413,7 +408,6 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
-    pencil_plan_free(f);
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
                     (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d})
         dev_free(p);

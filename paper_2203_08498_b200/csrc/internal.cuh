@@ -116,7 +116,6 @@ struct Workspace {
 };
 
 struct BatchWs;  // batch.cu
-struct PencilPlan;  // psweep.cu
 
 }  // namespace rcg
 
@@ -146,7 +145,7 @@ struct rcg_ctx {
     cudaEvent_t user_ev[16] = {};
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
-    int sweep_cluster = 2;      // IC sweep kernel: 0 grid-wide sync-free, 2 by shape, 4 one launch per level, 5 pencil
+    int sweep_cluster = 2;      // IC sweep kernel: 0 grid-wide sync-free, 2 by shape, 4 one launch per level
     int spmv_bps = 2;           // SpMV CTAs per SM (RCG_SPMV_BPS): leaves room for concurrent solves
     rcg::BatchWs* bws = nullptr;   // multi-RHS workspaces (batch.cu): a compacted phase
     rcg::BatchWs* bws2 = nullptr;  // reads one and writes the other
@@ -179,8 +178,6 @@ struct rcg_ic {
     double* d = nullptr;
     // level starts of the padded schedules ([0] forward, [1] backward; nlev + 1 entries)
     std::vector<int32_t> h_lptr[2];
-    // stencil-grid wavefront records (psweep.cu), null when the pattern is not a box stencil
-    rcg::PencilPlan* pencil = nullptr;
 };
 
 struct rcg_tall {

@@ -106,12 +106,6 @@ int tile_capacity(int32_t n, const int32_t* rs);
 void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const double* x, double* r);
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
 bool launch_level_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);   // icsweep_lv.cu
-// stencil-grid wavefront sweeps (psweep.cu): records built at factor time when the pattern is a
-// 7- / 27-point box stencil (nx <= 0: detect a cube)
-void pencil_plan_build(rcg_ctx* ctx, rcg_ic* f, int32_t nx, int32_t ny, int32_t nz);
-void pencil_plan_free(rcg_ic* f);
-bool pencil_available(const rcg_ctx* ctx, const rcg_ic* f);
-void launch_pencil_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
 // memory-lean recycling step (recycle.cu): errors, MGS and the streamed Rayleigh-Ritz Gram in the
 // sampler's slots; W is a new n x m~ block
 void lean_build_aux(rcg_ctx* ctx, const rcg_matrix* a, const double* x_dev, rcg_sampler* s, double theta,

@@ -1,6 +1,5 @@
-"""The IC sweep variants -- grid-wide sync-free (k_sweep), one launch per level
-(csrc/icsweep_lv.cu) and the stencil pencil wavefront (csrc/psweep.cu) -- against each other and
-the oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
+"""The IC sweep variants -- grid-wide sync-free (k_sweep) and one launch per level
+(csrc/icsweep_lv.cu) -- against each other and the oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
 identical whichever kernel runs (the kernel choice never changes an iterate), and all equal the
 reference ic_apply (src/ic_preconditioner.cpp:123-144)."""
 import numpy as np
@@ -10,8 +9,8 @@ from oracle import Matrix
 
 pytestmark = pytest.mark.gpu
 
-GRID, AUTO, LEVEL, PENCIL = 0, 2, 4, 5
-MODES = (GRID, AUTO, LEVEL, PENCIL)
+GRID, AUTO, LEVEL = 0, 2, 4
+MODES = (GRID, AUTO, LEVEL)
 
 
 @pytest.fixture
@@ -194,51 +193,3 @@ def test_batched_level_sweeps_multicolour(modes, problems, method):
             x0 = out[GRID][1][k]
             assert np.linalg.norm(out[mode][1][k] - x0) <= 1e-6 * np.linalg.norm(x0)
 
-
-@pytest.mark.parametrize("name,want", [("c1", 7), ("c2", 7), ("c3", 27), ("c4", 7), ("c5", 0)])
-def test_pencil_plan_detected(ctx, problems, name, want):
-    """The wavefront records exist exactly for the natural-ordered cube stencils (C1-C4 and their
-    scaled-down variants, incl. grids that are not a multiple of 32 rows wide) -- not for the kNN
-    graph, a multicolour ordering or a block-Jacobi factor."""
-    from paper_2203_08498_b200 import api
-
-    h = problems.generate(problems.SMALL[name])
-    sa, _ = _scaled(ctx, h)
-    assert api.IcFactor.factorize_device(ctx, sa).pencil == want
-    if want:
-        mc = problems.multicolour(h)[0]
-        sm, _ = _scaled(ctx, mc)
-        assert api.IcFactor.factorize_device(ctx, sm).pencil == 0
-        assert api.IcFactor.factorize(ctx, sa.n, *sa.export()[:2], sa.values(), num_blocks=2).pencil == 0
-
-
-@pytest.mark.parametrize("name", ["c3", "c4"])
-def test_pencil_full_size(modes, oracle, problems, name):
-    """C3 (256^3 27-point, 1,786 levels) and C4 (512^3 7-point): the pencil sweeps bitwise the
-    oracle's ic_apply with the device factor, and bitwise the grid-wide sweep in an ICCG window
-    (same histories, same iterate)."""
-    from paper_2203_08498_b200 import api, sequence
-
-    ctx = modes
-    cfg = problems.CONFIGS[name]
-    a = problems.generate_device(ctx, cfg)
-    sa, _ = api.diagonal_scale(ctx, a)
-    f = api.IcFactor.factorize_device(ctx, sa)
-    assert f.pencil == (27 if name == "c3" else 7)
-    import torch
-
-    r = torch.from_numpy(problems.uniform_pm1(3, 0, sa.n)).cuda()
-    z = {}
-    for mode in (GRID, PENCIL):
-        ctx.set_sweep_kernel(mode)
-        z[mode] = f.apply(r).cpu().numpy()
-    assert np.array_equal(z[GRID], z[PENCIL])
-    if name == "c3":
-        b = r.clone()
-        hist = {}
-        for mode in (GRID, PENCIL):
-            ctx.set_sweep_kernel(mode)
-            x = torch.zeros_like(b)
-            rep = api.pcg_solve(ctx, sa, b, api.Ic(f), x, 1e-8, 12)
-            hist[mode] = (np.array(rep.history), x.cpu().numpy())
-        assert np.array_equal(hist[GRID][0], hist[PENCIL][0]) and np.array_equal(hist[GRID][1], hist[PENCIL][1])

@@ -44,7 +44,7 @@ def main():
     for _ in range(reps):
         sa.spmv(r, z)
     sp = ctx.kernel_stats(0)
-    print(json.dumps({"config": cfg.name, "n": sa.n, "pencil": f.pencil, "mode": os.environ.get("RCG_SWEEP_CLUSTER", "2"), "fwd_levels": f.fwd_levels, "bwd_levels": f.bwd_levels,
+    print(json.dumps({"config": cfg.name, "n": sa.n, "mode": os.environ.get("RCG_SWEEP_CLUSTER", "2"), "fwd_levels": f.fwd_levels, "bwd_levels": f.bwd_levels,
                       "bps": os.environ.get("RCG_SWEEP_BPS", "4"),
                       "backoff": os.environ.get("RCG_SWEEP_BACKOFF_NS", "32"),
                       "fwd_us": round(fw[0] / fw[1] * 1e3, 1), "bwd_us": round(bw[0] / bw[1] * 1e3, 1),
