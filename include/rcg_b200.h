@@ -226,7 +226,7 @@ int rcg_deflated_pcg_solve(rcg_ctx* ctx, const rcg_matrix* a, const double* b, c
                            const rcg_basis* defl, double* x, const rcg_solver_config* cfg,
                            rcg_solve_report* rep);
 
-/* Batched independent solves (the sequence's solves 2..k, driver.cpp:181-195): nrhs <= 16
+/* Batched independent solves (the sequence's solves 2..k, driver.cpp:181-195): nrhs <= 24
  * right-hand sides of one matrix run through ONE kernel sequence.  B and X hold nrhs vectors
  * of length n back to back (B + k*n is right-hand side k).  Each rhs keeps its own scalars,
  * convergence flag and report; results equal separate solves up to reduction order. */

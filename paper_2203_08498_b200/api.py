@@ -524,8 +524,8 @@ def deflated_pcg_solve(ctx: Context, a: CsrMatrix, b, m, defl: Optional[Basis], 
 
 def _batch(fn, ctx, a, B, m, X, eps, max_iter, defl=None):
     R = len(B)
-    if not (1 <= R <= 16):
-        raise InvalidArgument("batch solve: 1..16 right-hand sides")
+    if not (1 <= R <= 24):
+        raise InvalidArgument("batch solve: 1..24 right-hand sides")
     if isinstance(B, np.ndarray) or isinstance(B, list) and isinstance(B[0], np.ndarray):
         Bm = np.ascontiguousarray(np.stack(list(B)) if isinstance(B, list) else B, dtype=np.float64)
     else:
@@ -559,7 +559,7 @@ def pcg_solve_batch(ctx: Context, a: CsrMatrix, B, m, X, eps: float = 1e-8, max_
 
 def deflated_pcg_solve_batch(ctx: Context, a: CsrMatrix, B, m, defl: Optional[Basis], X, eps: float = 1e-8,
                              max_iter: int = 1000):
-    """R <= 16 independent deflated_pcg_solve calls in one kernel sequence (see pcg_solve_batch)."""
+    """R <= 24 independent deflated_pcg_solve calls in one kernel sequence (see pcg_solve_batch)."""
     return _batch(lib.rcg_deflated_pcg_solve_batch, ctx, a, B, m, X, eps, max_iter, defl=defl)
 
 

@@ -25,14 +25,14 @@
 
 namespace rcg {
 
-constexpr int kRMax = 16;
-constexpr int kMaxRedB = 512;
+constexpr int kRMax = 24;
+constexpr int kMaxRedB = 768;  // basis columns x right-hand sides (32 x 24)
 constexpr int kDepChunkHost = 8;  // the sweeps' dependency chunk (icsweep.cu kDepChunk)
 #ifndef RCG_TALLT_UNROLL
 #define RCG_TALLT_UNROLL 8  // measured: 2 175 us, 4 150 us, 8 146 us (C2, RT 12)
 #endif
 constexpr int kTalltUnroll = RCG_TALLT_UNROLL;  // rows in flight per thread in k_b_tallt
-constexpr int kElemThreads = 192;  // a multiple of every RT (2, 4, 8, 12, 16): a thread keeps one rhs
+constexpr int kElemThreads = 192;  // a multiple of every RT (2, 4, 8, 12, 16, 24): a thread keeps one rhs
 
 struct BState {
     int iter;      // global iteration being executed (1-based)
@@ -1307,7 +1307,9 @@ struct BatchJob {
     int phases = 0;
 };
 
-static int pick_rt(int nrhs) { return nrhs <= 2 ? 2 : (nrhs + 3) / 4 * 4; }
+// RT: 2 for one or two right-hand sides, a multiple of 4 up to 16, else 24 (a multiple of the
+// 4-value chunks and of kElemThreads' per-row thread groups)
+static int pick_rt(int nrhs) { return nrhs <= 2 ? 2 : (nrhs <= 16 ? (nrhs + 3) / 4 * 4 : 24); }
 
 template <int RT>
 struct BatchSolve {
@@ -1725,7 +1727,8 @@ static void run_phase(int rt, BatchJob& job, int wsi, const BatchWs* from, int r
         case 4: phase<4>(job, wsi, from, rt_from, sel, iter); break;
         case 8: phase<8>(job, wsi, from, rt_from, sel, iter); break;
         case 12: phase<12>(job, wsi, from, rt_from, sel, iter); break;
-        default: phase<16>(job, wsi, from, rt_from, sel, iter); break;
+        case 16: phase<16>(job, wsi, from, rt_from, sel, iter); break;
+        default: phase<24>(job, wsi, from, rt_from, sel, iter); break;
     }
 }
 
@@ -1737,7 +1740,7 @@ static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const
                        double* X, const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps) {
     return guard([&] {
         require(ctx && a && reps && B && X, "batch solve: null argument");
-        require(nrhs >= 1 && nrhs <= kRMax, "batch solve: nrhs must be in [1, 16]");
+        require(nrhs >= 1 && nrhs <= kRMax, "batch solve: nrhs must be in [1, 24]");
         check_cfg(cfg);
         check_prec(m, a->n);
         if (defl && defl->k > 0) require(defl->n == a->n, "deflated_pcg_solve: W row count does not match A");

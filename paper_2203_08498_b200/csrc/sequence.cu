@@ -227,12 +227,12 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
             // (auto memory mode), the widest batch whose workspace fits (C4 on one GPU: a few
             // right-hand sides per kernel sequence instead of one), else unbatched
             bool batch = cfg->batch != 0;
-            int max_cnt = 16;
+            int max_cnt = 24;
             if (batch && cfg->memory == 0 && k_t > 1) {
                 size_t fr = 0, tot = 0;
                 RCG_CK(cudaMemGetInfo(&fr, &tot));
                 max_cnt = 0;
-                for (int rt : {16, 12, 8, 4, 2})
+                for (int rt : {24, 16, 12, 8, 4, 2})
                     if (static_cast<double>(fr) > 1.1 * 10.0 * 8.0 * rt * static_cast<double>(n)) {
                         max_cnt = rt;
                         break;

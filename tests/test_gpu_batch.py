@@ -14,8 +14,12 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c4"])
 @pytest.mark.parametrize("method", ["deflation", "sc", "iccg"])
-@pytest.mark.parametrize("nrhs", [3, 9])
+@pytest.mark.parametrize("nrhs", [3, 9, 19])
 def test_batch_matches_oracle(ctx, oracle, problems, name, method, nrhs):
+    """nrhs 3 / 9 / 19: kernel widths RT 4 / 12 / 24 (C3's 19 accelerated solves in one batch),
+    with compaction to narrower phases as right-hand sides converge."""
+    if nrhs == 19 and name != "c2":
+        pytest.skip("RT 24 on the SC / deflation / ICCG variants of one problem is enough")
     from oracle.sequence import run_sequence as oracle_sequence
     from paper_2203_08498_b200 import api
 
