@@ -214,7 +214,7 @@ def run_ours(args, rank, world, local_rank):
         return
     peak, peak_src = peaks()
     kernels, roof = kernel_report(stats, n, n_nnz, nnz_l, cfg.keep, args.steps, peak, peak_src,
-                                  levels=(prep.ic.fwd_levels, prep.ic.bwd_levels))
+                                  levels=(prep.ic.fwd_levels, prep.ic.bwd_levels), workload=cfg.name)
     line = {
         "metric": METRIC,
         "value": round(iters / (ms / 1e3), 2),
@@ -308,9 +308,11 @@ def cost_model_report(n, nnz, m_tilde, phases):
 HOP_FLOOR_US = 0.45
 
 
-def kernel_report(stats, n, nnz, nnz_l, m, steps, peak, peak_src, levels=None):
+def kernel_report(stats, n, nnz, nnz_l, m, steps, peak, peak_src, levels=None, workload=None):
+    # ncu DRAM bytes per launch, per workload (profiles/ncu_traffic.json: {workload: {class: ...}});
+    # a class without a capture on this workload reports null rather than another config's bytes
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    traffic = json.load(open(tp)) if os.path.exists(tp) else {}
+    traffic = (json.load(open(tp)) if os.path.exists(tp) else {}).get(workload, {})
     kernels, best = {}, None
     for c, (tot_ms, cnt, units) in stats.items():
         if cnt == 0:
@@ -336,6 +338,7 @@ def kernel_report(stats, n, nnz, nnz_l, m, steps, peak, peak_src, levels=None):
     roof = {"bound": "hbm", "kernel": CLASS_NAMES[best], "achieved": e["achieved_gbs"], "peak": peak, "unit": "GB/s",
             "frac": round(e["achieved_gbs"] / peak, 4), "frac_of_spec_8tbs": round(e["achieved_gbs"] / 8000.0, 4),
             "traffic": t["dram_bytes"] if isinstance(t, dict) else t,
+            "traffic_source": f"profiles/ncu_traffic.json[{workload}]" if t else "no ncu capture of this kernel on this workload",
             "peak_source": peak_src}
     if isinstance(t, dict):  # the ncu capture's launch carried rhs_per_launch right-hand sides
         roof["traffic_rhs_per_launch"] = t["rhs_per_launch"]

@@ -65,6 +65,8 @@ CsrMatrix poisson7(int g) {
 }
 
 // b = A x_k with x_k from a splitmix64 stream mapped to [-1, 1)
+bool g_perturb = false;  // the reference's own rounding-level spread (the parity bar's floor)
+
 Vector rhs(const CsrMatrix& a, int k) {
     std::uint64_t s = 0x9E3779B97F4A7C15ull * static_cast<std::uint64_t>(k + 1);
     Vector x(static_cast<std::size_t>(a.n()));
@@ -77,6 +79,13 @@ Vector rhs(const CsrMatrix& a, int k) {
     }
     Vector b;
     spmv(a, x, b);
+    if (g_perturb) {  // --perturb: every entry moved by one unit in the last place (seeded signs)
+        std::uint64_t t = 0xD1B54A32D192ED03ull * static_cast<std::uint64_t>(k + 7);
+        for (double& v : b) {
+            t ^= t << 13, t ^= t >> 7, t ^= t << 17;
+            v *= 1.0 + ((t & 1) ? 0x1.0p-52 : -0x1.0p-52);
+        }
+    }
     return b;
 }
 
@@ -266,6 +275,7 @@ int main(int argc, char** argv) {
                 else if (k == "--samples") m = std::atoi(v.c_str());
                 else if (k == "--keep") keep = std::atoi(v.c_str());
                 else if (k == "--w") w_in = v;
+                else if (k == "--perturb") g_perturb = v == "1";
             }
             return sequence_mode(out, csr, method, n_rhs, m, keep, w_in);
         }

@@ -42,7 +42,10 @@ def test_full_size_c5_iccg_solve(ctx, oracle, problems):
 
     cfg = problems.CONFIGS["c5"]
     h, a_o, sa = _scaled_pair(ctx, oracle, problems, "c5")
-    b = oracle.spmv(a_o, problems.normal(cfg.rhs_seed, 0, h.n))
+    # the sequence's first right-hand side, scaled (b = D^-1/2 A x_0): the golden's solve 1, whose
+    # reduction-order floor tools/make_goldens.py --floor measured
+    _, dis = oracle.diagonal_scale(Matrix.of(h))
+    b = dis * oracle.spmv(Matrix.of(h), problems.normal(cfg.rhs_seed, 0, h.n))
     f = api.IcFactor.factorize_device(ctx, sa)
     f_o = oracle.ic0_factorize(a_o)
     xg, xo = np.zeros(h.n), np.zeros(h.n)
@@ -50,4 +53,12 @@ def test_full_size_c5_iccg_solve(ctx, oracle, problems):
     ro = oracle.pcg_solve(a_o, b, xo, kind=1, ic=f_o, eps=cfg.eps, max_iter=cfg.max_iter)
     assert rg.converged and ro.converged and abs(rg.iterations - ro.iterations) <= 2
     if rg.iterations == ro.iterations:
-        assert np.linalg.norm(xg - xo) <= 1e-8 * np.linalg.norm(xo)
+        # the bar: max(1e-8, 10 x the oracle's own reduction-order floor of this solve, measured by
+        # tools/make_goldens.py --floor on the same operator and right-hand side)
+        import json
+        import os
+
+        gp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", cfg.name + ".json")
+        floor = json.load(open(gp)).get("solve1_floor", {}).get("rel_solution", 0.0) if os.path.exists(gp) else 0.0
+        rel = float(np.linalg.norm(xg - xo) / np.linalg.norm(xo))
+        assert rel <= max(1e-8, 10.0 * floor), (rel, floor)
