@@ -341,6 +341,19 @@ int rcg_comm_create_nccl(const void* id128, int nranks, int rank, rcg_comm** out
  * and a fixed-order sum; slabs never wait on each other inside a kernel) -- tests the distributed
  * iteration on one GPU */
 int rcg_comm_create_loopback(int nparts, rcg_comm** out);
+/* A host-staged transport over caller-supplied collectives (e.g. torch.distributed / gloo), one
+ * slab per process: allreduce sums buf[0..count) over the ranks in place (identical result on every
+ * rank); exchange sends send[send_off[q] .. + send_cnt[q]) to rank q and receives
+ * recv[recv_off[q] .. + recv_cnt[q]) from rank q, for every q with a nonzero count.  Both return 0
+ * on success.  Each collective synchronises the slab's stream (no kernel ever waits on another
+ * rank), so ranks may share a GPU -- the multi-process test transport of the NCCL path's
+ * iteration. */
+typedef int (*rcg_host_allreduce_fn)(void* user, double* buf, int count);
+typedef int (*rcg_host_exchange_fn)(void* user, const double* send, const int64_t* send_off,
+                                    const int64_t* send_cnt, double* recv, const int64_t* recv_off,
+                                    const int64_t* recv_cnt, int nranks);
+int rcg_comm_create_host(int nranks, int rank, rcg_host_allreduce_fn allreduce,
+                         rcg_host_exchange_fn exchange, void* user, rcg_comm** out);
 void rcg_comm_destroy(rcg_comm* c);
 /* distributed PCG (pcg.cpp:37-92 per rank with block-Jacobi IC or identity): nslabs = 1 with
  * NCCL, = nparts with loopback; b[s], x[s] are slab s's local rows (host or device) */

@@ -34,6 +34,10 @@ i64p = C.POINTER(C.c_int64)
 dp = C.POINTER(C.c_double)
 ip = C.POINTER(C.c_int)
 
+# host transport callbacks (rcg_comm_create_host)
+HostAllreduceFn = C.CFUNCTYPE(C.c_int, vp, dp, C.c_int)
+HostExchangeFn = C.CFUNCTYPE(C.c_int, vp, dp, i64p, i64p, dp, i64p, i64p, C.c_int)
+
 
 class SolverConfig(C.Structure):
     _fields_ = [("eps", C.c_double), ("max_iter", C.c_int), ("record_history", C.c_int)]
@@ -197,6 +201,7 @@ SIGNATURES = {
     "rcg_comm_nccl_unique_id": (C.c_int, vp),
     "rcg_comm_create_nccl": (C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)),
     "rcg_comm_create_loopback": (C.c_int, C.c_int, C.POINTER(vp)),
+    "rcg_comm_create_host": (C.c_int, C.c_int, C.c_int, HostAllreduceFn, HostExchangeFn, vp, C.POINTER(vp)),
     "rcg_comm_destroy": (None, vp),
     "rcg_dist_pcg_solve": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                            C.POINTER(SolverConfig), C.POINTER(SolveReport)),

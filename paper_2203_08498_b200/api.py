@@ -711,6 +711,49 @@ class Comm:
         check(lib.rcg_comm_create_loopback(int(nparts), C.byref(h)))
         return cls(h, nparts)
 
+    @classmethod
+    def host(cls, group=None) -> "Comm":
+        """Host-staged transport over torch.distributed (any backend with CPU tensors, e.g. gloo):
+        each collective synchronises the slab's stream and moves its values through host memory,
+        so ranks never wait on each other inside a kernel and may share one GPU
+        (rcg_comm_create_host).  The slow but exact stand-in for NCCL in multi-process tests."""
+        import torch
+        import torch.distributed as dist
+
+        nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+
+        def allreduce(_user, buf, count):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(count,)))
+                dist.all_reduce(t, group=group)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported as a status by the library
+                return 1
+
+        def exchange(_user, send, so, sc, recv, ro, rc, np_):
+            try:
+                reqs = []
+                for q in range(np_):
+                    if sc[q]:
+                        t = torch.from_numpy(np.ctypeslib.as_array(send, shape=(so[q] + sc[q],))[so[q]:])
+                        reqs.append(dist.isend(t, q, group=group))
+                    if rc[q]:
+                        t = torch.from_numpy(np.ctypeslib.as_array(recv, shape=(ro[q] + rc[q],))[ro[q]:])
+                        reqs.append(dist.irecv(t, q, group=group))
+                for r in reqs:
+                    r.wait()
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        cb_ar = L.HostAllreduceFn(allreduce)
+        cb_ex = L.HostExchangeFn(exchange)
+        h = C.c_void_p()
+        check(lib.rcg_comm_create_host(int(nranks), int(rank), cb_ar, cb_ex, None, C.byref(h)))
+        c = cls(h, nranks)
+        c._callbacks = (cb_ar, cb_ex)  # the library holds raw pointers to them
+        return c
+
     def __del__(self):
         if getattr(self, "h", None):
             lib.rcg_comm_destroy(self.h)

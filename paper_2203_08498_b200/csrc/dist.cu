@@ -497,6 +497,53 @@ struct NcclComm : rcg_comm {
     }
 };
 
+// --- host-staged: a caller-supplied host transport (torch.distributed over gloo, MPI, ...).  Every
+// collective synchronises the slab's stream and round-trips through host memory, so ranks never
+// wait on one another inside a kernel: several processes may share one GPU (the world-size-2
+// tests of this file's distributed iteration, tests/test_gpu_dist_host.py).  Slow by design.
+struct HostComm : rcg_comm {
+    int nranks = 1, rank = 0;
+    rcg_host_allreduce_fn ar = nullptr;
+    rcg_host_exchange_fn ex = nullptr;
+    void* user = nullptr;
+    std::vector<double> hbuf, hsend, hrecv;
+    std::vector<int64_t> so, sc, ro, rc;
+    int nparts() const override { return nranks; }
+    int local_slabs() const override { return 1; }
+    void allreduce(rcg_dslab* const* s, int ns, int count, int sel) override {
+        (void)ns;
+        rcg_dslab* d = s[0];
+        double* buf = sel ? d->gbuf : d->dsum;
+        hbuf.resize(std::max(count, 1));
+        RCG_CK(cudaMemcpyAsync(hbuf.data(), buf, sizeof(double) * count, cudaMemcpyDeviceToHost, d->ctx->stream));
+        RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+        if (ar(user, hbuf.data(), count) != 0) throw Error(RCG_E_CUDA, "host transport: allreduce callback failed");
+        RCG_CK(cudaMemcpyAsync(buf, hbuf.data(), sizeof(double) * count, cudaMemcpyHostToDevice, d->ctx->stream));
+        RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+    }
+    void halo(rcg_dslab* const* s, int ns, int which) override {
+        (void)ns;
+        rcg_dslab* d = s[0];
+        pack(d, which);
+        hsend.resize(std::max(d->nsend, 1));
+        hrecv.resize(std::max(d->nhalo, 1));
+        if (d->nsend > 0)
+            RCG_CK(cudaMemcpyAsync(hsend.data(), d->sendbuf, sizeof(double) * d->nsend, cudaMemcpyDeviceToHost,
+                                   d->ctx->stream));
+        RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+        so.assign(d->send_off.begin(), d->send_off.end());
+        sc.assign(d->send_count.begin(), d->send_count.end());
+        ro.assign(d->recv_off.begin(), d->recv_off.end());
+        rc.assign(d->recv_count.begin(), d->recv_count.end());
+        if (ex(user, hsend.data(), so.data(), sc.data(), hrecv.data(), ro.data(), rc.data(), nranks) != 0)
+            throw Error(RCG_E_CUDA, "host transport: halo exchange callback failed");
+        if (d->nhalo > 0)
+            RCG_CK(cudaMemcpyAsync(ext_of(d, which) + d->nloc, hrecv.data(), sizeof(double) * d->nhalo,
+                                   cudaMemcpyHostToDevice, d->ctx->stream));
+        RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+    }
+};
+
 // --- loopback: all slabs in this process (one GPU); stream-ordered copies, fixed-order sums
 struct LoopComm : rcg_comm {
     int np = 1;
@@ -1323,6 +1370,21 @@ int rcg_comm_create_loopback(int nparts, rcg_comm** out) {
         for (auto& e : c->ev_read) RCG_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->dptrs = static_cast<double**>(dev_alloc_bytes(sizeof(double*) * nparts));
         c->gptrs = static_cast<double**>(dev_alloc_bytes(sizeof(double*) * nparts));
+        *out = c;
+    });
+}
+
+int rcg_comm_create_host(int nranks, int rank, rcg_host_allreduce_fn allreduce, rcg_host_exchange_fn exchange,
+                         void* user, rcg_comm** out) {
+    return guard([&] {
+        require(out && allreduce && exchange && nranks >= 1 && rank >= 0 && rank < nranks,
+                "rcg_comm_create_host: bad argument");
+        auto* c = new HostComm();
+        c->nranks = nranks;
+        c->rank = rank;
+        c->ar = allreduce;
+        c->ex = exchange;
+        c->user = user;
         *out = c;
     });
 }

@@ -22,8 +22,8 @@ def bounds(n: int, nparts: int) -> np.ndarray:
 
 
 def block_factor(ctx: api.Context, plan: api.SlabPlan, shift: float = 0.0, device: bool = False) -> api.IcFactor:
-    """The slab's diagonal-block IC(0): host restatement, or (device=True) the device
-    factorisation -- bitwise the same factor (tests/test_gpu_icfactor.py), much faster on C4."""
+    """The slab's diagonal-block IC(0), factorised on the device either way (device=False passes
+    host arrays, which rcg_ic0_factorize uploads) -- the reference's factor bit for bit."""
     rs, ci, va = plan.diagonal_block()
     if device:
         return api.IcFactor.factorize_device(ctx, api.CsrMatrix(ctx, plan.nloc, rs, ci, va, validate=False), shift, 1)
@@ -98,27 +98,36 @@ class LoopbackSystem:
 
 
 class NcclRank:
-    """This process's slab of a G-GPU solve (rank = slab index), plumbing over torch.distributed
-    (NCCL backend): rank 0 creates the NCCL id, every rank builds its own plan / factor / slab."""
+    """This process's slab of a G-GPU solve (rank = slab index), plumbing over torch.distributed:
+    rank 0 creates the NCCL id, every rank builds its own plan / factor / slab.  transport="nccl"
+    (NCCL over NVLink, the product path) or "host" (rcg_comm_create_host over the process group's
+    own backend, e.g. gloo: every collective staged through host memory, so ranks may share one
+    GPU -- the multi-process test of the same distributed iteration)."""
 
-    def __init__(self, host, ctx: Optional[api.Context] = None, preconditioner: str = "ic"):
+    def __init__(self, host, ctx: Optional[api.Context] = None, preconditioner: str = "ic",
+                 transport: str = "nccl", device_factor: bool = True):
         import torch
         import torch.distributed as dist
 
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.ctx = ctx or api.Context(torch.cuda.current_device())
         self.plan = api.SlabPlan(host.n, host.row_start, host.col_idx, host.values, self.world, self.rank)
+        on_gpu = dist.get_backend() == "nccl"
 
         def allreduce_max(v: float) -> float:
-            t = torch.tensor([v], dtype=torch.float64, device="cuda")
+            t = torch.tensor([v], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item())
 
-        self.factor = agree_factors([self.ctx], [self.plan], allreduce_max)[0] if preconditioner == "ic" else None
+        self.factor = (agree_factors([self.ctx], [self.plan], allreduce_max, device_factor)[0]
+                       if preconditioner == "ic" else None)
         self.slab = api.DSlab(self.ctx, self.plan, self.factor)
-        obj = [api.Comm.unique_id() if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        self.comm = api.Comm.nccl(obj[0], self.world, self.rank)
+        if transport == "host":
+            self.comm = api.Comm.host()
+        else:
+            obj = [api.Comm.unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            self.comm = api.Comm.nccl(obj[0], self.world, self.rank)
 
     def basis(self, w_local: np.ndarray, kind: str = "deflation") -> api.DBasis:
         """This rank's rows of W, (m, nloc) -- collective over the ranks."""
