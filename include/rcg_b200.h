@@ -368,6 +368,14 @@ void rcg_dbasis_destroy(rcg_dbasis* b);
 /* distributed deflated PCG (basis kind DEFLATION, pcg.cpp:94-160) or SC-PCG around the block
  * IC(0) (kind SC, subspace_correction.cpp:27-57); basis null = rcg_dist_pcg_solve.  Per
  * iteration the m-vector W^T q (or W^T r) is allreduced before the replicated Cholesky solve. */
+/* The accelerated solves of the sequence over THIS process's slab, batched (driver.cpp:181-195
+ * over row slabs): nrhs <= 24 right-hand sides (B, X: nrhs x nloc, back to back, host or device)
+ * through one kernel sequence -- the single-GPU batched solver with its reductions allreduced over
+ * the ranks and p's halo rows exchanged (RT-interleaved) before each SpMV.  basis: deflation or
+ * subspace correction (null: block-Jacobi ICCG).  One slab per process (NCCL / host transports;
+ * loopback only at G = 1). */
+int rcg_dist_solve_batch(rcg_comm* comm, rcg_dslab* slab, const rcg_dbasis* basis, const double* B, double* X,
+                         const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps);
 int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
                    double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report);
 /* solve 1 of the sequence over slabs: rcg_dist_pcg_solve with the error-sampling observer

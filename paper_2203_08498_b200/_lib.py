@@ -210,6 +210,7 @@ SIGNATURES = {
     "rcg_seq_run": (C.c_int, vp, C.c_int, vp, vp, C.POINTER(SeqConfig), C.POINTER(SeqReport)),
     "rcg_dbasis_create": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_int, C.c_int, C.POINTER(vp)),
     "rcg_dbasis_destroy": (None, vp),
+    "rcg_dist_solve_batch": (C.c_int, vp, vp, vp, vp, vp, C.POINTER(SolverConfig), C.c_int, C.POINTER(SolveReport)),
     "rcg_dist_solve": (C.c_int, vp, C.c_int, C.POINTER(vp), vp, C.POINTER(vp), C.POINTER(vp),
                        C.POINTER(SolverConfig), C.POINTER(SolveReport)),
     "rcg_dist_pcg_solve_sampled": (C.c_int, vp, C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),

@@ -816,6 +816,29 @@ def dist_solve(comm: Comm, slabs, bs, xs, basis: Optional[DBasis] = None, eps: f
     return _finish(rep, bufs)
 
 
+def dist_solve_batch(comm: Comm, slab, B, X, basis: Optional[DBasis] = None, eps: float = 1e-8,
+                     max_iter: int = 1000):
+    """rcg_dist_solve_batch: up to 24 accelerated solves over this process's slab in ONE kernel
+    sequence (the batched solver with allreduced reductions and RT-interleaved halo exchanges).
+    B, X: (R, nloc) this slab's rows; returns one SolveReport per right-hand side."""
+    nloc = slab.plan.nloc
+    Bm = np.ascontiguousarray(np.stack(list(B)) if isinstance(B, list) else B, dtype=np.float64)
+    R = Bm.shape[0]
+    if not (1 <= R <= 24) or Bm.shape[-1] != nloc:
+        raise InvalidArgument("dist_solve_batch: B must be (R <= 24, nloc)")
+    _out(X, (R, nloc), "X")
+    cfg = _cfg(eps, max_iter)
+    reps = (L.SolveReport * R)()
+    bufs = []
+    for r in reps:
+        rb = _report(max(1, int(max_iter)))
+        r.cap, r.history, r.alphas, r.betas = rb[0].cap, rb[0].history, None, None
+        bufs.append(rb[1])
+    check(lib.rcg_dist_solve_batch(comm.h, slab.h, basis.h if basis is not None else None, _ptr(Bm), _ptr(X),
+                                   C.byref(cfg), R, reps))
+    return [_finish(r, b) for r, b in zip(reps, bufs)]
+
+
 def dist_pcg_solve_sampled(comm: Comm, slabs, samplers, bs, xs, eps: float = 1e-8,
                            max_iter: int = 1000) -> SolveReport:
     """Solve 1 of the sequence over row slabs (rcg_dist_pcg_solve_sampled): block-Jacobi PCG with

@@ -235,6 +235,7 @@ int sequence_mode(const std::string& out, const std::string& csr, const std::str
     for (int k = 1; k < n_rhs; ++k) {
         Vector xk(static_cast<std::size_t>(a.n()), 0.0);
         const Vector bk = scaling.scale_rhs(rhs(a0, k));
+        dump(out + "/rhs" + std::to_string(k) + ".bin", bk);  // the parity floor (tests/test_bridge.py)
         if (sc)
             rec.solve("accelerated", k, pcg_solve(a, bk, *sc, xk, cfg), xk);
         else

@@ -46,6 +46,11 @@ struct BState {
     double bnorm[kRMax], rho[kRMax], rho_prev[kRMax], beta[kRMax], alpha[kRMax], pq[kRMax], rr[kRMax],
         relres[kRMax], scal2[kRMax];
     unsigned int tick[8];
+    // row slabs (dist.cu): the reducing kernels' last block writes its local totals to dtot and
+    // stops; the host allreduces them over the ranks and k_b_fin runs the same finaliser
+    int defer;
+    int pad2;
+    double* dtot;
 };
 
 struct BatchWs {
@@ -286,6 +291,112 @@ __device__ __forceinline__ void chunk_acc(double (&accs)[RT], int c, F&& f) {
             for (int i = 0; i < 4; ++i) accs[4 * cc + i] = f(accs[4 * cc + i], i);
 }
 
+// ---- finalisers (per right-hand side k, from the summed totals): run by the reducing kernel's
+// last block, or -- row slabs -- by k_b_fin after the totals were allreduced over the ranks
+template <int RT>
+__device__ __forceinline__ void fin_resid(BState* st, const double* tot, int k, int defer_check) {
+    st->bnorm[k] = sqrt(tot[k]);
+    st->rr[k] = tot[RT + k];
+    st->rho[k] = tot[RT + k];
+    if (st->bnorm[k] == 0.0)
+        st->done[k] = kZeroRhs;
+    else if (!defer_check && sqrt(tot[RT + k]) <= st->eps * st->bnorm[k])
+        st->done[k] = kConverged;
+    else
+        st->done[k] = kRunning;
+}
+
+__device__ __forceinline__ void fin_rho(BState* st, const double* tot, int k, int add_sc) {
+    double rho = tot[k];
+    if (st->done[k] == kRunning) {
+        if (add_sc) rho = __dadd_rn(rho, st->scal2[k]);
+        st->rho[k] = rho;
+        if (rho <= 0.0) {
+            st->done[k] = kBroken;
+            st->status[k] = kBrkRz;
+        }
+        st->beta[k] = st->iter > 1 ? rho / st->rho_prev[k] : 0.0;
+    }
+}
+
+__device__ __forceinline__ void fin_pq(BState* st, const double* tot, int k) {
+    if (st->done[k] == kRunning) {
+        st->pq[k] = tot[k];
+        if (tot[k] <= 0.0) {
+            st->done[k] = kBroken;
+            st->status[k] = kBrkPAp;
+        }
+        st->alpha[k] = st->rho[k] / tot[k];
+    }
+}
+
+__device__ __forceinline__ void fin_projcheck(BState* st, const double* tot, int k) {
+    if (st->done[k] == kRunning) {
+        st->rr[k] = tot[k];
+        st->rho[k] = tot[k];
+        if (sqrt(tot[k]) <= st->eps * st->bnorm[k]) st->done[k] = kConverged;
+    }
+}
+
+// x, r update finaliser: threads k < RT, then thread 0 (after a block barrier) counts
+template <int RT>
+__device__ __forceinline__ void fin_xr(BState* st, const double* tot, double* hist, int64_t hist_ld, int identity) {
+    if (threadIdx.x < RT) {
+        const int k = threadIdx.x;
+        const int i = st->iter;
+        if (st->done[k] == kRunning) {
+            const double relres = sqrt(tot[k]) / st->bnorm[k];
+            st->rr[k] = tot[k];
+            st->relres[k] = relres;
+            st->iters[k] = i;
+            hist[k * hist_ld + (i - 1)] = relres;
+            hist[(RT + k) * hist_ld + (i - 1)] = st->alpha[k];
+            hist[(2 * RT + k) * hist_ld + (i - 1)] = st->beta[k];
+            st->rho_prev[k] = st->rho[k];
+            if (relres <= st->eps) {
+                st->done[k] = kConverged;
+            } else if (i >= st->max_iter) {
+                st->done[k] = kCapped;
+            } else if (identity) {
+                st->rho[k] = tot[k];
+                if (tot[k] <= 0.0) {
+                    st->done[k] = kBroken;
+                    st->status[k] = kBrkRz;
+                }
+                st->beta[k] = tot[k] / st->rho_prev[k];
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int k = 0; k < RT; ++k) c += st->done[k] == kRunning;
+        st->nrun = c;
+        st->iter = st->iter + 1;
+    }
+}
+
+// u[:,k] = (W^T A W)^-1 f[:,k] (one warp per rhs), and f.u per rhs when mode == 2
+template <int RT>
+__device__ __forceinline__ void fin_tallt(BState* st, const double* tot, const double* L, int m, double* u, int mode,
+                                          double (*fk)[128], double (*sol)[128]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int k = wid; k < RT; k += blockDim.x >> 5) {
+        for (int j = lane; j < m; j += 32) fk[wid][j] = tot[j * RT + k];
+        __syncwarp();
+        double* uk = sol[wid];
+        warp_chol_solve(L, m, fk[wid], uk, uk);
+        __syncwarp();
+        for (int j = lane; j < m; j += 32) u[j * RT + k] = uk[j];
+        if (mode == 2 && lane == 0) {
+            double fu = 0.0;
+            for (int j = 0; j < m; ++j) fu = fadd_mul(fu, fk[wid][j], uk[j]);
+            st->scal2[k] = fu;
+        }
+        __syncwarp();
+    }
+}
+
 // r = b - A x for all RT; finaliser: bnorm, rho = rr, already-converged / zero-rhs flags
 template <int RT>
 __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_residual(SpmvArgs a, int cap, const double* __restrict__ b,
@@ -330,17 +441,12 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_residu
         accs[RT + v] = rr[v];
     }
     block_sum_dyn<2 * RT>(accs, 2 * RT, scratch, vals);
-    if (grid_reduce_dyn(vals, 2 * RT, partials, &st->tick[0], tot) && threadIdx.x < RT) {
-        const int k = threadIdx.x;
-        st->bnorm[k] = sqrt(tot[k]);
-        st->rr[k] = tot[RT + k];
-        st->rho[k] = tot[RT + k];
-        if (st->bnorm[k] == 0.0)
-            st->done[k] = kZeroRhs;
-        else if (!defer_check && sqrt(tot[RT + k]) <= st->eps * st->bnorm[k])
-            st->done[k] = kConverged;
-        else
-            st->done[k] = kRunning;
+    if (grid_reduce_dyn(vals, 2 * RT, partials, &st->tick[0], tot)) {
+        if (st->defer) {
+            for (int t = threadIdx.x; t < 2 * RT; t += blockDim.x) st->dtot[t] = tot[t];
+            return;
+        }
+        if (threadIdx.x < RT) fin_resid<RT>(st, tot, threadIdx.x, defer_check);
     }
 }
 
@@ -707,18 +813,12 @@ __global__ void __launch_bounds__(kElemThreads) k_b_rho(const double* __restrict
         vals[threadIdx.x] = v;
     }
     __syncthreads();
-    if (grid_reduce_dyn(vals, RT, partials, &st->tick[5], tot) && threadIdx.x < RT) {
-        const int k = threadIdx.x;
-        double rho = tot[k];
-        if (st->done[k] == kRunning) {
-            if (add_sc) rho = __dadd_rn(rho, st->scal2[k]);
-            st->rho[k] = rho;
-            if (rho <= 0.0) {
-                st->done[k] = kBroken;
-                st->status[k] = kBrkRz;
-            }
-            st->beta[k] = st->iter > 1 ? rho / st->rho_prev[k] : 0.0;
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[5], tot)) {
+        if (st->defer) {
+            if (threadIdx.x < RT) st->dtot[threadIdx.x] = tot[threadIdx.x];
+            return;
         }
+        if (threadIdx.x < RT) fin_rho(st, tot, threadIdx.x, add_sc);
     }
 }
 
@@ -884,16 +984,12 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
     }
     if (project_later) return;
     block_sum_dyn<RT>(pq, RT, scratch, vals);
-    if (grid_reduce_dyn(vals, RT, partials, &st->tick[1], tot) && threadIdx.x < RT) {
-        const int k = threadIdx.x;
-        if (st->done[k] == kRunning) {
-            st->pq[k] = tot[k];
-            if (tot[k] <= 0.0) {
-                st->done[k] = kBroken;
-                st->status[k] = kBrkPAp;
-            }
-            st->alpha[k] = st->rho[k] / tot[k];
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[1], tot)) {
+        if (st->defer) {
+            if (threadIdx.x < RT) st->dtot[threadIdx.x] = tot[threadIdx.x];
+            return;
         }
+        if (threadIdx.x < RT) fin_pq(st, tot, threadIdx.x);
     }
 }
 
@@ -1004,22 +1100,46 @@ __global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const
         __syncthreads();
         if (threadIdx.x == 0) st->tick[2] = 0u;
     }
-    {
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        for (int k = wid; k < RT; k += blockDim.x >> 5) {
-            for (int j = lane; j < m; j += 32) fk[wid][j] = tot[j * RT + k];
-            __syncwarp();
-            double* uk = sol[wid];
-            warp_chol_solve(L, m, fk[wid], uk, uk);
-            __syncwarp();
-            for (int j = lane; j < m; j += 32) u[j * RT + k] = uk[j];
-            if (mode == 2 && lane == 0) {
-                double fu = 0.0;
-                for (int j = 0; j < m; ++j) fu = fadd_mul(fu, fk[wid][j], uk[j]);
-                st->scal2[k] = fu;
-            }
-            __syncwarp();
-        }
+    if (st->defer) {
+        for (int t = threadIdx.x; t < m * RT; t += blockDim.x) st->dtot[t] = tot[t];
+        return;
+    }
+    fin_tallt<RT>(st, tot, L, m, u, mode, fk, sol);
+}
+
+// The finalisers of the reducing kernels from allreduced totals (row slabs): which = 0 residual
+// (arg: defer_check), 1 rho (arg: add_sc), 2 (p, q), 3 projected-residual check, 4 x / r update
+// (arg: identity), 5 the m x RT projection coefficients (arg: tallt mode).  `guard` repeats the
+// producing kernel's early exit (nothing ran, nothing to finalise).
+template <int RT>
+__global__ void __launch_bounds__(kElemThreads) k_b_fin(BState* st, int which, int arg, int guard, const double* L, int m,
+                                                        double* u, double* hist, int64_t hist_ld) {
+    __shared__ double tot[kMaxRedB];
+    __shared__ double fk[6][128];
+    __shared__ double sol[6][128];
+    if (guard && st->nrun == 0) return;
+    const int cnt = which == 0 ? 2 * RT : (which == 5 ? m * RT : RT);
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) tot[t] = st->dtot[t];
+    __syncthreads();
+    switch (which) {
+        case 0:
+            if (threadIdx.x < RT) fin_resid<RT>(st, tot, threadIdx.x, arg);
+            break;
+        case 1:
+            if (threadIdx.x < RT) fin_rho(st, tot, threadIdx.x, arg);
+            break;
+        case 2:
+            if (threadIdx.x < RT) fin_pq(st, tot, threadIdx.x);
+            break;
+        case 3:
+            if (threadIdx.x < RT) fin_projcheck(st, tot, threadIdx.x);
+            break;
+        case 4:
+            fin_xr<RT>(st, tot, hist, hist_ld, arg);
+            break;
+        default:
+            fin_tallt<RT>(st, tot, L, m, u, arg, fk, sol);
+            break;
     }
 }
 
@@ -1098,21 +1218,16 @@ __global__ void __launch_bounds__(kElemThreads) k_b_deflate(double* __restrict__
 #pragma unroll
             for (int v = 0; v < VW; ++v) full[cc * VW + v] = acc[v];
     block_sum_dyn<RT>(full, RT, scratch, vals);
-    if (grid_reduce_dyn(vals, RT, partials, &st->tick[3], tot) && threadIdx.x < RT) {
-        const int k = threadIdx.x;
-        if (mode == 0) {
-            if (st->done[k] == kRunning) {
-                st->pq[k] = tot[k];
-                if (tot[k] <= 0.0) {
-                    st->done[k] = kBroken;
-                    st->status[k] = kBrkPAp;
-                }
-                st->alpha[k] = st->rho[k] / tot[k];
-            }
-        } else if (st->done[k] == kRunning) {
-            st->rr[k] = tot[k];
-            st->rho[k] = tot[k];
-            if (sqrt(tot[k]) <= st->eps * st->bnorm[k]) st->done[k] = kConverged;
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[3], tot)) {
+        if (st->defer) {
+            if (threadIdx.x < RT) st->dtot[threadIdx.x] = tot[threadIdx.x];
+            return;
+        }
+        if (threadIdx.x < RT) {
+            if (mode == 0)
+                fin_pq(st, tot, threadIdx.x);
+            else
+                fin_projcheck(st, tot, threadIdx.x);
         }
     }
 }
@@ -1151,39 +1266,11 @@ __global__ void __launch_bounds__(kElemThreads) k_b_xr(double* __restrict__ x, d
     }
     __syncthreads();
     if (grid_reduce_dyn(vals, RT, partials, &st->tick[4], tot)) {
-        if (threadIdx.x < RT) {
-            const int k = threadIdx.x;
-            const int i = st->iter;
-            if (st->done[k] == kRunning) {
-                const double relres = sqrt(tot[k]) / st->bnorm[k];
-                st->rr[k] = tot[k];
-                st->relres[k] = relres;
-                st->iters[k] = i;
-                hist[k * hist_ld + (i - 1)] = relres;
-                hist[(RT + k) * hist_ld + (i - 1)] = st->alpha[k];
-                hist[(2 * RT + k) * hist_ld + (i - 1)] = st->beta[k];
-                st->rho_prev[k] = st->rho[k];
-                if (relres <= st->eps) {
-                    st->done[k] = kConverged;
-                } else if (i >= st->max_iter) {
-                    st->done[k] = kCapped;
-                } else if (identity) {
-                    st->rho[k] = tot[k];
-                    if (tot[k] <= 0.0) {
-                        st->done[k] = kBroken;
-                        st->status[k] = kBrkRz;
-                    }
-                    st->beta[k] = tot[k] / st->rho_prev[k];
-                }
-            }
+        if (st->defer) {
+            if (threadIdx.x < RT) st->dtot[threadIdx.x] = tot[threadIdx.x];
+            return;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int c = 0;
-            for (int k = 0; k < RT; ++k) c += st->done[k] == kRunning;
-            st->nrun = c;
-            st->iter = st->iter + 1;
-        }
+        fin_xr<RT>(st, tot, hist, hist_ld, identity);
     }
 }
 
@@ -1237,6 +1324,8 @@ __global__ void k_b_carry_state(const BState* __restrict__ a, BState* __restrict
         b->eps = a->eps;
         b->nrun = sel.cnt;
         for (int j = 0; j < 8; ++j) b->tick[j] = 0u;
+        b->defer = a->defer;
+        b->dtot = a->dtot;
     }
     if (t < rt_out) {
         if (t < sel.cnt) {
@@ -1305,6 +1394,7 @@ struct BatchJob {
     int broken = -1;
     int broken_status = 0;
     int phases = 0;
+    BatchComm* comm = nullptr;  // row slabs (dist.cu): halo exchange + allreduced reductions
 };
 
 // RT: 2 for one or two right-hand sides, a multiple of 4 up to 16, else 24 (a multiple of the
@@ -1342,8 +1432,12 @@ struct BatchSolve {
         if (defl) mm = std::max(mm, defl->k);
         require(mm * RT <= kMaxRedB, "batch: basis columns x right-hand sides exceed the reduction capacity");
         require(mm <= 128, "batch: at most 128 basis columns");
-        const int64_t nrt = static_cast<int64_t>(n) * RT;
-        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + 3) / 4 : 1;  // >= RPW 4
+        // row slabs: every interleaved vector carries the halo rows after the owned ones (p's are
+        // filled by the exchange before each SpMV, x's before the initial residual)
+        const int64_t nrt = (static_cast<int64_t>(n) + (job.comm ? job.comm->nhalo : 0)) * RT;
+        // sweep tiles: the chunk-lane sweeps take RPW = 32 / (RT / 2) rows per warp tile (2 at RT 24)
+        constexpr int kRpw = 32 / (RT / 2);
+        int64_t ntiles = ic ? (std::max<int64_t>(std::max(m->ic->f_npos, m->ic->b_npos), n) + kRpw - 1) / kRpw : 1;
         const int64_t groups = (ntiles + kGroup - 1) / kGroup;
         const int64_t part = std::max<int64_t>(ntiles * RT, static_cast<int64_t>(kMaxRedB) * ctx->num_sms * 8);
         // history: relres, alpha, beta blocks of RT rows each (the CG coefficients feed the Lanczos estimate)
@@ -1446,6 +1540,8 @@ struct BatchSolve {
         h.iter = 1;
         h.max_iter = max_iter;
         h.eps = eps;
+        h.defer = job.comm ? 1 : 0;
+        h.dtot = job.comm ? job.comm->dtot : nullptr;
         std::memcpy(ctx->host_pinned, &h, sizeof(h));
         RCG_CK(cudaMemcpyAsync(w->st, ctx->host_pinned, sizeof(BState), cudaMemcpyHostToDevice, ctx->stream));
         const int64_t nrt = static_cast<int64_t>(n) * RT;
@@ -1454,21 +1550,26 @@ struct BatchSolve {
             launch_fill_bits(ctx, w->zs, nrt, kSentinelBits);
         }
         const bool dfl = defl && defl->k > 0;
+        if (job.comm) job.comm->halo(ctx, w->x, RT);
         k_b_residual<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(sargs(), bcap, w->b, w->x, w->r, w->st,
                                                                           w->partials, dfl ? 1 : 0);
         RCG_LAUNCHED(ctx);
+        reduce(0, 2 * RT, dfl ? 1 : 0, 0);
         if (dfl) {
             k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->r, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
+            reduce(5, defl->k * RT, 1, 0, defl->l, defl->k, w->u);
             k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr,
                                                                     n, w->partials, w->st, 1);
             RCG_LAUNCHED(ctx);
+            reduce(3, RT, 0, 0);
         }
         if (sc) {
             k_b_tallt<RT><<<tgrid(scb->k), kElemThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
                                                                   scb->l, w->u2, 2, w->st, 0);
             RCG_LAUNCHED(ctx);
+            reduce(5, scb->k * RT, 2, 0, scb->l, scb->k, w->u2);
         }
         k_b_count<<<1, 1, 0, ctx->stream>>>(w->st, RT);
         RCG_LAUNCHED(ctx);
@@ -1487,6 +1588,7 @@ struct BatchSolve {
             ba.r = w->r;
             ba.add_sc = sc ? 1 : 0;
             launch_b_sweep(true, ba);
+            reduce(1, RT, sc ? 1 : 0, 1);
             z = w->zs;
         }
         require(ic || !sc, "batch: subspace correction needs the IC inner preconditioner");
@@ -1498,20 +1600,29 @@ struct BatchSolve {
             RCG_LAUNCHED(ctx);
         }
         const bool dfl = defl && defl->k > 0;
+        if (job.comm) job.comm->halo(ctx, w->p, RT);
         {
             KTimer t(ctx, 5, RT);
             k_b_spmv_pq<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(sargs(), bcap, w->p, w->q, w->st,
                                                                              w->partials, dfl ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
+        if (!dfl) reduce(2, RT, 0, 1);
         if (dfl) {
-            KTimer t(ctx, 9, RT);
-            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n, w->partials,
-                                                                  defl->l, w->u, 1, w->st, 1);
-            RCG_LAUNCHED(ctx);
-            k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, n,
-                                                                    w->partials, w->st, 0);
-            RCG_LAUNCHED(ctx);
+            {
+                KTimer t(ctx, 9, RT);
+                k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n,
+                                                                      w->partials, defl->l, w->u, 1, w->st, 1);
+                RCG_LAUNCHED(ctx);
+            }
+            reduce(5, defl->k * RT, 1, 1, defl->l, defl->k, w->u);
+            {
+                KTimer t(ctx, 9, RT);
+                k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, n,
+                                                                        w->partials, w->st, 0);
+                RCG_LAUNCHED(ctx);
+            }
+            reduce(2, RT, 0, 1);
         }
         {
             KTimer t(ctx, 8, RT);
@@ -1519,12 +1630,25 @@ struct BatchSolve {
                                                                max_iter + 1, (!ic && !sc) ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
+        reduce(4, RT, (!ic && !sc) ? 1 : 0, 1);
         if (sc) {
-            KTimer t(ctx, 9, RT);
-            k_b_tallt<RT><<<tgrid(scb->k), kElemThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
-                                                                  scb->l, w->u2, 2, w->st, 1);
-            RCG_LAUNCHED(ctx);
+            {
+                KTimer t(ctx, 9, RT);
+                k_b_tallt<RT><<<tgrid(scb->k), kElemThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n,
+                                                                      w->partials, scb->l, w->u2, 2, w->st, 1);
+                RCG_LAUNCHED(ctx);
+            }
+            reduce(5, scb->k * RT, 2, 1, scb->l, scb->k, w->u2);
         }
+    }
+
+    // row slabs: the last reducing kernel wrote its local totals (BState::defer): sum them over the
+    // ranks and run its finaliser (k_b_fin); a no-op on one GPU, where the kernel finalised itself
+    void reduce(int which, int count, int arg, int guard, const double* L = nullptr, int mm = 0, double* u = nullptr) {
+        if (!job.comm) return;
+        job.comm->allreduce(ctx, count);
+        k_b_fin<RT><<<1, kElemThreads, 0, ctx->stream>>>(w->st, which, arg, guard, L, mm, u, w->hist, max_iter + 1);
+        RCG_LAUNCHED(ctx);
     }
 
     void launch_b_sweep(bool backward, SweepArgs& s) {
@@ -1568,7 +1692,7 @@ struct BatchSolve {
             }
             return;
         }
-        if (mode != 0) {
+        if (mode != 0 || job.comm) {  // (row slabs: rho always through k_b_rho's deferred finaliser)
             // chunk lanes: 16-byte chunks (measured faster than 32-byte), 4 parents per poll
             // chunk (register budget -> residency); 3x the single-sweep CTAs from RT = 12 on
             constexpr int rpw = 32 / (RT / 2);
@@ -1611,12 +1735,14 @@ struct BatchSolve {
             k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->aw, defl->ld, defl->k, w->x, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
+            reduce(5, defl->k * RT, 1, 0, defl->l, defl->k, w->u);
             k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
                                                                            w->st, 0);
             RCG_LAUNCHED(ctx);
             k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->b, n, w->partials,
                                                                   defl->l, w->u, 1, w->st, 0);
             RCG_LAUNCHED(ctx);
+            reduce(5, defl->k * RT, 1, 0, defl->l, defl->k, w->u);
             k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
                                                                            w->st, 1);
             RCG_LAUNCHED(ctx);
@@ -1770,6 +1896,41 @@ static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const
         }
     });
 }
+
+namespace rcg {
+
+// the batched solver over one row slab of a distributed system (dist.cu supplies the exchange
+// and the allreduce); B / X hold nrhs vectors of the slab's nloc rows, device or host
+void batch_solve_dist(rcg_ctx* ctx, const rcg_matrix* a, const rcg_prec* m, const rcg_basis* defl, BatchComm* comm,
+                      const double* B, double* X, const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps) {
+    require(ctx && a && reps && B && X && comm, "dist batch solve: null argument");
+    require(nrhs >= 1 && nrhs <= kRMax, "batch solve: nrhs must be in [1, 24]");
+    check_cfg(cfg);
+    check_prec(m, a->n);
+    const int32_t n = a->n;
+    Staged bs, xs;
+    stage_in(ctx, B, static_cast<int64_t>(n) * nrhs, bs);
+    stage_in(ctx, X, static_cast<int64_t>(n) * nrhs, xs);
+    Staged xo;
+    stage_out_begin(ctx, X, static_cast<int64_t>(n) * nrhs, xo);
+    if (xo.dev != xs.dev && nrhs > 0)
+        RCG_CK(cudaMemcpyAsync(xo.dev, xs.dev, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, ctx->stream));
+    BatchJob job{ctx, a, m, defl, n, nrhs, cfg->max_iter, cfg->eps, bs.dev, xo.dev, reps};
+    job.comm = comm;
+    run_phase(pick_rt(nrhs), job, 0, nullptr, 0, nullptr, 1);
+    stage_out_end(ctx, X, static_cast<int64_t>(n) * nrhs, xo);
+    RCG_CK(cudaStreamSynchronize(ctx->stream));
+    check_sweep_watchdog(ctx);
+    for (int k = 0; k < nrhs; ++k) reps[k].wall_time = job.wall / nrhs;
+    if (job.broken >= 0) {
+        const bool dfl = defl && defl->k > 0;
+        throw Error(RCG_E_BREAKDOWN, std::string(dfl ? "deflated pcg" : "pcg") + ": breakdown in right-hand side " +
+                                         std::to_string(job.broken) +
+                                         (job.broken_status == kBrkRz ? " ((r, z) <= 0)" : " ((p, A p) <= 0)"));
+    }
+}
+
+}  // namespace rcg
 
 extern "C" {
 

@@ -138,6 +138,8 @@ struct rcg_dslab {
     double* ubuf = nullptr;       // device: projection coefficients (m)
     double* u2buf = nullptr;      // device: subspace-correction coefficients (m)
     int64_t cap_g = 0;
+    double* sendbuf_rt = nullptr; // device: the batched solver's halo (nsend x RT interleaved)
+    int64_t cap_send_rt = 0;
 };
 
 // a row-partitioned basis: every slab holds its rows of W and AW, and the
@@ -281,6 +283,15 @@ __global__ void k_d_pack(const double* __restrict__ v, const int32_t* __restrict
     for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) out[t] = v[idx[t]];
 }
 
+// rt-interleaved rows (the batched solver's vectors): out[t rt + k] = v[idx[t] rt + k]
+__global__ void k_d_pack_rt(const double* __restrict__ v, const int32_t* __restrict__ idx, int32_t cnt, int rt,
+                            double* __restrict__ out) {
+    const int64_t total = static_cast<int64_t>(cnt) * rt;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[e] = v[static_cast<int64_t>(idx[e / rt]) * rt + e % rt];
+}
+
 // scalar updates from the global totals g (pcg.cpp:43-89): 0 initial (b,b),(r,r); 1 (r,z);
 // 2 (p,q); 3 (r,r) after the x/r update
 // flags: 1 = defer the initial check to the projected residual (deflation; stage 4), 2 = add
@@ -408,11 +419,27 @@ struct rcg_comm {
     virtual void allreduce(rcg_dslab* const* s, int ns, int count, int sel = 0) = 0;
     // halo of the ext vector `which` (0: x_ext, 1: p_ext)
     virtual void halo(rcg_dslab* const* s, int ns, int which) = 0;
+    // halo rows of an rt-interleaved vector of ONE local slab (the batched solver)
+    virtual void halo_rt(rcg_dslab* d, double* v, int rt) = 0;
 };
 
 namespace rcg {
 
 static double* ext_of(rcg_dslab* s, int which) { return which == 0 ? s->xe : s->pe; }
+
+// the rt-interleaved send rows of d (grows d->sendbuf_rt)
+static void pack_rt(rcg_dslab* d, const double* v, int rt) {
+    const int64_t need = static_cast<int64_t>(d->nsend) * rt;
+    if (need > d->cap_send_rt) {
+        dev_free(d->sendbuf_rt);
+        d->sendbuf_rt = dev_alloc(std::max<int64_t>(need, 1));
+        d->cap_send_rt = need;
+    }
+    if (d->nsend == 0) return;
+    const int g = std::max(1, static_cast<int>(std::min<int64_t>((need + 255) / 256, d->ctx->num_sms * 4)));
+    k_d_pack_rt<<<g, 256, 0, d->ctx->stream>>>(v, d->send_idx, d->nsend, rt, d->sendbuf_rt);
+    RCG_LAUNCHED(d->ctx);
+}
 
 static void pack(rcg_dslab* s, int which) {
     if (s->nsend == 0) return;
@@ -495,6 +522,22 @@ struct NcclComm : rcg_comm {
         }
         nc.check(nc.group_end(), "group end");
     }
+    void halo_rt(rcg_dslab* d, double* v, int rt) override {
+        pack_rt(d, v, rt);
+        Nccl& nc = Nccl::get();
+        nc.check(nc.group_start(), "group start");
+        for (int q = 0; q < nranks; ++q) {
+            if (d->send_count[q])
+                nc.check(nc.send(d->sendbuf_rt + static_cast<int64_t>(d->send_off[q]) * rt,
+                                 static_cast<size_t>(d->send_count[q]) * rt, ncclFloat64, q, comm, d->ctx->stream),
+                         "send");
+            if (d->recv_count[q])
+                nc.check(nc.recv(v + (static_cast<int64_t>(d->nloc) + d->recv_off[q]) * rt,
+                                 static_cast<size_t>(d->recv_count[q]) * rt, ncclFloat64, q, comm, d->ctx->stream),
+                         "recv");
+        }
+        nc.check(nc.group_end(), "group end");
+    }
 };
 
 // --- host-staged: a caller-supplied host transport (torch.distributed over gloo, MPI, ...).  Every
@@ -539,6 +582,29 @@ struct HostComm : rcg_comm {
             throw Error(RCG_E_CUDA, "host transport: halo exchange callback failed");
         if (d->nhalo > 0)
             RCG_CK(cudaMemcpyAsync(ext_of(d, which) + d->nloc, hrecv.data(), sizeof(double) * d->nhalo,
+                                   cudaMemcpyHostToDevice, d->ctx->stream));
+        RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+    }
+    void halo_rt(rcg_dslab* d, double* v, int rt) override {
+        pack_rt(d, v, rt);
+        const int64_t ns_ = static_cast<int64_t>(d->nsend) * rt, nr = static_cast<int64_t>(d->nhalo) * rt;
+        hsend.resize(std::max<int64_t>(ns_, 1));
+        hrecv.resize(std::max<int64_t>(nr, 1));
+        if (ns_ > 0)
+            RCG_CK(cudaMemcpyAsync(hsend.data(), d->sendbuf_rt, sizeof(double) * ns_, cudaMemcpyDeviceToHost,
+                                   d->ctx->stream));
+        RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+        so.resize(nranks), sc.resize(nranks), ro.resize(nranks), rc.resize(nranks);
+        for (int q = 0; q < nranks; ++q) {
+            so[q] = static_cast<int64_t>(d->send_off[q]) * rt;
+            sc[q] = static_cast<int64_t>(d->send_count[q]) * rt;
+            ro[q] = static_cast<int64_t>(d->recv_off[q]) * rt;
+            rc[q] = static_cast<int64_t>(d->recv_count[q]) * rt;
+        }
+        if (ex(user, hsend.data(), so.data(), sc.data(), hrecv.data(), ro.data(), rc.data(), nranks) != 0)
+            throw Error(RCG_E_CUDA, "host transport: halo exchange callback failed");
+        if (nr > 0)
+            RCG_CK(cudaMemcpyAsync(v + static_cast<int64_t>(d->nloc) * rt, hrecv.data(), sizeof(double) * nr,
                                    cudaMemcpyHostToDevice, d->ctx->stream));
         RCG_CK(cudaStreamSynchronize(d->ctx->stream));
     }
@@ -614,6 +680,11 @@ struct LoopComm : rcg_comm {
         for (int q = 0; q < ns; ++q)
             for (int b = 0; b < ns; ++b)
                 if (b != q && s[b]->recv_count[q]) RCG_CK(cudaStreamWaitEvent(s[q]->ctx->stream, ev_read[b], 0));
+    }
+    void halo_rt(rcg_dslab* d, double* v, int rt) override {
+        (void)v, (void)rt;
+        // batched slab solves run one slab per process; in loopback that is G = 1 (no halo rows)
+        require(np == 1 && d->nhalo == 0, "batched slab solves over the loopback transport need one slab (G = 1)");
     }
 };
 
@@ -1314,7 +1385,7 @@ void rcg_dslab_destroy(rcg_dslab* d) {
     cudaDeviceSynchronize();
     rcg_matrix_destroy(d->a);
     for (void* p : {(void*)d->send_idx, (void*)d->sendbuf, (void*)d->xe, (void*)d->pe, (void*)d->dsum, (void*)d->gbuf,
-                    (void*)d->ubuf, (void*)d->u2buf})
+                    (void*)d->ubuf, (void*)d->u2buf, (void*)d->sendbuf_rt})
         dev_free(p);
     delete d;
 }
@@ -1461,6 +1532,60 @@ static int dist_solve_impl(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, 
 int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
                    double* const* x, const rcg_solver_config* cfg, rcg_solve_report* report) {
     return dist_solve_impl(comm, nslabs, slabs, basis, nullptr, b, x, cfg, report);
+}
+
+// the batched solver over this process's slab: allreduces on the slab's gbuf, halo rows through
+// the transport (one slab per process)
+namespace rcg {
+struct DistBatchComm : BatchComm {
+    rcg_comm* comm = nullptr;
+    rcg_dslab* d = nullptr;
+    void allreduce(rcg_ctx* ctx, int count) override {
+        (void)ctx;
+        rcg_dslab* ds[1] = {d};
+        comm->allreduce(ds, 1, count, 1);
+    }
+    void halo(rcg_ctx* ctx, double* v, int rt) override {
+        (void)ctx;
+        comm->halo_rt(d, v, rt);
+    }
+};
+}  // namespace rcg
+
+int rcg_dist_solve_batch(rcg_comm* comm, rcg_dslab* slab, const rcg_dbasis* basis, const double* B, double* X,
+                         const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps) {
+    return guard([&] {
+        require(comm && slab && B && X && cfg && reps, "dist_solve_batch: null argument");
+        require(comm->local_slabs() == 1, "dist_solve_batch: one slab per process (loopback: G = 1)");
+        ensure_g(slab, 768);
+        DistBatchComm bc;
+        bc.comm = comm;
+        bc.d = slab;
+        bc.dtot = slab->gbuf;
+        bc.nhalo = slab->nhalo;
+        rcg_basis view{};
+        rcg_prec m{};
+        m.kind = slab->ic ? RCG_PREC_IC : RCG_PREC_IDENTITY;
+        m.ic = slab->ic;
+        const rcg_basis* defl = nullptr;
+        if (basis && basis->m > 0) {
+            view.n = slab->nloc;
+            view.k = basis->m;
+            view.ld = slab->nloc;
+            view.w = basis->w[0];
+            view.aw = basis->aw[0];
+            view.l = basis->l[0];
+            view.who = basis->kind == RCG_BASIS_SC ? 1 : 0;
+            if (basis->kind == RCG_BASIS_SC) {
+                require(slab->ic != nullptr, "dist_solve_batch: subspace correction needs the block IC(0)");
+                m.kind = RCG_PREC_SC;
+                m.sc = &view;
+            } else {
+                defl = &view;
+            }
+        }
+        batch_solve_dist(slab->ctx, slab->a, &m, defl, &bc, B, X, cfg, nrhs, reps);
+    });
 }
 
 int rcg_dist_pcg_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const double* const* b,

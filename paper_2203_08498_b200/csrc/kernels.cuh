@@ -37,6 +37,17 @@ struct SweepArgs {
     DevState* st;
 };
 
+// row-slab communication of the batched solver (batch.cu; implemented over rcg_comm in dist.cu)
+struct BatchComm {
+    virtual ~BatchComm() {}
+    virtual void allreduce(rcg_ctx* ctx, int count) = 0;     // dtot[0..count) summed over the ranks in place
+    virtual void halo(rcg_ctx* ctx, double* v, int rt) = 0;  // halo rows [nloc, nloc + nhalo) of an rt-interleaved v
+    double* dtot = nullptr;                                   // device, >= 768 doubles
+    int32_t nhalo = 0;
+};
+void batch_solve_dist(rcg_ctx* ctx, const rcg_matrix* a, const rcg_prec* m, const rcg_basis* defl, BatchComm* comm,
+                      const double* B, double* X, const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps);
+
 int spmv_grid(const rcg_ctx* ctx, int32_t n);
 int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos);
 void ensure_host_image(const rcg_ic* f);  // icfactor.cu

@@ -138,9 +138,10 @@ class NcclRank:
         return api.dist_solve(self.comm, [self.slab], [b_local], [x_local], basis, eps, max_iter)
 
     def sequence(self, bs_local, eps: float = 1e-8, max_iter: int = 1000, sampler_m: int = 16, keep: int = 8,
-                 kind: str = "deflation") -> dict:
+                 kind: str = "deflation", batch: bool = True) -> dict:
         """run_sequence over the ranks (collective): bs_local = this rank's rows of the scaled
-        right-hand sides; solutions are this rank's rows."""
+        right-hand sides; solutions are this rank's rows.  batch: solves 2..k through
+        rcg_dist_solve_batch (up to 24 per kernel sequence), else one at a time."""
         smp = api.SamplerState.method_a(self.ctx, sampler_m, max_iter, self.plan.nloc)
         x1 = np.zeros(self.plan.nloc)
         r1 = api.dist_pcg_solve_sampled(self.comm, [self.slab], [smp], [bs_local[0]], [x1], eps, max_iter)
@@ -148,7 +149,17 @@ class NcclRank:
                                                            kind=kind)
         out = {"iterations": [r1.iterations], "converged": [r1.converged], "solutions": [x1], "m_bar": m_bar,
                "ritz_values": vals, "m_tilde": m_tilde}
-        for b in bs_local[1:]:
+        rest = list(bs_local[1:])
+        if batch:
+            for k0 in range(0, len(rest), 24):
+                B = np.stack(rest[k0:k0 + 24])
+                X = np.zeros_like(B)
+                for r, x in zip(api.dist_solve_batch(self.comm, self.slab, B, X, basis, eps, max_iter), X):
+                    out["iterations"].append(r.iterations)
+                    out["converged"].append(r.converged)
+                    out["solutions"].append(x)
+            return out
+        for b in rest:
             x = np.zeros(self.plan.nloc)
             r = self.solve(b, x, eps, max_iter, basis)
             out["iterations"].append(r.iterations)

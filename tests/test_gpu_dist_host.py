@@ -64,7 +64,7 @@ def _worker(rank, world, port, name, out_dir):
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c4"])
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [1, 2, 3])
 def test_two_process_sequence_matches_block_jacobi(oracle, problems, tmp_path, name, world):
     import torch.multiprocessing as mp
 
