@@ -17,9 +17,11 @@ iterations per thread, the Rayleigh-Ritz step on real sampled errors, extrapolat
 oracle's full-run iteration mix (run_reference).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
-For N > 1 launch with torch.distributed.run; ranks run independent replicas of the workload
-(scaling "weak"); the row-slab partition (block-Jacobi IC(0), NCCL halo + allreduces) is measured
-on all N ranks as variants.row_slabs (one solve and one whole sequence).
+For N > 1 launch with torch.distributed.run: the SAME sequence over N row slabs, one per GPU
+(run_slabs: block-Jacobi IC(0) per slab, NCCL halo exchange + allreduces, the
+accelerated solves batched over the slabs; scaling "strong", the block-Jacobi iteration counts
+next to the single-GPU ones).  --replicas instead runs N independent single-GPU sequences
+(scaling "weak").
 """
 from __future__ import annotations
 
@@ -37,7 +39,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "PCG iters/s (fp64 sequence: ICCG solve 1 + RR + SC-ICCG solves)"
+METRIC = "PCG iters/s (fp64 sequence: ICCG solve 1 + RR + accelerated ICCG solves)"
 UNIT = "iters/s"
 
 
@@ -228,8 +230,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY.md 8(d); no network for SuiteSparse)",
-        "config": {**config_dict(cfg, n, n_nnz),
-                   **({"parallelism": f"replicas x{world}"} if world > 1 else {})},
+        "config": config_dict(cfg, n, n_nnz, world, replicas=True),
         "iterations_per_step": iters / args.steps / world,
         "time_to_solution_ms_per_rhs": round(ms / args.steps / cfg.n_rhs, 3),
         "driver": "rcg_seq_run (solve 1 with the device sampler, RR basis, solves 2..k batched)",
@@ -351,6 +352,95 @@ def kernel_report(stats, n, nnz, nnz_l, m, steps, peak, peak_src, levels=None, w
                                "note": "each level waits for its parents' publish -> observe hop; "
                                        "levels x hop floor bounds the sweep below the HBM roofline"}
     return kernels, roof
+
+
+def run_slabs(args, rank, world, local_rank):
+    """N > 1: the north star's multi-GPU path -- the SAME sequence (the config's matrix and
+    right-hand sides) over `world` row slabs at floor(b n / N), one per GPU: block-Jacobi IC(0) per
+    slab (ic0_factorize(a, 0, N), ic_preconditioner.cpp:97-121), NCCL halo exchange + allreduces,
+    solve 1 with the error sampler (rcg_dist_pcg_solve_sampled), the distributed recycling step
+    (rcg_dist_recycle) and the accelerated solves batched over the slabs (rcg_dist_solve_batch).
+    Strong scaling (total work fixed); the block-Jacobi iteration counts are reported next to the
+    single-GPU sequence's (rank 0 runs rcg_seq_run once, untimed)."""
+    import torch
+
+    from paper_2203_08498_b200 import api, dist, problems, sequence
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = api.Context(local_rank)
+    cfg = problems.CONFIGS[args.config]
+    host = problems.generate(cfg)
+    prep = sequence.prepare(ctx, cfg, host, validate=False)
+    pairs = sequence.rhs_all(prep)
+    kind = "sc" if cfg.method == "sc" else "deflation"
+    single = None
+    if rank == 0:  # the single-GPU sequence's iteration counts (the global IC(0)), untimed
+        seq1 = api.Sequence(ctx, prep.a_orig, "es-sc-iccg" if cfg.method == "sc" else "es-d-iccg", cfg.blocks)
+        B = np.stack([b for b, _ in pairs])
+        r1 = seq1.run(B, np.zeros_like(B), cfg.eps, cfg.max_iter, "A", cfg.sampler_m, keep_count=cfg.keep, batch=True)
+        single = [int(v) for v in r1["iterations"]]
+        del seq1, B
+    scaled = problems.HostCsr(host.n, host.row_start, host.col_idx, prep.a.values())
+    rk = dist.NcclRank(scaled, ctx=ctx, transport=args.slab_transport)
+    lo, hi = rk.plan.row_begin, rk.plan.row_end
+    n_glob, nnz_glob = host.n, host.nnz
+    del prep, host, scaled
+    bl_host = [np.ascontiguousarray(bs[lo:hi]) for _, bs in pairs]
+    bl_dev = [torch.from_numpy(v).to(dev) for v in bl_host]
+    last = {}
+
+    def step(bl):
+        out = rk.sequence(bl, cfg.eps, cfg.max_iter, cfg.sampler_m, cfg.keep, kind)
+        last.update(out)
+        return int(sum(out["iterations"]))
+
+    for _ in range(args.warmup):
+        step(bl_dev)
+    torch.distributed.barrier()
+    ctx.synchronize()
+    launches0 = ctx.launches
+    iters = 0
+    with Clocks(local_rank) as clk:
+        ctx.record(0)
+        for _ in range(args.steps):
+            iters += step(bl_dev)
+        ctx.record(1)
+        ms = ctx.elapsed_ms(0, 1)
+    launches = ctx.launches - launches0
+    torch.distributed.barrier()
+    ctx.record(2)
+    e2e_iters = 0
+    for _ in range(args.steps):
+        e2e_iters += step(bl_host)  # host right-hand sides and solutions: H2D / D2H inside the calls
+    ctx.record(3)
+    e2e_ms = ctx.elapsed_ms(2, 3)
+    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev if args.slab_transport == "nccl" else "cpu")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms, e2e_ms = t.tolist()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(iters / (ms / 1e3), 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md 8(d); no network for SuiteSparse)",
+        "config": config_dict(cfg, n_glob, nnz_glob, world),
+        "iterations_per_step": iters / args.steps,
+        "iterations_block_jacobi": [int(v) for v in last["iterations"]],
+        "iterations_single_gpu": single,
+        "m_bar": int(last["m_bar"]), "m_tilde": int(last["m_tilde"]),
+        "time_to_solution_ms_per_rhs": round(ms / args.steps / cfg.n_rhs, 3),
+        "driver": "rcg_dist_pcg_solve_sampled + rcg_dist_recycle + rcg_dist_solve_batch over "
+                  + ("NCCL" if args.slab_transport == "nccl" else "the host-staged gloo transport (test)")
+                  + " (dist.NcclRank)",
+        "e2e": {"value": round(e2e_iters / (e2e_ms / 1e3), 2), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * (hi - lo) * cfg.n_rhs, "d2h_bytes_per_step": 8 * (hi - lo) * cfg.n_rhs,
+                "note": "per rank (rank 0's slab); every rank moves its own rows"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
 
 
 def measure_row_slabs(api, prep, host, b_scaled, cfg, rank, world, dev, seq_rhs):
@@ -708,7 +798,7 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY.md 8(d); no network for SuiteSparse)",
-        "config": config_dict(cfg, st.n, st.nnz),
+        "config": config_dict(cfg, st.n, st.nnz, world, replicas=args.replicas),
         "time_to_solution_ms_per_rhs": round(t_seq / cfg.n_rhs * 1e3, 3),
         "time_to_solution_ms_per_rhs_throughput": round(t_seq / cfg.n_rhs / threads * 1e3, 3),
         "sequence_model": {"t_iccg_ms": round(t_iccg * 1e3, 3), "t_accelerated_ms": round(t_acc * 1e3, 3),
@@ -724,12 +814,15 @@ def run_reference(args, rank, world):
     }), flush=True)
 
 
-def config_dict(cfg, n, nnz):
-    """The workload's `config` -- identical in both arms (same_config)."""
+def config_dict(cfg, n, nnz, world=1, replicas=False):
+    """The workload's `config` -- identical in both arms for the same N (same_config); N > 1 is the
+    row-slab split of the same sequence (or N replicas with --replicas)."""
+    par = "1 GPU" if world == 1 else (f"replicas x{world}" if replicas else
+                                        f"row slabs x{world} (block-Jacobi IC(0), NCCL halo + allreduce)")
     return {"workload": cfg.name, "n": n, "nnz": nnz, "n_rhs": cfg.n_rhs, "samples": cfg.sampler_m,
             "m_tilde": cfg.keep, "method": cfg.method, "eps": cfg.eps, "rhs": cfg.rhs,
             "l2": "inputs larger than L2 (126 MB): A, the IC(0) factor and W / AW stream from HBM every iteration",
-            "parallelism": "1 GPU"}
+            "parallelism": par}
 
 
 def main():
@@ -744,6 +837,10 @@ def main():
                     help="also measure the multicolour operator and the row-slab path on this config")
     ap.add_argument("--no-variants", action="store_true", help=argparse.SUPPRESS)  # the default now
     ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--slab-transport", choices=["nccl", "host"], default="nccl",
+                    help=argparse.SUPPRESS)  # test only: the host-staged transport over gloo (ranks may share a GPU)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent single-GPU sequences (weak scaling) instead of row slabs")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -754,10 +851,14 @@ def main():
     if world > 1:
         import torch
 
+        local_rank %= max(1, torch.cuda.device_count())  # test runs may put several ranks on one GPU
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        torch.distributed.init_process_group("gloo" if args.slab_transport == "host" else "nccl")
     try:
-        run_ours(args, rank, world, local_rank)
+        if world > 1 and not args.replicas:
+            run_slabs(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch

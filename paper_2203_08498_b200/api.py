@@ -822,7 +822,12 @@ def dist_solve_batch(comm: Comm, slab, B, X, basis: Optional[DBasis] = None, eps
     sequence (the batched solver with allreduced reductions and RT-interleaved halo exchanges).
     B, X: (R, nloc) this slab's rows; returns one SolveReport per right-hand side."""
     nloc = slab.plan.nloc
-    Bm = np.ascontiguousarray(np.stack(list(B)) if isinstance(B, list) else B, dtype=np.float64)
+    if hasattr(B, "data_ptr") or (isinstance(B, list) and hasattr(B[0], "data_ptr")):  # CUDA tensors
+        import torch
+
+        Bm = (torch.stack(list(B)) if isinstance(B, list) else B).contiguous()
+    else:
+        Bm = np.ascontiguousarray(np.stack(list(B)) if isinstance(B, list) else B, dtype=np.float64)
     R = Bm.shape[0]
     if not (1 <= R <= 24) or Bm.shape[-1] != nloc:
         raise InvalidArgument("dist_solve_batch: B must be (R <= 24, nloc)")

@@ -142,8 +142,15 @@ class NcclRank:
         """run_sequence over the ranks (collective): bs_local = this rank's rows of the scaled
         right-hand sides; solutions are this rank's rows.  batch: solves 2..k through
         rcg_dist_solve_batch (up to 24 per kernel sequence), else one at a time."""
+        def zeros(like, shape):  # numpy host or CUDA torch, like the right-hand sides
+            if hasattr(like, "data_ptr"):
+                import torch
+
+                return torch.zeros(shape, dtype=torch.float64, device=like.device)
+            return np.zeros(shape)
+
         smp = api.SamplerState.method_a(self.ctx, sampler_m, max_iter, self.plan.nloc)
-        x1 = np.zeros(self.plan.nloc)
+        x1 = zeros(bs_local[0], self.plan.nloc)
         r1 = api.dist_pcg_solve_sampled(self.comm, [self.slab], [smp], [bs_local[0]], [x1], eps, max_iter)
         m_bar, vals, _, m_tilde, basis = api.dist_recycle(self.comm, [self.slab], [smp], [x1], keep_count=keep,
                                                            kind=kind)
@@ -152,15 +159,21 @@ class NcclRank:
         rest = list(bs_local[1:])
         if batch:
             for k0 in range(0, len(rest), 24):
-                B = np.stack(rest[k0:k0 + 24])
-                X = np.zeros_like(B)
+                chunk = rest[k0:k0 + 24]
+                if hasattr(chunk[0], "data_ptr"):
+                    import torch
+
+                    B = torch.stack(chunk)
+                else:
+                    B = np.stack(chunk)
+                X = zeros(chunk[0], tuple(B.shape))
                 for r, x in zip(api.dist_solve_batch(self.comm, self.slab, B, X, basis, eps, max_iter), X):
                     out["iterations"].append(r.iterations)
                     out["converged"].append(r.converged)
                     out["solutions"].append(x)
             return out
         for b in rest:
-            x = np.zeros(self.plan.nloc)
+            x = zeros(b, self.plan.nloc)
             r = self.solve(b, x, eps, max_iter, basis)
             out["iterations"].append(r.iterations)
             out["converged"].append(r.converged)

@@ -64,3 +64,34 @@ def test_bench_line_contract_on_gpu():
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1 and r["peak"] > 0 and r["achieved"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 1
     assert d["config"]["workload"] == "c3_q1_27pt_256" and "time_to_solution_ms_per_rhs" in d
+
+
+@pytest.mark.gpu
+def test_bench_row_slabs_two_ranks():
+    """bench.py --gpus 2 (the N > 1 headline: the sequence over two row slabs, run_slabs) under
+    torch.distributed.run, both ranks on the one GPU over the host-staged transport (gloo; NCCL
+    refuses two ranks per GPU): one JSON line, strong scaling, and block-Jacobi iteration counts
+    within +-2 of the oracle's ic0_factorize(a, 0, 2) sequence on C1."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--config", "c1", "--slab-transport", "host", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"].startswith("row slabs x2")
+    from oracle import Oracle
+    from oracle.sequence import run_sequence
+    from paper_2203_08498_b200 import problems
+
+    ref = run_sequence(Oracle(), problems.CONFIGS["c1"], problems.generate(problems.CONFIGS["c1"]), blocks=2)
+    assert len(d["iterations_block_jacobi"]) == len(ref["iterations"])
+    assert all(abs(a - b) <= 2 for a, b in zip(d["iterations_block_jacobi"], ref["iterations"])), (
+        d["iterations_block_jacobi"], ref["iterations"])
+    assert d["iterations_single_gpu"] and len(d["iterations_single_gpu"]) == len(ref["iterations"])
