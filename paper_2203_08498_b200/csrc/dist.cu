@@ -425,6 +425,14 @@ struct rcg_comm {
 
 namespace rcg {
 
+// host -> device into a slab buffer, ordered on the slab's (non-blocking) stream and complete on
+// return: a legacy cudaMemcpy from pageable memory may return before its DMA lands and is not
+// ordered with the slab stream's next copy / kernel (the host transport read stale Gram values)
+static void h2d_sync(rcg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    RCG_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    RCG_CK(cudaStreamSynchronize(ctx->stream));
+}
+
 static double* ext_of(rcg_dslab* s, int which) { return which == 0 ? s->xe : s->pe; }
 
 // the rt-interleaved send rows of d (grows d->sendbuf_rt)
@@ -553,15 +561,31 @@ struct HostComm : rcg_comm {
     std::vector<int64_t> so, sc, ro, rc;
     int nparts() const override { return nranks; }
     int local_slabs() const override { return 1; }
+    double* pin = nullptr;  // pinned staging of the allreduced values
+    int cap_pin = 0;
+    ~HostComm() override {
+        if (pin) cudaFreeHost(pin);
+    }
     void allreduce(rcg_dslab* const* s, int ns, int count, int sel) override {
         (void)ns;
         rcg_dslab* d = s[0];
         double* buf = sel ? d->gbuf : d->dsum;
+        if (count > cap_pin) {
+            if (pin) cudaFreeHost(pin);
+            RCG_CK(cudaMallocHost(&pin, sizeof(double) * std::max(count, 1)));
+            cap_pin = count;
+        }
         hbuf.resize(std::max(count, 1));
-        RCG_CK(cudaMemcpyAsync(hbuf.data(), buf, sizeof(double) * count, cudaMemcpyDeviceToHost, d->ctx->stream));
         RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+        RCG_CK(cudaMemcpyAsync(pin, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, d->ctx->stream));
+        RCG_CK(cudaStreamSynchronize(d->ctx->stream));
+        std::memcpy(hbuf.data(), pin, sizeof(double) * count);
+        static const bool dbg = std::getenv("RCG_HOSTCOMM_DEBUG") != nullptr;  // dev
+        if (dbg) std::fprintf(stderr, "[hostcomm r%d] allreduce sel %d count %d in %.6g", rank, sel, count, hbuf[0]);
         if (ar(user, hbuf.data(), count) != 0) throw Error(RCG_E_CUDA, "host transport: allreduce callback failed");
-        RCG_CK(cudaMemcpyAsync(buf, hbuf.data(), sizeof(double) * count, cudaMemcpyHostToDevice, d->ctx->stream));
+        if (dbg) std::fprintf(stderr, " out %.6g\n", hbuf[0]);
+        std::memcpy(pin, hbuf.data(), sizeof(double) * count);
+        RCG_CK(cudaMemcpyAsync(buf, pin, sizeof(double) * count, cudaMemcpyHostToDevice, d->ctx->stream));
         RCG_CK(cudaStreamSynchronize(d->ctx->stream));
     }
     void halo(rcg_dslab* const* s, int ns, int which) override {
@@ -638,11 +662,13 @@ struct LoopComm : rcg_comm {
             g[b] = s[b]->gbuf;
         }
         if (d != hd) {
-            RCG_CK(cudaMemcpy(dptrs, d.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice));
+            RCG_CK(cudaMemcpyAsync(dptrs, d.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice, cs));
+            RCG_CK(cudaStreamSynchronize(cs));
             hd = d;
         }
         if (g != hg) {
-            RCG_CK(cudaMemcpy(gptrs, g.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice));
+            RCG_CK(cudaMemcpyAsync(gptrs, g.data(), sizeof(double*) * ns, cudaMemcpyHostToDevice, cs));
+            RCG_CK(cudaStreamSynchronize(cs));
             hg = g;
         }
     }
@@ -1056,7 +1082,7 @@ static rcg_dbasis* dbasis_create(rcg_comm* comm, int ns, rcg_dslab* const* sl, c
         for (int s = 0; s < ns; ++s) {
             rcg_dslab* d = sl[s];
             gram_host(d->ctx, B->w[s], d->nloc, m, B->aw[s], d->nloc, m, d->nloc, true, g);
-            RCG_CK(cudaMemcpy(d->gbuf, g.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice));
+            h2d_sync(d->ctx, d->gbuf, g.data(), sizeof(double) * m * m);
         }
         comm->allreduce(sl, ns, m * m, 1);
         for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
@@ -1067,7 +1093,7 @@ static rcg_dbasis* dbasis_create(rcg_comm* comm, int ns, rcg_dslab* const* sl, c
         int bad = -1;
         if (!chol_factor_host(m, g, B->h_l, &bad)) throw Error(RCG_E_BREAKDOWN, "distributed basis: W^T A W not SPD");
         for (int s = 0; s < ns; ++s)
-            RCG_CK(cudaMemcpy(B->l[s], B->h_l.data(), sizeof(double) * m * m, cudaMemcpyHostToDevice));
+            h2d_sync(sl[s]->ctx, B->l[s], B->h_l.data(), sizeof(double) * m * m);
     } catch (...) {
         for (auto p : B->w) dev_free(p);
         for (auto p : B->aw) dev_free(p);
@@ -1174,7 +1200,7 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
                 RCG_CK(cudaMemcpyAsync(hz.data(), L[s].nz, sizeof(int) * k0, cudaMemcpyDeviceToHost, sl[s]->ctx->stream));
                 RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
                 std::vector<double> hd(hz.begin(), hz.end());
-                RCG_CK(cudaMemcpy(sl[s]->gbuf, hd.data(), sizeof(double) * k0, cudaMemcpyHostToDevice));
+                h2d_sync(sl[s]->ctx, sl[s]->gbuf, hd.data(), sizeof(double) * k0);
             }
             comm->allreduce(sl, ns, k0, 1);
             for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
@@ -1272,7 +1298,7 @@ static rcg_dbasis* dist_recycle(rcg_comm* comm, int ns, rcg_dslab* const* sl, rc
                 g = sloc[s];
             else
                 gram_host(d->ctx, L[s].q, d->nloc, kept, L[s].aq, d->nloc, kept, d->nloc, true, g);
-            RCG_CK(cudaMemcpy(d->gbuf, g.data(), sizeof(double) * kept * kept, cudaMemcpyHostToDevice));
+            h2d_sync(d->ctx, d->gbuf, g.data(), sizeof(double) * kept * kept);
         }
         comm->allreduce(sl, ns, kept * kept, 1);
         for (int s = 0; s < ns; ++s) RCG_CK(cudaStreamSynchronize(sl[s]->ctx->stream));
@@ -1363,7 +1389,7 @@ int rcg_dslab_create(rcg_ctx* ctx, const rcg_slab_plan* p, const rcg_ic* ic, rcg
             d->nsend = p->nparts > 0 ? d->send_off[p->nparts - 1] + d->send_count[p->nparts - 1] : 0;
             d->send_idx = static_cast<int32_t*>(dev_alloc_bytes(sizeof(int32_t) * std::max(d->nsend, 1)));
             if (d->nsend)
-                RCG_CK(cudaMemcpy(d->send_idx, p->send_idx, sizeof(int32_t) * d->nsend, cudaMemcpyHostToDevice));
+                h2d_sync(d->ctx, d->send_idx, p->send_idx, sizeof(int32_t) * d->nsend);
             d->sendbuf = dev_alloc(std::max(d->nsend, 1));
             d->xe = dev_alloc(static_cast<int64_t>(d->nloc) + d->nhalo);
             d->pe = dev_alloc(static_cast<int64_t>(d->nloc) + d->nhalo);

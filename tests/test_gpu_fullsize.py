@@ -62,3 +62,32 @@ def test_full_size_c5_iccg_solve(ctx, oracle, problems):
         floor = json.load(open(gp)).get("solve1_floor", {}).get("rel_solution", 0.0) if os.path.exists(gp) else 0.0
         rel = float(np.linalg.norm(xg - xo) / np.linalg.norm(xo))
         assert rel <= max(1e-8, 10.0 * floor), (rel, floor)
+
+
+@pytest.mark.parametrize("name", ["c5", "c3"])
+def test_full_size_rr_on_shared_errors(ctx, oracle, problems, parity_log, name):
+    """The Rayleigh-Ritz step at full size on SHARED inputs: the errors the GPU
+    sampled in solve 1 (C3: 64 x 16.8M, C5: 48 x 4M), run through the GPU's build_aux_matrix and
+    the oracle's (MGS -> A Q -> Q^T A Q -> Jacobi, recycling.cpp:81-96) -- m_bar equal and every
+    Ritz value within 1e-6.  (With each side's own samples the Ritz values also carry solve 1's
+    rounding, which the reference itself shows: tests/test_gpu_golden.py.)"""
+    from paper_2203_08498_b200 import api
+
+    cfg = problems.CONFIGS[name]
+    h, a_o, sa = _scaled_pair(ctx, oracle, problems, name)
+    f = api.IcFactor.factorize_device(ctx, sa)
+    _, dis = oracle.diagonal_scale(Matrix.of(h))
+    b = dis * oracle.spmv(Matrix.of(h), problems.normal(cfg.rhs_seed, 0, h.n))
+    s = api.SamplerState.method_a(ctx, cfg.sampler_m, cfg.max_iter, h.n)
+    x = np.zeros(h.n)
+    api.pcg_solve(ctx, sa, b, api.Ic(f), x, cfg.eps, cfg.max_iter, observer=s)
+    e_dev = api.harvest_errors(ctx, x, s)
+    errors = e_dev.columns()
+    gmb, gvals, _, _ = api.build_aux_matrix(ctx, sa, e_dev, float("inf"))
+    del e_dev
+    mb, vals, _ = oracle.build_aux(a_o, errors, float("inf"))
+    vals = np.asarray(vals)[:mb]
+    rel = float(np.max(np.abs(np.asarray(gvals)[:mb] - vals) / np.abs(vals)))
+    parity_log(f"fullsize_rr_shared:{name}", m_bar=(gmb, mb), check="ritz_rel", achieved=rel, bar=1e-6)
+    assert gmb == mb
+    assert rel <= 1e-6, rel
