@@ -225,17 +225,23 @@ constexpr int bspmv_min_blocks(int rt) { return rt >= 8 ? RCG_BSPMV_WIDE_BLOCKS 
 template <int RT, class Body>
 __device__ __forceinline__ void bspmv_chunks(const SpmvArgs& a, const double* __restrict__ x, int cap, Body&& body) {
     constexpr int G = RT / 4;
+    // lane -> (row, chunk) with a FIXED chunk per lane (c = lane % G): 32 / G rows per pass, the
+    // lanes beyond (32 / G) G idle (2 of 32 at G = 3 and 6) -- so a thread's per-rhs sums need
+    // only its own chunk's 4 accumulators, not all RT (RT 24 spilled with RT accumulators)
+    constexpr int RPP = 32 / G;                   // rows per pass
+    constexpr int NPASS = (32 + RPP - 1) / RPP;   // passes per 32-row tile
     const int lane = threadIdx.x & 31;
     csr_tiles(a.rs, a.ci, a.va, a.n, cap,
               [&](int32_t r0, int32_t my_b, int32_t my_e, const double* vsrc, const int32_t* csrc, int32_t off) {
 #pragma unroll 1
-                  for (int pass = 0; pass < G; ++pass) {
-                      const int item = pass * 32 + lane;
-                      const int32_t row = r0 + item / G;
-                      const int c = item % G;
-                      const int32_t b = __shfl_sync(0xffffffffu, my_b, item / G);
-                      const int32_t e = __shfl_sync(0xffffffffu, my_e, item / G);
-                      if (row < a.n) {
+                  for (int pass = 0; pass < NPASS; ++pass) {
+                      const int rit = pass * RPP + lane / G;  // row within the tile
+                      const bool lane_on = lane < RPP * G && rit < 32;
+                      const int32_t row = r0 + rit;
+                      const int c = lane % G;
+                      const int32_t b = __shfl_sync(0xffffffffu, my_b, rit & 31);
+                      const int32_t e = __shfl_sync(0xffffffffu, my_e, rit & 31);
+                      if (lane_on && row < a.n) {
                           double acc[4] = {0.0, 0.0, 0.0, 0.0};
                           if constexpr (RT <= 4) {
                               // one chunk per row: gathers issued kBGather entries at a time
@@ -409,6 +415,7 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_residu
 #pragma unroll
     for (int v = 0; v < RT; ++v) bb[v] = rr[v] = 0.0;
     if constexpr (RT % 4 == 0) {
+        double bb4[4] = {0.0, 0.0, 0.0, 0.0}, rr4[4] = {0.0, 0.0, 0.0, 0.0};  // this lane's chunk
         bspmv_chunks<RT>(a, x, cap, [&](int32_t row, int c, const double (&acc)[4]) {
             const int64_t o = static_cast<int64_t>(row) * RT + 4 * c;
             double bi[4], ri[4];
@@ -418,9 +425,15 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_residu
                 ri[i] = __dsub_rn(bi[i], acc[i]);
                 r[o + i] = ri[i];
             }
-            chunk_acc<RT>(bb, c, [&](double s, int i) { return fadd_mul(s, bi[i], bi[i]); });
-            chunk_acc<RT>(rr, c, [&](double s, int i) { return fadd_mul(s, ri[i], ri[i]); });
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                bb4[i] = fadd_mul(bb4[i], bi[i], bi[i]);
+                rr4[i] = fadd_mul(rr4[i], ri[i], ri[i]);
+            }
         });
+        const int c = (threadIdx.x & 31) % (RT / 4);
+        chunk_acc<RT>(bb, c, [&](double s, int i) { return __dadd_rn(s, bb4[i]); });
+        chunk_acc<RT>(rr, c, [&](double s, int i) { return __dadd_rn(s, rr4[i]); });
     } else {
         bspmv_rows<RT>(a, x, cap, [&](int32_t row, const double (&acc)[RT]) {
 #pragma unroll
@@ -963,6 +976,7 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
 #pragma unroll
     for (int v = 0; v < RT; ++v) pq[v] = 0.0;
     if constexpr (RT % 4 == 0) {
+        double pq4[4] = {0.0, 0.0, 0.0, 0.0};  // this lane's fixed chunk (bspmv_chunks)
         bspmv_chunks<RT>(a, p, cap, [&](int32_t row, int c, const double (&acc)[4]) {
             const int64_t o = static_cast<int64_t>(row) * RT + 4 * c;
             double pi[4];
@@ -971,8 +985,10 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
                 q[o + i] = acc[i];
                 pi[i] = p[o + i];
             }
-            chunk_acc<RT>(pq, c, [&](double s, int i) { return fadd_mul(s, pi[i], acc[i]); });
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pq4[i] = fadd_mul(pq4[i], pi[i], acc[i]);
         });
+        chunk_acc<RT>(pq, (threadIdx.x & 31) % (RT / 4), [&](double s, int i) { return __dadd_rn(s, pq4[i]); });
     } else {
         bspmv_rows<RT>(a, p, cap, [&](int32_t row, const double (&acc)[RT]) {
 #pragma unroll
@@ -1695,19 +1711,34 @@ struct BatchSolve {
         if (mode != 0 || job.comm) {  // (row slabs: rho always through k_b_rho's deferred finaliser)
             // chunk lanes: 16-byte chunks (measured faster than 32-byte), 4 parents per poll
             // chunk (register budget -> residency); 3x the single-sweep CTAs from RT = 12 on
-            constexpr int rpw = 32 / (RT / 2);
             // (re-measured end of round 1, C2 fwd / bwd: RT 12 x1 992/1298, x2 632/788, x3 578/657,
             // x4 620/681 us; RT 4 x2 497/535, x3 506/559 us.  32-byte chunks (VW 4, half the
             // polling lanes) again slower: RT 12 700/828, RT 8 660/739, RT 16 668/744 us)
+            // RT 24 with 16-byte chunks leaves 8 of 32 lanes idle (2 rows x 12 lanes per warp) and
+            // writes 2.5x the rho tile partials; RCG_BSWEEP_VW=4 selects 32-byte chunks there (5 rows
+            // x 6 lanes) -- A/B switch
+            static const int vw_env = std::getenv("RCG_BSWEEP_VW") ? std::atoi(std::getenv("RCG_BSWEEP_VW")) : 0;
+            const bool vw4 = RT == 24 && vw_env == 4;
+            const int rpw = vw4 ? 32 / (RT / 4) : 32 / (RT / 2);
             const int cmul = RT >= 12 ? 3 : 2;
             const int ntiles = (s.npos + rpw * 4 - 1) / (rpw * 4);  // CTAs of 4 warp tiles
             const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps0 * cmul));
             const bool rho = backward && s.r;
             if (rho) s.partials = w->tpart;
-            if (backward)
-                k_b_sweepc<true, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
-            else
-                k_b_sweepc<false, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+            if constexpr (RT == 24) {
+                if (vw4) {
+                    if (backward)
+                        k_b_sweepc<true, RT, 4, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+                    else
+                        k_b_sweepc<false, RT, 4, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+                }
+            }
+            if (!vw4) {
+                if (backward)
+                    k_b_sweepc<true, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+                else
+                    k_b_sweepc<false, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+            }
             RCG_LAUNCHED(ctx);
             if (rho) {
                 const int64_t tiles = (s.npos + rpw - 1) / rpw;
