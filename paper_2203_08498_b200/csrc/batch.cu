@@ -1895,6 +1895,7 @@ using namespace rcg;
 
 static int batch_entry(rcg_ctx* ctx, const rcg_matrix* a, const double* B, const rcg_prec* m, const rcg_basis* defl,
                        double* X, const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps) {
+    NvtxRange range("batched solves");
     return guard([&] {
         require(ctx && a && reps && B && X, "batch solve: null argument");
         require(nrhs >= 1 && nrhs <= kRMax, "batch solve: nrhs must be in [1, 24]");

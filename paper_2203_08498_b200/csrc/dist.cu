@@ -1580,6 +1580,7 @@ struct DistBatchComm : BatchComm {
 
 int rcg_dist_solve_batch(rcg_comm* comm, rcg_dslab* slab, const rcg_dbasis* basis, const double* B, double* X,
                          const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps) {
+    NvtxRange range("rcg_dist_solve_batch");
     return guard([&] {
         require(comm && slab && B && X && cfg && reps, "dist_solve_batch: null argument");
         require(comm->local_slabs() == 1, "dist_solve_batch: one slab per process (loopback: G = 1)");

@@ -19,6 +19,8 @@
 #include "rcg_b200.h"
 #include "host_error.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx (no-ops otherwise)
+
 namespace rcg {
 
 // ------------------------------------------------------------------ errors (host_error.h)
@@ -34,6 +36,15 @@ namespace rcg {
         if (e__ != cudaSuccess) ::rcg::throw_cuda(e__, "launch", __FILE__, __LINE__); \
         (ctx)->launches++;                                                         \
     } while (0)
+
+// NVTX range over a scope (the hot-path phases: K1-K16 of SURVEY 8(a) as the C-ABI entry points,
+// the sequence's solve 1 / recycling / accelerated phases)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // a C-ABI status from a nested entry point, rethrown with its message
 inline void ck(int rc) {

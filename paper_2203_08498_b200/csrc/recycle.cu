@@ -811,6 +811,7 @@ int rcg_rayleigh_ritz(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* e, doub
 
 int rcg_build_aux_matrix(rcg_ctx* ctx, const rcg_matrix* a, const rcg_tall* errors, double theta, int keep_count,
                          int* m_bar, double* values, double* theta_used, rcg_tall** w) {
+    NvtxRange range("rcg_build_aux_matrix");
     return guard([&] {
         *w = nullptr;
         *m_bar = 0;

@@ -102,6 +102,7 @@ void rcg_seq_destroy(rcg_seq* s) {
 }
 
 int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq_config* cfg, rcg_seq_report* rep) {
+    NvtxRange range("rcg_seq_run");
     return guard([&] {
         require(s && rhs && x && cfg && rep, "rcg_seq_run: null argument");
         if (k_t < 1) throw Error(RCG_E_PARSE, "config: k_t must be >= 1");
@@ -182,6 +183,7 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
             }
             ck(rcg_pcg_solve(ctx, s->a, bs, &inner, xs, &scfg, smp, RCG_PAYLOAD_X, &reps[0]));
             // the auxiliary basis (driver.cpp:163-184)
+            nvtxRangePushA("recycling + basis");
             rep->m_bar = rep->m_tilde = 0;
             rep->theta_used = cfg->theta;
             rep->w_build_time = 0.0;
@@ -244,6 +246,8 @@ int rcg_seq_run(rcg_seq* s, int k_t, const double* rhs, double* x, const rcg_seq
                 k_scale_rows<<<g, kStreamThreads, 0, ctx->stream>>>(s->dis, bst.dev + n, bs + n, n, total - n);
                 RCG_LAUNCHED(ctx);
             }
+            nvtxRangePop();
+            NvtxRange acc("accelerated solves");
             for (int k = 1; k < k_t;) {
                 const int cnt = batch ? std::min(max_cnt, k_t - k) : 1;
                 double* B = bs + static_cast<int64_t>(k) * n;

@@ -815,11 +815,13 @@ extern "C" {
 
 int rcg_pcg_solve(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const rcg_prec* m, double* x,
                   const rcg_solver_config* cfg, rcg_sampler* observer, int payload, rcg_solve_report* rep) {
+    NvtxRange r(observer ? "rcg_pcg_solve (sampled)" : "rcg_pcg_solve");
     return solve_common(ctx, a, b, m, nullptr, x, cfg, observer, payload, rep, false, 0, 0, nullptr, 0);
 }
 
 int rcg_deflated_pcg_solve(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const rcg_prec* m,
                            const rcg_basis* defl, double* x, const rcg_solver_config* cfg, rcg_solve_report* rep) {
+    NvtxRange r("rcg_deflated_pcg_solve");
     return solve_common(ctx, a, b, m, defl, x, cfg, nullptr, 0, rep, false, 0, 0, nullptr, 1);
 }
 
