@@ -1094,11 +1094,14 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
 // (mode 1) and f.u (mode 2).  Host grid: X x P (BatchSolve::tgrid).
 template <int RT>
 __device__ __host__ constexpr int tallt_jc() {
-    return RT <= 8 ? 4 : 2;   // RT 4 with 8 columns spilled (R 4 slower than R 8)
+    // columns per pass: y is re-read from L2 once per pass (m / JC passes), so wide passes matter
+    // at large RT (C3, RT 24, m 32: JC 2 -> 16 passes, 6.5 ms; the shared-memory block sum below
+    // keeps JC 6 within the register budget); RT 4 with 8 columns spilled
+    return RT <= 8 ? 4 : 6;
 }
 
 template <int RT>
-__global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
+__global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 3) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
                                                             const double* __restrict__ y, int32_t n,
                                                             double* partials, const double* __restrict__ L,
                                                             double* __restrict__ u, int mode, BState* st,
@@ -1106,11 +1109,10 @@ __global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const
     constexpr int JC = tallt_jc<RT>();
     constexpr int VW = RT % 4 == 0 ? 4 : 2;  // values per thread: G = RT/VW threads per row
     constexpr int G = RT / VW;
-    __shared__ double scratch[RT >= 12 ? 32 * JC * RT : kElemThreads * JC * (RT % 4 == 0 ? 4 : 2)];
-    __shared__ double bvals[JC * RT];
+    __shared__ double scratch[kElemThreads * JC * (RT % 4 == 0 ? 4 : 2)];  // >= 2 x 6 x 128: fk / sol below
     __shared__ double tot[kMaxRedB];
-    __shared__ double fk[6][128];
-    __shared__ double sol[6][128];
+    double (*fk)[128] = reinterpret_cast<double (*)[128]>(scratch);           // the finaliser's operands,
+    double (*sol)[128] = reinterpret_cast<double (*)[128]>(scratch + 6 * 128);  // after the block sums
     __shared__ bool s_last;
     if (respect_done && st->nrun == 0) return;
     const int P = (m + JC - 1) / JC;
@@ -1120,8 +1122,7 @@ __global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const
     if (x < X) {
         const int32_t per = (n + X - 1) / X;
         const int32_t i0 = x * per, i1 = min(n, i0 + per);
-        const int c = threadIdx.x % G;  // kElemThreads % G == 0: fixed chunk
-        double acc[JC][VW];
+        double acc[JC][VW];  // kElemThreads % G == 0: each thread keeps one chunk
 #pragma unroll
         for (int jc = 0; jc < JC; ++jc)
 #pragma unroll
@@ -1145,21 +1146,7 @@ __global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const
                     for (int v = 0; v < VW; ++v) acc[jc][v] = fadd_mul(acc[jc][v], wj, yv[v]);
                 }
         }
-        if constexpr (RT >= 12) {
-            double full[JC * RT];  // this thread's chunk, zeros elsewhere (adding 0.0 is exact)
-#pragma unroll
-            for (int t = 0; t < JC * RT; ++t) full[t] = 0.0;
-#pragma unroll
-            for (int cc = 0; cc < G; ++cc)
-                if (cc == c)
-#pragma unroll
-                    for (int jc = 0; jc < JC; ++jc)
-#pragma unroll
-                        for (int v = 0; v < VW; ++v) full[jc * RT + cc * VW + v] = acc[jc][v];
-            block_sum_dyn<JC * RT>(full, mc * RT, scratch, bvals);
-            for (int t = threadIdx.x; t < mc * RT; t += blockDim.x)
-                partials[static_cast<int64_t>(j0 * RT + t) * X + x] = bvals[t];
-        } else {
+        {
             // block sum per output (jc, k): the threads of chunk c = k / VW in thread order (fixed),
             // through shared memory (a per-thread JC x RT array spills at RT <= 8, JC = 4)
 #pragma unroll
@@ -1601,10 +1588,10 @@ struct BatchSolve {
         start_iter = iter;
     }
 
-    // k_b_tallt grid: X row ranges x P sibling column passes, about 4 CTAs per SM
+    // k_b_tallt grid: X row ranges x P sibling column passes, one wave (3-4 CTAs per SM)
     int tgrid(int mcols) const {
         const int P = std::max(1, (mcols + tallt_jc<RT>() - 1) / tallt_jc<RT>());
-        const int X = std::max(1, std::min((n + 255) / 256, ctx->num_sms * (RT <= 8 ? 4 : 6) / P));  // one wave
+        const int X = std::max(1, std::min((n + 255) / 256, ctx->num_sms * (RT <= 8 ? 4 : 3) / P));  // one wave
         return X * P;
     }  // (kElemThreads threads per CTA)
 
@@ -1825,8 +1812,10 @@ struct BatchSolve {
             // RT 24 with 16-byte chunks leaves 8 of 32 lanes idle (2 rows x 12 lanes per warp) and
             // writes 2.5x the rho tile partials; RCG_BSWEEP_VW=4 selects 32-byte chunks there (5 rows
             // x 6 lanes) -- A/B switch
+            // measured on C3 at RT 24 (ms per launch, VW 2 / VW 4): forward 8.18 / 5.84, backward
+            // 12.80 / 13.79 -- 32-byte chunks for the forward sweep only (RCG_BSWEEP_VW=2 / 4 forces)
             static const int vw_env = std::getenv("RCG_BSWEEP_VW") ? std::atoi(std::getenv("RCG_BSWEEP_VW")) : 0;
-            const bool vw4 = RT == 24 && vw_env == 4;
+            const bool vw4 = RT == 24 && (vw_env == 4 || (vw_env == 0 && !backward));
             const int rpw = vw4 ? 32 / (RT / 4) : 32 / (RT / 2);
             const int cmul = RT >= 12 ? 3 : 2;
             const int ntiles = (s.npos + rpw * 4 - 1) / (rpw * 4);  // CTAs of 4 warp tiles
