@@ -1085,6 +1085,199 @@ __global__ void __launch_bounds__(kSpmvThreads, bspmv_min_blocks(RT)) k_b_spmv_p
     }
 }
 
+// ---- stencil-grid batched SpMV (natural-ordered N^3 grids with the 7- or 27-point pattern: C1-C4).
+// The generic gather path reads each p row (RT values) from L2 once per matrix entry that
+// references it -- 27 times on C3, ~86 GB per RT-24 SpMV: L2-bound (~6,300 B/cycle).  Here a CTA
+// owns TX consecutive rows of one x-line; the p rows of the 9 (27-point) or 5 (7-point) x-segments
+// they touch are staged once into shared memory by cp.async.bulk (contiguous: RT-interleaved rows),
+// and every gather is a shared-memory read.  Each (row, chunk) sums its row's entries in stored
+// order from 0.0 with separate roundings -- bitwise the generic kernel's q; (p, q) per rhs is a
+// fixed-order block + grid sum (the same finaliser).
+__global__ void k_grid_check(const int32_t* __restrict__ rs, const int32_t* __restrict__ ci, int32_t N, int st,
+                             int* __restrict__ bad) {
+    const int64_t n = static_cast<int64_t>(N) * N * N;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int x = static_cast<int>(i % N), y = static_cast<int>((i / N) % N), z = static_cast<int>(i / (int64_t(N) * N));
+        int32_t e = rs[i];
+        const int32_t end = rs[i + 1];
+        bool ok = true;
+        for (int dz = -1; dz <= 1 && ok; ++dz)
+            for (int dy = -1; dy <= 1 && ok; ++dy)
+                for (int dx = -1; dx <= 1 && ok; ++dx) {
+                    const int nd = (dx != 0) + (dy != 0) + (dz != 0);
+                    if (st == 7 && nd > 1) continue;
+                    if (x + dx < 0 || x + dx >= N || y + dy < 0 || y + dy >= N || z + dz < 0 || z + dz >= N) continue;
+                    const int64_t j = i + dx + static_cast<int64_t>(N) * dy + static_cast<int64_t>(N) * N * dz;
+                    if (e >= end || ci[e] != j) ok = false;
+                    ++e;
+                }
+        if (!ok || e != end) atomicExch(bad, 1);
+    }
+}
+
+constexpr int kGridSpmvThreads = 256;
+
+template <int RT, int ST>
+__global__ void __launch_bounds__(kGridSpmvThreads) k_b_spmv_grid(SpmvArgs a, int32_t N, const double* __restrict__ p,
+                                                                  double* __restrict__ q, BState* st, double* partials,
+                                                                  int project_later) {
+    constexpr int G = RT / 4;
+    constexpr int TX = kGridSpmvThreads / G;       // rows per tile
+    constexpr int NSEG = ST == 27 ? 9 : 5;
+    constexpr int SEGR = TX + 2;                   // staged rows per segment (x0-1 .. x0+TX)
+    extern __shared__ __align__(16) unsigned char gsm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(gsm);
+    double* seg = reinterpret_cast<double*>(gsm + 16);
+    __shared__ double scratch[RT * 32];
+    __shared__ double vals[RT];
+    __shared__ double tot[RT];
+    if (st->nrun == 0) return;
+    const int tid = threadIdx.x;
+    const int tiles_per_line = (N + TX - 1) / TX;
+    const int64_t lines = static_cast<int64_t>(N) * N;
+    const int64_t ntiles = lines * tiles_per_line;
+    const int64_t N2 = static_cast<int64_t>(N) * N;
+    if (tid == 0) {
+        mbar_init(bar);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    unsigned phase = 0;
+    double pq4[4] = {0.0, 0.0, 0.0, 0.0};
+    const int c = tid % G;
+    const int rloc = tid / G;  // row within the tile (< TX when tid < TX G)
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t line = t / tiles_per_line;
+        const int x0 = static_cast<int>(t % tiles_per_line) * TX;
+        const int y = static_cast<int>(line % N), z = static_cast<int>(line / N);
+        const int xa = max(x0 - 1, 0), xb = min(x0 + TX, N - 1);  // staged x range [xa, xb]
+        const int cnt = xb - xa + 1;
+        // stage the segments (dy, dz): rows (xa..xb, y+dy, z+dz), RT values each
+        if (tid == 0) {
+            unsigned bytes = 0;
+            for (int sidx = 0; sidx < NSEG; ++sidx) {
+                int dy, dz;
+                if (ST == 27) {
+                    dz = sidx / 3 - 1;
+                    dy = sidx % 3 - 1;
+                } else {
+                    const int o[5][2] = {{0, -1}, {-1, 0}, {0, 0}, {1, 0}, {0, 1}};  // (dy, dz)
+                    dy = o[sidx][0];
+                    dz = o[sidx][1];
+                }
+                if (y + dy < 0 || y + dy >= N || z + dz < 0 || z + dz >= N) continue;
+                bytes += static_cast<unsigned>(cnt) * RT * 8u;
+            }
+            fence_proxy_async();  // the previous tile's generic reads of the segments precede these writes
+            mbar_expect_tx(bar, bytes);
+            for (int sidx = 0; sidx < NSEG; ++sidx) {
+                int dy, dz;
+                if (ST == 27) {
+                    dz = sidx / 3 - 1;
+                    dy = sidx % 3 - 1;
+                } else {
+                    const int o[5][2] = {{0, -1}, {-1, 0}, {0, 0}, {1, 0}, {0, 1}};
+                    dy = o[sidx][0];
+                    dz = o[sidx][1];
+                }
+                if (y + dy < 0 || y + dy >= N || z + dz < 0 || z + dz >= N) continue;
+                const int64_t r0 = xa + static_cast<int64_t>(N) * (y + dy) + N2 * (z + dz);
+                bulk_g2s(seg + static_cast<int64_t>(sidx) * SEGR * RT, p + r0 * RT, static_cast<unsigned>(cnt) * RT * 8u, bar);
+            }
+        }
+        while (!mbar_try_wait(bar, phase)) {
+        }
+        phase ^= 1u;
+        const int x = x0 + rloc;
+        if (tid < TX * G && x < N) {
+            const int64_t i = x + static_cast<int64_t>(N) * y + N2 * z;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            const int32_t b = __ldg(a.rs + i), e = __ldg(a.rs + i + 1);
+            for (int32_t k = b; k < e; ++k) {
+                const int64_t j = __ldg(a.ci + k);
+                const double av = __ldg(a.va + k);
+                // j -> (dx, dy, dz) relative to i (each in -1..1, N >= 4: by comparisons, no
+                // division) -> (segment, staged row); dxp = dx + 1 etc.
+                int64_t d = j - i;
+                const int dz = d < -(N2 >> 1) ? -1 : (d > (N2 >> 1) ? 1 : 0);
+                d -= dz * N2;
+                const int dy = d < -(N >> 1) ? -1 : (d > (N >> 1) ? 1 : 0);
+                d -= static_cast<int64_t>(dy) * N;
+                const int dzp = dz + 1, dyp = dy + 1, dxp = static_cast<int>(d) + 1;
+                int sidx;
+                if (ST == 27) {
+                    sidx = dzp * 3 + dyp;
+                } else {
+                    sidx = dzp == 0 ? 0 : (dzp == 2 ? 4 : (dyp == 0 ? 1 : (dyp == 2 ? 3 : 2)));
+                }
+                const int xr = x + dxp - 1 - xa;
+                const double* src = seg + (static_cast<int64_t>(sidx) * SEGR + xr) * RT + 4 * c;
+                const double4 pv = *reinterpret_cast<const double4*>(src);
+                acc[0] = fadd_mul(acc[0], av, pv.x);
+                acc[1] = fadd_mul(acc[1], av, pv.y);
+                acc[2] = fadd_mul(acc[2], av, pv.z);
+                acc[3] = fadd_mul(acc[3], av, pv.w);
+            }
+            const int64_t o = i * RT + 4 * c;
+            const double* pself = seg + (static_cast<int64_t>(ST == 27 ? 4 : 2) * SEGR + (x - xa)) * RT + 4 * c;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                q[o + v] = acc[v];
+                pq4[v] = fadd_mul(pq4[v], pself[v], acc[v]);
+            }
+        }
+        __syncthreads();  // the staged segments are free for the next tile
+    }
+    if (project_later) return;
+    double pq[RT];
+#pragma unroll
+    for (int v = 0; v < RT; ++v) pq[v] = 0.0;
+    if (tid < TX * G) chunk_acc<RT>(pq, c, [&](double s, int v) { return __dadd_rn(s, pq4[v]); });
+    block_sum_dyn<RT>(pq, RT, scratch, vals);
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[1], tot)) {
+        if (st->defer) {
+            if (tid < RT) st->dtot[tid] = tot[tid];
+            return;
+        }
+        if (tid < RT) fin_pq(st, tot, tid);
+    }
+}
+
+template <int RT, int ST>
+size_t grid_spmv_smem() {
+    constexpr int TX = kGridSpmvThreads / (RT / 4);
+    return 16 + static_cast<size_t>(ST == 27 ? 9 : 5) * (TX + 2) * RT * 8;
+}
+
+// the stencil of a matrix's pattern (cached): 7 / 27 for a natural-ordered N^3 box, else 0
+static int grid_info(rcg_ctx* ctx, const rcg_matrix* a) {
+    if (a->grid_st >= 0) return a->grid_st;
+    a->grid_st = 0;
+    if (std::getenv("RCG_GRID_SPMV") && std::atoi(std::getenv("RCG_GRID_SPMV")) == 0) return 0;
+    const int64_t n = a->n;
+    const int32_t N = static_cast<int32_t>(std::llround(std::cbrt(static_cast<double>(n))));
+    if (N < 4 || static_cast<int64_t>(N) * N * N != n) return 0;
+    int st = 0;
+    if (a->nnz == 7 * n - 6LL * N * N) st = 7;
+    else if (a->nnz == (3LL * N - 2) * (3LL * N - 2) * (3LL * N - 2)) st = 27;
+    if (!st) return 0;
+    int* bad = static_cast<int*>(dev_alloc_bytes(sizeof(int)));
+    RCG_CK(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    const int g = std::max(1, static_cast<int>(std::min<int64_t>((n + 255) / 256, ctx->num_sms * 8)));
+    k_grid_check<<<g, 256, 0, ctx->stream>>>(a->rs, a->ci, N, st, bad);
+    RCG_LAUNCHED(ctx);
+    int h = 0;
+    RCG_CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    RCG_CK(cudaStreamSynchronize(ctx->stream));
+    dev_free(bad);
+    if (!h) {
+        a->grid_st = st;
+        a->gN = N;
+    }
+    return a->grid_st;
+}
+
 // f[j][k] = W_j . y_k for every (j, k).  Lane per row (each y row read as RT/2 16-byte loads,
 // W_j[i] loads coalesced), JC columns x RT values in registers.  The m/JC column passes run as
 // SIBLING CTAs over the same contiguous row range (consecutive block ids, so they are resident
@@ -1682,8 +1875,9 @@ struct BatchSolve {
         if (job.comm) job.comm->halo(ctx, w->p, RT);
         {
             KTimer t(ctx, 5, RT);
-            k_b_spmv_pq<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(sargs(), bcap, w->p, w->q, w->st,
-                                                                             w->partials, dfl ? 1 : 0);
+            if (!launch_grid_spmv(dfl))
+                k_b_spmv_pq<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(sargs(), bcap, w->p, w->q,
+                                                                                 w->st, w->partials, dfl ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
         if (!dfl) reduce(2, RT, 0, 1);
@@ -1718,6 +1912,35 @@ struct BatchSolve {
                 RCG_LAUNCHED(ctx);
             }
             reduce(5, scb->k * RT, 2, 1, scb->l, scb->k, w->u2);
+        }
+    }
+
+    // q = A p on a stencil grid through shared-memory staged segments (RT a multiple of 4)
+    bool launch_grid_spmv(bool dfl) {
+        if constexpr (RT % 4 != 0) {
+            return false;
+        } else {
+            if (job.comm) return false;
+            const int gst = grid_info(ctx, a);
+            if (gst == 0) return false;
+            static bool attr = false;
+            if (!attr) {
+                for (const void* k : {reinterpret_cast<const void*>(k_b_spmv_grid<RT, 27>),
+                                      reinterpret_cast<const void*>(k_b_spmv_grid<RT, 7>)})
+                    RCG_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                attr = true;
+            }
+            const size_t smem = gst == 27 ? grid_spmv_smem<RT, 27>() : grid_spmv_smem<RT, 7>();
+            if (smem > 200 * 1024) return false;
+            const int per_sm = std::max(1, static_cast<int>((220 * 1024) / (smem + 8 * 1024)));
+            const int grid = ctx->num_sms * std::min(per_sm, 4);
+            if (gst == 27)
+                k_b_spmv_grid<RT, 27><<<grid, kGridSpmvThreads, smem, ctx->stream>>>(sargs(), a->gN, w->p, w->q, w->st,
+                                                                                    w->partials, dfl ? 1 : 0);
+            else
+                k_b_spmv_grid<RT, 7><<<grid, kGridSpmvThreads, smem, ctx->stream>>>(sargs(), a->gN, w->p, w->q, w->st,
+                                                                                   w->partials, dfl ? 1 : 0);
+            return true;
         }
     }
 

@@ -169,6 +169,10 @@ struct rcg_matrix {
     int32_t* ci = nullptr;
     double* va = nullptr;
     int cap = 256;  // pipelined SpMV stage capacity (entries)
+    // natural-ordered cube stencil (7 / 27-point) detected from the pattern (batch.cu grid_info):
+    // -1 not yet checked, 0 no, 7 / 27 yes with edge gN
+    mutable int grid_st = -1;
+    mutable int32_t gN = 0;
 };
 
 struct rcg_ic {

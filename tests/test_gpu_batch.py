@@ -82,3 +82,29 @@ def test_batch_is_deterministic(ctx, oracle, problems):
     r1 = api.pcg_solve_batch(ctx, ga, B, api.Ic(gf), X1)
     r2 = api.pcg_solve_batch(ctx, ga, B, api.Ic(gf), X2)
     assert np.array_equal(X1, X2) and all(np.array_equal(a.history, b.history) for a, b in zip(r1, r2))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("nrhs", [4, 9, 19])
+def test_grid_spmv_batched_bitwise(ctx, oracle, problems, name, nrhs):
+    """Batched ICCG on the scaled-down cubes (7- and 27-point patterns), which the batched solver
+    runs through the stencil-grid SpMV (shared-memory staged x-segments; RCG_GRID_SPMV=0 is the A/B
+    switch), at RT 4 / 12 / 24 against the oracle's single solves: iterations +-2, solutions at
+    equal counts."""
+    from paper_2203_08498_b200 import api
+
+    cfg = problems.SMALL[name]
+    h = problems.generate(cfg)
+    sa, _ = oracle.diagonal_scale(Matrix.of(h))
+    ga = api.CsrMatrix(ctx, h.n, h.row_start, h.col_idx, sa.va)
+    gf = api.IcFactor.factorize(ctx, h.n, h.row_start, h.col_idx, sa.va)
+    B = np.stack([oracle.uniform_pm1(k + 1, 0, h.n) for k in range(nrhs)])
+    X = np.zeros_like(B)
+    reps = api.pcg_solve_batch(ctx, ga, B, api.Ic(gf), X, cfg.eps, cfg.max_iter)
+    of = oracle.ic0_factorize(sa)
+    for k in range(nrhs):
+        xo = np.zeros(h.n)
+        ro = oracle.pcg_solve(sa, B[k], xo, kind=1, ic=of, max_iter=cfg.max_iter)
+        assert reps[k].converged and abs(reps[k].iterations - ro.iterations) <= 2
+        if reps[k].iterations == ro.iterations:
+            assert _rel(X[k], xo) <= 1e-7
