@@ -66,9 +66,8 @@ int rcg_ctx_kernel_stats(rcg_ctx* ctx, int cls, double* total_ms, int64_t* launc
 int rcg_ctx_kernel_units(rcg_ctx* ctx, int cls, int64_t* units);
 void rcg_ctx_reset_stats(rcg_ctx* ctx);
 /* IC sweep kernel selection (no effect on results: every variant is bitwise identical):
- * 0 = grid-wide sync-free sweep (k_sweep), 2 = default (one CTA -- icsweep_cta.cu -- for factors
- * of <= 64K rows, one launch per level -- icsweep_lv.cu -- when the average level holds >= 600K
- * rows, else k_sweep), 4 = one launch per level always, 6 = one CTA always;
+ * 0 = grid-wide sync-free sweep (k_sweep), 2 = default (one launch per level -- icsweep_lv.cu --
+ * when the average level holds >= 600K rows, else k_sweep), 4 = one launch per level always;
  * RCG_SWEEP_CLUSTER overrides at context creation */
 int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode);
 

@@ -112,9 +112,8 @@ class Context:
         check(lib.rcg_ctx_set_profiling(self.h, 1 if on else 0))
 
     def set_sweep_kernel(self, mode: int):
-        """IC sweep kernel: 0 grid-wide sync-free, 2 default (one CTA for small factors, per-level
-        launches for wide levels, else grid-wide), 4 per-level launches always, 6 one CTA always.
-        Results are bitwise identical either way."""
+        """IC sweep kernel: 0 grid-wide sync-free, 2 default (per-level launches for wide levels,
+        else grid-wide), 4 per-level launches always.  Results are bitwise identical either way."""
         check(lib.rcg_ctx_set_sweep_kernel(self.h, int(mode)))
 
     def record(self, slot: int):

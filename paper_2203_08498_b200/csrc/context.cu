@@ -375,7 +375,7 @@ int rcg_ctx_create(int device, rcg_ctx** out) {
         if (const char* e = std::getenv("RCG_SWEEP_BACKOFF_NS")) c->sweep_backoff_ns = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("RCG_SWEEP_CLUSTER")) {
             const int m = std::atoi(e);
-            if (m == 0 || m == 2 || m == 4 || m == 6) c->sweep_cluster = m;
+            if (m == 0 || m == 2 || m == 4) c->sweep_cluster = m;
         }
         if (const char* e = std::getenv("RCG_SPMV_BPS")) c->spmv_bps = std::max(1, std::atoi(e));
         RCG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -426,8 +426,8 @@ int64_t rcg_ctx_launch_count(const rcg_ctx* ctx) { return ctx ? ctx->launches : 
 
 int rcg_ctx_set_sweep_kernel(rcg_ctx* ctx, int mode) {
     return guard([&] {
-        require(ctx != nullptr && (mode == 0 || mode == 2 || mode == 4 || mode == 6),
-                "rcg_ctx_set_sweep_kernel: mode must be 0 (grid-wide), 2 (by shape), 4 (per level) or 6 (one CTA)");
+        require(ctx != nullptr && (mode == 0 || mode == 2 || mode == 4),
+                "rcg_ctx_set_sweep_kernel: mode must be 0 (grid-wide), 2 (by shape) or 4 (per level)");
         ctx->sweep_cluster = mode;
     });
 }

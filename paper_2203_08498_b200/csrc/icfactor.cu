@@ -540,7 +540,6 @@ static void factorize_device(rcg_ctx* ctx, const rcg_matrix* A, double shift, in
         RCG_CK(cudaGetLastError());
     }
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    upload_level_ptrs(ctx, f);
     mark("value gathers");
 }
 

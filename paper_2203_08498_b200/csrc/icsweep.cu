@@ -207,7 +207,6 @@ int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos) {
 
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
-    if (launch_cta_sweep(ctx, f, backward, a)) return;    // small factors: one CTA (icsweep_cta.cu)
     if (launch_level_sweep(ctx, f, backward, a)) return;  // wide levels: one launch per level (icsweep_lv.cu)
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
     const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
@@ -342,19 +341,6 @@ static void finish_ic(rcg_ctx* ctx, rcg_ic* f) {
     f->b_val = upload(ctx, pval);
     f->d = upload(ctx, f->h_d);
     RCG_CK(cudaStreamSynchronize(ctx->stream));
-    upload_level_ptrs(ctx, f);
-}
-
-void upload_level_ptrs(rcg_ctx* ctx, rcg_ic* f) {
-    for (int k = 0; k < 2; ++k) {
-        dev_free(f->d_lptr[k]);
-        f->d_lptr[k] = nullptr;
-        if (f->h_lptr[k].empty()) continue;
-        f->d_lptr[k] = static_cast<int32_t*>(dev_alloc_bytes(sizeof(int32_t) * f->h_lptr[k].size()));
-        RCG_CK(cudaMemcpyAsync(f->d_lptr[k], f->h_lptr[k].data(), sizeof(int32_t) * f->h_lptr[k].size(),
-                               cudaMemcpyHostToDevice, ctx->stream));
-    }
-    RCG_CK(cudaStreamSynchronize(ctx->stream));
 }
 
 }  // namespace rcg
@@ -423,8 +409,7 @@ int rcg_ic_create(rcg_ctx* ctx, int32_t n, int num_blocks, const int32_t* block_
 void rcg_ic_destroy(rcg_ic* f) {
     if (!f) return;
     for (void* p : {(void*)f->f_perm, (void*)f->f_prs, (void*)f->f_col, (void*)f->f_val, (void*)f->b_perm,
-                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d, (void*)f->d_lptr[0],
-                    (void*)f->d_lptr[1]})
+                    (void*)f->b_prs, (void*)f->b_col, (void*)f->b_val, (void*)f->d})
         dev_free(p);
     delete f;
 }

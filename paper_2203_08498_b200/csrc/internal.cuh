@@ -156,7 +156,7 @@ struct rcg_ctx {
     cudaEvent_t user_ev[16] = {};
     int sweep_bps = 0;          // resident sweep CTAs per SM; 0 = by DAG shape (RCG_SWEEP_BPS)
     int sweep_backoff_ns = 0;   // dependency-wait sleep between polls (RCG_SWEEP_BACKOFF_NS)
-    int sweep_cluster = 2;      // IC sweep kernel: 0 grid-wide sync-free, 2 by shape, 4 one launch per level, 6 one CTA
+    int sweep_cluster = 2;      // IC sweep kernel: 0 grid-wide sync-free, 2 by shape, 4 one launch per level
     int spmv_bps = 2;           // SpMV CTAs per SM (RCG_SPMV_BPS): leaves room for concurrent solves
     rcg::BatchWs* bws = nullptr;   // multi-RHS workspaces (batch.cu): a compacted phase
     rcg::BatchWs* bws2 = nullptr;  // reads one and writes the other
@@ -191,10 +191,8 @@ struct rcg_ic {
     int32_t *b_perm = nullptr, *b_prs = nullptr, *b_col = nullptr;
     double* b_val = nullptr;
     double* d = nullptr;
-    // level starts of the padded schedules ([0] forward, [1] backward; nlev + 1 entries), and a
-    // device copy (the one-CTA sweeps of small factors, icsweep_cta.cu)
+    // level starts of the padded schedules ([0] forward, [1] backward; nlev + 1 entries)
     std::vector<int32_t> h_lptr[2];
-    int32_t* d_lptr[2] = {nullptr, nullptr};
 };
 
 struct rcg_tall {

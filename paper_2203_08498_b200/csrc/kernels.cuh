@@ -117,8 +117,6 @@ int tile_capacity(int32_t n, const int32_t* rs);
 void launch_residual(rcg_ctx* ctx, const rcg_matrix* a, const double* b, const double* x, double* r);
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);
 bool launch_level_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);   // icsweep_lv.cu
-bool launch_cta_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& args);     // icsweep_cta.cu
-void upload_level_ptrs(rcg_ctx* ctx, rcg_ic* f);                                          // icsweep.cu
 // memory-lean recycling step (recycle.cu): errors, MGS and the streamed Rayleigh-Ritz Gram in the
 // sampler's slots; W is a new n x m~ block
 void lean_build_aux(rcg_ctx* ctx, const rcg_matrix* a, const double* x_dev, rcg_sampler* s, double theta,

@@ -1,6 +1,5 @@
-"""The IC sweep variants -- grid-wide sync-free (k_sweep), one launch per level
-(csrc/icsweep_lv.cu) and the one-CTA level-synchronous sweep of small factors
-(csrc/icsweep_cta.cu) -- against each other and the oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
+"""The IC sweep variants -- grid-wide sync-free (k_sweep) and one launch per level
+(csrc/icsweep_lv.cu) -- against each other and the oracle: the sweep output, the (r, z) reduction and whole PCG / SC-PCG solves must be BITWISE
 identical whichever kernel runs (the kernel choice never changes an iterate), and all equal the
 reference ic_apply (src/ic_preconditioner.cpp:123-144)."""
 import numpy as np
@@ -10,8 +9,8 @@ from oracle import Matrix
 
 pytestmark = pytest.mark.gpu
 
-GRID, AUTO, LEVEL, CTA = 0, 2, 4, 6
-MODES = (GRID, AUTO, LEVEL, CTA)
+GRID, AUTO, LEVEL = 0, 2, 4
+MODES = (GRID, AUTO, LEVEL)
 
 
 @pytest.fixture
