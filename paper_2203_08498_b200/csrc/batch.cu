@@ -68,8 +68,6 @@ struct BatchWs {
     int64_t cap_groups = 0;
     double* tpart = nullptr;  // chunk-lane sweep tile partials
     int64_t cap_tpart = 0;
-    double* rowc = nullptr;   // one-CTA sweep: per-position (r, z) products
-    int64_t cap_rowc = 0;
     int* tickets = nullptr;
 };
 
@@ -77,7 +75,7 @@ static void free_ws(BatchWs*& w) {
     if (!w) return;
     for (void* p : {(void*)w->b, (void*)w->x, (void*)w->r, (void*)w->zs, (void*)w->p, (void*)w->q, (void*)w->y,
                     (void*)w->st, (void*)w->hist, (void*)w->u, (void*)w->u2, (void*)w->partials, (void*)w->gpart,
-                    (void*)w->gcount, (void*)w->tpart, (void*)w->tickets, (void*)w->rowc})
+                    (void*)w->gcount, (void*)w->tpart, (void*)w->tickets})
         dev_free(p);
     delete w;
     w = nullptr;
@@ -802,80 +800,6 @@ __global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
             a.tickets[0] = 0;
             a.tickets[1] = 0;
         }
-    }
-}
-
-// One CTA, level-synchronous (small factors, C1: icsweep_cta.cu's batched counterpart): items
-// (position, chunk of VW values) of a level over the CTA, a barrier between levels.  Row
-// arithmetic is k_b_sweepc's (bitwise).  For rho the per-row products go to `rowc` (position-major,
-// RT per position) and are summed per chunk-lane tile of RPW positions in k_b_sweepc's order
-// (row 0 of the tile, then rows 1..RPW-1), so k_b_rho sees the same tile partials.
-template <bool BWD, int RT, int VW>
-__global__ void __launch_bounds__(1024, 1) k_b_sweep_cta(SweepArgs a, BState* st, const int32_t* __restrict__ lptr,
-                                                          int nlev, double* __restrict__ rowc, int rpw) {
-    constexpr int G = RT / VW;
-    if (st->nrun == 0) return;
-    const int tid = threadIdx.x;
-    const bool rho = BWD && a.r;
-    for (int l = 0; l < nlev; ++l) {
-        const int32_t l0 = __ldg(lptr + l), l1 = __ldg(lptr + l + 1);
-        const int64_t items = static_cast<int64_t>(l1 - l0) * G;
-        for (int64_t it = tid; it < items; it += 1024) {
-            const int32_t pos = l0 + static_cast<int32_t>(it / G);
-            const int c = static_cast<int>(it % G);
-            const int32_t row = __ldg(a.perm + pos);
-            double contrib[VW];
-#pragma unroll
-            for (int v = 0; v < VW; ++v) contrib[v] = 0.0;
-            if (row >= 0) {
-                const int64_t me = static_cast<int64_t>(row) * RT + VW * c;
-                double sv[VW];
-                const double dr = BWD ? __ldg(a.d + row) : 1.0;
-#pragma unroll
-                for (int v = 0; v < VW; ++v) sv[v] = BWD ? __ddiv_rn(a.in[me + v], dr) : a.in[me + v];
-                const int32_t b = __ldg(a.prs + pos), e = __ldg(a.prs + pos + 1);
-                for (int32_t k0 = b; k0 < e; k0 += 4) {  // four parents' chunks in flight, then in order
-                    const int mm = min(4, e - k0);
-                    double lv[4], dep[4][VW];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (j < mm) {
-                            lv[j] = __ldg(a.pval + k0 + j);
-                            const double* src = a.out + static_cast<int64_t>(__ldg(a.pcol + k0 + j)) * RT + VW * c;
-#pragma unroll
-                            for (int v = 0; v < VW; ++v) dep[j][v] = __ldcg(src + v);  // earlier levels: final
-                        }
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (j < mm)
-#pragma unroll
-                            for (int v = 0; v < VW; ++v) sv[v] = fsub_mul(sv[v], lv[j], dep[j][v]);
-                }
-#pragma unroll
-                for (int v = 0; v < VW; ++v) {
-                    if (rho) contrib[v] = __dmul_rn(a.r[me + v], sv[v]);
-                    a.out[me + v] = publishable(sv[v]);
-                }
-            }
-            if (rho)
-#pragma unroll
-                for (int v = 0; v < VW; ++v) rowc[static_cast<int64_t>(pos) * RT + VW * c + v] = contrib[v];
-        }
-        __syncthreads();
-    }
-    if (!rho) return;
-    // tile partials in k_b_sweepc's order: tile t = positions [t rpw, t rpw + rpw) (beyond npos: 0)
-    const int64_t tiles = (static_cast<int64_t>(a.npos) + rpw - 1) / rpw;
-    for (int64_t o = tid; o < tiles * RT; o += 1024) {
-        const int64_t t = o / RT;
-        const int k = static_cast<int>(o % RT);
-        double tot = 0.0;
-        for (int r = 0; r < rpw; ++r) {
-            const int64_t pos = t * rpw + r;
-            const double v = pos < a.npos ? rowc[pos * RT + k] : 0.0;
-            tot = r == 0 ? v : __dadd_rn(tot, v);
-        }
-        a.partials[o] = tot;
     }
 }
 
@@ -1968,38 +1892,6 @@ struct BatchSolve {
         // (default shape rule of icsweep_lv.cu: >= 600K rows per level; mode 4 always).  Forced on
         // natural orderings at RT 8 it wins only on C4 (fwd 27.3 -> 20.8, bwd 37.7 -> 33.4 ms) and
         // loses on C5 (707 -> 842 us) and C3 (4.1 -> 17.3 ms)
-        // small factors (C1): one CTA, level-synchronous (mode 2 up to RCG_SWEEP_CTA_N rows, mode 6 always)
-        static const int64_t cta_n = std::getenv("RCG_SWEEP_CTA_N") ? std::atoll(std::getenv("RCG_SWEEP_CTA_N")) : 65536LL;
-        if (f->d_lptr[backward ? 1 : 0] &&
-            (ctx->sweep_cluster == 6 || (ctx->sweep_cluster == 2 && static_cast<int64_t>(f->n) <= cta_n))) {
-            const bool rho = backward && s.r;
-            constexpr int rpw = 32 / (RT / 2);  // the chunk-lane sweep's tile (VW 2)
-            double* rowc = nullptr;
-            if (rho) {
-                const int64_t need = static_cast<int64_t>(s.npos) * RT;
-                if (need > w->cap_rowc) {
-                    dev_free(w->rowc);
-                    w->rowc = dev_alloc(need);
-                    w->cap_rowc = need;
-                }
-                rowc = w->rowc;
-                s.partials = w->tpart;
-            }
-            const int nl = backward ? f->bwd_levels : f->fwd_levels;
-            if (backward)
-                k_b_sweep_cta<true, RT, 2><<<1, 1024, 0, ctx->stream>>>(s, w->st, f->d_lptr[1], nl, rowc, rpw);
-            else
-                k_b_sweep_cta<false, RT, 2><<<1, 1024, 0, ctx->stream>>>(s, w->st, f->d_lptr[0], nl, rowc, rpw);
-            RCG_LAUNCHED(ctx);
-            if (rho) {
-                const int64_t tiles = (s.npos + rpw - 1) / rpw;
-                const int g = static_cast<int>(std::max<int64_t>(
-                    1, std::min<int64_t>((tiles * RT + kElemThreads * 4 - 1) / (kElemThreads * 4), ctx->num_sms * 8)));
-                k_b_rho<RT><<<g, kElemThreads, 0, ctx->stream>>>(w->tpart, tiles, w->partials, w->st, s.add_sc);
-                RCG_LAUNCHED(ctx);
-            }
-            return;
-        }
         const std::vector<int32_t>& lp = f->h_lptr[backward ? 1 : 0];
         const int nlev = backward ? f->bwd_levels : f->fwd_levels;
         const bool level_ok = static_cast<int>(lp.size()) == nlev + 1 && nlev > 0;

@@ -193,35 +193,3 @@ def test_batched_level_sweeps_multicolour(modes, problems, method):
             x0 = out[GRID][1][k]
             assert np.linalg.norm(out[mode][1][k] - x0) <= 1e-6 * np.linalg.norm(x0)
 
-
-
-@pytest.mark.parametrize("method", ["deflation", "sc"])
-def test_batched_cta_sweeps_c1_bitwise(modes, problems, method):
-    """C1's batched accelerated solves (RT 4) under the grid-wide chunk-lane sweep and the one-CTA
-    level-synchronous sweep (the default for small factors): identical iteration counts and
-    bitwise identical solutions (the rho tile partials are formed in the chunk-lane order)."""
-    from paper_2203_08498_b200 import api, sequence
-
-    ctx = modes
-    cfg = problems.CONFIGS["c1"]
-    h = problems.generate(cfg)
-    p = sequence.prepare(ctx, cfg, h, validate=False)
-    bs = [sequence.rhs(p, k)[1] for k in range(cfg.n_rhs)]
-    s = api.SamplerState.method_a(ctx, cfg.sampler_m, cfg.max_iter, h.n)
-    x0 = np.zeros(h.n)
-    api.pcg_solve(ctx, p.a, bs[0], api.Ic(p.ic), x0, cfg.eps, cfg.max_iter, observer=s)
-    _, _, _, w = api.build_aux_matrix(ctx, p.a, api.harvest_errors(ctx, x0, s), 1e-3, keep_count=cfg.keep)
-    basis = api.Basis(ctx, p.a, w, method)
-    B = np.stack(bs[1:])
-    out = {}
-    for mode in (GRID, CTA, AUTO):
-        ctx.set_sweep_kernel(mode)
-        X = np.zeros_like(B)
-        if method == "sc":
-            reps = api.pcg_solve_batch(ctx, p.a, B, api.Sc(basis, p.ic), X, cfg.eps, cfg.max_iter)
-        else:
-            reps = api.deflated_pcg_solve_batch(ctx, p.a, B, api.Ic(p.ic), basis, X, cfg.eps, cfg.max_iter)
-        out[mode] = ([r.iterations for r in reps], X)
-    for mode in (CTA, AUTO):
-        assert out[mode][0] == out[GRID][0]
-        assert np.array_equal(out[mode][1], out[GRID][1]), mode
