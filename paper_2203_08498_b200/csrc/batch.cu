@@ -1211,14 +1211,13 @@ static int grid_info(rcg_ctx* ctx, const rcg_matrix* a) {
 // (mode 1) and f.u (mode 2).  Host grid: X x P (BatchSolve::tgrid).
 template <int RT>
 __device__ __host__ constexpr int tallt_jc() {
-    // columns per pass: y is re-read from L2 once per pass (m / JC passes), so wide passes matter
-    // at large RT (C3, RT 24, m 32: JC 2 -> 16 passes, 6.5 ms; the shared-memory block sum below
-    // keeps JC 6 within the register budget); RT 4 with 8 columns spilled
-    return RT <= 8 ? 4 : 6;
+    // columns per pass (m / JC sibling passes over the same rows): measured on C3 at RT 24, m 32:
+    // JC 2 6.5 ms, JC 6 7.8 ms (3 CTAs per SM, y partly re-read from DRAM); RT 4 with 8 columns spilled
+    return RT <= 8 ? 4 : 2;
 }
 
 template <int RT>
-__global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 3) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
+__global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const double* __restrict__ W, int64_t ldw, int m,
                                                             const double* __restrict__ y, int32_t n,
                                                             double* partials, const double* __restrict__ L,
                                                             double* __restrict__ u, int mode, BState* st,
@@ -1705,10 +1704,10 @@ struct BatchSolve {
         start_iter = iter;
     }
 
-    // k_b_tallt grid: X row ranges x P sibling column passes, one wave (3-4 CTAs per SM)
+    // k_b_tallt grid: X row ranges x P sibling column passes, one wave (4-6 CTAs per SM)
     int tgrid(int mcols) const {
         const int P = std::max(1, (mcols + tallt_jc<RT>() - 1) / tallt_jc<RT>());
-        const int X = std::max(1, std::min((n + 255) / 256, ctx->num_sms * (RT <= 8 ? 4 : 3) / P));  // one wave
+        const int X = std::max(1, std::min((n + 255) / 256, ctx->num_sms * (RT <= 8 ? 4 : 6) / P));  // one wave
         return X * P;
     }  // (kElemThreads threads per CTA)
 
