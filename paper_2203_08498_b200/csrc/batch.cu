@@ -1302,6 +1302,115 @@ __global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const
     fin_tallt<RT>(st, tot, L, m, u, mode, fk, sol);
 }
 
+// f[j][k] = W_j . y_k, register-blocked (RT a multiple of 4, m <= 128): the CTA stages a tile of
+// kWtyRows rows of W (m columns) and of y (RT values per row) in shared memory once, and each
+// thread accumulates a 4 (columns) x 4 (rhs) block of outputs over the tile rows of its row group
+// -- 8 shared-memory loads per 16 multiply-adds, W and y read from HBM once.  (k_b_tallt's sibling
+// passes re-read y m / 2 times and were bound by L1 / shared-memory traffic at RT 24: 6.5 ms on C3.)
+// Determinism: each thread sums its rows in order (separate roundings), the row groups and the
+// CTAs are combined in a fixed order; the finaliser is k_b_tallt's.
+constexpr int kWtyThreads = 256;
+constexpr int kWtyRows = 64;
+constexpr int kWtyLd = kWtyRows + 1;  // padded W-tile row: the warp's ~6 columns in distinct banks
+
+template <int RT>
+__global__ void __launch_bounds__(kWtyThreads) k_b_wty(const double* __restrict__ W, int64_t ldw, int m,
+                                                        const double* __restrict__ y, int32_t n, double* partials,
+                                                        const double* __restrict__ L, double* __restrict__ u, int mode,
+                                                        BState* st, int respect_done) {
+    constexpr int KB = RT / 4;  // rhs blocks of 4
+    extern __shared__ __align__(16) double wsm[];  // [m][kWtyLd] W tile, then [kWtyRows][RT] y tile
+    double* ysm = wsm + ((static_cast<int64_t>(m) * kWtyLd + 3) & ~int64_t(3));  // 32-byte aligned
+    __shared__ double tot[kMaxRedB];
+    __shared__ double fk[6][128];
+    __shared__ double sol[6][128];
+    __shared__ bool s_last;
+    if (respect_done && st->nrun == 0) return;
+    const int JB = (m + 3) / 4;
+    const int nblk = JB * KB;                         // 4 x 4 output blocks
+    const int groups = max(1, kWtyThreads / nblk);    // row groups
+    const int tid = threadIdx.x;
+    const int blk = tid % nblk, grp = tid / nblk;
+    const bool active = grp < groups && nblk <= kWtyThreads;
+    const int j0 = (blk / KB) * 4, k0 = (blk % KB) * 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    const int64_t ntile = (static_cast<int64_t>(n) + kWtyRows - 1) / kWtyRows;
+    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const int64_t i0 = t * kWtyRows;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(kWtyRows), static_cast<int64_t>(n) - i0));
+        for (int e = tid; e < m * kWtyRows; e += kWtyThreads) {
+            const int j = e / kWtyRows, r = e % kWtyRows;
+            wsm[j * kWtyLd + r] = r < rows ? __ldg(W + j * ldw + i0 + r) : 0.0;
+        }
+        for (int e = tid; e < kWtyRows * RT; e += kWtyThreads)
+            ysm[e] = e < rows * RT ? __ldg(y + i0 * RT + e) : 0.0;
+        __syncthreads();
+        if (active)
+            for (int r = grp; r < rows; r += groups) {
+                double wv[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) wv[a] = j0 + a < m ? wsm[(j0 + a) * kWtyLd + r] : 0.0;
+                const double4 yv = *reinterpret_cast<const double4*>(ysm + r * RT + k0);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    acc[a][0] = fadd_mul(acc[a][0], wv[a], yv.x);
+                    acc[a][1] = fadd_mul(acc[a][1], wv[a], yv.y);
+                    acc[a][2] = fadd_mul(acc[a][2], wv[a], yv.z);
+                    acc[a][3] = fadd_mul(acc[a][3], wv[a], yv.w);
+                }
+            }
+        __syncthreads();
+    }
+    // row groups in order -> the CTA's partial of every output (wsm reused: [groups][m * RT])
+    if (active)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (j0 + a < m) wsm[static_cast<int64_t>(grp) * m * RT + (j0 + a) * RT + k0 + b] = acc[a][b];
+    __syncthreads();
+    const int X = gridDim.x;
+    for (int o = tid; o < m * RT; o += kWtyThreads) {
+        double sv = 0.0;
+        for (int g = 0; g < groups; ++g) sv = __dadd_rn(sv, wsm[static_cast<int64_t>(g) * m * RT + o]);
+        partials[static_cast<int64_t>(o) * X + blockIdx.x] = sv;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&st->tick[2], 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    {
+        const int lane = tid & 31, wid = tid >> 5, nw = kWtyThreads >> 5;
+        for (int o = wid; o < m * RT; o += nw) {
+            double sv = 0.0;
+            for (int xx = lane; xx < X; xx += 32) sv = __dadd_rn(sv, __ldcg(partials + static_cast<int64_t>(o) * X + xx));
+            sv = warp_sum(sv);
+            if (lane == 0) tot[o] = sv;
+        }
+        __syncthreads();
+        if (tid == 0) st->tick[2] = 0u;
+    }
+    if (st->defer) {
+        for (int t = tid; t < m * RT; t += kWtyThreads) st->dtot[t] = tot[t];
+        return;
+    }
+    fin_tallt<RT>(st, tot, L, m, u, mode, fk, sol);
+}
+
+template <int RT>
+size_t wty_smem(int m) {
+    const int nblk = ((m + 3) / 4) * (RT / 4);
+    const int groups = std::max(1, kWtyThreads / nblk);
+    const size_t tiles = ((static_cast<size_t>(m) * kWtyLd + 3) & ~size_t(3)) + static_cast<size_t>(kWtyRows) * RT;
+    return sizeof(double) * std::max(tiles, static_cast<size_t>(groups) * m * RT);
+}
+
 // The finalisers of the reducing kernels from allreduced totals (row slabs): which = 0 residual
 // (arg: defer_check), 1 rho (arg: add_sc), 2 (p, q), 3 projected-residual check, 4 x / r update
 // (arg: identity), 5 the m x RT projection coefficients (arg: tallt mode).  `guard` repeats the
@@ -1704,6 +1813,31 @@ struct BatchSolve {
         start_iter = iter;
     }
 
+    // W^T y with the finaliser (u = (W^T A W)^-1 f, or f.u for mode 2): the register-blocked
+    // k_b_wty where RT is a multiple of 4 (RCG_WTY=0: the sibling-pass k_b_tallt)
+    void launch_wty(const double* Wm, int64_t ld, int mcols, const double* yv, const double* Lf, double* uo, int mode,
+                    int respect_done) {
+        static const int use = std::getenv("RCG_WTY") ? std::atoi(std::getenv("RCG_WTY")) : 1;
+        if constexpr (RT % 4 == 0) {
+            if (use && mcols >= 1 && mcols <= 128 && static_cast<int64_t>(mcols) * RT <= kMaxRedB) {
+                static bool attr = false;
+                if (!attr) {
+                    RCG_CK(cudaFuncSetAttribute(k_b_wty<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+                    attr = true;
+                }
+                const size_t smem = wty_smem<RT>(mcols);
+                const int64_t ntile = (static_cast<int64_t>(n) + kWtyRows - 1) / kWtyRows;
+                const int per_sm = std::max(1, std::min(4, static_cast<int>((200 * 1024) / (smem + 20 * 1024))));
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntile, ctx->num_sms * per_sm)));
+                k_b_wty<RT><<<grid, kWtyThreads, smem, ctx->stream>>>(Wm, ld, mcols, yv, n, w->partials, Lf, uo, mode,
+                                                                      w->st, respect_done);
+                return;
+            }
+        }
+        k_b_tallt<RT><<<tgrid(mcols), kElemThreads, 0, ctx->stream>>>(Wm, ld, mcols, yv, n, w->partials, Lf, uo, mode,
+                                                                       w->st, respect_done);
+    }
+
     // k_b_tallt grid: X row ranges x P sibling column passes, one wave (4-6 CTAs per SM)
     int tgrid(int mcols) const {
         const int P = std::max(1, (mcols + tallt_jc<RT>() - 1) / tallt_jc<RT>());
@@ -1751,8 +1885,7 @@ struct BatchSolve {
         RCG_LAUNCHED(ctx);
         reduce(0, 2 * RT, dfl ? 1 : 0, 0);
         if (dfl) {
-            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->r, n, w->partials,
-                                                                  defl->l, w->u, 1, w->st, 0);
+            launch_wty(defl->w, defl->ld, defl->k, w->r, defl->l, w->u, 1, 0);
             RCG_LAUNCHED(ctx);
             reduce(5, defl->k * RT, 1, 0, defl->l, defl->k, w->u);
             k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr,
@@ -1761,8 +1894,7 @@ struct BatchSolve {
             reduce(3, RT, 0, 0);
         }
         if (sc) {
-            k_b_tallt<RT><<<tgrid(scb->k), kElemThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n, w->partials,
-                                                                  scb->l, w->u2, 2, w->st, 0);
+            launch_wty(scb->w, scb->ld, scb->k, w->r, scb->l, w->u2, 2, 0);
             RCG_LAUNCHED(ctx);
             reduce(5, scb->k * RT, 2, 0, scb->l, scb->k, w->u2);
         }
@@ -1807,8 +1939,7 @@ struct BatchSolve {
         if (dfl) {
             {
                 KTimer t(ctx, 9, RT);
-                k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->q, n,
-                                                                      w->partials, defl->l, w->u, 1, w->st, 1);
+                launch_wty(defl->w, defl->ld, defl->k, w->q, defl->l, w->u, 1, 1);
                 RCG_LAUNCHED(ctx);
             }
             reduce(5, defl->k * RT, 1, 1, defl->l, defl->k, w->u);
@@ -1830,8 +1961,7 @@ struct BatchSolve {
         if (sc) {
             {
                 KTimer t(ctx, 9, RT);
-                k_b_tallt<RT><<<tgrid(scb->k), kElemThreads, 0, ctx->stream>>>(scb->w, scb->ld, scb->k, w->r, n,
-                                                                      w->partials, scb->l, w->u2, 2, w->st, 1);
+                launch_wty(scb->w, scb->ld, scb->k, w->r, scb->l, w->u2, 2, 1);
                 RCG_LAUNCHED(ctx);
             }
             reduce(5, scb->k * RT, 2, 1, scb->l, scb->k, w->u2);
@@ -1974,15 +2104,13 @@ struct BatchSolve {
         k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, nullptr, 0, 0, nullptr, n, w->st, 2);
         RCG_LAUNCHED(ctx);
         if (defl && defl->k > 0) {  // x = P x + W (W^T A W)^-1 W^T b (pcg.cpp:152-157), finished slots
-            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->aw, defl->ld, defl->k, w->x, n, w->partials,
-                                                                  defl->l, w->u, 1, w->st, 0);
+            launch_wty(defl->aw, defl->ld, defl->k, w->x, defl->l, w->u, 1, 0);
             RCG_LAUNCHED(ctx);
             reduce(5, defl->k * RT, 1, 0, defl->l, defl->k, w->u);
             k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
                                                                            w->st, 0);
             RCG_LAUNCHED(ctx);
-            k_b_tallt<RT><<<tgrid(defl->k), kElemThreads, 0, ctx->stream>>>(defl->w, defl->ld, defl->k, w->b, n, w->partials,
-                                                                  defl->l, w->u, 1, w->st, 0);
+            launch_wty(defl->w, defl->ld, defl->k, w->b, defl->l, w->u, 1, 0);
             RCG_LAUNCHED(ctx);
             reduce(5, defl->k * RT, 1, 0, defl->l, defl->k, w->u);
             k_b_finish_combine<RT><<<sg, kStreamThreads, 0, ctx->stream>>>(w->x, defl->w, defl->ld, defl->k, w->u, n,
