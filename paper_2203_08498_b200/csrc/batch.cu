@@ -1455,7 +1455,7 @@ __global__ void __launch_bounds__(kElemThreads) k_b_fin(BState* st, int which, i
 // multiple of every G), u staged in shared memory (read as broadcasts: the m-loop is instruction-
 // bound at m = 32 otherwise); each value's update runs over j in order (subtract_combination).
 template <int RT>
-__global__ void __launch_bounds__(kElemThreads) k_b_deflate(double* __restrict__ y, const double* __restrict__ Cm,
+__global__ void __launch_bounds__(kElemThreads, 2) k_b_deflate(double* __restrict__ y, const double* __restrict__ Cm,
                                                             int64_t ldc, int m, const double* __restrict__ u,
                                                             const double* __restrict__ p, int32_t n, double* partials,
                                                             BState* st, int mode) {
@@ -1475,45 +1475,64 @@ __global__ void __launch_bounds__(kElemThreads) k_b_deflate(double* __restrict__
     double acc[VW];
 #pragma unroll
     for (int v = 0; v < VW; ++v) acc[v] = 0.0;
-    const int64_t items = static_cast<int64_t>(n) * G;
+    // blocks of DR rows x one chunk per item: the coefficients u[j][chunk] of four columns are
+    // loaded from shared memory once per block (not once per row) and the DR rows' C_j values are
+    // one 32-byte load per column -- shared-memory traffic / DR (it bound the kernel at RT 24)
+    constexpr int DR = 4;
+    const int64_t nblk = (static_cast<int64_t>(n) + DR - 1) / DR;
+    const int64_t items = nblk * G;
     for (int64_t it = blockIdx.x * static_cast<int64_t>(kElemThreads) + threadIdx.x; it < items;
          it += static_cast<int64_t>(gridDim.x) * kElemThreads) {
-        const int64_t i = it / G;
-        const int64_t e0 = it * VW;
-        double yv[VW];
+        const int64_t i0 = (it / G) * DR;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(DR), static_cast<int64_t>(n) - i0));
+        double yv[DR][VW];
 #pragma unroll
-        for (int v = 0; v < VW / 2; ++v) {
-            const double2 t = reinterpret_cast<const double2*>(y + e0)[v];
-            yv[2 * v] = t.x;
-            yv[2 * v + 1] = t.y;
-        }
-        for (int j0 = 0; j0 < m; j0 += 8) {  // eight column loads in flight, then the updates in order
-            const int mm = min(8, m - j0);
-            double cj[8];
+        for (int r = 0; r < DR; ++r)
+            if (r < nr)
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-                if (t < mm) cj[t] = __ldg(Cm + (j0 + t) * ldc + i);
+                for (int v = 0; v < VW; ++v) yv[r][v] = y[(i0 + r) * RT + k0 + v];
+        for (int j0 = 0; j0 < m; j0 += 4) {  // four columns' loads in flight, then the updates in j order
+            const int mm = min(4, m - j0);
+            double cj[4][DR], uj[4][VW];
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
+            for (int t = 0; t < 4; ++t)
+                if (t < mm) {
+                    const double* col = Cm + (j0 + t) * ldc + i0;
+                    if (nr == DR) {
+                        // ldc % 32 == 0 and i0 % 4 == 0: two aligned 16-byte loads
+                        const double2 c01 = __ldg(reinterpret_cast<const double2*>(col));
+                        const double2 c23 = __ldg(reinterpret_cast<const double2*>(col) + 1);
+                        cj[t][0] = c01.x, cj[t][1] = c01.y, cj[t][2] = c23.x, cj[t][3] = c23.y;
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < DR; ++r) cj[t][r] = r < nr ? __ldg(col + r) : 0.0;
+                    }
+#pragma unroll
+                    for (int v = 0; v < VW; ++v) uj[t][v] = us[(j0 + t) * RT + k0 + v];
+                }
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
                 if (t < mm)
 #pragma unroll
-                    for (int v = 0; v < VW; ++v) yv[v] = fsub_mul(yv[v], us[(j0 + t) * RT + k0 + v], cj[t]);
-        }
-        double pv[VW];
-        if (mode == 0) {
+                    for (int r = 0; r < DR; ++r)
 #pragma unroll
-            for (int v = 0; v < VW / 2; ++v) {
-                const double2 t = reinterpret_cast<const double2*>(p + e0)[v];
-                pv[2 * v] = t.x;
-                pv[2 * v + 1] = t.y;
-            }
+                        for (int v = 0; v < VW; ++v) yv[r][v] = fsub_mul(yv[r][v], uj[t][v], cj[t][r]);
         }
 #pragma unroll
-        for (int v = 0; v < VW; ++v)
-            if (run[k0 + v]) {
-                y[e0 + v] = yv[v];
-                acc[v] = mode == 0 ? fadd_mul(acc[v], pv[v], yv[v]) : fadd_mul(acc[v], yv[v], yv[v]);
-            }
+        for (int r = 0; r < DR; ++r) {
+            if (r >= nr) break;
+            const int64_t e0 = (i0 + r) * RT + k0;
+            double pv[VW];
+            if (mode == 0)
+#pragma unroll
+                for (int v = 0; v < VW; ++v) pv[v] = p[e0 + v];
+#pragma unroll
+            for (int v = 0; v < VW; ++v)
+                if (run[k0 + v]) {
+                    y[e0 + v] = yv[r][v];
+                    acc[v] = mode == 0 ? fadd_mul(acc[v], pv[v], yv[r][v]) : fadd_mul(acc[v], yv[r][v], yv[r][v]);
+                }
+        }
     }
     double full[RT];  // this thread's chunk, zeros elsewhere (adding 0.0 is exact)
 #pragma unroll
