@@ -2082,7 +2082,8 @@ struct BatchSolve {
             static const int vw_env = std::getenv("RCG_BSWEEP_VW") ? std::atoi(std::getenv("RCG_BSWEEP_VW")) : 0;
             const bool vw4 = RT == 24 && (vw_env == 4 || (vw_env == 0 && !backward));
             const int rpw = vw4 ? 32 / (RT / 4) : 32 / (RT / 2);
-            const int cmul = RT >= 12 ? 3 : 2;
+            static const int cmul_env = std::getenv("RCG_BSWEEP_CMUL") ? std::atoi(std::getenv("RCG_BSWEEP_CMUL")) : 0;
+            const int cmul = cmul_env > 0 ? cmul_env : (RT >= 12 ? 3 : 2);
             const int ntiles = (s.npos + rpw * 4 - 1) / (rpw * 4);  // CTAs of 4 warp tiles
             const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps0 * cmul));
             const bool rho = backward && s.r;
