@@ -1324,8 +1324,8 @@ __global__ void __launch_bounds__(kWtyThreads) k_b_wty(const double* __restrict_
     extern __shared__ __align__(16) double wsm[];  // [m][kWtyLd] W tile, then [kWtyRows][RT] y tile
     double* ysm = wsm + ((static_cast<int64_t>(m) * kWtyLd + 3) & ~int64_t(3));  // 32-byte aligned
     __shared__ double tot[kMaxRedB];
-    __shared__ double fk[6][128];
-    __shared__ double sol[6][128];
+    __shared__ double fk[kWtyThreads / 32][128];  // fin_tallt: one row per warp
+    __shared__ double sol[kWtyThreads / 32][128];
     __shared__ bool s_last;
     if (respect_done && st->nrun == 0) return;
     const int JB = (m + 3) / 4;
