@@ -682,28 +682,39 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
 // and polling stay those of RT = 2 whatever RT is, the row's values are published chunk by chunk
 // with no coordination between lanes, and a level costs about what it costs at RT = 2.
 template <bool BWD, int RT, int VW, int CH>
-__global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
+__global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, BState* st) {
     constexpr int G = RT / VW;
     constexpr int RPW = 32 / G;
+    constexpr bool ORD = VW == 2;  // consume in order as parents arrive (measured: helps 16-byte chunks only)
+    constexpr unsigned kFull = 0xffffffffu;
     if (st->nrun == 0) return;
     const int lane = threadIdx.x & 31;
     const int rl = lane / G, c = lane % G;
     const bool lane_on = rl < RPW;
     const int ntiles = (a.npos + RPW - 1) / RPW;
+    const bool rho = BWD && a.r;
+    // (measured and dropped: software-pipelining the tiles per warp -- ticket two tiles ahead, row
+    // map and row data one tile ahead -- C3 RT 16 fwd / bwd 4.8 / 6.9 -> 5.5 / 8.8 ms, C2 RT 12 bwd
+    // 0.66 -> 1.03 ms: rows taken early only spin on parents of later levels.)  The r chunk of
+    // the (r, z) partial is requested with the row's input, not after the publish.
+    auto take = [&]() {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&a.tickets[0], 1);
+        return t;
+    };
     while (true) {
-        int tile = 0;
-        if (lane == 0) tile = atomicAdd(&a.tickets[0], 1);
-        tile = __shfl_sync(0xffffffffu, tile, 0);
+        const int tile = __shfl_sync(kFull, take(), 0);
         if (tile >= ntiles) break;
         const int pos = tile * RPW + rl;
+        const int32_t row = (lane_on && pos < a.npos) ? __ldg(a.perm + pos) : -1;
         double contrib[VW];
 #pragma unroll
         for (int v = 0; v < VW; ++v) contrib[v] = 0.0;
-        const int32_t row = (lane_on && pos < a.npos) ? __ldg(a.perm + pos) : -1;
         if (row >= 0) {
             const int64_t me = static_cast<int64_t>(row) * RT + VW * c;
             const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
             double s[VW];
+            double rr[BWD ? VW : 1];
             {
                 const double dr = BWD ? __ldg(a.d + row) : 1.0;
 #pragma unroll
@@ -711,6 +722,16 @@ __global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
                     const double2 t = reinterpret_cast<const double2*>(a.in + me)[v];
                     s[2 * v] = BWD ? __ddiv_rn(t.x, dr) : t.x;
                     s[2 * v + 1] = BWD ? __ddiv_rn(t.y, dr) : t.y;
+                }
+            }
+            if constexpr (BWD) {
+                if (rho) {
+#pragma unroll
+                    for (int v = 0; v < VW / 2; ++v) {
+                        const double2 t = reinterpret_cast<const double2*>(a.r + me)[v];
+                        rr[2 * v] = t.x;
+                        rr[2 * v + 1] = t.y;
+                    }
                 }
             }
             unsigned spins = 0;
@@ -729,19 +750,38 @@ __global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
                     if (j < cnt) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + VW * c, dep[j]);
+                int used = 0;
                 while (true) {
-                    bool any = false;
+                    if constexpr (ORD) {
 #pragma unroll
-                    for (int j = 0; j < CH; ++j)
-                        if (j < cnt)
+                        for (int j = 0; j < CH; ++j)
+                            if (j == used && j < cnt) {
+                                bool m = false;
 #pragma unroll
-                            for (int v = 0; v < VW; ++v) any |= is_sentinel(dep[j][v]);
-                    if (!any) {
+                                for (int v = 0; v < VW; ++v) m |= is_sentinel(dep[j][v]);
+                                if (!m) {
+#pragma unroll
+                                    for (int v = 0; v < VW; ++v) s[v] = fsub_mul(s[v], val[j], dep[j][v]);
+                                    used = j + 1;
+                                }
+                            }
+                    } else {
+                        bool any = false;
 #pragma unroll
                         for (int j = 0; j < CH; ++j)
                             if (j < cnt)
 #pragma unroll
-                                for (int v = 0; v < VW; ++v) s[v] = fsub_mul(s[v], val[j], dep[j][v]);
+                                for (int v = 0; v < VW; ++v) any |= is_sentinel(dep[j][v]);
+                        if (!any) {
+#pragma unroll
+                            for (int j = 0; j < CH; ++j)
+                                if (j < cnt)
+#pragma unroll
+                                    for (int v = 0; v < VW; ++v) s[v] = fsub_mul(s[v], val[j], dep[j][v]);
+                            used = cnt;
+                        }
+                    }
+                    if (used >= cnt) {
                         if (last) {
                             double t[VW];
 #pragma unroll
@@ -753,7 +793,7 @@ __global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
                     if (a.backoff_ns) __nanosleep(a.backoff_ns);
 #pragma unroll
                     for (int j = 0; j < CH; ++j)
-                        if (j < cnt) {
+                        if (j >= used && j < cnt) {
                             bool m = false;
 #pragma unroll
                             for (int v = 0; v < VW; ++v) m |= is_sentinel(dep[j][v]);
@@ -770,16 +810,14 @@ __global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
                 }
                 if (last) break;
             }
-            if (BWD && a.r) {
+            if constexpr (BWD) {
+                if (rho) {
 #pragma unroll
-                for (int v = 0; v < VW / 2; ++v) {
-                    const double2 t = reinterpret_cast<const double2*>(a.r + me)[v];
-                    contrib[2 * v] = __dmul_rn(t.x, s[2 * v]);
-                    contrib[2 * v + 1] = __dmul_rn(t.y, s[2 * v + 1]);
+                    for (int v = 0; v < VW; ++v) contrib[v] = __dmul_rn(rr[v], s[v]);
                 }
             }
         }
-        if (BWD && a.r) {
+        if (rho) {
             // per-tile partials: chunk c's RPW rows sit on lanes c, c+G, ..., summed in row order
             // (RPW-1 strided shuffles per value); k_b_rho sums the tiles in a fixed order
             double tot[VW];
@@ -788,7 +826,7 @@ __global__ void __launch_bounds__(128) k_b_sweepc(SweepArgs a, BState* st) {
 #pragma unroll
             for (int r = 1; r < RPW; ++r)
 #pragma unroll
-                for (int v = 0; v < VW; ++v) tot[v] = __dadd_rn(tot[v], __shfl_sync(0xffffffffu, contrib[v], c + r * G));
+                for (int v = 0; v < VW; ++v) tot[v] = __dadd_rn(tot[v], __shfl_sync(kFull, contrib[v], c + r * G));
             if (lane < G)
 #pragma unroll
                 for (int v = 0; v < VW; ++v) a.partials[static_cast<int64_t>(tile) * RT + lane * VW + v] = tot[v];
@@ -2088,20 +2126,18 @@ struct BatchSolve {
             const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps0 * cmul));
             const bool rho = backward && s.r;
             if (rho) s.partials = w->tpart;
+            // (measured and dropped, C3 RT 24 fwd / bwd ms: 7 parents per chunk 6.9 / 14.4, 13 per
+            // chunk -- 147 registers -- slower still; L1-cached first loads of the older parents
+            // 7.4 / 16.4: stale sentinel sectors in L1 cost more re-polls than the hits save)
+            auto go = [&](auto kern) { kern<<<grid, 128, 0, ctx->stream>>>(s, w->st); };
+            bool launched = false;
             if constexpr (RT == 24) {
                 if (vw4) {
-                    if (backward)
-                        k_b_sweepc<true, RT, 4, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
-                    else
-                        k_b_sweepc<false, RT, 4, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
+                    launched = true;
+                    backward ? go(k_b_sweepc<true, RT, 4, 4>) : go(k_b_sweepc<false, RT, 4, 4>);
                 }
             }
-            if (!vw4) {
-                if (backward)
-                    k_b_sweepc<true, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
-                else
-                    k_b_sweepc<false, RT, 2, 4><<<grid, 128, 0, ctx->stream>>>(s, w->st);
-            }
+            if (!launched) backward ? go(k_b_sweepc<true, RT, 2, 4>) : go(k_b_sweepc<false, RT, 2, 4>);
             RCG_LAUNCHED(ctx);
             if (rho) {
                 const int64_t tiles = (s.npos + rpw - 1) / rpw;

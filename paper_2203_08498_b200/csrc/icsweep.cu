@@ -30,6 +30,7 @@
 namespace rcg {
 
 constexpr int kDepChunk = 8;
+constexpr int kDepChunkWide = 16;  // factors of more than kDepChunk entries per row (27-point: 13)
 
 constexpr int kTile = 32;  // positions per ticket: one warp
 
@@ -73,8 +74,8 @@ __device__ __forceinline__ bool tile_reduce(double v, int tile, int ntiles, Swee
 // tiles of the level-sorted order from an atomic ticket until none is left (tickets are
 // monotone, so every row a warp can wait on belongs to a running warp: no deadlock).  Bounding
 // the resident CTAs bounds how many future-level rows spin at once.
-template <bool BWD>
-__global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
+template <bool BWD, int CH>
+__global__ void __launch_bounds__(kSweepThreads, CH > 8 ? 4 : 8) k_sweep(SweepArgs a) {
     if (a.st->done) return;
     const int lane = threadIdx.x & 31;
     const int ntiles = (a.npos + kTile - 1) / kTile;
@@ -94,45 +95,53 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
             } else {
                 s = a.in[row];
             }
-            // Entries in chunks of kDepChunk: all parents of a chunk are loaded together and
-            // the missing ones re-polled together (one L2 round trip after the last parent is
-            // published).  On the last chunk the row is published from inside the wait loop, so
-            // a lane never waits for slower lanes of its warp before releasing its dependants.
+            // Entries in chunks of CH: all parents of a chunk are loaded together and the missing
+            // ones re-polled together (one L2 round trip after the last parent is published;
+            // consuming them in order as they arrive measured slower: C3 fwd 3.5 -> 4.2 ms).  A row that fits one chunk has
+            // every parent in flight from the start: in the BACKWARD sweep the first entry
+            // (column i + 1) is the parent published last, so with several chunks every later
+            // chunk was a dependent L2 round trip on the level's critical path (CH = 16 for
+            // factors of more than 8 entries per row).  On the last chunk the row is published
+            // from inside the wait loop, so a lane never waits for slower lanes of its warp.
             unsigned spins = 0;
-            for (int32_t e0 = beg;; e0 += kDepChunk) {
-                const int cnt = min(kDepChunk, end - e0);
-                const bool last = e0 + kDepChunk >= end;
-                int32_t col[kDepChunk];
-                double val[kDepChunk], dep[kDepChunk];
+            for (int32_t e0 = beg;; e0 += CH) {
+                const int cnt = min(CH, end - e0);
+                const bool last = e0 + CH >= end;
+                int32_t col[CH];
+                double val[CH], dep[CH];
 #pragma unroll
-                for (int j = 0; j < kDepChunk; ++j)
+                for (int j = 0; j < CH; ++j)
                     if (j < cnt) {
                         col[j] = __ldg(a.pcol + e0 + j);
                         val[j] = __ldg(a.pval + e0 + j);
                     }
 #pragma unroll
-                for (int j = 0; j < kDepChunk; ++j)
+                for (int j = 0; j < CH; ++j)
                     if (j < cnt) dep[j] = ld_relaxed(a.out + col[j]);
+                int used = 0;
                 while (true) {
                     bool missing = false;
 #pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
+                    for (int j = 0; j < CH; ++j)
                         if (j < cnt && is_sentinel(dep[j])) missing = true;
                     if (!missing) {
 #pragma unroll
-                        for (int j = 0; j < kDepChunk; ++j)
+                        for (int j = 0; j < CH; ++j)
                             if (j < cnt) s = fsub_mul(s, val[j], dep[j]);
+                        used = cnt;
+                    }
+                    if (used >= cnt) {
                         if (last) st_relaxed(a.out + row, publishable(s));
                         break;
                     }
                     if (a.backoff_ns) __nanosleep(a.backoff_ns);
 #pragma unroll
-                    for (int j = 0; j < kDepChunk; ++j)
-                        if (j < cnt && is_sentinel(dep[j])) dep[j] = ld_relaxed(a.out + col[j]);
+                    for (int j = 0; j < CH; ++j)
+                        if (j >= used && j < cnt && is_sentinel(dep[j])) dep[j] = ld_relaxed(a.out + col[j]);
                     if (++spins == (1u << 24)) {  // bounded: a schedule fault is an error, never a hang
                         atomicExch(&a.tickets[3], 1);
 #pragma unroll
-                        for (int j = 0; j < kDepChunk; ++j)
+                        for (int j = 0; j < CH; ++j)
                             if (j < cnt && is_sentinel(dep[j])) dep[j] = 0.0;
                     }
                 }
@@ -168,8 +177,10 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep(SweepArgs a) {
 void sweep_prepare_kernels() {
     static bool done = false;
     if (done) return;
-    set_carveout(reinterpret_cast<const void*>(k_sweep<false>));
-    set_carveout(reinterpret_cast<const void*>(k_sweep<true>));
+    set_carveout(reinterpret_cast<const void*>(k_sweep<false, kDepChunk>));
+    set_carveout(reinterpret_cast<const void*>(k_sweep<true, kDepChunk>));
+    set_carveout(reinterpret_cast<const void*>(k_sweep<false, kDepChunkWide>));
+    set_carveout(reinterpret_cast<const void*>(k_sweep<true, kDepChunkWide>));
     done = true;
 }
 
@@ -194,29 +205,38 @@ SweepArgs sweep_args(rcg_ctx* ctx, const rcg_ic* f, bool backward) {
 // levels can use only spin and add L2 polling traffic, and too few leave a wide level's rows
 // waiting on their load chains.  Measured on B200 with 32-row warp tiles:
 //   rows/level   5.5K (C2)  9.4K (C3, 27-pt)  87K (C4)  262K (C2 multicolour)
-//   best         2          fwd 2 / bwd 1     3         8
-// A backward row with more than one chunk of parents (kDepChunk) spins on more lines per poll.
+//   best         2          2                 3         8
+// (C3's backward sweep: 5.5 ms at 1 CTA per SM with two dependency chunks, 3.7 ms at 2 with every
+// parent in flight -- kDepChunkWide; 4.9 ms at 3)
 int sweep_ctas_per_sm(const rcg_ic* f, bool backward, int64_t npos) {
     const int levels = backward ? f->bwd_levels : f->fwd_levels;
     const int64_t rows_per_level = levels > 0 ? npos / levels : npos;
     if (rows_per_level >= 200000) return 8;
     if (rows_per_level >= 32768) return 3;
     const double entries_per_row = f->n > 0 ? static_cast<double>(f->nnz_l) / f->n : 0.0;
-    return backward && entries_per_row > kDepChunk ? 1 : 2;
+    (void)entries_per_row;  // (round 1: 1 CTA per SM for long backward rows -- the wide chunk removed the reason)
+    return 2;
 }
 
 void launch_sweep(rcg_ctx* ctx, const rcg_ic* f, bool backward, SweepArgs& a) {
     if (f->n == 0) return;
     if (launch_level_sweep(ctx, f, backward, a)) return;  // wide levels: one launch per level (icsweep_lv.cu)
     const int ntiles = (a.npos + kSweepThreads - 1) / kSweepThreads;
-    const int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
+    static const int bps_bwd_env = std::getenv("RCG_SWEEP_BPS_BWD") ? std::atoi(std::getenv("RCG_SWEEP_BPS_BWD")) : 0;  // A/B
+    int bps = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, backward, a.npos);
+    if (backward && bps_bwd_env > 0) bps = bps_bwd_env;
     const int grid = std::max(1, std::min(ntiles, ctx->num_sms * bps));
     a.backoff_ns = ctx->sweep_backoff_ns;
     KTimer t(ctx, backward ? 2 : 1);
+    // RCG_SWEEP_CH=8 / 16 forces the dependency chunk (A/B); default: wide for long backward rows
+    static const int ch_env = std::getenv("RCG_SWEEP_CH") ? std::atoi(std::getenv("RCG_SWEEP_CH")) : 0;
+    const double entries_per_row = static_cast<double>(f->nnz_l) / f->n;
+    const bool wide = ch_env ? ch_env > kDepChunk : (backward && entries_per_row > kDepChunk);
+    auto go = [&](auto kern) { kern<<<grid, kSweepThreads, 0, ctx->stream>>>(a); };
     if (backward)
-        k_sweep<true><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
+        wide ? go(k_sweep<true, kDepChunkWide>) : go(k_sweep<true, kDepChunk>);
     else
-        k_sweep<false><<<grid, kSweepThreads, 0, ctx->stream>>>(a);
+        wide ? go(k_sweep<false, kDepChunkWide>) : go(k_sweep<false, kDepChunk>);
     RCG_LAUNCHED(ctx);
 }
 

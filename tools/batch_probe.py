@@ -14,7 +14,7 @@ def main():
     ctx = api.Context(0)
     h = problems.generate(cfg)
     p = sequence.prepare(ctx, cfg, h, validate=False)
-    bs = [sequence.rhs(p, k % cfg.n_rhs)[1] for k in range(16)]
+    bs = [sequence.rhs(p, k % cfg.n_rhs)[1] for k in range(24)]
     for R in [int(v) for v in os.environ.get("RS", "1,2,4,8,9,12,16").split(",")]:
         B = np.stack(bs[:R])
         for rep in range(2):

@@ -27,9 +27,14 @@ def main():
     basis = api.Basis(ctx, p.a, w, "sc" if kind == "sc" else "deflation")
     B = np.stack([sequence.rhs(p, k % cfg.n_rhs)[1] for k in range(R)])
     X = np.zeros_like(B)
+    # three single-RHS ICCG iterations first (k_sweep / k_spmv_pq / k_pupdate / k_xr for the capture)
+    x1 = np.zeros(h.n)
+    api.pcg_solve(ctx, p.a, B[0], api.Ic(p.ic), x1, cfg.eps, 3)
     ctx.set_profiling(True)
     ctx.reset_stats()
-    if kind == "sc":
+    if kind == "none":
+        api.pcg_solve_batch(ctx, p.a, B, api.Ic(p.ic), X, cfg.eps, iters)
+    elif kind == "sc":
         api.pcg_solve_batch(ctx, p.a, B, api.Sc(basis, p.ic), X, cfg.eps, iters)
     else:
         api.deflated_pcg_solve_batch(ctx, p.a, B, api.Ic(p.ic), basis, X, cfg.eps, iters)
