@@ -1351,7 +1351,8 @@ __global__ void __launch_bounds__(kElemThreads, RT <= 8 ? 4 : 6) k_b_tallt(const
 // CTAs are combined in a fixed order; the finaliser is k_b_tallt's.
 constexpr int kWtyThreads = 256;
 constexpr int kWtyRows = 64;
-constexpr int kWtyLd = kWtyRows + 1;  // padded W-tile row: the warp's ~6 columns in distinct banks
+constexpr int kWtyLd = kWtyRows + 2;  // padded W-tile row (16-byte multiple for the bulk copies); a thread's columns
+                                     // are jb, jb + JB, ...: the warp's ~6 consecutive jb fall in distinct banks
 
 template <int RT>
 __global__ void __launch_bounds__(kWtyThreads) k_b_wty(const double* __restrict__ W, int64_t ldw, int m,
@@ -1359,8 +1360,7 @@ __global__ void __launch_bounds__(kWtyThreads) k_b_wty(const double* __restrict_
                                                         const double* __restrict__ L, double* __restrict__ u, int mode,
                                                         BState* st, int respect_done) {
     constexpr int KB = RT / 4;  // rhs blocks of 4
-    extern __shared__ __align__(16) double wsm[];  // [m][kWtyLd] W tile, then [kWtyRows][RT] y tile
-    double* ysm = wsm + ((static_cast<int64_t>(m) * kWtyLd + 3) & ~int64_t(3));  // 32-byte aligned
+    extern __shared__ __align__(16) double wsm[];  // two stages of: [m][kWtyLd] W tile, [kWtyRows][RT] y tile
     __shared__ double tot[kMaxRedB];
     __shared__ double fk[kWtyThreads / 32][128];  // fin_tallt: one row per warp
     __shared__ double sol[kWtyThreads / 32][128];
@@ -1372,28 +1372,65 @@ __global__ void __launch_bounds__(kWtyThreads) k_b_wty(const double* __restrict_
     const int tid = threadIdx.x;
     const int blk = tid % nblk, grp = tid / nblk;
     const bool active = grp < groups && nblk <= kWtyThreads;
-    const int j0 = (blk / KB) * 4, k0 = (blk % KB) * 4;
+    const int jb = blk / KB, k0 = (blk % KB) * 4;  // columns jb + a JB, a = 0..3
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    // Two stages filled by the TMA bulk engine: one warp requests the NEXT tile (m column segments
+    // of 512 bytes and the contiguous y tile, completion on the stage's mbarrier) before the
+    // current one is summed -- the synchronous version stalled every tile on its own loads (ncu:
+    // 2.0 TB/s at RT 24).  The ragged last tile is filled by plain loads.
     const int64_t ntile = (static_cast<int64_t>(n) + kWtyRows - 1) / kWtyRows;
-    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    const int64_t w_d = (static_cast<int64_t>(m) * kWtyLd + 3) & ~int64_t(3);
+    const int64_t stage_d = w_d + static_cast<int64_t>(kWtyRows) * RT;
+    __shared__ uint64_t bar[2];
+    if (tid == 0) {
+        mbar_init(&bar[0]);
+        mbar_init(&bar[1]);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int lane_i = tid & 31;
+    auto is_full = [&](int64_t t) { return (t + 1) * kWtyRows <= static_cast<int64_t>(n); };
+    auto request = [&](int64_t t, int sidx) {  // warp 0
+        double* ws = wsm + sidx * stage_d;
+        const int64_t i0 = t * kWtyRows;
+        if (lane_i == 0) mbar_expect_tx(&bar[sidx], static_cast<unsigned>(8 * (m * kWtyRows + kWtyRows * RT)));
+        __syncwarp();
+        for (int j = lane_i; j < m; j += 32) bulk_g2s(ws + j * kWtyLd, W + j * ldw + i0, kWtyRows * 8, &bar[sidx]);
+        if (lane_i == 0) bulk_g2s(ws + w_d, y + i0 * RT, kWtyRows * RT * 8, &bar[sidx]);
+    };
+    if (blockIdx.x < ntile && is_full(blockIdx.x) && tid < 32) request(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x, ++it) {
+        const int sidx = it & 1;
         const int64_t i0 = t * kWtyRows;
         const int rows = static_cast<int>(min(static_cast<int64_t>(kWtyRows), static_cast<int64_t>(n) - i0));
-        for (int e = tid; e < m * kWtyRows; e += kWtyThreads) {
-            const int j = e / kWtyRows, r = e % kWtyRows;
-            wsm[j * kWtyLd + r] = r < rows ? __ldg(W + j * ldw + i0 + r) : 0.0;
+        const int64_t tn = t + gridDim.x;
+        if (tn < ntile && is_full(tn) && tid < 32) {
+            fence_proxy_async();
+            request(tn, sidx ^ 1);
         }
-        for (int e = tid; e < kWtyRows * RT; e += kWtyThreads)
-            ysm[e] = e < rows * RT ? __ldg(y + i0 * RT + e) : 0.0;
-        __syncthreads();
+        double* ws = wsm + sidx * stage_d;
+        double* ysm = ws + w_d;
+        if (is_full(t)) {
+            while (!mbar_try_wait(&bar[sidx], (it >> 1) & 1)) {
+            }
+        } else {
+            for (int e = tid; e < m * kWtyRows; e += kWtyThreads) {
+                const int j = e / kWtyRows, r = e % kWtyRows;
+                ws[j * kWtyLd + r] = r < rows ? __ldg(W + j * ldw + i0 + r) : 0.0;
+            }
+            for (int e = tid; e < kWtyRows * RT; e += kWtyThreads) ysm[e] = e < rows * RT ? __ldg(y + i0 * RT + e) : 0.0;
+            __syncthreads();
+        }
         if (active)
             for (int r = grp; r < rows; r += groups) {
                 double wv[4];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) wv[a] = j0 + a < m ? wsm[(j0 + a) * kWtyLd + r] : 0.0;
+                for (int a = 0; a < 4; ++a) wv[a] = jb + a * JB < m ? ws[(jb + a * JB) * kWtyLd + r] : 0.0;
                 const double4 yv = *reinterpret_cast<const double4*>(ysm + r * RT + k0);
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
@@ -1411,7 +1448,7 @@ __global__ void __launch_bounds__(kWtyThreads) k_b_wty(const double* __restrict_
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-                if (j0 + a < m) wsm[static_cast<int64_t>(grp) * m * RT + (j0 + a) * RT + k0 + b] = acc[a][b];
+                if (jb + a * JB < m) wsm[static_cast<int64_t>(grp) * m * RT + (jb + a * JB) * RT + k0 + b] = acc[a][b];
     __syncthreads();
     const int X = gridDim.x;
     for (int o = tid; o < m * RT; o += kWtyThreads) {
@@ -1447,7 +1484,7 @@ template <int RT>
 size_t wty_smem(int m) {
     const int nblk = ((m + 3) / 4) * (RT / 4);
     const int groups = std::max(1, kWtyThreads / nblk);
-    const size_t tiles = ((static_cast<size_t>(m) * kWtyLd + 3) & ~size_t(3)) + static_cast<size_t>(kWtyRows) * RT;
+    const size_t tiles = 2 * (((static_cast<size_t>(m) * kWtyLd + 3) & ~size_t(3)) + static_cast<size_t>(kWtyRows) * RT);
     return sizeof(double) * std::max(tiles, static_cast<size_t>(groups) * m * RT);
 }
 
@@ -1536,8 +1573,9 @@ __global__ void __launch_bounds__(kElemThreads, 2) k_b_deflate(double* __restric
             for (int t = 0; t < 4; ++t)
                 if (t < mm) {
                     const double* col = Cm + (j0 + t) * ldc + i0;
-                    if (nr == DR) {
-                        // ldc % 32 == 0 and i0 % 4 == 0: two aligned 16-byte loads
+                    if (nr == DR && (ldc & 1) == 0) {
+                        // even ldc (32-row padded blocks; a row slab's ld is its row count) and
+                        // i0 % 4 == 0: two aligned 16-byte loads
                         const double2 c01 = __ldg(reinterpret_cast<const double2*>(col));
                         const double2 c23 = __ldg(reinterpret_cast<const double2*>(col) + 1);
                         cj[t][0] = c01.x, cj[t][1] = c01.y, cj[t][2] = c23.x, cj[t][3] = c23.y;
@@ -1580,6 +1618,152 @@ __global__ void __launch_bounds__(kElemThreads, 2) k_b_deflate(double* __restric
         if (cc == c)
 #pragma unroll
             for (int v = 0; v < VW; ++v) full[cc * VW + v] = acc[v];
+    block_sum_dyn<RT>(full, RT, scratch, vals);
+    if (grid_reduce_dyn(vals, RT, partials, &st->tick[3], tot)) {
+        if (st->defer) {
+            if (threadIdx.x < RT) st->dtot[threadIdx.x] = tot[threadIdx.x];
+            return;
+        }
+        if (threadIdx.x < RT) {
+            if (mode == 0)
+                fin_pq(st, tot, threadIdx.x);
+            else
+                fin_projcheck(st, tot, threadIdx.x);
+        }
+    }
+}
+
+// k_b_deflate with the operands staged by the TMA bulk engine (RT 16 / 24, m <= 48).  The
+// register version keeps only ~8 KB per SM in flight (a warp's 16-byte C_j loads hit 5-6 distinct
+// addresses; 146 registers, 2 CTAs per SM: ncu 2.4 TB/s at RT 24); here a CTA walks 64-row tiles,
+// one elected warp requests the NEXT tile -- m column segments of 512 bytes, the y tile and the p
+// tile, one cp.async.bulk each, completion on the stage's mbarrier -- while the CTA updates the
+// current one out of shared memory: 40 KB per CTA in flight at m = 32, RT = 24.  A thread owns 4
+// consecutive rows x one 4-value chunk (C_j and u_j are one 32-byte shared load each per 16
+// updates); every value's update runs over j in order (subtract_combination), bitwise k_b_deflate.
+constexpr int kDtRows = 64;
+template <int RT>
+constexpr int dt_threads() { return kDtRows / 4 * (RT / 4); }
+template <int RT>
+size_t dt_smem(int m, bool with_p) {
+    return sizeof(double) * (static_cast<size_t>(m) * RT + 2 * (static_cast<size_t>(m) * kDtRows + kDtRows * RT * (with_p ? 2 : 1))) + 16;
+}
+
+template <int RT>
+__global__ void __launch_bounds__(dt_threads<RT>()) k_b_deflate_t(double* __restrict__ y, const double* __restrict__ Cm,
+                                                                  int64_t ldc, int m, const double* __restrict__ u,
+                                                                  const double* __restrict__ p, int32_t n,
+                                                                  double* partials, BState* st, int mode) {
+    constexpr int G = RT / 4;
+    constexpr int TR = kDtRows;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ double scratch[32 * RT];
+    __shared__ double vals[RT];
+    __shared__ double tot[RT];
+    __shared__ int run[RT];
+    if (st->nrun == 0 && mode == 0) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    double* us = reinterpret_cast<double*>(dsm);
+    const int64_t ss = static_cast<int64_t>(m) * TR + TR * RT * (p ? 2 : 1);  // doubles per stage
+    double* stage0 = us + static_cast<int64_t>(m) * RT;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stage0 + 2 * ss);
+    if (tid == 0) {
+        mbar_init(&bar[0]);
+        mbar_init(&bar[1]);
+        fence_mbar_init();
+    }
+    for (int t = tid; t < m * RT; t += blockDim.x) us[t] = u[t];
+    if (tid < RT) run[tid] = mode == 1 || st->done[tid] == kRunning;
+    __syncthreads();
+    const int64_t ntile = (static_cast<int64_t>(n) + TR - 1) / TR;
+    const unsigned tile_bytes = static_cast<unsigned>(sizeof(double) * ss);
+    auto is_full = [&](int64_t t) { return (t + 1) * TR <= static_cast<int64_t>(n); };
+    auto issue = [&](int64_t t, int sidx) {  // warp 0: lane j requests column j (+ y, p by lanes 0, 1)
+        double* C = stage0 + sidx * ss;
+        const int64_t i0 = t * TR;
+        if (lane == 0) mbar_expect_tx(&bar[sidx], tile_bytes);
+        __syncwarp();
+        for (int j = lane; j < m; j += 32) bulk_g2s(C + j * TR, Cm + j * ldc + i0, TR * 8, &bar[sidx]);
+        if (lane == 0) bulk_g2s(C + m * TR, y + i0 * RT, TR * RT * 8, &bar[sidx]);
+        if (lane == 1 && p) bulk_g2s(C + m * TR + TR * RT, p + i0 * RT, TR * RT * 8, &bar[sidx]);
+    };
+    const int rb = tid / G, c = tid % G, k0 = c * 4, r0 = rb * 4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t t = blockIdx.x;
+    if (t < ntile && is_full(t) && tid < 32) issue(t, 0);
+    for (int k = 0; t < ntile; t += gridDim.x, ++k) {
+        const int sidx = k & 1;
+        const int64_t tn = t + gridDim.x;
+        if (tn < ntile && is_full(tn) && tid < 32) {
+            fence_proxy_async();  // the stage's generic reads of two tiles ago before the async writes
+            issue(tn, sidx ^ 1);
+        }
+        double* C = stage0 + sidx * ss;
+        double* ys = C + m * TR;
+        double* ps = ys + TR * RT;
+        const int64_t i0 = t * TR;
+        if (is_full(t)) {
+            while (!mbar_try_wait(&bar[sidx], (k >> 1) & 1)) {
+            }
+        } else {  // the ragged last tile: plain loads, zero padding
+            const int rows = static_cast<int>(static_cast<int64_t>(n) - i0);
+            for (int e = tid; e < m * TR; e += blockDim.x) {
+                const int j = e / TR, r = e % TR;
+                C[e] = r < rows ? __ldg(Cm + j * ldc + i0 + r) : 0.0;
+            }
+            for (int e = tid; e < TR * RT; e += blockDim.x) {
+                ys[e] = e < rows * RT ? y[i0 * RT + e] : 0.0;
+                if (p) ps[e] = e < rows * RT ? p[i0 * RT + e] : 0.0;
+            }
+            __syncthreads();
+        }
+        double yv[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double4 t4 = *reinterpret_cast<const double4*>(ys + (r0 + r) * RT + k0);
+            yv[r][0] = t4.x, yv[r][1] = t4.y, yv[r][2] = t4.z, yv[r][3] = t4.w;
+        }
+#pragma unroll 4
+        for (int j = 0; j < m; ++j) {
+            const double4 cj4 = *reinterpret_cast<const double4*>(C + j * TR + r0);
+            const double4 uj4 = *reinterpret_cast<const double4*>(us + j * RT + k0);
+            const double cj[4] = {cj4.x, cj4.y, cj4.z, cj4.w};
+            const double uj[4] = {uj4.x, uj4.y, uj4.z, uj4.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) yv[r][v] = fsub_mul(yv[r][v], uj[v], cj[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (i0 + r0 + r >= static_cast<int64_t>(n)) break;
+            const int64_t e0 = (i0 + r0 + r) * RT + k0;
+            const double4 o4 = *reinterpret_cast<const double4*>(ys + (r0 + r) * RT + k0);
+            const double old[4] = {o4.x, o4.y, o4.z, o4.w};
+            double pv[4] = {0.0, 0.0, 0.0, 0.0};
+            if (mode == 0) {
+                const double4 p4 = *reinterpret_cast<const double4*>(ps + (r0 + r) * RT + k0);
+                pv[0] = p4.x, pv[1] = p4.y, pv[2] = p4.z, pv[3] = p4.w;
+            }
+            double out[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                out[v] = run[k0 + v] ? yv[r][v] : old[v];
+                if (run[k0 + v])
+                    acc[v] = mode == 0 ? fadd_mul(acc[v], pv[v], yv[r][v]) : fadd_mul(acc[v], yv[r][v], yv[r][v]);
+            }
+            *reinterpret_cast<double4*>(y + e0) = make_double4(out[0], out[1], out[2], out[3]);
+        }
+        __syncthreads();  // the stage is free for the tile after next
+    }
+    double full[RT];  // this thread's chunk, zeros elsewhere (adding 0.0 is exact)
+#pragma unroll
+    for (int q = 0; q < RT; ++q) full[q] = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < G; ++cc)
+        if (cc == c)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) full[cc * 4 + v] = acc[v];
     block_sum_dyn<RT>(full, RT, scratch, vals);
     if (grid_reduce_dyn(vals, RT, partials, &st->tick[3], tot)) {
         if (st->defer) {
@@ -1878,7 +2062,7 @@ struct BatchSolve {
                     int respect_done) {
         static const int use = std::getenv("RCG_WTY") ? std::atoi(std::getenv("RCG_WTY")) : 1;
         if constexpr (RT % 4 == 0) {
-            if (use && mcols >= 1 && mcols <= 128 && static_cast<int64_t>(mcols) * RT <= kMaxRedB) {
+            if (use && mcols >= 1 && mcols <= 128 && static_cast<int64_t>(mcols) * RT <= kMaxRedB && ld % 2 == 0) {
                 static bool attr = false;
                 if (!attr) {
                     RCG_CK(cudaFuncSetAttribute(k_b_wty<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -1895,6 +2079,30 @@ struct BatchSolve {
         }
         k_b_tallt<RT><<<tgrid(mcols), kElemThreads, 0, ctx->stream>>>(Wm, ld, mcols, yv, n, w->partials, Lf, uo, mode,
                                                                        w->st, respect_done);
+    }
+
+    // y -= C u (+ (p, y) or the projected-residual check): the TMA-staged kernel at RT 16 / 24
+    // (RCG_DEFLATE_T=0: the register kernel)
+    void launch_deflate(double* yv, const double* Cm, int64_t ldc, int mcols, const double* uv, const double* pv,
+                        int mode) {
+        static const int use = std::getenv("RCG_DEFLATE_T") ? std::atoi(std::getenv("RCG_DEFLATE_T")) : 1;
+        if constexpr (RT == 16 || RT == 24) {
+            if (use && mcols >= 1 && mcols <= 48 && ldc % 2 == 0 && n >= kDtRows) {
+                static bool attr = false;
+                if (!attr) {
+                    RCG_CK(cudaFuncSetAttribute(k_b_deflate_t<RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                    attr = true;
+                }
+                const size_t smem = dt_smem<RT>(mcols, pv != nullptr);
+                const int64_t ntile = (static_cast<int64_t>(n) + kDtRows - 1) / kDtRows;
+                const int per_sm = std::max(1, std::min(3, static_cast<int>((220 * 1024) / (smem + 16 * 1024))));
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntile, ctx->num_sms * per_sm)));
+                k_b_deflate_t<RT><<<grid, dt_threads<RT>(), smem, ctx->stream>>>(yv, Cm, ldc, mcols, uv, pv, n, w->partials,
+                                                                               w->st, mode);
+                return;
+            }
+        }
+        k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(yv, Cm, ldc, mcols, uv, pv, n, w->partials, w->st, mode);
     }
 
     // k_b_tallt grid: X row ranges x P sibling column passes, one wave (4-6 CTAs per SM)
@@ -1947,8 +2155,7 @@ struct BatchSolve {
             launch_wty(defl->w, defl->ld, defl->k, w->r, defl->l, w->u, 1, 0);
             RCG_LAUNCHED(ctx);
             reduce(5, defl->k * RT, 1, 0, defl->l, defl->k, w->u);
-            k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr,
-                                                                    n, w->partials, w->st, 1);
+            launch_deflate(w->r, defl->aw, defl->ld, defl->k, w->u, nullptr, 1);
             RCG_LAUNCHED(ctx);
             reduce(3, RT, 0, 0);
         }
@@ -2004,8 +2211,7 @@ struct BatchSolve {
             reduce(5, defl->k * RT, 1, 1, defl->l, defl->k, w->u);
             {
                 KTimer t(ctx, 9, RT);
-                k_b_deflate<RT><<<eg, kElemThreads, 0, ctx->stream>>>(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, n,
-                                                                        w->partials, w->st, 0);
+                launch_deflate(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, 0);
                 RCG_LAUNCHED(ctx);
             }
             reduce(2, RT, 0, 1);

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+run() { echo "== $*" >> gpurun_out/ab8.log; env "$@" >> gpurun_out/ab8.log 2>&1; }
+run A=default timeout 600 python tools/profile_batched.py c3 24 20 deflation
+run RCG_DEFLATE_T=0 timeout 600 python tools/profile_batched.py c3 24 20 deflation
+run A=default timeout 600 python tools/profile_batched.py c3 16 20 sc
+timeout 1500 python -m pytest tests/test_gpu_batch.py tests/test_gpu_dist.py tests/test_gpu_dist_host.py tests/test_gpu_sequence.py tests/test_gpu_golden.py -m gpu -q -p no:cacheprovider > gpurun_out/ab8_tests.log 2>&1
