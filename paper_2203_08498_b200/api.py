@@ -721,9 +721,12 @@ class Comm:
         import torch.distributed as dist
 
         nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+        calls = {"allreduce": 0, "allreduce_values": 0, "exchange": 0}  # collectives issued (tests / reports)
 
         def allreduce(_user, buf, count):
             try:
+                calls["allreduce"] += 1
+                calls["allreduce_values"] += int(count)
                 t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(count,)))
                 dist.all_reduce(t, group=group)
                 return 0
@@ -732,6 +735,7 @@ class Comm:
 
         def exchange(_user, send, so, sc, recv, ro, rc, np_):
             try:
+                calls["exchange"] += 1
                 reqs = []
                 for q in range(np_):
                     if sc[q]:
@@ -752,6 +756,7 @@ class Comm:
         check(lib.rcg_comm_create_host(int(nranks), int(rank), cb_ar, cb_ex, None, C.byref(h)))
         c = cls(h, nranks)
         c._callbacks = (cb_ar, cb_ex)  # the library holds raw pointers to them
+        c.calls = calls
         return c
 
     def __del__(self):

@@ -1490,17 +1490,20 @@ size_t wty_smem(int m) {
 
 // The finalisers of the reducing kernels from allreduced totals (row slabs): which = 0 residual
 // (arg: defer_check), 1 rho (arg: add_sc), 2 (p, q), 3 projected-residual check, 4 x / r update
-// (arg: identity), 5 the m x RT projection coefficients (arg: tallt mode).  `guard` repeats the
-// producing kernel's early exit (nothing ran, nothing to finalise).
+// (arg: identity), 5 the m x RT projection coefficients (arg: tallt mode), 6 the projection
+// coefficients of W^T q TOGETHER with (p, q) of the projected q (one allreduce of m RT + RT values,
+// SURVEY 8(e)): with f = W^T q = (A W)^T p and u = (W^T A W)^-1 f, (p, q - A W u) = (p, q) - f . u.
+// `off` is where the totals start in dtot (a deferred check's totals wait behind the next
+// reduction's); `guard` repeats the producing kernel's early exit (nothing ran, nothing to finalise).
 template <int RT>
 __global__ void __launch_bounds__(kElemThreads) k_b_fin(BState* st, int which, int arg, int guard, const double* L, int m,
-                                                        double* u, double* hist, int64_t hist_ld) {
-    __shared__ double tot[kMaxRedB];
+                                                        double* u, double* hist, int64_t hist_ld, int off) {
+    __shared__ double tot[kMaxRedB + kRMax];
     __shared__ double fk[6][128];
     __shared__ double sol[6][128];
     if (guard && st->nrun == 0) return;
-    const int cnt = which == 0 ? 2 * RT : (which == 5 ? m * RT : RT);
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) tot[t] = st->dtot[t];
+    const int cnt = which == 0 ? 2 * RT : (which == 5 ? m * RT : (which == 6 ? m * RT + RT : RT));
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) tot[t] = st->dtot[off + t];
     __syncthreads();
     switch (which) {
         case 0:
@@ -1518,10 +1521,28 @@ __global__ void __launch_bounds__(kElemThreads) k_b_fin(BState* st, int which, i
         case 4:
             fin_xr<RT>(st, tot, hist, hist_ld, arg);
             break;
+        case 6: {
+            fin_tallt<RT>(st, tot, L, m, u, arg, fk, sol);
+            __syncthreads();  // u (global, written by this block's warps) is visible past the barrier
+            if (threadIdx.x < RT) {
+                const int k = threadIdx.x;
+                double fu = 0.0;
+                for (int j = 0; j < m; ++j) fu = fadd_mul(fu, tot[j * RT + k], u[j * RT + k]);
+                tot[m * RT + k] = __dsub_rn(tot[m * RT + k], fu);
+                fin_pq(st, tot + m * RT, k);
+            }
+            break;
+        }
         default:
             fin_tallt<RT>(st, tot, L, m, u, arg, fk, sol);
             break;
     }
+}
+
+// row slabs: move a reducing kernel's local totals behind the next reduction's, so that one
+// allreduce carries both (dtot[src .. src + cnt) -> dtot[dst ..))
+__global__ void k_b_stash(BState* st, int src, int dst, int cnt) {
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) st->dtot[dst + t] = st->dtot[src + t];
 }
 
 // y -= sum_j u[j][k] C_j (running rhs) with (p, y) -> alpha (mode 0) or the projected initial
@@ -2181,7 +2202,14 @@ struct BatchSolve {
             ba.r = w->r;
             ba.add_sc = sc ? 1 : 0;
             launch_b_sweep(true, ba);
-            reduce(1, RT, sc ? 1 : 0, 1);
+            if (pending_rr) {  // [rho | the previous iteration's (r, r)] in one allreduce: check, then rho
+                pending_rr = false;
+                job.comm->allreduce(ctx, 2 * RT);
+                fin(4, 0, 1, RT);
+                fin(1, 0, 1, 0);
+            } else {
+                reduce(1, RT, sc ? 1 : 0, 1);
+            }
             z = w->zs;
         }
         require(ic || !sc, "batch: subspace correction needs the IC inner preconditioner");
@@ -2193,16 +2221,34 @@ struct BatchSolve {
             RCG_LAUNCHED(ctx);
         }
         const bool dfl = defl && defl->k > 0;
+        const bool fuse = job.comm && fuse_enabled();
         if (job.comm) job.comm->halo(ctx, w->p, RT);
         {
             KTimer t(ctx, 5, RT);
             if (!launch_grid_spmv(dfl))
-                k_b_spmv_pq<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(sargs(), bcap, w->p, w->q,
-                                                                                 w->st, w->partials, dfl ? 1 : 0);
+                k_b_spmv_pq<RT><<<pg, kSpmvThreads, pipe_smem_bytes(bcap), ctx->stream>>>(
+                    sargs(), bcap, w->p, w->q, w->st, w->partials, dfl && !fuse ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
         if (!dfl) reduce(2, RT, 0, 1);
-        if (dfl) {
+        if (dfl && fuse) {
+            // the SpMV left the local (p, q) in dtot[0..RT): behind W^T q's m RT totals, one allreduce,
+            // one finaliser (u, then alpha from (p, q) - f . u); the update's own (p, q) is not used
+            const int mk = defl->k * RT;
+            stash(0, mk, RT);
+            {
+                KTimer t(ctx, 9, RT);
+                launch_wty(defl->w, defl->ld, defl->k, w->q, defl->l, w->u, 1, 1);
+                RCG_LAUNCHED(ctx);
+            }
+            job.comm->allreduce(ctx, mk + RT);
+            fin(6, 1, 1, 0, defl->l, defl->k, w->u);
+            {
+                KTimer t(ctx, 9, RT);
+                launch_deflate(w->q, defl->aw, defl->ld, defl->k, w->u, w->p, 0);
+                RCG_LAUNCHED(ctx);
+            }
+        } else if (dfl) {
             {
                 KTimer t(ctx, 9, RT);
                 launch_wty(defl->w, defl->ld, defl->k, w->q, defl->l, w->u, 1, 1);
@@ -2222,7 +2268,12 @@ struct BatchSolve {
                                                                max_iter + 1, (!ic && !sc) ? 1 : 0);
             RCG_LAUNCHED(ctx);
         }
-        reduce(4, RT, (!ic && !sc) ? 1 : 0, 1);
+        if (fuse && ic && !sc) {  // the check waits for the next iteration's (r, z) allreduce
+            stash(0, RT, RT);
+            pending_rr = true;
+        } else {
+            reduce(4, RT, (!ic && !sc) ? 1 : 0, 1);
+        }
         if (sc) {
             {
                 KTimer t(ctx, 9, RT);
@@ -2267,8 +2318,31 @@ struct BatchSolve {
     void reduce(int which, int count, int arg, int guard, const double* L = nullptr, int mm = 0, double* u = nullptr) {
         if (!job.comm) return;
         job.comm->allreduce(ctx, count);
-        k_b_fin<RT><<<1, kElemThreads, 0, ctx->stream>>>(w->st, which, arg, guard, L, mm, u, w->hist, max_iter + 1);
+        fin(which, arg, guard, 0, L, mm, u);
+    }
+    void fin(int which, int arg, int guard, int off, const double* L = nullptr, int mm = 0, double* u = nullptr) {
+        k_b_fin<RT><<<1, kElemThreads, 0, ctx->stream>>>(w->st, which, arg, guard, L, mm, u, w->hist, max_iter + 1, off);
         RCG_LAUNCHED(ctx);
+    }
+    void stash(int src, int dst, int cnt) {
+        k_b_stash<<<1, 32, 0, ctx->stream>>>(w->st, src, dst, cnt);
+        RCG_LAUNCHED(ctx);
+    }
+    // row slabs, fused reductions (RCG_DIST_FUSE=0 keeps one allreduce per dot):
+    // (p, q) travels with W^T q, and the convergence check's (r, r) waits for the next iteration's
+    // (r, z) -- two allreduces per deflated iteration instead of four.  The deferred check is
+    // flushed before the host reads the running count (run()).
+    static bool fuse_enabled() {  // (read per call: the A/B test switches it inside one process)
+        const char* e = std::getenv("RCG_DIST_FUSE");
+        return !(e && std::atoi(e) == 0);
+    }
+    bool pending_rr = false;
+    void flush_pending() {
+        if (!pending_rr) return;
+        pending_rr = false;
+        stash(RT, 0, RT);
+        job.comm->allreduce(ctx, RT);
+        fin(4, 0, 1, 0);
     }
 
     void launch_b_sweep(bool backward, SweepArgs& s) {
@@ -2396,6 +2470,7 @@ struct BatchSolve {
         bool have_prev = false;
         while (enq < max_iter) {
             for (int j = 0; j < batch && enq < max_iter; ++j, ++enq) iteration();
+            flush_pending();
             RCG_CK(cudaMemcpyAsync((void*)(flags + slot), &w->st->nrun, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
             RCG_CK(cudaEventRecord(evs[slot], ctx->stream));
             if (enq >= max_iter) break;

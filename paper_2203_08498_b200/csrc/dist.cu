@@ -1584,7 +1584,7 @@ int rcg_dist_solve_batch(rcg_comm* comm, rcg_dslab* slab, const rcg_dbasis* basi
     return guard([&] {
         require(comm && slab && B && X && cfg && reps, "dist_solve_batch: null argument");
         require(comm->local_slabs() == 1, "dist_solve_batch: one slab per process (loopback: G = 1)");
-        ensure_g(slab, 768);
+        ensure_g(slab, 768 + 2 * 24);  // m RT projection totals + a fused (p, q) / deferred (r, r) row
         DistBatchComm bc;
         bc.comm = comm;
         bc.d = slab;

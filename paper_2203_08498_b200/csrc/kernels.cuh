@@ -42,7 +42,7 @@ struct BatchComm {
     virtual ~BatchComm() {}
     virtual void allreduce(rcg_ctx* ctx, int count) = 0;     // dtot[0..count) summed over the ranks in place
     virtual void halo(rcg_ctx* ctx, double* v, int rt) = 0;  // halo rows [nloc, nloc + nhalo) of an rt-interleaved v
-    double* dtot = nullptr;                                   // device, >= 768 doubles
+    double* dtot = nullptr;                                   // device, >= 768 + 48 doubles (fused reductions)
     int32_t nhalo = 0;
 };
 void batch_solve_dist(rcg_ctx* ctx, const rcg_matrix* a, const rcg_prec* m, const rcg_basis* defl, BatchComm* comm,

@@ -112,3 +112,90 @@ def _floor(oracle, h, ref, blocks, cfg):
             oracle.pcg_solve(sa, ref["scaled_rhs"][0], x, kind=1, ic=f, eps=cfg.eps, max_iter=cfg.max_iter)
         out = max(out, float(np.linalg.norm(x - ref["solutions"][0]) / np.linalg.norm(ref["solutions"][0])))
     return out
+
+
+def _fuse_worker(rank, world, port, name, out_dir):
+    """Solve 1 + recycling once, then the batched accelerated solves twice on the same basis:
+    one allreduce per dot (RCG_DIST_FUSE=0), then the fused reductions (default)."""
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from oracle import Matrix, Oracle
+        from oracle.sequence import rhs_set
+        from paper_2203_08498_b200 import api, problems
+        from paper_2203_08498_b200 import dist as pdist
+
+        o = Oracle()
+        cfg = problems.SMALL[name]
+        h = problems.generate(cfg)
+        sa, dis = o.diagonal_scale(Matrix.of(h))
+        host = problems.HostCsr(h.n, sa.rs, sa.ci, sa.va)
+        _, bs = rhs_set(o, cfg, h, Matrix.of(h), dis)
+        r = pdist.NcclRank(host, transport="host")
+        lo, hi = r.plan.row_begin, r.plan.row_end
+        smp = api.SamplerState.method_a(r.ctx, cfg.sampler_m, cfg.max_iter, r.plan.nloc)
+        x1 = np.zeros(r.plan.nloc)
+        api.dist_pcg_solve_sampled(r.comm, [r.slab], [smp], [bs[0][lo:hi]], [x1], cfg.eps, cfg.max_iter)
+        kind = "sc" if cfg.method == "sc" else "deflation"
+        *_, basis = api.dist_recycle(r.comm, [r.slab], [smp], [x1], keep_count=cfg.keep, kind=kind)
+        B = np.stack([b[lo:hi] for b in bs[1:]])
+        res = {}
+        for tag, env in (("plain", "0"), ("fused", "1")):
+            os.environ["RCG_DIST_FUSE"] = env
+            before = dict(r.comm.calls)
+            X = np.zeros_like(B)
+            reps = api.dist_solve_batch(r.comm, r.slab, B, X, basis, cfg.eps, cfg.max_iter)
+            res[tag + "_its"] = np.array([q.iterations for q in reps])
+            res[tag + "_conv"] = np.array([q.converged for q in reps])
+            res[tag + "_x"] = X
+            res[tag + "_allreduces"] = r.comm.calls["allreduce"] - before["allreduce"]
+            res[tag + "_values"] = r.comm.calls["allreduce_values"] - before["allreduce_values"]
+        np.savez(os.path.join(out_dir, f"fuse{rank}.npz"), lo=lo, **res)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_fused_allreduces_match_one_per_dot(problems, tmp_path, name, parity_log):
+    """(p, q) travels with W^T q and the convergence check's (r, r) with the next
+    (r, z).  Two processes over the host transport: the fused batched slab solves against the
+    one-allreduce-per-dot ones on the same basis -- iterations within one step, solutions at the
+    solver tolerance, and the collectives per iteration counted (deflation: 4 -> ~2)."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_fuse_worker, args=(r, world, port, name, str(tmp_path))) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    parts = sorted((np.load(tmp_path / f"fuse{r}.npz") for r in range(world)), key=lambda q: int(q["lo"]))
+    a, b = parts
+    for tag in ("plain", "fused"):  # every rank made the same decisions
+        assert np.array_equal(a[tag + "_its"], b[tag + "_its"]) and all(a[tag + "_conv"])
+        assert int(a[tag + "_allreduces"]) == int(b[tag + "_allreduces"])
+    assert np.all(np.abs(a["plain_its"] - a["fused_its"]) <= 1), (a["plain_its"], a["fused_its"])
+    xp = np.concatenate([q["plain_x"] for q in parts], axis=1)
+    xf = np.concatenate([q["fused_x"] for q in parts], axis=1)
+    rel = max(float(np.linalg.norm(u - v) / np.linalg.norm(u)) for u, v in zip(xp, xf))
+    assert rel <= 1e-7, rel
+    n_plain, n_fused = int(a["plain_allreduces"]), int(a["fused_allreduces"])
+    iters = int(a["plain_its"].max())
+    parity_log(f"fused_allreduces[{name}]", plain_per_iteration=n_plain / iters, fused_per_iteration=n_fused / iters,
+               solution_rel=rel, bar=1e-7)
+    deflation = problems.SMALL[name].method != "sc"
+    # deflation: 4 -> 2 per iteration (+ one flush per enqueued batch); SC keeps (r, r) apart: 4 -> 4
+    assert n_fused <= (0.65 if deflation else 1.0) * n_plain, (n_plain, n_fused)
