@@ -806,13 +806,47 @@ struct DistSolve {
         return a;
     }
 
-    void scalar(int stage) {
+    void scalar(int stage, int goff = 0) {
         for (int s = 0; s < ns; ++s) {
             rcg_ctx* ctx = sl[s]->ctx;
-            k_d_scalar<<<1, 1, 0, ctx->stream>>>(ctx->ws.st, sl[s]->dsum, stage, ctx->ws.hist, ctx->ws.alph,
+            k_d_scalar<<<1, 1, 0, ctx->stream>>>(ctx->ws.st, sl[s]->dsum + goff, stage, ctx->ws.hist, ctx->ws.alph,
                                                  ctx->ws.bet, ic ? 0 : 1, flags());
             RCG_LAUNCHED(ctx);
         }
+    }
+
+    // Fused reductions (RCG_DIST_FUSE=0 keeps one allreduce per dot): with the IC
+    // preconditioner the convergence check's (r, r) waits in dsum[1] for the next iteration's
+    // (r, z) in dsum[0] -- one allreduce of two values instead of two of one.  Nothing between
+    // the x / r update and the next sweeps reads the check's outcome, so every value is bitwise
+    // the unfused loop's; a finished solve costs one extra pair of sweeps.  The pending check is
+    // flushed before the host reads the stop flag (run()).
+    bool pending_rr = false;
+    bool fuse_rr() const {
+        const char* e = std::getenv("RCG_DIST_FUSE");
+        return ic && !sc && !(e && std::atoi(e) == 0);
+    }
+    // the (r, r) check (pcg.cpp:80-88) and the observer (sampling.cpp error_sampling_observer)
+    void check_and_sample(int goff) {
+        scalar(3, goff);
+        if (!smp) return;
+        for (int s = 0; s < ns; ++s) {
+            rcg_dslab* d = sl[s];
+            rcg_ctx* ctx = d->ctx;
+            rcg_sampler* sp = smp[s];
+            k_d_sched<<<1, 1, 0, ctx->stream>>>(ctx->ws.st, ctx->ws.smp_pending, sp->occupied, sp->stored_iter,
+                                                sp->thresholds);
+            RCG_LAUNCHED(ctx);
+            k_d_sample<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
+                d->xe, ctx->ws.r, sp->slots, sp->ld, ctx->ws.smp_pending, ctx->ws.st, d->nloc);
+            RCG_LAUNCHED(ctx);
+        }
+    }
+    void flush_pending() {
+        if (!pending_rr) return;
+        pending_rr = false;
+        comm->allreduce(sl, ns, 2);  // (dsum[0] rides along unused)
+        check_and_sample(1);
     }
 
     // f = C^T y over the local rows -> allreduce (m values) -> out = (W^T A W)^-1 f on every slab
@@ -881,7 +915,13 @@ struct DistSolve {
                     ctx->ws.r, ctx->ws.zs, d->nloc, ctx->ws.partials, ctx->ws.st, d->dsum);
                 RCG_LAUNCHED(ctx);
             }
-            comm->allreduce(sl, ns, 1);
+            if (pending_rr) {  // [(r, z) | the previous iteration's (r, r)]: check + observer, then rho
+                pending_rr = false;
+                comm->allreduce(sl, ns, 2);
+                check_and_sample(1);
+            } else {
+                comm->allreduce(sl, ns, 1);
+            }
             scalar(1);  // (+ f . u with subspace correction)
         }
         for (int s = 0; s < ns; ++s) {
@@ -917,28 +957,20 @@ struct DistSolve {
         }
         comm->allreduce(sl, ns, 1);
         scalar(2);
+        const bool defer_rr = fuse_rr();
         for (int s = 0; s < ns; ++s) {
             rcg_dslab* d = sl[s];
             rcg_ctx* ctx = d->ctx;
             KTimer t(ctx, 3);
             k_d_xr<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
-                d->xe, ctx->ws.r, d->pe, ctx->ws.q, d->nloc, ctx->ws.partials, ctx->ws.st, d->dsum);
+                d->xe, ctx->ws.r, d->pe, ctx->ws.q, d->nloc, ctx->ws.partials, ctx->ws.st, d->dsum + (defer_rr ? 1 : 0));
             RCG_LAUNCHED(ctx);
         }
-        comm->allreduce(sl, ns, 1);
-        scalar(3);
-        if (smp) {  // the observer (sampling.cpp error_sampling_observer): schedule + snapshot
-            for (int s = 0; s < ns; ++s) {
-                rcg_dslab* d = sl[s];
-                rcg_ctx* ctx = d->ctx;
-                rcg_sampler* sp = smp[s];
-                k_d_sched<<<1, 1, 0, ctx->stream>>>(ctx->ws.st, ctx->ws.smp_pending, sp->occupied, sp->stored_iter,
-                                                    sp->thresholds);
-                RCG_LAUNCHED(ctx);
-                k_d_sample<<<stream_grid(ctx, d->nloc), kStreamThreads, 0, ctx->stream>>>(
-                    d->xe, ctx->ws.r, sp->slots, sp->ld, ctx->ws.smp_pending, ctx->ws.st, d->nloc);
-                RCG_LAUNCHED(ctx);
-            }
+        if (defer_rr) {
+            pending_rr = true;
+        } else {
+            comm->allreduce(sl, ns, 1);
+            check_and_sample(0);
         }
         if (sc) {  // W^T r for the next apply (subspace_correction.cpp:50-51)
             std::vector<double*> rs(ns);
@@ -962,6 +994,7 @@ struct DistSolve {
         bool have_prev = false;
         while (true) {
             for (int j = 0; j < batch && enq < max_iter; ++j, ++enq) iteration();
+            flush_pending();
             RCG_CK(cudaMemcpyAsync((void*)(flags_h + slot), &c0->ws.st->done, sizeof(int), cudaMemcpyDeviceToHost,
                                    c0->stream));
             RCG_CK(cudaEventRecord(evs[slot], c0->stream));

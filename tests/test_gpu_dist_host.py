@@ -142,13 +142,22 @@ def _fuse_worker(rank, world, port, name, out_dir):
         _, bs = rhs_set(o, cfg, h, Matrix.of(h), dis)
         r = pdist.NcclRank(host, transport="host")
         lo, hi = r.plan.row_begin, r.plan.row_end
-        smp = api.SamplerState.method_a(r.ctx, cfg.sampler_m, cfg.max_iter, r.plan.nloc)
-        x1 = np.zeros(r.plan.nloc)
-        api.dist_pcg_solve_sampled(r.comm, [r.slab], [smp], [bs[0][lo:hi]], [x1], cfg.eps, cfg.max_iter)
+        res = {}
+        # solve 1 (ICCG with the sampler): the deferred check changes no value -- bitwise
+        for tag, env in (("s1plain", "0"), ("s1fused", "1")):
+            os.environ["RCG_DIST_FUSE"] = env
+            before = dict(r.comm.calls)
+            smp = api.SamplerState.method_a(r.ctx, cfg.sampler_m, cfg.max_iter, r.plan.nloc)
+            x1 = np.zeros(r.plan.nloc)
+            r1 = api.dist_pcg_solve_sampled(r.comm, [r.slab], [smp], [bs[0][lo:hi]], [x1], cfg.eps, cfg.max_iter)
+            res[tag + "_x"] = x1
+            res[tag + "_its"] = np.array([r1.iterations])
+            res[tag + "_hist"] = np.asarray(r1.history)
+            res[tag + "_slots"] = np.asarray(smp.state()[1])
+            res[tag + "_allreduces"] = r.comm.calls["allreduce"] - before["allreduce"]
         kind = "sc" if cfg.method == "sc" else "deflation"
         *_, basis = api.dist_recycle(r.comm, [r.slab], [smp], [x1], keep_count=cfg.keep, kind=kind)
         B = np.stack([b[lo:hi] for b in bs[1:]])
-        res = {}
         for tag, env in (("plain", "0"), ("fused", "1")):
             os.environ["RCG_DIST_FUSE"] = env
             before = dict(r.comm.calls)
@@ -187,6 +196,13 @@ def test_fused_allreduces_match_one_per_dot(problems, tmp_path, name, parity_log
     for tag in ("plain", "fused"):  # every rank made the same decisions
         assert np.array_equal(a[tag + "_its"], b[tag + "_its"]) and all(a[tag + "_conv"])
         assert int(a[tag + "_allreduces"]) == int(b[tag + "_allreduces"])
+    for q in parts:  # solve 1: identical values, the sampler's slots included
+        assert np.array_equal(q["s1plain_x"], q["s1fused_x"]) and np.array_equal(q["s1plain_hist"], q["s1fused_hist"])
+        assert np.array_equal(q["s1plain_slots"], q["s1fused_slots"])
+    its1 = int(a["s1plain_its"][0])
+    s1p, s1f = int(a["s1plain_allreduces"]), int(a["s1fused_allreduces"])
+    parity_log(f"fused_allreduces_solve1[{name}]", plain_per_iteration=s1p / its1, fused_per_iteration=s1f / its1)
+    assert s1f <= 0.8 * s1p, (s1p, s1f)  # 3 -> 2 per iteration (+ one flush per enqueued batch)
     assert np.all(np.abs(a["plain_its"] - a["fused_its"]) <= 1), (a["plain_its"], a["fused_its"])
     xp = np.concatenate([q["plain_x"] for q in parts], axis=1)
     xf = np.concatenate([q["fused_x"] for q in parts], axis=1)
