@@ -44,7 +44,7 @@ def num(d, u, key, scale_to):
         return None
     v = float(v.replace(",", ""))
     unit = u.get(key, "")
-    mult = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
+    mult = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
             "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1.0)
     return v * mult
 
