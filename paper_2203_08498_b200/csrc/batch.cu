@@ -713,6 +713,24 @@ __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, 
         if (row >= 0) {
             const int64_t me = static_cast<int64_t>(row) * RT + VW * c;
             const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
+            if (a.prefetch) {
+                // the row's whole entry record (columns and coefficients stream from HBM) is requested
+                // now, one 32-byte sector per lane of the row group: the chunks after the first then
+                // hit cache instead of paying one DRAM round trip each AFTER the wait on the newest
+                // parent -- which, backward, is the row's first entry, so those trips sat on the
+                // level chain (C3 RT 24 backward: 7.1 us per level against the forward's 3.4)
+                const uintptr_t v0 = reinterpret_cast<uintptr_t>(a.pval + beg) & ~uintptr_t(31);
+                const uintptr_t v1 = reinterpret_cast<uintptr_t>(a.pval + end);
+                const uintptr_t c0 = reinterpret_cast<uintptr_t>(a.pcol + beg) & ~uintptr_t(31);
+                const uintptr_t c1 = reinterpret_cast<uintptr_t>(a.pcol + end);
+                if (a.prefetch == 1) {
+                    for (uintptr_t q = v0 + 32u * c; q < v1; q += 32u * G) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                    for (uintptr_t q = c0 + 32u * c; q < c1; q += 32u * G) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                } else {
+                    for (uintptr_t q = v0 + 32u * c; q < v1; q += 32u * G) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+                    for (uintptr_t q = c0 + 32u * c; q < c1; q += 32u * G) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+                }
+            }
             double s[VW];
             double rr[BWD ? VW : 1];
             {
@@ -2355,6 +2373,10 @@ struct BatchSolve {
         int bps0 = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, false, s.npos);
         if (ctx->sweep_bps <= 0 && f->n > 0 && static_cast<double>(f->nnz_l) / f->n > kDepChunkHost) bps0 = std::max(bps0, 3);
         s.backoff_ns = ctx->sweep_backoff_ns;
+        {  // RCG_BSWEEP_PF: 0 off, 1 L2, 2 L1; bit 2 (|4): backward sweep only
+            static const int pf_env = std::getenv("RCG_BSWEEP_PF") ? std::atoi(std::getenv("RCG_BSWEEP_PF")) : 0;
+            s.prefetch = ((pf_env & 4) && !backward) ? 0 : (pf_env & 3);
+        }
         KTimer t(ctx, backward ? 7 : 6, RT);
         // very wide levels (the multicolour orderings): one launch per level, no polling
         // (default shape rule of icsweep_lv.cu: >= 600K rows per level; mode 4 always).  Forced on
