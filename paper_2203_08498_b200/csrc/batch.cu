@@ -681,8 +681,14 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
 // lane sweeping its own 16-byte chunk exactly like the single-pair (RT = 2) sweep: per-lane work
 // and polling stay those of RT = 2 whatever RT is, the row's values are published chunk by chunk
 // with no coordination between lanes, and a level costs about what it costs at RT = 2.
-template <bool BWD, int RT, int VW, int CH>
+// DEEP (backward, 27-point rows): the parents past the first two chunks are old (two or more
+// levels back); their values are requested BEFORE the wait on the newest parents, by cp.async
+// (L2 -> shared memory, no destination registers), and read from shared memory when their chunk
+// comes up -- a value still unpublished then (sentinel) falls back to the polling loads.
+template <bool BWD, int RT, int VW, int CH, bool DEEP = false>
 __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, BState* st) {
+    constexpr int KS = 8;  // stashed parents per lane
+    __shared__ __align__(16) double stash_mem[DEEP ? KS * 128 * VW : 2];
     constexpr int G = RT / VW;
     constexpr int RPW = 32 / G;
     constexpr bool ORD = VW == 2;  // consume in order as parents arrive (measured: helps 16-byte chunks only)
@@ -731,6 +737,26 @@ __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, 
                     for (uintptr_t q = c0 + 32u * c; q < c1; q += 32u * G) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
                 }
             }
+            const int32_t sbeg = beg + 2 * CH;
+            const int ns = DEEP ? max(0, min(KS, end - sbeg)) : 0;
+            if constexpr (DEEP) {
+                int32_t sc_[KS];
+#pragma unroll
+                for (int j = 0; j < KS; ++j)
+                    if (j < ns) sc_[j] = __ldg(a.pcol + sbeg + j);
+#pragma unroll
+                for (int j = 0; j < KS; ++j)
+                    if (j < ns) {
+                        const double* src = a.out + static_cast<int64_t>(sc_[j]) * RT + VW * c;
+#pragma unroll
+                        for (int h = 0; h < VW / 2; ++h) {
+                            const unsigned dst = static_cast<unsigned>(
+                                __cvta_generic_to_shared(stash_mem + ((j * (VW / 2) + h) * 128 + threadIdx.x) * 2));
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 2 * h) : "memory");
+                        }
+                    }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
             double s[VW];
             double rr[BWD ? VW : 1];
             {
@@ -765,9 +791,28 @@ __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, 
                         col[j] = __ldg(a.pcol + e0 + j);
                         val[j] = __ldg(a.pval + e0 + j);
                     }
+                if constexpr (DEEP) {
+                    if (e0 >= sbeg && ns > 0) asm volatile("cp.async.wait_all;" ::: "memory");
+                }
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
-                    if (j < cnt) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + VW * c, dep[j]);
+                    if (j < cnt) {
+                        bool stashed = false;
+                        if constexpr (DEEP) {
+                            const int si = e0 + j - sbeg;
+                            if (si >= 0 && si < ns) {
+                                stashed = true;
+#pragma unroll
+                                for (int h = 0; h < VW / 2; ++h) {
+                                    const double2 t = *reinterpret_cast<const double2*>(
+                                        stash_mem + ((si * (VW / 2) + h) * 128 + threadIdx.x) * 2);
+                                    dep[j][2 * h] = t.x;
+                                    dep[j][2 * h + 1] = t.y;
+                                }
+                            }
+                        }
+                        if (!stashed) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + VW * c, dep[j]);
+                    }
                 int used = 0;
                 while (true) {
                     if constexpr (ORD) {
@@ -2439,7 +2484,13 @@ struct BatchSolve {
                     backward ? go(k_b_sweepc<true, RT, 4, 4>) : go(k_b_sweepc<false, RT, 4, 4>);
                 }
             }
-            if (!launched) backward ? go(k_b_sweepc<true, RT, 2, 4>) : go(k_b_sweepc<false, RT, 2, 4>);
+            if (!launched) {
+                static const int pf_env = std::getenv("RCG_BSWEEP_PF") ? std::atoi(std::getenv("RCG_BSWEEP_PF")) : 0;
+                if (backward && (pf_env & 8))
+                    go(k_b_sweepc<true, RT, 2, 4, true>);
+                else
+                    backward ? go(k_b_sweepc<true, RT, 2, 4>) : go(k_b_sweepc<false, RT, 2, 4>);
+            }
             RCG_LAUNCHED(ctx);
             if (rho) {
                 const int64_t tiles = (s.npos + rpw - 1) / rpw;
