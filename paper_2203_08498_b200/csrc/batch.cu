@@ -2334,6 +2334,20 @@ struct BatchSolve {
         if (fuse && ic && !sc) {  // the check waits for the next iteration's (r, z) allreduce
             stash(0, RT, RT);
             pending_rr = true;
+        } else if (fuse && sc) {
+            // subspace correction: (r, r) travels with W^T r (subspace_correction.cpp:50-51) -- the
+            // check first, then the coefficients, as unfused; W^T r of a just-finished solve is wasted
+            const int mk = scb->k * RT;
+            stash(0, mk, RT);
+            {
+                KTimer t(ctx, 9, RT);
+                launch_wty(scb->w, scb->ld, scb->k, w->r, scb->l, w->u2, 2, 1);
+                RCG_LAUNCHED(ctx);
+            }
+            job.comm->allreduce(ctx, mk + RT);
+            fin(4, 0, 1, mk);
+            fin(5, 2, 1, 0, scb->l, scb->k, w->u2);
+            return;
         } else {
             reduce(4, RT, (!ic && !sc) ? 1 : 0, 1);
         }

@@ -213,5 +213,5 @@ def test_fused_allreduces_match_one_per_dot(problems, tmp_path, name, parity_log
     parity_log(f"fused_allreduces[{name}]", plain_per_iteration=n_plain / iters, fused_per_iteration=n_fused / iters,
                solution_rel=rel, bar=1e-7)
     deflation = problems.SMALL[name].method != "sc"
-    # deflation: 4 -> 2 per iteration (+ one flush per enqueued batch); SC keeps (r, r) apart: 4 -> 4
-    assert n_fused <= (0.65 if deflation else 1.0) * n_plain, (n_plain, n_fused)
+    # deflation: 4 -> 2 per iteration (+ one flush per enqueued batch); SC ((r, r) with W^T r): 4 -> 3
+    assert n_fused <= (0.65 if deflation else 0.85) * n_plain, (n_plain, n_fused)
