@@ -681,14 +681,8 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
 // lane sweeping its own 16-byte chunk exactly like the single-pair (RT = 2) sweep: per-lane work
 // and polling stay those of RT = 2 whatever RT is, the row's values are published chunk by chunk
 // with no coordination between lanes, and a level costs about what it costs at RT = 2.
-// DEEP (backward, 27-point rows): the parents past the first two chunks are old (two or more
-// levels back); their values are requested BEFORE the wait on the newest parents, by cp.async
-// (L2 -> shared memory, no destination registers), and read from shared memory when their chunk
-// comes up -- a value still unpublished then (sentinel) falls back to the polling loads.
-template <bool BWD, int RT, int VW, int CH, bool DEEP = false>
+template <bool BWD, int RT, int VW, int CH>
 __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, BState* st) {
-    constexpr int KS = 8;  // stashed parents per lane
-    __shared__ __align__(16) double stash_mem[DEEP ? KS * 128 * VW : 2];
     constexpr int G = RT / VW;
     constexpr int RPW = 32 / G;
     constexpr bool ORD = VW == 2;  // consume in order as parents arrive (measured: helps 16-byte chunks only)
@@ -703,6 +697,12 @@ __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, 
     // map and row data one tile ahead -- C3 RT 16 fwd / bwd 4.8 / 6.9 -> 5.5 / 8.8 ms, C2 RT 12 bwd
     // 0.66 -> 1.03 ms: rows taken early only spin on parents of later levels.)  The r chunk of
     // the (r, z) partial is requested with the row's input, not after the publish.
+    // (measured and dropped, round 2, C3 RT 24 fwd / bwd ms per launch against 6.14 / 12.10:
+    // prefetching the row's whole entry record (pcol / pval sectors) to L1 or L2 before the first
+    // chunk 6.38 / 12.92; additionally requesting the parents past the first two chunks by
+    // cp.async into shared memory before the wait on the newest ones (no destination registers)
+    // -- / 19.4: the chain is not bound by the later chunks' round trips, and the extra requests
+    // compete with the polling loads for the L2 ports.)
     auto take = [&]() {
         int t = 0;
         if (lane == 0) t = atomicAdd(&a.tickets[0], 1);
@@ -719,44 +719,6 @@ __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, 
         if (row >= 0) {
             const int64_t me = static_cast<int64_t>(row) * RT + VW * c;
             const int32_t beg = __ldg(a.prs + pos), end = __ldg(a.prs + pos + 1);
-            if (a.prefetch) {
-                // the row's whole entry record (columns and coefficients stream from HBM) is requested
-                // now, one 32-byte sector per lane of the row group: the chunks after the first then
-                // hit cache instead of paying one DRAM round trip each AFTER the wait on the newest
-                // parent -- which, backward, is the row's first entry, so those trips sat on the
-                // level chain (C3 RT 24 backward: 7.1 us per level against the forward's 3.4)
-                const uintptr_t v0 = reinterpret_cast<uintptr_t>(a.pval + beg) & ~uintptr_t(31);
-                const uintptr_t v1 = reinterpret_cast<uintptr_t>(a.pval + end);
-                const uintptr_t c0 = reinterpret_cast<uintptr_t>(a.pcol + beg) & ~uintptr_t(31);
-                const uintptr_t c1 = reinterpret_cast<uintptr_t>(a.pcol + end);
-                if (a.prefetch == 1) {
-                    for (uintptr_t q = v0 + 32u * c; q < v1; q += 32u * G) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
-                    for (uintptr_t q = c0 + 32u * c; q < c1; q += 32u * G) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
-                } else {
-                    for (uintptr_t q = v0 + 32u * c; q < v1; q += 32u * G) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
-                    for (uintptr_t q = c0 + 32u * c; q < c1; q += 32u * G) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
-                }
-            }
-            const int32_t sbeg = beg + 2 * CH;
-            const int ns = DEEP ? max(0, min(KS, end - sbeg)) : 0;
-            if constexpr (DEEP) {
-                int32_t sc_[KS];
-#pragma unroll
-                for (int j = 0; j < KS; ++j)
-                    if (j < ns) sc_[j] = __ldg(a.pcol + sbeg + j);
-#pragma unroll
-                for (int j = 0; j < KS; ++j)
-                    if (j < ns) {
-                        const double* src = a.out + static_cast<int64_t>(sc_[j]) * RT + VW * c;
-#pragma unroll
-                        for (int h = 0; h < VW / 2; ++h) {
-                            const unsigned dst = static_cast<unsigned>(
-                                __cvta_generic_to_shared(stash_mem + ((j * (VW / 2) + h) * 128 + threadIdx.x) * 2));
-                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 2 * h) : "memory");
-                        }
-                    }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
             double s[VW];
             double rr[BWD ? VW : 1];
             {
@@ -791,28 +753,9 @@ __global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, 
                         col[j] = __ldg(a.pcol + e0 + j);
                         val[j] = __ldg(a.pval + e0 + j);
                     }
-                if constexpr (DEEP) {
-                    if (e0 >= sbeg && ns > 0) asm volatile("cp.async.wait_all;" ::: "memory");
-                }
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
-                    if (j < cnt) {
-                        bool stashed = false;
-                        if constexpr (DEEP) {
-                            const int si = e0 + j - sbeg;
-                            if (si >= 0 && si < ns) {
-                                stashed = true;
-#pragma unroll
-                                for (int h = 0; h < VW / 2; ++h) {
-                                    const double2 t = *reinterpret_cast<const double2*>(
-                                        stash_mem + ((si * (VW / 2) + h) * 128 + threadIdx.x) * 2);
-                                    dep[j][2 * h] = t.x;
-                                    dep[j][2 * h + 1] = t.y;
-                                }
-                            }
-                        }
-                        if (!stashed) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + VW * c, dep[j]);
-                    }
+                    if (j < cnt) RelVec<VW>::ld(a.out + static_cast<int64_t>(col[j]) * RT + VW * c, dep[j]);
                 int used = 0;
                 while (true) {
                     if constexpr (ORD) {
@@ -2432,10 +2375,6 @@ struct BatchSolve {
         int bps0 = ctx->sweep_bps > 0 ? ctx->sweep_bps : sweep_ctas_per_sm(f, false, s.npos);
         if (ctx->sweep_bps <= 0 && f->n > 0 && static_cast<double>(f->nnz_l) / f->n > kDepChunkHost) bps0 = std::max(bps0, 3);
         s.backoff_ns = ctx->sweep_backoff_ns;
-        {  // RCG_BSWEEP_PF: 0 off, 1 L2, 2 L1; bit 2 (|4): backward sweep only
-            static const int pf_env = std::getenv("RCG_BSWEEP_PF") ? std::atoi(std::getenv("RCG_BSWEEP_PF")) : 0;
-            s.prefetch = ((pf_env & 4) && !backward) ? 0 : (pf_env & 3);
-        }
         KTimer t(ctx, backward ? 7 : 6, RT);
         // very wide levels (the multicolour orderings): one launch per level, no polling
         // (default shape rule of icsweep_lv.cu: >= 600K rows per level; mode 4 always).  Forced on
@@ -2498,13 +2437,7 @@ struct BatchSolve {
                     backward ? go(k_b_sweepc<true, RT, 4, 4>) : go(k_b_sweepc<false, RT, 4, 4>);
                 }
             }
-            if (!launched) {
-                static const int pf_env = std::getenv("RCG_BSWEEP_PF") ? std::atoi(std::getenv("RCG_BSWEEP_PF")) : 0;
-                if (backward && (pf_env & 8))
-                    go(k_b_sweepc<true, RT, 2, 4, true>);
-                else
-                    backward ? go(k_b_sweepc<true, RT, 2, 4>) : go(k_b_sweepc<false, RT, 2, 4>);
-            }
+            if (!launched) backward ? go(k_b_sweepc<true, RT, 2, 4>) : go(k_b_sweepc<false, RT, 2, 4>);
             RCG_LAUNCHED(ctx);
             if (rho) {
                 const int64_t tiles = (s.npos + rpw - 1) / rpw;

@@ -30,7 +30,6 @@ struct SweepArgs {
     const double* r;       // backward: rho = (r, z) partials when non-null
     int add_sc;            // backward: rho += (W^T r) . u (subspace correction)
     int backoff_ns;        // first __nanosleep of a dependency wait
-    int prefetch;          // batched chunk-lane sweeps: prefetch a row's entry records (0 off, 1 L2, 2 L1)
     int* tickets;          // [0] tile ticket, [1] exit count, [2] group ticket
     double* partials;
     double* gpart;
