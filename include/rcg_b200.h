@@ -373,7 +373,10 @@ void rcg_dbasis_destroy(rcg_dbasis* b);
  * through one kernel sequence -- the single-GPU batched solver with its reductions allreduced over
  * the ranks and p's halo rows exchanged (RT-interleaved) before each SpMV.  basis: deflation or
  * subspace correction (null: block-Jacobi ICCG).  One slab per process (NCCL / host transports;
- * loopback only at G = 1). */
+ * loopback only at G = 1).  Reductions are fused (pcg.cpp:63-89 has one per dot): (p, q) travels
+ * with W^T q, the (r, r) of the convergence check with the next iteration's (r, z) (subspace
+ * correction: with W^T r) -- two allreduces per deflated iteration; environment RCG_DIST_FUSE=0
+ * keeps one allreduce per dot. */
 int rcg_dist_solve_batch(rcg_comm* comm, rcg_dslab* slab, const rcg_dbasis* basis, const double* B, double* X,
                          const rcg_solver_config* cfg, int nrhs, rcg_solve_report* reps);
 int rcg_dist_solve(rcg_comm* comm, int nslabs, rcg_dslab* const* slabs, const rcg_dbasis* basis, const double* const* b,
