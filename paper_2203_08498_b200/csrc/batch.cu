@@ -681,8 +681,11 @@ __global__ void __launch_bounds__(128) k_b_sweep(SweepArgs a, BState* st) {
 // lane sweeping its own 16-byte chunk exactly like the single-pair (RT = 2) sweep: per-lane work
 // and polling stay those of RT = 2 whatever RT is, the row's values are published chunk by chunk
 // with no coordination between lanes, and a level costs about what it costs at RT = 2.
+#ifndef RCG_BSWEEPC_BWD_MINB
+#define RCG_BSWEEPC_BWD_MINB 8  // (dev A/B: resident CTAs per SM the backward 16-byte-chunk sweep is compiled for)
+#endif
 template <bool BWD, int RT, int VW, int CH>
-__global__ void __launch_bounds__(128, VW == 2 ? 8 : 6) k_b_sweepc(SweepArgs a, BState* st) {
+__global__ void __launch_bounds__(128, VW == 2 ? (BWD ? RCG_BSWEEPC_BWD_MINB : 8) : 6) k_b_sweepc(SweepArgs a, BState* st) {
     constexpr int G = RT / VW;
     constexpr int RPW = 32 / G;
     constexpr bool ORD = VW == 2;  // consume in order as parents arrive (measured: helps 16-byte chunks only)
